@@ -1,0 +1,342 @@
+#!/usr/bin/env python
+"""Throughput of the B200 ComFree-Sim contact-resolution step (one JSON line).
+
+Workload (BASELINE.json metric, config 4 "dense pile"): per GPU 1024 worlds x
+500 free bodies (spheres / boxes / capsules) x 2000 contacts, condim 3, 4-facet
+cone, dt = 0.002, synthetic seeded inputs (harness/scenes.py c4_pile).  One
+step = S0 (world offsets from the sorted world ids) + the fused S1-S7 kernel,
+inputs resident in HBM; the per-step footprint (184 MB) exceeds the 126 MB L2
+and L2 is additionally flushed between timed steps.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N   (weak scaling: 1024 worlds per GPU)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "world-steps/s (dense pile, 1024 worlds x 2000 contacts per GPU)"
+BYTES_PER_CONTACT = 64      # c0..c3 float4 streams, read once
+BYTES_PER_BODY = 104        # 52 B state read + 52 B written
+SEG_BYTES_PER_CONTACT = 4   # S0 reads the world id
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--worlds", type=int, default=1024, help="worlds per GPU")
+    ap.add_argument("--contacts", type=int, default=2000, help="contacts per world")
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi-equivalent sampling (NVML) during the timed region."""
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        nv = self.nv
+        names = {getattr(nv, k): k for k in dir(nv) if k.startswith("nvmlClocksEventReason")
+                 and isinstance(getattr(nv, k), int)} if nv else {}
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in names.items():
+                    if bit and (r & bit) == bit and name not in ("nvmlClocksEventReasonNone",
+                                                                 "nvmlClocksEventReasonAll",
+                                                                 "nvmlClocksEventReasonGpuIdle"):
+                        self.reasons.add(name.replace("nvmlClocksEventReason", ""))
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    """dram bytes per launch of the fused step kernel from the committed ncu
+    --set full capture (profiles/), or None."""
+    p = os.path.join(ROOT, "profiles", "step_kernel_traffic.json")
+    try:
+        return json.load(open(p))
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------- oracle (CPU) timing
+def cpu_oracle_rate(scene, st, contacts, cfg, seconds: float, max_worlds: int):
+    """The fp64 oracle as it stands, OpenMP across worlds on all host cores,
+    repeated steps over a bounded sample of the workload's worlds."""
+    import oracle
+    W = min(max_worlds, st.n_worlds)
+    sel = np.nonzero(contacts.world < W)[0]
+    c = contacts.take(sel)
+    s = st.world_slice(0, W)
+    cores = os.cpu_count() or 1
+    oracle.step(cfg, scene, s, c, None, n_threads=cores)   # warm
+    n = 0
+    t0 = time.perf_counter()
+    while True:
+        oracle.step(cfg, scene, s, c, None, n_threads=cores)
+        n += 1
+        if time.perf_counter() - t0 >= seconds:
+            break
+    dt = time.perf_counter() - t0
+    return dict(value=n * W / dt, unit="world-steps/s", cores=cores, kind="oracle",
+                sample=f"{n} oracle steps x {W} worlds of the same workload ({c.n} contacts), fp64, "
+                       f"{dt:.1f} s, OpenMP over worlds")
+
+
+# ---------------------------------------------------------------- main arms
+def run_reference(args, rank, world_size):
+    from harness import scenes
+    from harness.types import Config
+    if rank != 0:
+        return
+    cfg = Config()
+    W = args.worlds
+    scene, st, c = scenes.c4_pile(n_worlds=W, contacts_per_world=args.contacts)
+    import oracle
+    cores = os.cpu_count() or 1
+    # each step: a bounded sample of the workload (64 worlds) so K steps finish in minutes
+    Ws = min(64, W)
+    sel = np.nonzero(c.world < Ws)[0]
+    cs = c.take(sel)
+    ss = st.world_slice(0, Ws)
+    for _ in range(args.warmup):
+        ss = oracle.step(cfg, scene, ss, cs, None, n_threads=cores)["state"].astype(np.float32)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        ss = oracle.step(cfg, scene, ss, cs, None, n_threads=cores)["state"].astype(np.float32)
+    dt = time.perf_counter() - t0
+    v = args.steps * Ws / dt
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "world-steps/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "c4 dense pile", "worlds_per_gpu": W, "contacts_per_world": args.contacts,
+                       "bodies_per_world": 500, "facets_per_contact": 4, "dt": cfg.dt,
+                       "sample_worlds_per_step": Ws},
+            "cpu_baseline": {"value": v, "unit": "world-steps/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{args.steps} steps x {Ws} of {W} worlds, fp64 oracle, OpenMP over worlds"},
+            "e2e": {"value": v, "unit": "world-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world_size, local):
+    import torch
+    import torch.distributed as dist
+    import paper_2603_12185_b200 as cf
+    from harness import scenes
+    from harness.types import Config
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world_size > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = Config()
+    W = args.worlds
+    scene, st, c = scenes.c4_pile(n_worlds=W, contacts_per_world=args.contacts, world_offset=rank * W)
+    ctx = cf.Context(cfg, device=local)
+    ctx.load_scene(scene, W, st)
+    dc = cf.DeviceContacts.from_host(c, dev)
+    assert dc.sorted
+    stream = torch.cuda.current_stream()
+    flush = None if args.no_flush else torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def one_step():
+        ctx.step(dc, None, dt=cfg.dt, stream=stream)
+
+    for _ in range(max(args.warmup, 3)):
+        one_step()
+    torch.cuda.synchronize()
+    launches0 = ctx.kernel_launches
+    ctx.get_timing()                       # clear
+    ctx.set_timing(True)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if world_size > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clock = ClockSampler(local)
+    with clock:
+        for i in range(args.steps):
+            if flush is not None:
+                flush.zero_()              # evict L2 between timed steps (untimed)
+            evs[i][0].record(stream)
+            one_step()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+    if world_size > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = float(sum(step_ms))
+    launches = ctx.kernel_launches - launches0
+    kt = ctx.get_timing()
+    ctx.set_timing(False)
+    if world_size > 1:
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    world_steps = W * world_size * args.steps
+    value = world_steps / (total_ms * 1e-3)
+    contacts_per_s = value * args.contacts
+
+    # roofline of the dominant kernel (fused step): algorithmic bytes per launch / its event time
+    B = scene.n_bodies
+    alg_bytes = W * (args.contacts * BYTES_PER_CONTACT + B * BYTES_PER_BODY)
+    k_ms = kt["step_ms"] / max(kt["step_launches"], 1)
+    peak, peak_kind = peaks()
+    achieved = alg_bytes / (k_ms * 1e-3) / 1e9
+    tr = ncu_traffic()
+    traffic = None
+    if tr and tr.get("worlds") == W and tr.get("contacts_per_world") == args.contacts:
+        traffic = tr.get("dram_bytes_per_launch")
+
+    # stats after the timed region (NCCL all-reduce of a per-rank summary)
+    final = ctx.get_state()
+    ke = float(np.sum(final["vel"].astype(np.float64) ** 2))
+    finite = bool(np.isfinite(final["vel"]).all() and np.isfinite(final["pos"]).all())
+    if world_size > 1:
+        t = torch.tensor([ke, float(finite)], device=dev, dtype=torch.float64)
+        dist.all_reduce(t)
+
+    # e2e: the same metric through the C ABI with HOST buffers (pinned), H2D of the
+    # step's contacts and D2H of the resulting state inside the timed region
+    hc = cf.HostContacts.from_arrays(c, pin=True)
+    e2e_steps = max(1, args.e2e_steps)
+    ctx.step(hc, None, dt=cfg.dt)          # warm the staging buffers
+    out_host = {k: torch.empty(v.shape, dtype=torch.float32).pin_memory().numpy() for k, v in final.items()}
+    from paper_2603_12185_b200 import _lib
+    import ctypes as ct
+    st_h = _lib.comfree_state(*[out_host[k].ctypes.data if out_host[k].size else None
+                                for k in ("pos", "quat", "vel", "omega", "qpos", "qvel")], _lib.MEM_HOST)
+    if world_size > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        ctx.step(hc, None, dt=cfg.dt, stream=stream)
+        rc = ctx._lib.comfree_get_state(ctx.h, 0, W, ct.byref(st_h), stream.cuda_stream)
+        ctx._check(rc, "comfree_get_state")
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1)
+    if world_size > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = W * world_size * e2e_steps / (e2e_ms * 1e-3)
+    h2d = hc.h2d_bytes()
+    d2h = sum(v.nbytes for v in out_host.values())
+
+    cpu = None
+    if rank == 0 and world_size == 1:
+        cpu = cpu_oracle_rate(scene, st, c, cfg, args.cpu_seconds, max_worlds=W)
+    if world_size > 1:
+        dist.barrier()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "world-steps/s", "n_gpus": world_size,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": "c4 dense pile", "worlds_per_gpu": W, "contacts_per_world": args.contacts,
+                       "bodies_per_world": B, "facets_per_contact": 4, "condim": 3, "dt": cfg.dt,
+                       "l2": "flushed between timed steps (256 MB write); per-step footprint 184 MB > 126 MB L2"
+                       if flush is not None else "not flushed; per-step footprint 184 MB > 126 MB L2",
+                       "parallelism": f"world-sharded x{world_size}"},
+            "contacts_per_s": contacts_per_s,
+            "gpu_launches": int(launches),
+            "kernel_ms": {"fused_step": k_ms, "segment_s0": kt["segment_ms"] / max(kt["step_launches"], 1)},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
+                         "kernel": "k_step (S1-S7 fused)",
+                         "algorithmic_bytes_per_launch": alg_bytes},
+            "clocks": clock.summary(),
+            "e2e": {"value": e2e_value, "unit": "world-steps/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "steps": e2e_steps},
+            "cpu_baseline": cpu,
+            "context": "paper: 2-3x MJWarp throughput in dense contact on one RTX 4090 (PAPER.md P:11, P:274); "
+                       "full-step numbers, not this path alone",
+            "final_state_finite": finite,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world_size > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    rank, world_size, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world_size)
+        return
+    run_ours(args, rank, world_size, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -149,8 +149,11 @@ def random_instance(seed, n_worlds=3, n_bodies=5, contacts_per_world=12, n_trees
     B, T, nd = n_bodies, n_trees, tree_ndof
     W = n_worlds
     Q = T * nd
-    inv_m = (1.0 / rng.uniform(0.05, 2.0, B)).astype(np.float32)
-    inv_I = (1.0 / rng.uniform(2e-5, 5e-3, (B, 3))).astype(np.float32)
+    mass = rng.uniform(0.05, 2.0, B)
+    rad = rng.uniform(0.02, 0.08, B)                    # body size sets inertia and lever arms
+    inertia = 0.4 * mass[:, None] * rad[:, None] ** 2 * rng.uniform(0.7, 1.3, (B, 3))
+    inv_m = (1.0 / mass).astype(np.float32)
+    inv_I = (1.0 / inertia).astype(np.float32)
     if locked_frac > 0:
         lk = rng.random(B) < locked_frac
         inv_I[lk] = 0
@@ -162,8 +165,11 @@ def random_instance(seed, n_worlds=3, n_bodies=5, contacts_per_world=12, n_trees
                rng.uniform(-1, 1, (W, Q)).astype(np.float32),
                rng.normal(0, 0.5, (W, Q)).astype(np.float32))
     inputs = Inputs()
-    if with_fext:
-        inputs.f_ext = rng.normal(0, 0.5, (W, B, 6)).astype(np.float32)
+    if with_fext:                                       # ~0.5 g and ~5 rad/s^2 scale pushes
+        fe = rng.normal(0, 1.0, (W, B, 6))
+        fe[..., :3] *= 0.5 * 9.81 * mass[None, :, None]
+        fe[..., 3:] *= 5.0 * inertia[None, :, :]
+        inputs.f_ext = fe.astype(np.float32)
     if T:
         Ls = np.zeros((W, T, 10), np.float32)
         for w in range(W):
@@ -207,7 +213,14 @@ def random_instance(seed, n_worlds=3, n_bodies=5, contacts_per_world=12, n_trees
         nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
         t1 = np.cross(nrm, rng.normal(size=(n, 3)))
         t1 /= np.linalg.norm(t1, axis=1, keepdims=True)
+        # contact point on the surface of a free side (lever arm ~ body size)
         p = rng.uniform(-0.25, 0.25, (n, 3))
+        u = rng.normal(size=(n, 3))
+        u /= np.linalg.norm(u, axis=1, keepdims=True)
+        for k in range(n):
+            side = kinds[k, 1] if kinds[k, 1] >= 0 else kinds[k, 0]
+            if side >= 0:
+                p[k] = st.pos[w, side] + rad[side] * u[k]
         phi = rng.uniform(-3e-3, 5e-4, n)
         c0 = np.concatenate([p, phi[:, None]], 1).astype(np.float32)
         c1 = np.concatenate([nrm, rng.uniform(0.0, 1.2, (n, 1))], 1).astype(np.float32)

@@ -1,0 +1,268 @@
+/*
+ * comfree.h — C ABI of the B200-native ComFree-Sim contact-resolution step.
+ *
+ * One call of comfree_step() runs, for every world and every contact, the
+ * complementarity-free contact-resolution step of arXiv 2603.12185 (PAPER.md
+ * §III, Algorithm 1):
+ *   S0  world segmentation of the contact set C               ("the detected contact set C")
+ *   S1  smooth prediction  v_s = v + M^-1 (tau - c) dt          Eq. (2)
+ *   S2  contact kinematics (v_c, omega_c) = J v_s               Eq. (4)-(5) P:109-123
+ *   S3  dual-cone impedance K = k M(phi)/dt, D = d M(phi)/dt    Eq. (12)-(13) P:209-233
+ *   S4  per-facet closed-form impulse                           Eq. (7)-(9) P:142-180
+ *         lambda = ( -K (J~ v_s dt + phi) - D J~ v_s )_+   (sign of Eq. (9); Alg. 1 P:260 is garbled)
+ *   S5  facet impulses -> contact wrench (sum_f J~_f^T Lambda_f regrouped)
+ *   S6  per-world scatter of J^T Lambda (Kernel III)
+ *   S7  v+ = v_s + M^-1 p (Eq. (10)) and semi-implicit integration
+ *   S8  articulated chains: M^-1 through per-chain Cholesky factors
+ * with lambda a step-averaged wrench and Lambda = lambda dt the impulse.
+ *
+ * Conventions (see DESIGN.md for every reading of the paper):
+ *  - fp32 everywhere on the device; quaternions (w,x,y,z) scalar first;
+ *    angular velocities in the world frame.
+ *  - Body ids inside a contact: >= 0 free 6-DoF body of the world,
+ *    -1 static (world-fixed), -(2+t) articulated chain t (J rows supplied).
+ *  - The normal n points from side a to side b; J v = motion of b relative
+ *    to a, so n . v_c > 0 separates.  phi > 0 separated, < 0 penetrating.
+ *  - condim (MuJoCo style): 1 normal only, 3 + tangential (n_t facets),
+ *    4 + torsional (2 facets), 6 + rolling (n_rol facets).  Facet order per
+ *    contact: tangential j = 0..n_t-1 with d_j = (cos 2 pi j/n_t, sin 2 pi j/n_t)
+ *    in the (t1, t2 = n x t1) basis, then torsional (+1, -1), then rolling.
+ *
+ * Ownership: the library owns world state and scratch (allocated in
+ * comfree_load_scene).  Every other buffer belongs to the caller and is only
+ * borrowed for the stream-ordered duration of the call.  Device pointers
+ * must be 16-byte aligned where a float4 stream is named.
+ *
+ * Streams: all work is enqueued on the caller's stream (a cudaStream_t passed
+ * as void*, NULL = legacy default stream).  No call synchronises except
+ * comfree_get_state / comfree_get_stats / comfree_get_world_stats /
+ * comfree_segment_info and calls given HOST buffers.
+ *
+ * Errors: no C++ exception crosses the ABI.  Argument and validation errors
+ * are returned synchronously.  Errors detected on the device (non-finite
+ * state, unsorted contacts under COMFREE_CONTACTS_SORTED, out-of-range ids)
+ * are latched and returned by the next synchronising call; the message is in
+ * comfree_last_error().  A context is not thread-safe: single owner.
+ */
+#ifndef COMFREE_H
+#define COMFREE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define COMFREE_ABI_VERSION 1
+
+typedef enum {
+  COMFREE_OK = 0,
+  COMFREE_ERR_INVALID_ARGUMENT = 1, /* NULL / out-of-range argument */
+  COMFREE_ERR_VALIDATION = 2,       /* config or scene violates a documented invariant */
+  COMFREE_ERR_CAPACITY = 3,         /* allocation failed or size limit exceeded */
+  COMFREE_ERR_NONFINITE = 4,        /* a world produced a non-finite state */
+  COMFREE_ERR_CUDA = 5,             /* CUDA runtime error */
+  COMFREE_ERR_STATE = 6             /* call out of order (e.g. step before load_scene) */
+} comfree_status;
+
+/* memory location of caller buffers */
+enum { COMFREE_MEM_DEVICE = 0, COMFREE_MEM_HOST = 1 };
+
+/* comfree_config.flags */
+enum {
+  COMFREE_FLAG_STATS = 1u << 0,         /* per-world statistics every step */
+  COMFREE_FLAG_DETERMINISTIC = 1u << 1, /* run-to-run bitwise identical scatter order */
+  COMFREE_FLAG_NO_FINITE_CHECK = 1u << 2
+};
+
+/* comfree_contacts.flags */
+enum {
+  COMFREE_CONTACTS_SORTED = 1u << 0     /* world[] is non-decreasing (verified on device) */
+};
+
+typedef struct comfree_ctx comfree_ctx;   /* opaque, single owner */
+
+/* Global parameters.  Eq. (12) k_user, d_user; Eq. (13) r_min,
+ * r_max, width w, midpoint m, power p (MuJoCo solimp defaults
+ * 0.9, 0.95, 0.001, 0.5, 2); Eq. (7) facet counts n_t, n_rol (even, n_t >= 4,
+ * n_rol >= 2; the torsional channel always has 2 facets); gravity acts on
+ * every free body with inv_mass > 0 (part of tau - c in Eq. (2)).
+ * Validation: k_user > 0, d_user >= 0, 0 < r_min <= r_max < 1, width > 0,
+ * 0 < midpoint < 1, power >= 1, n_t, n_rol even, 4 <= n_t <= 32,
+ * 2 <= n_rol <= 32, finite gravity. */
+typedef struct {
+  float k_user, d_user;
+  float r_min, r_max, width, midpoint, power;
+  int32_t n_t, n_rol;
+  float gravity[3];
+  uint32_t flags;
+} comfree_config;
+
+/* Per-scene body parameters shared by every world (HOST pointers, copied).
+ * inv_mass[i] >= 0 and inv_inertia[i][0..2] >= 0 (principal body-frame
+ * inverse inertia; 0 locks that DoF).  Articulated chains: n_trees chains of
+ * tree_ndof in 1..4 DoFs each; their inertia comes per step as Cholesky
+ * factors in comfree_worlds (the upstream CRBA is not part of this step). */
+typedef struct {
+  int32_t n_bodies;
+  const float* inv_mass;     /* [n_bodies] */
+  const float* inv_inertia;  /* [n_bodies][3] */
+  int32_t n_trees;
+  int32_t tree_ndof;
+} comfree_scene;
+
+/* World state in the public layout (row-major, world-major):
+ *   pos [W][n_bodies][3], quat [W][n_bodies][4], vel [W][n_bodies][3],
+ *   omega [W][n_bodies][3], qpos [W][Q], qvel [W][Q] with Q = n_trees*tree_ndof
+ * (qpos/qvel may be NULL when Q == 0).  location: COMFREE_MEM_*. */
+typedef struct {
+  float* pos;
+  float* quat;
+  float* vel;
+  float* omega;
+  float* qpos;
+  float* qvel;
+  int32_t location;
+} comfree_state;
+
+/* Which worlds one step advances, and their per-step non-contact inputs. */
+typedef struct {
+  int64_t first_world;       /* step worlds [first_world, first_world + n_worlds) */
+  int64_t n_worlds;
+  const float* f_ext;        /* [n_worlds][n_bodies][6] world-frame force | torque, or NULL */
+  const float* tree_L;       /* [n_worlds][n_trees][10] packed lower-triangular Cholesky
+                                factor of each chain's M, L[i(i+1)/2 + j]; required if n_trees */
+  const float* tree_tau;     /* [n_worlds][Q] tau - c of the chains; required if n_trees */
+  int32_t location;
+} comfree_worlds;
+
+/* The detected contact set C, contact-major SoA float4 streams:
+ *   c0[n] = (p.x, p.y, p.z, phi)      contact point (world), signed gap
+ *   c1[n] = (n.x, n.y, n.z, mu_t)     unit normal a->b, tangential friction
+ *   c2[n] = (t1.x, t1.y, t1.z, mu_tor) unit first tangent (orthogonal to n),
+ *                                      torsional friction (a length)
+ *   c3[n] = (body_a, body_b, bits(mu_rol), condim)  int32 x 4
+ *   jrow [12][n][4]: stream s = side*6 + row (side 0 = a, 1 = b): rows 0-2
+ *       linear velocity of the contact point, rows 3-5 angular velocity, of
+ *       an articulated side, one column per chain DoF; NULL if no chains.
+ * Segmentation (S0): if off != NULL contacts are grouped by world and
+ * off[n_worlds + 1] is their CSR (no S0 work).  Otherwise world[n] (relative
+ * to first_world) is used; with COMFREE_CONTACTS_SORTED it must be
+ * non-decreasing (checked) and only offsets are built; without it contacts
+ * are stably sorted by world on the device.
+ * Outputs (optional): impulses[F] = Lambda_f (N s) of every facet, at
+ * foff[c] + facet for contact c in input order; foff[n + 1] its exclusive
+ * prefix (int64).  Output pointers follow `location`. */
+typedef struct {
+  int64_t n_contacts;
+  const int32_t* world;
+  const int64_t* off;
+  const float* c0;
+  const float* c1;
+  const float* c2;
+  const int32_t* c3;
+  const float* jrow;
+  float* impulses;
+  int64_t* foff;
+  int64_t impulses_capacity; /* elements available at impulses (checked) */
+  uint32_t flags;
+  int32_t location;
+} comfree_contacts;
+
+/* Aggregate statistics of the last step. */
+typedef struct {
+  int64_t n_worlds;
+  int64_t contacts;
+  int64_t active_facets;          /* facets with Lambda > 0 */
+  float max_penetration;          /* max(0, -phi) over contacts */
+  double kinetic_energy;          /* sum over worlds, after the step */
+  int64_t first_nonfinite_world;  /* -1 if none */
+} comfree_stats;
+
+/* Per-world statistics record (COMFREE_FLAG_STATS). */
+typedef struct {
+  int32_t contacts;
+  int32_t active_facets;
+  float max_penetration;
+  float kinetic_energy;
+} comfree_world_stats;
+
+/* ---- API ---------------------------------------------------------------- */
+
+int comfree_abi_version(void);
+const char* comfree_status_string(comfree_status s);
+
+/* Fill *cfg with the paper's defaults (k=0.1, d=0.001 as in P:390; solimp
+ * defaults; n_t = n_rol = 4; gravity (0,0,-9.81); flags 0).  CPU only. */
+comfree_status comfree_default_config(comfree_config* cfg);
+
+/* Check a config against the invariants above without touching the GPU. */
+comfree_status comfree_validate_config(const comfree_config* cfg);
+
+/* Check scene parameters (HOST) without touching the GPU. */
+comfree_status comfree_validate_scene(const comfree_scene* scene);
+
+/* Facets per contact for a condim under cfg (Eq. (7)-(8) facet sets); -1 if
+ * condim is not one of 1, 3, 4, 6. */
+int32_t comfree_facets_per_contact(const comfree_config* cfg, int32_t condim);
+
+/* Create a context on CUDA device `cuda_device`.  *out owned by the caller,
+ * release with comfree_destroy. */
+comfree_status comfree_create(const comfree_config* cfg, int cuda_device, comfree_ctx** out);
+
+/* Allocate state for n_worlds copies of the scene and set the initial state
+ * (any location; NULL -> zero velocities, identity orientations, zero
+ * positions).  Synchronous. */
+comfree_status comfree_load_scene(comfree_ctx* ctx, const comfree_scene* scene, int64_t n_worlds,
+                                  const comfree_state* initial);
+
+/* One step of duration dt > 0 for the worlds in *worlds with contacts *c.
+ * Asynchronous on `stream` when every buffer is on the device. */
+comfree_status comfree_step(comfree_ctx* ctx, const comfree_worlds* worlds,
+                            const comfree_contacts* c, float dt, void* stream);
+
+/* Copy the state of worlds [first_world, first_world + n_worlds) out to *out
+ * (public layout, arrays sized for n_worlds).  Synchronises `stream`,
+ * surfaces latched device errors. */
+comfree_status comfree_get_state(comfree_ctx* ctx, int64_t first_world, int64_t n_worlds,
+                                  comfree_state* out, void* stream);
+
+/* Overwrite the state of worlds [first_world, first_world + n_worlds)
+ * (snapshots, MPPI resets). */
+comfree_status comfree_set_state(comfree_ctx* ctx, int64_t first_world, int64_t n_worlds,
+                                  const comfree_state* in, void* stream);
+
+/* Aggregate statistics of the last step (requires COMFREE_FLAG_STATS for
+ * contacts / facets / penetration / energy; the non-finite check is always
+ * on unless COMFREE_FLAG_NO_FINITE_CHECK).  Synchronises. */
+comfree_status comfree_get_stats(comfree_ctx* ctx, comfree_stats* out, void* stream);
+
+/* Per-world statistics of the last step into out[n_worlds] (location).  */
+comfree_status comfree_get_world_stats(comfree_ctx* ctx, int64_t first_world, int64_t n_worlds,
+                                       comfree_world_stats* out, int32_t location, void* stream);
+
+/* S0 results of the last step (device scratch copied to HOST arrays):
+ * off[n_worlds + 1] int64, perm[n_contacts] int32 (stable world order; the
+ * identity when the input was already grouped).  Synchronises. */
+comfree_status comfree_segment_info(comfree_ctx* ctx, int64_t* off, int32_t* perm, void* stream);
+
+/* Instrumentation: while enabled, every comfree_step records CUDA events on
+ * its own stream around the S0 kernels and around the fused step kernel. */
+comfree_status comfree_set_timing(comfree_ctx* ctx, int enable);
+
+/* Sums of the recorded device durations since the previous call, in ms:
+ * out[0] fused step kernel, out[1] S0 kernels, out[2] number of fused-step
+ * launches timed.  Synchronises the recorded events; clears the record. */
+comfree_status comfree_get_timing(comfree_ctx* ctx, double out[3]);
+
+/* Number of kernels this context has launched so far (instrumentation). */
+int64_t comfree_kernel_launches(const comfree_ctx* ctx);
+
+void comfree_destroy(comfree_ctx* ctx);
+const char* comfree_last_error(const comfree_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* COMFREE_H */

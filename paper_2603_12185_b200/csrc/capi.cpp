@@ -1,0 +1,684 @@
+// capi.cpp — host side of the C ABI (include/comfree.h): validation,
+// library-owned device memory, stream-ordered dispatch of S0 and the fused
+// step kernel, host-buffer staging and latched device errors.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "comfree.h"
+#include "internal.h"
+
+namespace {
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+};
+
+cudaError_t ensure(DevBuf& b, size_t bytes) {
+  if (b.p && b.cap >= bytes) return cudaSuccess;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.cap = 0;
+  size_t nb = std::max<size_t>(256, bytes + bytes / 4);
+  cudaError_t e = cudaMalloc(&b.p, nb);
+  if (e == cudaSuccess) b.cap = nb;
+  return e;
+}
+
+void release(DevBuf& b) {
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.cap = 0;
+}
+
+int64_t round4(int64_t x) { return (x + 3) & ~int64_t(3); }
+
+}  // namespace
+
+struct comfree_ctx {
+  comfree_config cfg{};
+  int device = 0;
+  std::string err;
+  bool loaded = false;
+  cf::SceneDev sc{};
+  int64_t W = 0;
+  float* slab = nullptr;
+  float* inv_mass = nullptr;
+  float* inv_inertia = nullptr;
+  comfree_world_stats* wstats = nullptr;
+  int* d_err = nullptr;
+  unsigned long long* d_first_bad = nullptr;
+  // S0 scratch
+  DevBuf off, keys, perm, iota, s0, s1, s2, s3, sj, nf, foff, cub_tmp;
+  // host-input staging
+  DevBuf in_world, in_off, in_c0, in_c1, in_c2, in_c3, in_jrow, in_fext, in_L, in_tau, imp;
+  DevBuf st_tmp;
+  int64_t launches = 0;
+  int64_t last_first = 0, last_nw = 0, last_nc = 0;
+  bool last_sorted_copy = false;
+  bool stats_valid = false;
+  float2 dir_t[32], dir_r[32];
+  // instrumentation: event pairs recorded on the step's stream
+  bool timing = false;
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<int, int>> ev_step, ev_seg;  // indices into ev_pool
+  size_t ev_used = 0;
+};
+
+namespace {
+
+comfree_status fail(comfree_ctx* ctx, comfree_status s, const char* fmt, ...) {
+  if (ctx) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    ctx->err = buf;
+  }
+  return s;
+}
+
+#define CUDA_TRY(ctx, expr)                                                                  \
+  do {                                                                                       \
+    cudaError_t e_ = (expr);                                                                 \
+    if (e_ != cudaSuccess)                                                                   \
+      return fail(ctx, COMFREE_ERR_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_),   \
+                  __FILE__, __LINE__);                                                       \
+  } while (0)
+
+bool finite(float x) { return std::isfinite(x); }
+
+// Eq. (7): symmetric unit directions d_j = (cos 2 pi j/n, sin 2 pi j/n); exact
+// zeros / ones where the angle is a multiple of a quarter turn.
+void directions(int n, float2* out) {
+  for (int j = 0; j < 32; ++j) out[j] = make_float2(0.f, 0.f);
+  for (int j = 0; j < n && j < 32; ++j) {
+    double th = 2.0 * M_PI * j / n;
+    double c = std::cos(th), s = std::sin(th);
+    if (std::fabs(c) < 1e-12) c = 0.0;
+    if (std::fabs(s) < 1e-12) s = 0.0;
+    if (std::fabs(std::fabs(c) - 1.0) < 1e-12) c = c > 0 ? 1.0 : -1.0;
+    if (std::fabs(std::fabs(s) - 1.0) < 1e-12) s = s > 0 ? 1.0 : -1.0;
+    out[j] = make_float2((float)c, (float)s);
+  }
+}
+
+comfree_status check_latched(comfree_ctx* ctx, cudaStream_t s) {
+  CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  int e = 0;
+  unsigned long long bad = ~0ull;
+  CUDA_TRY(ctx, cudaMemcpy(&e, ctx->d_err, sizeof e, cudaMemcpyDeviceToHost));
+  if (e == 0) return COMFREE_OK;
+  CUDA_TRY(ctx, cudaMemcpy(&bad, ctx->d_first_bad, sizeof bad, cudaMemcpyDeviceToHost));
+  const int zero = 0;
+  const unsigned long long none = ~0ull;
+  CUDA_TRY(ctx, cudaMemcpy(ctx->d_err, &zero, sizeof zero, cudaMemcpyHostToDevice));
+  CUDA_TRY(ctx, cudaMemcpy(ctx->d_first_bad, &none, sizeof none, cudaMemcpyHostToDevice));
+  if (e & (cf::ERR_UNSORTED | cf::ERR_WORLD_RANGE | cf::ERR_BODY_RANGE | cf::ERR_CONDIM | cf::ERR_IMPULSE_CAP))
+    return fail(ctx, COMFREE_ERR_VALIDATION, "device validation failed (flags 0x%x):%s%s%s%s%s", e,
+                (e & cf::ERR_UNSORTED) ? " contacts not sorted by world;" : "",
+                (e & cf::ERR_WORLD_RANGE) ? " world id out of range;" : "",
+                (e & cf::ERR_BODY_RANGE) ? " body id out of range or chain side without J rows;" : "",
+                (e & cf::ERR_CONDIM) ? " condim not in {1,3,4,6};" : "",
+                (e & cf::ERR_IMPULSE_CAP) ? " impulses buffer too small;" : "");
+  return fail(ctx, COMFREE_ERR_NONFINITE, "non-finite state in world %lld", (long long)bad);
+}
+
+// Copy a caller buffer to device staging when it lives on the host.
+template <typename T>
+comfree_status stage(comfree_ctx* ctx, DevBuf& buf, const T* src, size_t count, int loc, cudaStream_t s,
+                     const T** out) {
+  if (!src || loc == COMFREE_MEM_DEVICE) {
+    *out = src;
+    return COMFREE_OK;
+  }
+  CUDA_TRY(ctx, ensure(buf, count * sizeof(T)));
+  CUDA_TRY(ctx, cudaMemcpyAsync(buf.p, src, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  *out = static_cast<const T*>(buf.p);
+  return COMFREE_OK;
+}
+
+cudaEvent_t next_event(comfree_ctx* ctx, int* idx) {
+  if (ctx->ev_used == ctx->ev_pool.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    ctx->ev_pool.push_back(e);
+  }
+  *idx = (int)ctx->ev_used;
+  return ctx->ev_pool[ctx->ev_used++];
+}
+
+}  // namespace
+
+extern "C" {
+
+int comfree_abi_version(void) { return COMFREE_ABI_VERSION; }
+
+const char* comfree_status_string(comfree_status s) {
+  switch (s) {
+    case COMFREE_OK: return "ok";
+    case COMFREE_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case COMFREE_ERR_VALIDATION: return "validation error";
+    case COMFREE_ERR_CAPACITY: return "capacity exceeded";
+    case COMFREE_ERR_NONFINITE: return "non-finite state";
+    case COMFREE_ERR_CUDA: return "CUDA error";
+    case COMFREE_ERR_STATE: return "invalid call order";
+  }
+  return "unknown status";
+}
+
+comfree_status comfree_default_config(comfree_config* c) {
+  if (!c) return COMFREE_ERR_INVALID_ARGUMENT;
+  c->k_user = 0.1f;
+  c->d_user = 0.001f;
+  c->r_min = 0.9f;    // P:233 defaults
+  c->r_max = 0.95f;
+  c->width = 0.001f;
+  c->midpoint = 0.5f;
+  c->power = 2.0f;
+  c->n_t = 4;
+  c->n_rol = 4;
+  c->gravity[0] = 0.f;
+  c->gravity[1] = 0.f;
+  c->gravity[2] = -9.81f;
+  c->flags = 0;
+  return COMFREE_OK;
+}
+
+comfree_status comfree_validate_config(const comfree_config* c) {
+  if (!c) return COMFREE_ERR_INVALID_ARGUMENT;
+  bool ok = finite(c->k_user) && c->k_user > 0 && finite(c->d_user) && c->d_user >= 0;
+  ok = ok && c->r_min > 0 && c->r_min <= c->r_max && c->r_max < 1;
+  ok = ok && finite(c->width) && c->width > 0 && c->midpoint > 0 && c->midpoint < 1;
+  ok = ok && finite(c->power) && c->power >= 1;
+  ok = ok && c->n_t >= 4 && c->n_t <= 32 && c->n_t % 2 == 0;
+  ok = ok && c->n_rol >= 2 && c->n_rol <= 32 && c->n_rol % 2 == 0;
+  ok = ok && finite(c->gravity[0]) && finite(c->gravity[1]) && finite(c->gravity[2]);
+  return ok ? COMFREE_OK : COMFREE_ERR_VALIDATION;
+}
+
+comfree_status comfree_validate_scene(const comfree_scene* s) {
+  if (!s) return COMFREE_ERR_INVALID_ARGUMENT;
+  if (s->n_bodies < 0 || s->n_trees < 0) return COMFREE_ERR_VALIDATION;
+  if (s->n_bodies > 0 && (!s->inv_mass || !s->inv_inertia)) return COMFREE_ERR_INVALID_ARGUMENT;
+  if (s->n_trees > 0 && (s->tree_ndof < 1 || s->tree_ndof > 4)) return COMFREE_ERR_VALIDATION;
+  for (int i = 0; i < s->n_bodies; ++i) {
+    if (!(finite(s->inv_mass[i]) && s->inv_mass[i] >= 0)) return COMFREE_ERR_VALIDATION;
+    for (int k = 0; k < 3; ++k)
+      if (!(finite(s->inv_inertia[3 * i + k]) && s->inv_inertia[3 * i + k] >= 0)) return COMFREE_ERR_VALIDATION;
+  }
+  return COMFREE_OK;
+}
+
+int32_t comfree_facets_per_contact(const comfree_config* c, int32_t condim) {
+  if (!c) return -1;
+  switch (condim) {
+    case 1: return 1;
+    case 3: return c->n_t;
+    case 4: return c->n_t + 2;
+    case 6: return c->n_t + 2 + c->n_rol;
+  }
+  return -1;
+}
+
+comfree_status comfree_create(const comfree_config* cfg, int device, comfree_ctx** out) {
+  if (!cfg || !out) return COMFREE_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  comfree_status v = comfree_validate_config(cfg);
+  if (v != COMFREE_OK) return v;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+    cudaGetLastError();
+    return COMFREE_ERR_CUDA;
+  }
+  comfree_ctx* ctx = new (std::nothrow) comfree_ctx();
+  if (!ctx) return COMFREE_ERR_CAPACITY;
+  ctx->cfg = *cfg;
+  ctx->device = device;
+  directions(cfg->n_t, ctx->dir_t);
+  directions(cfg->n_rol, ctx->dir_r);
+  if (cudaSetDevice(device) != cudaSuccess || cudaMalloc(&ctx->d_err, sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&ctx->d_first_bad, sizeof(unsigned long long)) != cudaSuccess) {
+    delete ctx;
+    return COMFREE_ERR_CUDA;
+  }
+  const unsigned long long none = ~0ull;
+  cudaMemset(ctx->d_err, 0, sizeof(int));
+  cudaMemcpy(ctx->d_first_bad, &none, sizeof none, cudaMemcpyHostToDevice);
+  *out = ctx;
+  return COMFREE_OK;
+}
+
+static comfree_status set_state_impl(comfree_ctx* ctx, int64_t first, int64_t nw, const comfree_state* in,
+                                     cudaStream_t s) {
+  const cf::SceneDev& sc = ctx->sc;
+  const float *pos = in ? in->pos : nullptr, *quat = in ? in->quat : nullptr, *vel = in ? in->vel : nullptr,
+              *om = in ? in->omega : nullptr, *qp = in ? in->qpos : nullptr, *qv = in ? in->qvel : nullptr;
+  if (in && in->location == COMFREE_MEM_HOST) {
+    const size_t nb = (size_t)nw * sc.B, nq = (size_t)nw * sc.Q;
+    const size_t total = nb * 13 + nq * 2;
+    CUDA_TRY(ctx, ensure(ctx->st_tmp, std::max<size_t>(1, total) * sizeof(float)));
+    float* d = static_cast<float*>(ctx->st_tmp.p);
+    float* dp[6] = {d, d + 3 * nb, d + 7 * nb, d + 10 * nb, d + 13 * nb, d + 13 * nb + nq};
+    const float* hp[6] = {pos, quat, vel, om, qp, qv};
+    const size_t cnt[6] = {3 * nb, 4 * nb, 3 * nb, 3 * nb, nq, nq};
+    const float* res[6];
+    for (int k = 0; k < 6; ++k) {
+      res[k] = nullptr;
+      if (hp[k] && cnt[k]) {
+        CUDA_TRY(ctx, cudaMemcpyAsync(dp[k], hp[k], cnt[k] * sizeof(float), cudaMemcpyHostToDevice, s));
+        res[k] = dp[k];
+      }
+    }
+    pos = res[0]; quat = res[1]; vel = res[2]; om = res[3]; qp = res[4]; qv = res[5];
+  }
+  CUDA_TRY(ctx, cf::launch_public_to_slab(pos, quat, vel, om, qp, qv, nw, sc, ctx->slab + (size_t)first * sc.slab, s));
+  ctx->launches += 1;
+  if (in && in->location == COMFREE_MEM_HOST) CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  return COMFREE_OK;
+}
+
+comfree_status comfree_load_scene(comfree_ctx* ctx, const comfree_scene* scene, int64_t n_worlds,
+                                  const comfree_state* initial) {
+  if (!ctx || !scene || n_worlds < 0) return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "load_scene: bad argument");
+  comfree_status v = comfree_validate_scene(scene);
+  if (v != COMFREE_OK) return fail(ctx, v, "load_scene: scene violates an invariant (masses, inertias >= 0, 1 <= tree_ndof <= 4)");
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  if (ctx->slab) { cudaFree(ctx->slab); ctx->slab = nullptr; }
+  if (ctx->inv_mass) { cudaFree(ctx->inv_mass); ctx->inv_mass = nullptr; }
+  if (ctx->inv_inertia) { cudaFree(ctx->inv_inertia); ctx->inv_inertia = nullptr; }
+  if (ctx->wstats) { cudaFree(ctx->wstats); ctx->wstats = nullptr; }
+  ctx->loaded = false;
+  cf::SceneDev& sc = ctx->sc;
+  sc.B = scene->n_bodies;
+  sc.Bp = (int)round4(std::max(1, scene->n_bodies));
+  sc.T = scene->n_trees;
+  sc.nd = scene->n_trees ? scene->tree_ndof : 0;
+  sc.Q = sc.T * sc.nd;
+  sc.Qp = (int)round4(sc.Q);
+  sc.slab = cf::N_BODY_PLANES * sc.Bp + 2 * sc.Qp;
+  ctx->W = n_worlds;
+  const size_t slab_bytes = std::max<size_t>(16, (size_t)n_worlds * sc.slab * sizeof(float));
+  CUDA_TRY(ctx, cudaMalloc(&ctx->slab, slab_bytes));
+  CUDA_TRY(ctx, cudaMalloc(&ctx->inv_mass, sc.Bp * sizeof(float)));
+  CUDA_TRY(ctx, cudaMalloc(&ctx->inv_inertia, 3 * sc.Bp * sizeof(float)));
+  CUDA_TRY(ctx, cudaMalloc(&ctx->wstats, std::max<int64_t>(1, n_worlds) * sizeof(comfree_world_stats)));
+  std::string h(4 * sc.Bp * sizeof(float), '\0');
+  float* hm = reinterpret_cast<float*>(&h[0]);
+  for (int i = 0; i < sc.Bp; ++i) {
+    hm[i] = i < sc.B ? scene->inv_mass[i] : 0.f;
+    for (int k = 0; k < 3; ++k) hm[sc.Bp + k * sc.Bp + i] = i < sc.B ? scene->inv_inertia[3 * i + k] : 0.f;
+  }
+  CUDA_TRY(ctx, cudaMemcpy(ctx->inv_mass, hm, sc.Bp * sizeof(float), cudaMemcpyHostToDevice));
+  CUDA_TRY(ctx, cudaMemcpy(ctx->inv_inertia, hm + sc.Bp, 3 * sc.Bp * sizeof(float), cudaMemcpyHostToDevice));
+  sc.inv_mass = ctx->inv_mass;
+  sc.inv_inertia = ctx->inv_inertia;
+  ctx->loaded = true;
+  comfree_status st = set_state_impl(ctx, 0, n_worlds, initial, 0);
+  if (st != COMFREE_OK) return st;
+  CUDA_TRY(ctx, cudaDeviceSynchronize());
+  ctx->stats_valid = false;
+  return COMFREE_OK;
+}
+
+static int pick_wpw(const cf::SceneDev& sc, int64_t n_contacts, int64_t n_worlds) {
+  const int64_t avgc = n_worlds ? n_contacts / n_worlds : 0;
+  const int64_t work = std::max<int64_t>(sc.B + sc.T, avgc);
+  int wpw = work <= 64 ? 1 : work <= 256 ? 2 : work <= 768 ? 4 : 8;
+  while (wpw < 8 && cf::step_smem_bytes(sc, wpw) > 200 * 1024) wpw *= 2;
+  return wpw;
+}
+
+comfree_status comfree_step(comfree_ctx* ctx, const comfree_worlds* wd, const comfree_contacts* c, float dt,
+                            void* stream) {
+  if (!ctx) return COMFREE_ERR_INVALID_ARGUMENT;
+  if (!ctx->loaded) return fail(ctx, COMFREE_ERR_STATE, "step before load_scene");
+  if (!wd || !c) return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "step: null descriptor");
+  if (!(dt > 0) || !finite(dt)) return fail(ctx, COMFREE_ERR_VALIDATION, "step: dt must be finite and > 0");
+  const int64_t first = wd->first_world, nw = wd->n_worlds, n = c->n_contacts;
+  if (first < 0 || nw < 0 || first + nw > ctx->W) return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "step: world range outside the loaded batch");
+  if (n < 0 || n > INT32_MAX) return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "step: n_contacts out of range");
+  if (n > 0 && (!c->c0 || !c->c1 || !c->c2 || !c->c3)) return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "step: contact streams required");
+  if (n > 0 && !c->off && !c->world) return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "step: world[] or off[] required");
+  const cf::SceneDev& sc = ctx->sc;
+  if (sc.T > 0 && nw > 0 && (!wd->tree_L || !wd->tree_tau)) return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "step: chains need tree_L and tree_tau");
+  if (c->location != COMFREE_MEM_DEVICE && c->location != COMFREE_MEM_HOST) return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "step: bad contacts location");
+  if (c->impulses && c->impulses_capacity < 0) return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "step: impulses_capacity");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  const int loc = c->location;
+  const bool host_io = (loc == COMFREE_MEM_HOST) || (wd->location == COMFREE_MEM_HOST);
+
+  // ---- stage inputs ----
+  const int32_t* world = nullptr;
+  const int64_t* off_in = nullptr;
+  const float *c0 = nullptr, *c1 = nullptr, *c2 = nullptr, *jrow = nullptr;
+  const int32_t* c3 = nullptr;
+  comfree_status st;
+  if ((st = stage(ctx, ctx->in_world, c->off ? nullptr : c->world, (size_t)n, loc, s, &world)) != COMFREE_OK) return st;
+  if ((st = stage(ctx, ctx->in_off, c->off, (size_t)nw + 1, loc, s, &off_in)) != COMFREE_OK) return st;
+  if ((st = stage(ctx, ctx->in_c0, c->c0, (size_t)n * 4, loc, s, &c0)) != COMFREE_OK) return st;
+  if ((st = stage(ctx, ctx->in_c1, c->c1, (size_t)n * 4, loc, s, &c1)) != COMFREE_OK) return st;
+  if ((st = stage(ctx, ctx->in_c2, c->c2, (size_t)n * 4, loc, s, &c2)) != COMFREE_OK) return st;
+  if ((st = stage(ctx, ctx->in_c3, c->c3, (size_t)n * 4, loc, s, &c3)) != COMFREE_OK) return st;
+  if ((st = stage(ctx, ctx->in_jrow, c->jrow, (size_t)n * 48, loc, s, &jrow)) != COMFREE_OK) return st;
+  const float *fext = nullptr, *tL = nullptr, *ttau = nullptr;
+  const int wloc = wd->location;
+  if ((st = stage(ctx, ctx->in_fext, wd->f_ext, (size_t)nw * sc.B * 6, wloc, s, &fext)) != COMFREE_OK) return st;
+  if ((st = stage(ctx, ctx->in_L, sc.T ? wd->tree_L : nullptr, (size_t)nw * sc.T * 10, wloc, s, &tL)) != COMFREE_OK) return st;
+  if ((st = stage(ctx, ctx->in_tau, sc.T ? wd->tree_tau : nullptr, (size_t)nw * sc.Q, wloc, s, &ttau)) != COMFREE_OK) return st;
+
+  // ---- S0: segmentation ----
+  const int64_t* off = off_in;
+  const int32_t* perm = nullptr;
+  const float4 *k0 = (const float4*)c0, *k1 = (const float4*)c1, *k2 = (const float4*)c2, *kj = (const float4*)jrow;
+  const int4* k3 = (const int4*)c3;
+  ctx->last_sorted_copy = false;
+  int seg_e0 = -1, seg_e1 = -1;
+  if (!off && ctx->timing) {
+    cudaEvent_t e = next_event(ctx, &seg_e0);
+    if (e) cudaEventRecord(e, s);
+  }
+  if (!off) {
+    CUDA_TRY(ctx, ensure(ctx->off, (size_t)(nw + 1) * sizeof(int64_t)));
+    int64_t* doff = static_cast<int64_t*>(ctx->off.p);
+    if (c->flags & COMFREE_CONTACTS_SORTED) {
+      CUDA_TRY(ctx, cf::launch_offsets_sorted(world, n, nw, doff, ctx->d_err, s));
+      ctx->launches += 1;
+    } else {
+      CUDA_TRY(ctx, ensure(ctx->keys, std::max<size_t>(1, n) * sizeof(int32_t)));
+      CUDA_TRY(ctx, ensure(ctx->perm, std::max<size_t>(1, n) * sizeof(int32_t)));
+      CUDA_TRY(ctx, ensure(ctx->iota, std::max<size_t>(1, n) * sizeof(int32_t)));
+      size_t tb = 0;
+      CUDA_TRY(ctx, cf::sort_by_world(world, n, nw, nullptr, nullptr, nullptr, nullptr, &tb, s));
+      CUDA_TRY(ctx, ensure(ctx->cub_tmp, tb));
+      tb = ctx->cub_tmp.cap;
+      CUDA_TRY(ctx, cf::launch_check_world_range(world, n, nw, ctx->d_err, s));
+      CUDA_TRY(ctx, cf::launch_iota(static_cast<int32_t*>(ctx->iota.p), n, s));
+      if (n > 0)
+        CUDA_TRY(ctx, cf::sort_by_world(world, n, nw, static_cast<int32_t*>(ctx->keys.p), static_cast<int32_t*>(ctx->perm.p),
+                                        static_cast<int32_t*>(ctx->iota.p), ctx->cub_tmp.p, &tb, s));
+      CUDA_TRY(ctx, cf::launch_offsets_sorted(static_cast<int32_t*>(ctx->keys.p), n, nw, doff, ctx->d_err, s));
+      CUDA_TRY(ctx, ensure(ctx->s0, std::max<size_t>(1, n) * 16));
+      CUDA_TRY(ctx, ensure(ctx->s1, std::max<size_t>(1, n) * 16));
+      CUDA_TRY(ctx, ensure(ctx->s2, std::max<size_t>(1, n) * 16));
+      CUDA_TRY(ctx, ensure(ctx->s3, std::max<size_t>(1, n) * 16));
+      if (jrow) CUDA_TRY(ctx, ensure(ctx->sj, std::max<size_t>(1, n) * 16 * 12));
+      CUDA_TRY(ctx, cf::launch_gather_contacts(static_cast<int32_t*>(ctx->perm.p), n, k0, k1, k2, k3, kj,
+                                               (float4*)ctx->s0.p, (float4*)ctx->s1.p, (float4*)ctx->s2.p,
+                                               (int4*)ctx->s3.p, jrow ? (float4*)ctx->sj.p : nullptr, s));
+      ctx->launches += 5;
+      k0 = (const float4*)ctx->s0.p; k1 = (const float4*)ctx->s1.p; k2 = (const float4*)ctx->s2.p;
+      k3 = (const int4*)ctx->s3.p; kj = jrow ? (const float4*)ctx->sj.p : nullptr;
+      perm = static_cast<int32_t*>(ctx->perm.p);
+      ctx->last_sorted_copy = true;
+    }
+    off = doff;
+    if (seg_e0 >= 0) {
+      cudaEvent_t e = next_event(ctx, &seg_e1);
+      if (e) {
+        cudaEventRecord(e, s);
+        ctx->ev_seg.push_back({seg_e0, seg_e1});
+      }
+    }
+  }
+
+  // ---- facet offsets for impulse output ----
+  const int64_t* foff = nullptr;
+  float* imp = nullptr;
+  int64_t imp_cap = 0;
+  if (c->impulses || c->foff) {
+    CUDA_TRY(ctx, ensure(ctx->foff, (size_t)(n + 1) * sizeof(int64_t)));
+    CUDA_TRY(ctx, ensure(ctx->nf, (size_t)(n + 1) * sizeof(int32_t)));
+    size_t tb = 0;
+    CUDA_TRY(ctx, cf::facet_offsets(nullptr, n, ctx->cfg.n_t, ctx->cfg.n_rol, nullptr, nullptr, nullptr, &tb, nullptr, s));
+    CUDA_TRY(ctx, ensure(ctx->cub_tmp, std::max(tb, ctx->cub_tmp.cap)));
+    tb = ctx->cub_tmp.cap;
+    CUDA_TRY(ctx, cf::facet_offsets((const int4*)c3, n, ctx->cfg.n_t, ctx->cfg.n_rol, static_cast<int32_t*>(ctx->nf.p),
+                                    static_cast<int64_t*>(ctx->foff.p), ctx->cub_tmp.p, &tb, ctx->d_err, s));
+    ctx->launches += 2;
+    foff = static_cast<const int64_t*>(ctx->foff.p);
+    if (c->impulses) {
+      imp_cap = c->impulses_capacity;
+      if (loc == COMFREE_MEM_HOST) {
+        CUDA_TRY(ctx, ensure(ctx->imp, std::max<size_t>(1, imp_cap) * sizeof(float)));
+        imp = static_cast<float*>(ctx->imp.p);
+      } else {
+        imp = c->impulses;
+      }
+    }
+  }
+
+  // ---- fused step ----
+  cf::StepParams P{};
+  const comfree_config& cf_ = ctx->cfg;
+  P.k = cf_.k_user;
+  P.d = cf_.d_user;
+  P.kappa = cf_.k_user * dt + cf_.d_user;
+  P.dt = dt;
+  P.r_min = cf_.r_min;
+  P.r_span = cf_.r_max - cf_.r_min;
+  P.inv_width = 1.0f / cf_.width;
+  P.mid = cf_.midpoint;
+  P.power = cf_.power;
+  P.power_is_2 = cf_.power == 2.0f;
+  for (int k = 0; k < 3; ++k) P.g[k] = cf_.gravity[k];
+  P.n_t = cf_.n_t;
+  P.n_rol = cf_.n_rol;
+  std::memcpy(P.dir_t, ctx->dir_t, sizeof P.dir_t);
+  std::memcpy(P.dir_r, ctx->dir_r, sizeof P.dir_r);
+  P.sc = sc;
+  P.slab = ctx->slab + (size_t)first * sc.slab;
+  P.n_worlds = nw;
+  P.f_ext = fext;
+  P.tree_L = tL;
+  P.tree_tau = ttau;
+  P.off = off;
+  P.c0 = k0; P.c1 = k1; P.c2 = k2; P.c3 = k3; P.jrow = kj;
+  P.n_contacts = n;
+  P.perm = perm;
+  P.foff = foff;
+  P.impulses = imp;
+  P.impulses_cap = imp_cap;
+  P.wstats = (cf_.flags & COMFREE_FLAG_STATS) ? ctx->wstats + first : nullptr;
+  P.err = ctx->d_err;
+  P.first_bad = ctx->d_first_bad;
+  P.world_base = first;
+  P.check_finite = !(cf_.flags & COMFREE_FLAG_NO_FINITE_CHECK);
+  P.deterministic = (cf_.flags & COMFREE_FLAG_DETERMINISTIC) != 0;
+  const int wpw = pick_wpw(sc, n, nw);
+  if (cf::step_smem_bytes(sc, wpw) > 227 * 1024)
+    return fail(ctx, COMFREE_ERR_CAPACITY, "step: %d bodies per world need %zu B of shared memory (> 227 KB)", sc.B,
+                cf::step_smem_bytes(sc, wpw));
+  int st_e0 = -1, st_e1 = -1;
+  if (ctx->timing) {
+    cudaEvent_t e = next_event(ctx, &st_e0);
+    if (e) cudaEventRecord(e, s);
+  }
+  CUDA_TRY(ctx, cf::launch_step(P, wpw, s));
+  if (st_e0 >= 0) {
+    cudaEvent_t e = next_event(ctx, &st_e1);
+    if (e) {
+      cudaEventRecord(e, s);
+      ctx->ev_step.push_back({st_e0, st_e1});
+    }
+  }
+  ctx->launches += nw > 0 ? 1 : 0;
+  ctx->last_first = first;
+  ctx->last_nw = nw;
+  ctx->last_nc = n;
+  ctx->stats_valid = (cf_.flags & COMFREE_FLAG_STATS) != 0;
+
+  // ---- outputs to host ----
+  if (c->foff && foff) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(c->foff, foff, (size_t)(n + 1) * sizeof(int64_t),
+                                  loc == COMFREE_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s));
+  }
+  if (c->impulses && loc == COMFREE_MEM_HOST && imp_cap > 0) {
+    CUDA_TRY(ctx, cudaMemcpyAsync(c->impulses, imp, (size_t)imp_cap * sizeof(float), cudaMemcpyDeviceToHost, s));
+  }
+  if (host_io) return check_latched(ctx, s);
+  return COMFREE_OK;
+}
+
+static comfree_status get_state_impl(comfree_ctx* ctx, int64_t first, int64_t nw, comfree_state* out,
+                                     cudaStream_t s) {
+  const cf::SceneDev& sc = ctx->sc;
+  const float* src = ctx->slab + (size_t)first * sc.slab;
+  if (out->location == COMFREE_MEM_DEVICE) {
+    CUDA_TRY(ctx, cf::launch_slab_to_public(src, nw, sc, out->pos, out->quat, out->vel, out->omega, out->qpos, out->qvel, s));
+    ctx->launches += 1;
+    return COMFREE_OK;
+  }
+  const size_t nb = (size_t)nw * sc.B, nq = (size_t)nw * sc.Q;
+  CUDA_TRY(ctx, ensure(ctx->st_tmp, std::max<size_t>(1, nb * 13 + nq * 2) * sizeof(float)));
+  float* d = static_cast<float*>(ctx->st_tmp.p);
+  float* dp[6] = {d, d + 3 * nb, d + 7 * nb, d + 10 * nb, d + 13 * nb, d + 13 * nb + nq};
+  float* hp[6] = {out->pos, out->quat, out->vel, out->omega, out->qpos, out->qvel};
+  const size_t cnt[6] = {3 * nb, 4 * nb, 3 * nb, 3 * nb, nq, nq};
+  CUDA_TRY(ctx, cf::launch_slab_to_public(src, nw, sc, hp[0] ? dp[0] : nullptr, hp[1] ? dp[1] : nullptr,
+                                          hp[2] ? dp[2] : nullptr, hp[3] ? dp[3] : nullptr,
+                                          hp[4] ? dp[4] : nullptr, hp[5] ? dp[5] : nullptr, s));
+  ctx->launches += 1;
+  for (int k = 0; k < 6; ++k)
+    if (hp[k] && cnt[k])
+      CUDA_TRY(ctx, cudaMemcpyAsync(hp[k], dp[k], cnt[k] * sizeof(float), cudaMemcpyDeviceToHost, s));
+  return COMFREE_OK;
+}
+
+comfree_status comfree_get_state(comfree_ctx* ctx, int64_t first, int64_t nw, comfree_state* out, void* stream) {
+  if (!ctx || !out) return COMFREE_ERR_INVALID_ARGUMENT;
+  if (!ctx->loaded) return fail(ctx, COMFREE_ERR_STATE, "get_state before load_scene");
+  if (first < 0 || nw < 0 || first + nw > ctx->W) return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "get_state: range");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  comfree_status st = get_state_impl(ctx, first, nw, out, s);
+  if (st != COMFREE_OK) return st;
+  return check_latched(ctx, s);
+}
+
+comfree_status comfree_set_state(comfree_ctx* ctx, int64_t first, int64_t nw, const comfree_state* in, void* stream) {
+  if (!ctx || !in) return COMFREE_ERR_INVALID_ARGUMENT;
+  if (!ctx->loaded) return fail(ctx, COMFREE_ERR_STATE, "set_state before load_scene");
+  if (first < 0 || nw < 0 || first + nw > ctx->W) return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "set_state: range");
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  return set_state_impl(ctx, first, nw, in, static_cast<cudaStream_t>(stream));
+}
+
+comfree_status comfree_get_world_stats(comfree_ctx* ctx, int64_t first, int64_t nw, comfree_world_stats* out,
+                                       int32_t location, void* stream) {
+  if (!ctx || !out) return COMFREE_ERR_INVALID_ARGUMENT;
+  if (!ctx->loaded) return fail(ctx, COMFREE_ERR_STATE, "get_world_stats before load_scene");
+  if (!ctx->stats_valid) return fail(ctx, COMFREE_ERR_STATE, "no statistics: set COMFREE_FLAG_STATS and step");
+  if (first < 0 || nw < 0 || first + nw > ctx->W) return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "get_world_stats: range");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(ctx, cudaMemcpyAsync(out, ctx->wstats + first, (size_t)nw * sizeof(comfree_world_stats),
+                                location == COMFREE_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s));
+  return check_latched(ctx, s);
+}
+
+comfree_status comfree_get_stats(comfree_ctx* ctx, comfree_stats* out, void* stream) {
+  if (!ctx || !out) return COMFREE_ERR_INVALID_ARGUMENT;
+  if (!ctx->loaded) return fail(ctx, COMFREE_ERR_STATE, "get_stats before load_scene");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::memset(out, 0, sizeof *out);
+  out->n_worlds = ctx->last_nw;
+  out->first_nonfinite_world = -1;
+  CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  int e = 0;
+  unsigned long long bad = ~0ull;
+  CUDA_TRY(ctx, cudaMemcpy(&e, ctx->d_err, sizeof e, cudaMemcpyDeviceToHost));
+  CUDA_TRY(ctx, cudaMemcpy(&bad, ctx->d_first_bad, sizeof bad, cudaMemcpyDeviceToHost));
+  if (e & cf::ERR_NONFINITE) out->first_nonfinite_world = (int64_t)bad;
+  if (ctx->stats_valid && ctx->last_nw > 0) {
+    std::string h((size_t)ctx->last_nw * sizeof(comfree_world_stats), '\0');
+    comfree_world_stats* ws = reinterpret_cast<comfree_world_stats*>(&h[0]);
+    CUDA_TRY(ctx, cudaMemcpy(ws, ctx->wstats + ctx->last_first, h.size(), cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < ctx->last_nw; ++i) {
+      out->contacts += ws[i].contacts;
+      out->active_facets += ws[i].active_facets;
+      out->max_penetration = std::max(out->max_penetration, ws[i].max_penetration);
+      out->kinetic_energy += ws[i].kinetic_energy;
+    }
+  }
+  return check_latched(ctx, s);
+}
+
+comfree_status comfree_segment_info(comfree_ctx* ctx, int64_t* off, int32_t* perm, void* stream) {
+  if (!ctx || !off) return COMFREE_ERR_INVALID_ARGUMENT;
+  if (!ctx->loaded) return fail(ctx, COMFREE_ERR_STATE, "segment_info before load_scene");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  if (!ctx->off.p) return fail(ctx, COMFREE_ERR_STATE, "segment_info: last step had caller-supplied off[]");
+  CUDA_TRY(ctx, cudaMemcpy(off, ctx->off.p, (size_t)(ctx->last_nw + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost));
+  if (perm) {
+    if (ctx->last_sorted_copy) {
+      CUDA_TRY(ctx, cudaMemcpy(perm, ctx->perm.p, (size_t)ctx->last_nc * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    } else {
+      for (int64_t i = 0; i < ctx->last_nc; ++i) perm[i] = (int32_t)i;
+    }
+  }
+  return check_latched(ctx, s);
+}
+
+comfree_status comfree_set_timing(comfree_ctx* ctx, int enable) {
+  if (!ctx) return COMFREE_ERR_INVALID_ARGUMENT;
+  ctx->timing = enable != 0;
+  return COMFREE_OK;
+}
+
+comfree_status comfree_get_timing(comfree_ctx* ctx, double out[3]) {
+  if (!ctx || !out) return COMFREE_ERR_INVALID_ARGUMENT;
+  out[0] = out[1] = out[2] = 0.0;
+  for (auto& pr : ctx->ev_step) {
+    float ms = 0.f;
+    CUDA_TRY(ctx, cudaEventSynchronize(ctx->ev_pool[pr.second]));
+    CUDA_TRY(ctx, cudaEventElapsedTime(&ms, ctx->ev_pool[pr.first], ctx->ev_pool[pr.second]));
+    out[0] += ms;
+    out[2] += 1.0;
+  }
+  for (auto& pr : ctx->ev_seg) {
+    float ms = 0.f;
+    CUDA_TRY(ctx, cudaEventSynchronize(ctx->ev_pool[pr.second]));
+    CUDA_TRY(ctx, cudaEventElapsedTime(&ms, ctx->ev_pool[pr.first], ctx->ev_pool[pr.second]));
+    out[1] += ms;
+  }
+  ctx->ev_step.clear();
+  ctx->ev_seg.clear();
+  ctx->ev_used = 0;
+  return COMFREE_OK;
+}
+
+int64_t comfree_kernel_launches(const comfree_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+void comfree_destroy(comfree_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  DevBuf* bufs[] = {&ctx->off, &ctx->keys, &ctx->perm, &ctx->iota, &ctx->s0, &ctx->s1, &ctx->s2, &ctx->s3,
+                    &ctx->sj, &ctx->nf, &ctx->foff, &ctx->cub_tmp, &ctx->in_world, &ctx->in_off, &ctx->in_c0,
+                    &ctx->in_c1, &ctx->in_c2, &ctx->in_c3, &ctx->in_jrow, &ctx->in_fext, &ctx->in_L,
+                    &ctx->in_tau, &ctx->imp, &ctx->st_tmp};
+  for (DevBuf* b : bufs) release(*b);
+  for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
+  if (ctx->slab) cudaFree(ctx->slab);
+  if (ctx->inv_mass) cudaFree(ctx->inv_mass);
+  if (ctx->inv_inertia) cudaFree(ctx->inv_inertia);
+  if (ctx->wstats) cudaFree(ctx->wstats);
+  if (ctx->d_err) cudaFree(ctx->d_err);
+  if (ctx->d_first_bad) cudaFree(ctx->d_first_bad);
+  delete ctx;
+}
+
+const char* comfree_last_error(const comfree_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+}  // extern "C"

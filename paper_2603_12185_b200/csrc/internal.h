@@ -1,0 +1,95 @@
+// internal.h — device-side parameter blocks and kernel launchers of the
+// ComFree-Sim step (not part of the ABI; see include/comfree.h).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "comfree.h"
+
+namespace cf {
+
+// Device error word bits (latched, surfaced by the next synchronising call).
+enum : int {
+  ERR_NONFINITE = 1,
+  ERR_UNSORTED = 2,     // COMFREE_CONTACTS_SORTED promised but world[] decreases
+  ERR_WORLD_RANGE = 4,  // world id outside [0, n_worlds)
+  ERR_BODY_RANGE = 8,   // body id out of range / tree side without J rows
+  ERR_CONDIM = 16,      // condim not in {1,3,4,6}
+  ERR_IMPULSE_CAP = 32  // impulses buffer too small
+};
+
+// State slab: per world, 13 planes of Bp floats (px py pz qw qx qy qz vx vy vz
+// wx wy wz) followed by 2 planes of Qp floats (qpos, qvel).  Bp, Qp are
+// multiples of 4 so each plane is 16-byte aligned.
+enum { PL_PX = 0, PL_QW = 3, PL_VX = 7, PL_WX = 10, N_BODY_PLANES = 13 };
+
+struct SceneDev {
+  int B, Bp, T, nd, Q, Qp;
+  int slab;                     // floats per world
+  const float* inv_mass;        // [Bp]
+  const float* inv_inertia;     // [3][Bp]
+};
+
+struct StepParams {
+  // Eq. (12)-(13) parameters
+  float k, d, kappa, dt;
+  float r_min, r_span, inv_width, mid, power;
+  int power_is_2;
+  float g[3];
+  int n_t, n_rol;
+  float2 dir_t[32];             // (cos, sin)(2 pi j / n_t), Eq. (7)
+  float2 dir_r[32];
+  SceneDev sc;
+  float* slab;                  // world 0 of the step range
+  int64_t n_worlds;
+  const float* f_ext;           // [n_worlds][B][6] or null
+  const float* tree_L;          // [n_worlds][T][10]
+  const float* tree_tau;        // [n_worlds][Q]
+  // contacts, grouped by world (possibly a permuted copy)
+  const int64_t* off;           // [n_worlds + 1]
+  const float4* c0;
+  const float4* c1;
+  const float4* c2;
+  const int4* c3;
+  const float4* jrow;           // [12][n_contacts] or null
+  int64_t n_contacts;
+  const int32_t* perm;          // sorted position -> input index, or null (identity)
+  const int64_t* foff;          // [n_contacts + 1] facet offsets (input order) or null
+  float* impulses;              // or null
+  int64_t impulses_cap;
+  comfree_world_stats* wstats;  // [n_worlds] or null
+  int* err;                     // device error word
+  unsigned long long* first_bad;// min world id with a non-finite state
+  int64_t world_base;           // absolute id of world 0 of the range (error reporting)
+  int check_finite;
+  int deterministic;
+};
+
+// Launchers (return cudaError_t of the launch).
+cudaError_t launch_step(const StepParams& p, int warps_per_world, cudaStream_t s);
+size_t step_smem_bytes(const SceneDev& sc, int warps_per_world);
+
+// S0
+cudaError_t launch_offsets_sorted(const int32_t* world, int64_t n, int64_t n_worlds, int64_t* off,
+                                  int* err, cudaStream_t s);
+cudaError_t launch_check_world_range(const int32_t* world, int64_t n, int64_t n_worlds, int* err,
+                                     cudaStream_t s);
+cudaError_t sort_by_world(const int32_t* world, int64_t n, int64_t n_worlds, int32_t* keys_out,
+                          int32_t* perm_out, int32_t* iota_tmp, void* temp, size_t* temp_bytes,
+                          cudaStream_t s);
+cudaError_t launch_gather_contacts(const int32_t* perm, int64_t n, const float4* c0, const float4* c1,
+                                   const float4* c2, const int4* c3, const float4* jrow, float4* o0,
+                                   float4* o1, float4* o2, int4* o3, float4* ojrow, cudaStream_t s);
+cudaError_t facet_offsets(const int4* c3, int64_t n, int n_t, int n_rol, int32_t* nf_tmp,
+                          int64_t* foff, void* temp, size_t* temp_bytes, int* err, cudaStream_t s);
+cudaError_t launch_iota(int32_t* out, int64_t n, cudaStream_t s);
+
+// state layout conversion
+cudaError_t launch_public_to_slab(const float* pos, const float* quat, const float* vel,
+                                  const float* omega, const float* qpos, const float* qvel,
+                                  int64_t n_worlds, const SceneDev& sc, float* slab, cudaStream_t s);
+cudaError_t launch_slab_to_public(const float* slab, int64_t n_worlds, const SceneDev& sc,
+                                  float* pos, float* quat, float* vel, float* omega, float* qpos,
+                                  float* qvel, cudaStream_t s);
+
+}  // namespace cf

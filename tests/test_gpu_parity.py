@@ -1,0 +1,247 @@
+"""Parity of the CUDA path (through the C ABI) with the fp64 oracle.
+
+Tolerance (BASELINE.json north star): per step, from identical fp32 states,
+|d| <= 1e-5 |ref| + 1e-6 on v+, omega+, chain qd+ and every facet impulse
+Lambda_f; positions/orientations within fp32 rounding; integer outputs
+(off, perm, foff) bit-exact; 100-step trajectories within 1e-3 relative.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+from harness import scenes
+from harness.types import Config, Contacts, Inputs, State
+from _gpu import assert_close, compare_step, gpu_step
+from _helpers import run_trajectory
+
+pytestmark = pytest.mark.gpu
+
+CFG = Config()
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2603_12185_b200 as cf
+    cf._lib.load()
+
+
+# ---------------------------------------------------------------- random mixed instances
+@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("cfg", [CFG, CFG.with_(n_t=8, n_rol=6), CFG.with_(n_t=6, n_rol=2, power=3.0)],
+                         ids=["nt4", "nt8", "nt6p3"])
+def test_random_mixed_step(seed, cfg):
+    """Every condim, free/static sides, ragged worlds (incl. empty), unsorted ids."""
+    cpw = [0, 3, 40, 257, 1, 70][seed % 6:] + [0, 3, 40, 257, 1, 70][:seed % 6]
+    scene, st, c, inp = scenes.random_instance(500 + seed, n_worlds=6, n_bodies=9, contacts_per_world=cpw)
+    c = scenes.shuffle_contacts(c, seed)
+    o = oracle.step(cfg, scene, st, c, inp)
+    g = gpu_step(cfg, scene, st, c, inp)
+    compare_step(g, o)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_random_articulated_step(seed):
+    """Chains (S8): tree sides with J rows, Cholesky M^-1, mixed with free bodies."""
+    nd = [4, 3, 2, 1][seed]
+    scene, st, c, inp = scenes.random_instance(600 + seed, n_worlds=5, n_bodies=3, contacts_per_world=[30, 0, 7, 64, 33],
+                                               n_trees=4, tree_ndof=nd)
+    o = oracle.step(CFG, scene, st, c, inp)
+    g = gpu_step(CFG, scene, st, c, inp)
+    compare_step(g, o)
+
+
+def test_locked_dofs_and_no_fext():
+    scene, st, c, inp = scenes.random_instance(700, n_worlds=4, n_bodies=6, contacts_per_world=25,
+                                               with_fext=False, locked_frac=0.5)
+    o = oracle.step(CFG, scene, st, c, inp)
+    g = gpu_step(CFG, scene, st, c, inp)
+    compare_step(g, o)
+
+
+def test_max_facet_counts():
+    cfg = CFG.with_(n_t=32, n_rol=32)
+    scene, st, c, inp = scenes.random_instance(701, n_worlds=3, n_bodies=4, contacts_per_world=20,
+                                               condims=(6,))
+    compare_step(gpu_step(cfg, scene, st, c, inp), oracle.step(cfg, scene, st, c, inp))
+
+
+def test_no_contacts_and_empty_worlds():
+    scene, st, c, inp = scenes.random_instance(702, n_worlds=3, n_bodies=4, contacts_per_world=[0, 0, 0])
+    assert c.n == 0
+    compare_step(gpu_step(CFG, scene, st, c, inp, impulses=False), oracle.step(CFG, scene, st, c, inp))
+
+
+# ---------------------------------------------------------------- paper-shaped workloads
+def test_c4_pile_small_step():
+    """Dense pile (config 4 shape) at a size the oracle finishes quickly:
+    several 256-contact tiles per world plus a ragged tail."""
+    scene, st, c = scenes.c4_pile(n_worlds=6, contacts_per_world=2000 + 77)
+    o = oracle.step(CFG, scene, st, c, None)
+    g = gpu_step(CFG, scene, st, c, None)
+    compare_step(g, o)
+
+
+def test_c3_hand_step():
+    scene, st, c, inp = scenes.c3_hand(n_worlds=64)
+    o = oracle.step(CFG, scene, st, c, inp)
+    g = gpu_step(CFG, scene, st, c, inp)
+    compare_step(g, o)
+
+
+def test_c4_full_size_sampled_worlds():
+    """BASELINE config 4 at full size (1024 worlds x 500 bodies x 2000
+    contacts) in the bench's launch configuration; sampled worlds checked
+    against the oracle one by one."""
+    import torch
+    import paper_2603_12185_b200 as cf
+    scene, st, c = scenes.c4_pile(n_worlds=1024, contacts_per_world=2000)
+    ctx = cf.Context(CFG)
+    ctx.load_scene(scene, 1024, st)
+    dc = cf.DeviceContacts.from_host(c)
+    ctx.step(dc, None, dt=CFG.dt)
+    out = ctx.get_state()
+    for w in (0, 1, 147, 511, 777, 1023):
+        sel = np.nonzero(c.world == w)[0]
+        cw = c.take(sel)
+        cw.world = np.zeros(len(sel), np.int32)
+        o = oracle.step(CFG, scene, st.world_slice(w, w + 1), cw, None)
+        gst = State(*(out[k][w:w + 1] for k in ("pos", "quat", "vel", "omega", "qpos", "qvel")))
+        compare_step(dict(state=gst), o)
+
+
+# ---------------------------------------------------------------- S0 integer outputs
+@pytest.mark.parametrize("seed", range(3))
+def test_segmentation_bit_exact(seed):
+    import paper_2603_12185_b200 as cf
+    scene, st, c, inp = scenes.random_instance(800 + seed, n_worlds=37, n_bodies=3,
+                                               contacts_per_world=list(np.random.default_rng(seed).integers(0, 90, 37)))
+    c = scenes.shuffle_contacts(c, seed)
+    g = gpu_step(CFG, scene, st, c, inp, sorted_hint=False)
+    off_g, perm_g = g["ctx"].segment_info(37, c.n)
+    off_o, perm_o, foff_o = oracle.segment(c, 37, CFG)
+    np.testing.assert_array_equal(off_g, off_o)
+    np.testing.assert_array_equal(perm_g, perm_o)
+    np.testing.assert_array_equal(g["foff"], foff_o)
+
+
+def test_sorted_path_offsets_bit_exact():
+    scene, st, c = scenes.c4_pile(n_worlds=5, contacts_per_world=300)
+    keep = np.ones(c.n, bool)
+    keep[(c.world == 2)] = False                 # an empty world in the middle
+    c = c.take(np.nonzero(keep)[0])
+    g = gpu_step(CFG, scene, st, c, None, sorted_hint=True)
+    off_g, perm_g = g["ctx"].segment_info(5, c.n)
+    off_o, perm_o, _ = oracle.segment(c, 5, CFG)
+    np.testing.assert_array_equal(off_g, off_o)
+    np.testing.assert_array_equal(perm_g, perm_o)
+
+
+# ---------------------------------------------------------------- host-buffer (e2e) path
+def test_host_buffers_match_device_path():
+    scene, st, c, inp = scenes.random_instance(900, n_worlds=4, n_bodies=5, contacts_per_world=33)
+    o = oracle.step(CFG, scene, st, c, inp)
+    g = gpu_step(CFG, scene, st, c, inp, host=True)
+    compare_step(g, o)
+
+
+def test_sub_range_step_leaves_other_worlds():
+    import paper_2603_12185_b200 as cf
+    scene, st, c = scenes.c4_pile(n_worlds=6, contacts_per_world=200)
+    ctx = cf.Context(CFG)
+    ctx.load_scene(scene, 6, st)
+    sel = np.nonzero((c.world >= 2) & (c.world < 4))[0]
+    cs = c.take(sel)
+    cs.world = cs.world - 2
+    ctx.step(cf.DeviceContacts.from_host(cs), None, first_world=2, n_worlds=2)
+    out = ctx.get_state()
+    for w in (0, 1, 4, 5):
+        np.testing.assert_array_equal(out["vel"][w], st.vel[w])
+        np.testing.assert_array_equal(out["pos"][w], st.pos[w])
+    cw = cs.take(np.arange(cs.n))
+    o = oracle.step(CFG, scene, st.world_slice(2, 4), cw, None)
+    gst = State(*(out[k][2:4] for k in ("pos", "quat", "vel", "omega", "qpos", "qvel")))
+    compare_step(dict(state=gst), o)
+
+
+# ---------------------------------------------------------------- errors surface
+def test_nonfinite_state_reported_with_world():
+    import paper_2603_12185_b200 as cf
+    scene, st, c = scenes.c4_pile(n_worlds=4, contacts_per_world=50)
+    st.vel[2, 7, 0] = np.nan
+    ctx = cf.Context(CFG)
+    ctx.load_scene(scene, 4, st)
+    ctx.step(cf.DeviceContacts.from_host(c), None)
+    with pytest.raises(cf.ComfreeError) as ei:
+        ctx.get_state()
+    assert ei.value.status == 4 and "world 2" in str(ei.value)
+
+
+def test_invalid_body_id_and_unsorted_lie_are_validation_errors():
+    import paper_2603_12185_b200 as cf
+    scene, st, c = scenes.c4_pile(n_worlds=3, contacts_per_world=40)
+    bad = c.take(np.arange(c.n))
+    bad.body_b[5] = 10_000
+    ctx = cf.Context(CFG)
+    ctx.load_scene(scene, 3, st)
+    ctx.step(cf.DeviceContacts.from_host(bad), None)
+    with pytest.raises(cf.ComfreeError) as ei:
+        ctx.get_state()
+    assert ei.value.status == 2
+    sh = scenes.shuffle_contacts(c, 1)
+    ctx.step(cf.DeviceContacts.from_host(sh), None, sorted_hint=True)
+    with pytest.raises(cf.ComfreeError) as ei:
+        ctx.get_state()
+    assert ei.value.status == 2 and "sorted" in str(ei.value)
+
+
+def test_stats_match_oracle():
+    import paper_2603_12185_b200 as cf
+    scene, st, c, inp = scenes.random_instance(901, n_worlds=5, n_bodies=6, contacts_per_world=[10, 0, 30, 5, 60])
+    g = gpu_step(CFG, scene, st, c, inp, flags=cf.FLAG_STATS)
+    ws = g["ctx"].get_world_stats()
+    o = oracle.step(CFG, scene, st, c, inp)
+    np.testing.assert_array_equal(ws["contacts"], o["stats"][:, 0].astype(np.int32))
+    assert np.all(np.abs(ws["active_facets"] - o["stats"][:, 1]) <= 2)     # fp decides near the clamp
+    assert_close(ws["max_penetration"], o["stats"][:, 2], what="max_pen")
+    assert_close(ws["kinetic_energy"], o["stats"][:, 3], rtol=1e-4, atol=1e-6, what="KE")
+
+
+# ---------------------------------------------------------------- trajectories (100 steps)
+def _traj_compare(cfg, scene, st, geo, steps=100, rtol=1e-3):
+    import paper_2603_12185_b200 as cf
+    ctx = cf.Context(cfg)
+    ctx.load_scene(scene, st.n_worlds, st)
+
+    def gstep(s, c):
+        r = gpu_step(cfg, scene, s, c, None, impulses=False, ctx=ctx)
+        return r["state"], None
+
+    def ostep(s, c):
+        o = oracle.step(cfg, scene, s, c, None)
+        return o["state"], None
+    sg, _ = run_trajectory(gstep, geo, st, steps)
+    so, _ = run_trajectory(ostep, geo, st.astype(np.float64), steps)
+    for k in ("pos", "vel"):
+        a, b = getattr(sg, k), getattr(so, k)
+        scale = np.max(np.abs(b)) + 1e-3
+        assert np.max(np.abs(a - b)) <= rtol * scale, (k, np.max(np.abs(a - b)), scale)
+
+
+def test_trajectory_c1_sphere_and_sliding_box():
+    scene, st, geo = scenes.c1_scene(box_omega=(0.1, 0.1, 0.1))
+    _traj_compare(CFG, scene, st, geo)
+
+
+def test_trajectory_c2a_incline():
+    scene, st, geos, th = scenes.c2a_incline(np.linspace(0.1, 1.5, 8))
+    _traj_compare(CFG, scene, st, geos)
+
+
+def test_trajectory_c2b_stack_6d():
+    scene, st, geo = scenes.c2b_stack()
+    _traj_compare(CFG.with_(n_t=8, n_rol=8), scene, st, geo)
