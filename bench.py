@@ -35,7 +35,7 @@ SEG_BYTES_PER_CONTACT = 4   # S0 reads the world id
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--worlds", type=int, default=1024, help="worlds per GPU")
@@ -84,7 +84,7 @@ class ClockSampler:
                         self.reasons.add(name.replace("nvmlClocksEventReason", ""))
             except Exception:
                 pass
-            time.sleep(0.02)
+            time.sleep(0.002)
 
     def __enter__(self):
         if self.nv:

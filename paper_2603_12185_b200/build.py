@@ -17,7 +17,7 @@ OBJDIR = os.path.join(HERE, "_build")
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["step.cu", "segment.cu", "state.cu"]
+CU_SOURCES = ["step.cu", "step_w1.cu", "step_w2.cu", "step_w4.cu", "step_w8.cu", "segment.cu", "state.cu"]
 CPP_SOURCES = ["capi.cpp"]
 
 
@@ -30,16 +30,22 @@ def _stale(target, deps):
 
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(OBJDIR, exist_ok=True)
-    headers = [os.path.join(CSRC, "internal.h"), os.path.join(INCLUDE, "comfree.h")]
+    headers = [os.path.join(CSRC, "internal.h"), os.path.join(CSRC, "step_impl.cuh"),
+               os.path.join(INCLUDE, "comfree.h")]
     objs = []
+    jobs = []
     for src in CU_SOURCES:
         s = os.path.join(CSRC, src)
         o = os.path.join(OBJDIR, src + ".o")
         objs.append(o)
         if force or _stale(o, [s] + headers):
-            cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-                   "-Xptxas", "-v" if verbose else "-O3", "-I", INCLUDE, "-I", CSRC, "-c", s, "-o", o]
-            subprocess.check_call(cmd)
+            jobs.append([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+                         "-Xptxas", "-v" if verbose else "-O3", "-I", INCLUDE, "-I", CSRC, "-c", s, "-o", o])
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        for rc in ex.map(lambda c: subprocess.run(c).returncode, jobs):
+            if rc != 0:
+                raise subprocess.CalledProcessError(rc, "nvcc")
     for src in CPP_SOURCES:
         s = os.path.join(CSRC, src)
         o = os.path.join(OBJDIR, src + ".o")

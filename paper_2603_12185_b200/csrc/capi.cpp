@@ -469,6 +469,8 @@ comfree_status comfree_step(comfree_ctx* ctx, const comfree_worlds* wd, const co
   P.r_span = cf_.r_max - cf_.r_min;
   P.inv_width = 1.0f / cf_.width;
   P.mid = cf_.midpoint;
+  P.inv_mid = 1.0f / cf_.midpoint;
+  P.inv_1m_mid = 1.0f / (1.0f - cf_.midpoint);
   P.power = cf_.power;
   P.power_is_2 = cf_.power == 2.0f;
   for (int k = 0; k < 3; ++k) P.g[k] = cf_.gravity[k];

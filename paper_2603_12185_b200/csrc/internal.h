@@ -33,7 +33,7 @@ struct SceneDev {
 struct StepParams {
   // Eq. (12)-(13) parameters
   float k, d, kappa, dt;
-  float r_min, r_span, inv_width, mid, power;
+  float r_min, r_span, inv_width, mid, inv_mid, inv_1m_mid, power;
   int power_is_2;
   float g[3];
   int n_t, n_rol;

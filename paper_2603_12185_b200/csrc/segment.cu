@@ -17,13 +17,11 @@
 namespace cf {
 
 // off[k] = first position whose world id >= k, for k in [0, W]; every entry is
-// written exactly once when the ids are non-decreasing.
-__global__ void k_offsets_sorted(const int32_t* __restrict__ world, int64_t n, int64_t W,
-                                 int64_t* __restrict__ off, int* err) {
-  int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c > n) return;
-  int64_t prev = (c == 0) ? -1 : (int64_t)world[c - 1];
-  int64_t cur = (c == n) ? W : (int64_t)world[c];
+// written exactly once when the ids are non-decreasing.  Each thread scans 8
+// consecutive ids (two 128-bit loads when aligned) so the 4 B/contact read is
+// issued by one wave of threads.
+__device__ __forceinline__ void boundary(int64_t c, int64_t prev, int64_t cur, int64_t n, int64_t W,
+                                         int64_t* __restrict__ off, int* err) {
   if (c < n && (cur < 0 || cur >= W)) {
     atomicOr(err, ERR_WORLD_RANGE);
     return;
@@ -34,6 +32,31 @@ __global__ void k_offsets_sorted(const int32_t* __restrict__ world, int64_t n, i
   }
   if (prev < -1) prev = -1;
   for (int64_t k = prev + 1; k <= cur && k <= W; ++k) off[k] = c;
+}
+
+__global__ void k_offsets_sorted(const int32_t* __restrict__ world, int64_t n, int64_t W,
+                                 int64_t* __restrict__ off, int* err) {
+  const int64_t c0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (c0 > n) return;
+  int32_t v[8];
+  const bool aligned = ((reinterpret_cast<uintptr_t>(world) & 15) == 0);
+  if (aligned && c0 + 8 <= n) {
+    const int4 a = __ldg(reinterpret_cast<const int4*>(world + c0));
+    const int4 b = __ldg(reinterpret_cast<const int4*>(world + c0 + 4));
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = (c0 + j < n) ? __ldg(world + c0 + j) : (int32_t)W;
+  }
+  int64_t prev = (c0 == 0) ? -1 : (int64_t)__ldg(world + c0 - 1);
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int64_t c = c0 + j;
+    if (c > n) break;
+    const int64_t cur = (c == n) ? W : (int64_t)v[j];
+    if (cur != prev || c == n) boundary(c, prev, cur, n, W, off, err);
+    prev = cur;
+  }
 }
 
 __global__ void k_check_range(const int32_t* __restrict__ world, int64_t n, int64_t W, int* err) {
@@ -85,7 +108,7 @@ static unsigned blocks_for(int64_t n, int t = 256) { return (unsigned)((n + t - 
 
 cudaError_t launch_offsets_sorted(const int32_t* world, int64_t n, int64_t W, int64_t* off, int* err,
                                   cudaStream_t s) {
-  k_offsets_sorted<<<blocks_for(n + 1), 256, 0, s>>>(world, n, W, off, err);
+  k_offsets_sorted<<<blocks_for((n + 1 + 7) / 8), 256, 0, s>>>(world, n, W, off, err);
   return cudaGetLastError();
 }
 

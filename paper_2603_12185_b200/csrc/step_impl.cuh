@@ -1,0 +1,682 @@
+// step_impl.cuh — the fused ComFree-Sim contact-resolution step (S1-S8), sm_100a.
+//
+// One "world group" of WPW warps owns one world for the whole step:
+//   prologue  S1  per body: smooth prediction v_s, omega_s (Eq. (2), P:91-97;
+//                 Alg. 1 Kernel I) and the world inverse inertia
+//                 R diag(I_b^-1) R^T; per chain: qd_s = qd + L^-T L^-1 (tau - c) dt.
+//                 Records go to shared memory (the per-world body slab).
+//   main loop     one lane per contact over the contact-major SoA float4 streams
+//                 (128-bit non-allocating loads, next contact prefetched):
+//             S2  relative twist of b w.r.t. a at the contact point (Eq. (4)-(5))
+//             S3  M(phi) = r/(1-r) / (tr_a + tr_b) (Eq. (12)-(13))
+//             S4  every facet f: Lambda_f = M (-k phi - kappa s_f)_+,
+//                 s_f = J~_f v_s (Eq. (7)-(9), sign of Eq. (9)),
+//                 kappa = k dt + d (K dt = k M, D dt = d M; Eq. (12) literal)
+//             S5  facet impulses regrouped into the contact wrench (f_c, tau_c)
+//                 = sum_f J~_f^T Lambda_f in contact space; symmetric facet
+//                 pairs are differenced exactly (2a when both are active)
+//             S6  J^T (f_c, tau_c) scattered into per-world shared-memory
+//                 accumulators (Alg. 1 Kernel III): a warp first sums
+//                 runs of equal body ids, then one 128-bit + one 64-bit
+//                 shared-memory CAS per run and side — no global atomics
+//   epilogue  S7  v+ = v_s + M^-1 p (Eq. (10), Alg. 1 Kernel IV), semi-implicit
+//                 Euler with the exp-map quaternion update; chains q+ = q + qd+ dt;
+//                 finite check and per-world statistics.
+// WPW = 8: one 256-thread CTA per world (dense piles); WPW = 1: eight worlds per
+// CTA, one warp each (hand + cube).  TREES / IMP compile the articulated sides
+// and the per-facet impulse output in or out.
+#pragma once
+#include <cuda_runtime.h>
+#include <math.h>
+
+#include "internal.h"
+
+namespace cf {
+
+static constexpr int kWarps = 8;
+static constexpr int kThreads = kWarps * 32;
+
+struct GroupLayout {  // float offsets inside one group's shared-memory window
+  int rec, quat, acc0, acc1, tq, tL, tacc, red, total;
+};
+
+__host__ __device__ inline GroupLayout group_layout(const SceneDev& sc) {
+  GroupLayout L;
+  int o = 0;
+  L.rec = o;  o += 16 * sc.Bp;   // float4 rec[4][Bp]: (v_s,im) (w_s,Ixx) (x,Iyy) (Izz,Ixy,Ixz,Iyz)
+  L.quat = o; o += 4 * sc.Bp;    // float4 quat[Bp] (step-start orientation)
+  L.acc0 = o; o += 4 * sc.Bp;    // float4 p[Bp] = (p_lin.xyz, p_ang.x)
+  L.acc1 = o; o += 2 * sc.Bp;    // float2 p[Bp] = (p_ang.y, p_ang.z)
+  o = (o + 3) & ~3;
+  L.tq = o;   o += 4 * sc.T;     // float4 qd_s[T]
+  L.tL = o;   o += 12 * sc.T;    // float L[T][12] (10 used)
+  L.tacc = o; o += 4 * sc.T;     // float p_chain[T][4]
+  L.red = o;  o += 16;           // reductions
+  L.total = (o + 3) & ~3;
+  return L;
+}
+
+template <int WPW>
+__device__ __forceinline__ void group_sync(int group) {
+  if (WPW == 1) {
+    __syncwarp();
+  } else if (WPW == kWarps) {
+    __syncthreads();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(group + 1), "r"(WPW * 32) : "memory");
+  }
+}
+
+// 128-bit streaming loads: read once, do not allocate in L1.
+__device__ __forceinline__ float4 ld_stream(const float4* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ int4 ld_stream(const int4* p) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// TMA bulk prefetch of [p, p + bytes) into L2 (16-byte aligned, multiple of 16);
+// issued in pieces of at most 64 KB.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
+  const char* c = static_cast<const char*>(p);
+  while (bytes > 0) {
+    const uint32_t n = bytes > 65536u ? 65536u : bytes;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(c), "r"(n) : "memory");
+    c += n;
+    bytes -= n;
+  }
+}
+
+__device__ __forceinline__ float3 cross3(float3 a, float3 b) {
+  return make_float3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
+}
+__device__ __forceinline__ float dot3(float3 a, float3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ float dot4(float4 a, float4 b) { return a.x * b.x + a.y * b.y + a.z * b.z + a.w * b.w; }
+__device__ __forceinline__ int tri(int i, int j) { return i * (i + 1) / 2 + j; }
+
+// x <- (L L^T)^-1 x for a chain of nd <= 4 DoFs (forward then backward substitution)
+__device__ __forceinline__ void chol_solve(const float* L, int nd, float x[4]) {
+  float y[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (i < nd) {
+      float s = x[i];
+#pragma unroll
+      for (int j = 0; j < i; ++j) s -= L[tri(i, j)] * y[j];
+      y[i] = s / L[tri(i, i)];
+    }
+  }
+#pragma unroll
+  for (int i = 3; i >= 0; --i) {
+    if (i < nd) {
+      float s = y[i];
+#pragma unroll
+      for (int j = i + 1; j < 4; ++j)
+        if (j < nd) s -= L[tri(j, i)] * x[j];
+      x[i] = s / L[tri(i, i)];
+    }
+  }
+}
+
+// ||L^-1 v||^2 = v^T M^-1 v (forward substitution only)
+__device__ __forceinline__ float chol_quad(const float* L, int nd, float4 v4) {
+  const float v[4] = {v4.x, v4.y, v4.z, v4.w};
+  float y[4] = {0.f, 0.f, 0.f, 0.f};
+  float acc = 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (i < nd) {
+      float s = v[i];
+#pragma unroll
+      for (int j = 0; j < i; ++j) s -= L[tri(i, j)] * y[j];
+      y[i] = s / L[tri(i, i)];
+      acc += y[i] * y[i];
+    }
+  }
+  return acc;
+}
+
+// Eq. (13): r(|phi|) with x clamped to [0, 1] (reading R7); branch-free.
+template <bool FAST>
+__device__ __forceinline__ float impedance_r(const StepParams& P, float phi) {
+  const float x = fminf(fabsf(phi) * P.inv_width, 1.0f);
+  const float m = P.mid;
+  const float ulo = x * P.inv_mid, uhi = (1.0f - x) * P.inv_1m_mid;
+  const float plo = FAST ? ulo * ulo : __powf(ulo, P.power);   // FAST: p = 2
+  const float phi_ = FAST ? uhi * uhi : __powf(uhi, P.power);
+  const float g = x < m ? m * plo : 1.0f - (1.0f - m) * phi_;
+  return P.r_min + P.r_span * g;
+}
+
+// One symmetric facet pair (+d, -d) of a channel: L+- = (A +- a)_+.  The pair's
+// contribution to the channel's friction sum is L+ - L- = 2a exactly while both
+// are active (no cancellation against A).
+__device__ __forceinline__ void facet_pair(float A, float a, float& Lp, float& Lm, float& diff) {
+  Lp = fmaxf(A + a, 0.f);
+  Lm = fmaxf(A - a, 0.f);
+  diff = (A >= fabsf(a)) ? 2.f * a : Lp - Lm;
+}
+
+// Facets of one 2-D channel (tangential or rolling), d_j and d_{j+n/2} = -d_j:
+// N += sum L, F += sum L d.  NT = 4 is the exact axis set.
+template <int NT, bool IMP>
+__device__ __forceinline__ void channel2(float A, float kmu, float w1, float w2, const float2* dir, int n,
+                                         float& N, float& F1, float& F2, int& act, float* out, float Mc) {
+  if (NT == 4) {
+    float L0, L2, d0, L1, L3, d1;
+    facet_pair(A, kmu * w1, L0, L2, d0);
+    facet_pair(A, kmu * w2, L1, L3, d1);
+    N += (L0 + L2) + (L1 + L3);
+    F1 += d0;
+    F2 += d1;
+    act += (L0 > 0.f) + (L1 > 0.f) + (L2 > 0.f) + (L3 > 0.f);
+    if (IMP && out) { out[0] = Mc * L0; out[1] = Mc * L1; out[2] = Mc * L2; out[3] = Mc * L3; }
+  } else {
+    const int h = n >> 1;
+    for (int j = 0; j < h; ++j) {
+      const float2 d = dir[j];
+      float Lp, Lm, df;
+      facet_pair(A, kmu * fmaf(d.x, w1, d.y * w2), Lp, Lm, df);
+      N += Lp + Lm;
+      F1 = fmaf(df, d.x, F1);
+      F2 = fmaf(df, d.y, F2);
+      act += (Lp > 0.f) + (Lm > 0.f);
+      if (IMP && out) { out[j] = Mc * Lp; out[j + h] = Mc * Lm; }
+    }
+  }
+}
+
+// Inclusive segmented sum of v[6] over runs of equal `key` in consecutive lanes
+// (Hillis-Steele inside each run, bounded by the longest run of the warp).
+// Returns true on the last lane of each run, which then holds the run total.
+__device__ __forceinline__ bool seg_sum6(int key, float v[6], int lane) {
+  const unsigned full = 0xffffffffu;
+  const int prev = __shfl_up_sync(full, key, 1);
+  const int next = __shfl_down_sync(full, key, 1);
+  const bool head = lane == 0 || prev != key;
+  const bool tail = lane == 31 || next != key;
+  const unsigned heads = __ballot_sync(full, head);
+  if (heads == full) return tail;  // every run has length one (warp-uniform)
+  const int start = 31 - __clz(heads & (full >> (31 - lane)));
+  const int pos = lane - start;
+  const int maxpos = (int)__reduce_max_sync(full, (unsigned)pos);
+  for (int o = 1; o <= maxpos; o <<= 1) {
+#pragma unroll
+    for (int kk = 0; kk < 6; ++kk) {
+      const float u = __shfl_up_sync(full, v[kk], o);
+      if (pos >= o) v[kk] += u;
+    }
+  }
+  return tail;
+}
+
+// Shared-memory float accumulation by 128-bit / 64-bit compare-and-swap
+// (sm_100a has no native shared-memory float add; one CAS covers 4 / 2 floats).
+__device__ __forceinline__ void smem_add4(float4* p, float a, float b, float c, float d) {
+  unsigned __int128* q = reinterpret_cast<unsigned __int128*>(p);
+  unsigned __int128 old = *q, assumed;
+  do {
+    assumed = old;
+    float4 f = *reinterpret_cast<const float4*>(&assumed);
+    f.x += a; f.y += b; f.z += c; f.w += d;
+    old = atomicCAS(q, assumed, *reinterpret_cast<const unsigned __int128*>(&f));
+  } while (old != assumed);
+}
+__device__ __forceinline__ void smem_add2(float2* p, float a, float b) {
+  unsigned long long* q = reinterpret_cast<unsigned long long*>(p);
+  unsigned long long old = *q, assumed;
+  do {
+    assumed = old;
+    float2 f = *reinterpret_cast<const float2*>(&assumed);
+    f.x += a; f.y += b;
+    old = atomicCAS(q, assumed, *reinterpret_cast<const unsigned long long*>(&f));
+  } while (old != assumed);
+}
+
+template <int WPW, bool FAST, bool TREES, bool IMP>
+__global__ void __launch_bounds__(kThreads, 4) k_step(const __grid_constant__ StepParams P) {
+  extern __shared__ float4 smem4[];
+  float* smem = reinterpret_cast<float*>(smem4);
+  const SceneDev& sc = P.sc;
+  const GroupLayout GL = group_layout(sc);
+  constexpr int kGroups = kWarps / WPW;
+  constexpr int kGT = WPW * 32;
+  const int group = threadIdx.x / kGT;
+  const int gt = threadIdx.x % kGT;
+  const int lane = threadIdx.x & 31;
+  const int64_t w = (int64_t)blockIdx.x * kGroups + group;
+  if (w >= P.n_worlds) return;  // whole group leaves together
+
+  float* G = smem + (size_t)group * GL.total;
+  float4* rec = reinterpret_cast<float4*>(G + GL.rec);
+  float4* quat_s = reinterpret_cast<float4*>(G + GL.quat);
+  float4* acc0 = reinterpret_cast<float4*>(G + GL.acc0);
+  float2* acc1 = reinterpret_cast<float2*>(G + GL.acc1);
+  float4* tq = reinterpret_cast<float4*>(G + GL.tq);
+  float* tL = G + GL.tL;
+  float* tacc = G + GL.tacc;
+  float* red = G + GL.red;
+  const int B = sc.B, Bp = sc.Bp, T = sc.T, nd = sc.nd;
+  float* slab = P.slab + (size_t)w * sc.slab;
+  const float dt = P.dt;
+  const bool stats = P.wstats != nullptr;
+
+  // Contact range of this world.
+  const int64_t cbeg = P.off[w];
+  const int nloc = (int)(P.off[w + 1] - cbeg);
+  const float4* C0p = P.c0 + cbeg;
+  const float4* C1p = P.c1 + cbeg;
+  const float4* C2p = P.c2 + cbeg;
+  const int4* C3p = P.c3 + cbeg;
+  const float k = P.k, kappa = P.kappa;
+  int n_active = 0;
+  float max_pen = 0.f;
+  float4 C0 = make_float4(0.f, 0.f, 0.f, 0.f), C1 = C0, C2 = C0;
+  int4 C3 = make_int4(-1, -1, 0, 0);
+  int base = gt & ~31;
+  // ---------------- S1: smooth prediction (Kernel I) ----------------
+  for (int i = gt; i < B; i += kGT) {
+    const float3 x = make_float3(slab[0 * Bp + i], slab[1 * Bp + i], slab[2 * Bp + i]);
+    const float4 q = make_float4(slab[3 * Bp + i], slab[4 * Bp + i], slab[5 * Bp + i], slab[6 * Bp + i]);
+    const float3 v = make_float3(slab[7 * Bp + i], slab[8 * Bp + i], slab[9 * Bp + i]);
+    const float3 om = make_float3(slab[10 * Bp + i], slab[11 * Bp + i], slab[12 * Bp + i]);
+    const float im = sc.inv_mass[i];
+    const float3 ib = make_float3(sc.inv_inertia[i], sc.inv_inertia[Bp + i], sc.inv_inertia[2 * Bp + i]);
+    // rotation of the normalised quaternion (reading R15)
+    const float qn = rsqrtf(q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w);
+    const float qw = q.x * qn, qx = q.y * qn, qy = q.z * qn, qz = q.w * qn;
+    const float R00 = 1.f - 2.f * (qy * qy + qz * qz), R01 = 2.f * (qx * qy - qw * qz), R02 = 2.f * (qx * qz + qw * qy);
+    const float R10 = 2.f * (qx * qy + qw * qz), R11 = 1.f - 2.f * (qx * qx + qz * qz), R12 = 2.f * (qy * qz - qw * qx);
+    const float R20 = 2.f * (qx * qz - qw * qy), R21 = 2.f * (qy * qz + qw * qx), R22 = 1.f - 2.f * (qx * qx + qy * qy);
+    // Iw^-1 = R diag(ib) R^T
+    const float Ixx = R00 * R00 * ib.x + R01 * R01 * ib.y + R02 * R02 * ib.z;
+    const float Iyy = R10 * R10 * ib.x + R11 * R11 * ib.y + R12 * R12 * ib.z;
+    const float Izz = R20 * R20 * ib.x + R21 * R21 * ib.y + R22 * R22 * ib.z;
+    const float Ixy = R00 * R10 * ib.x + R01 * R11 * ib.y + R02 * R12 * ib.z;
+    const float Ixz = R00 * R20 * ib.x + R01 * R21 * ib.y + R02 * R22 * ib.z;
+    const float Iyz = R10 * R20 * ib.x + R11 * R21 * ib.y + R12 * R22 * ib.z;
+    float3 fl = make_float3(0.f, 0.f, 0.f), ta = make_float3(0.f, 0.f, 0.f);
+    if (P.f_ext) {
+      const float* fe = P.f_ext + ((size_t)w * B + i) * 6;
+      fl = make_float3(fe[0], fe[1], fe[2]);
+      ta = make_float3(fe[3], fe[4], fe[5]);
+    }
+    float3 vs = v;
+    if (im > 0.f) {  // gravity only on translating bodies (reading R14)
+      vs.x += (im * fl.x + P.g[0]) * dt;
+      vs.y += (im * fl.y + P.g[1]) * dt;
+      vs.z += (im * fl.z + P.g[2]) * dt;
+    }
+    // bias c = omega x (Iw omega), Iw = R diag(1/ib) R^T on unlocked axes
+    float3 wl = make_float3(R00 * om.x + R10 * om.y + R20 * om.z, R01 * om.x + R11 * om.y + R21 * om.z,
+                            R02 * om.x + R12 * om.y + R22 * om.z);
+    wl.x *= ib.x > 0.f ? __frcp_rn(ib.x) : 0.f;
+    wl.y *= ib.y > 0.f ? __frcp_rn(ib.y) : 0.f;
+    wl.z *= ib.z > 0.f ? __frcp_rn(ib.z) : 0.f;
+    const float3 Iwo = make_float3(R00 * wl.x + R01 * wl.y + R02 * wl.z, R10 * wl.x + R11 * wl.y + R12 * wl.z,
+                                   R20 * wl.x + R21 * wl.y + R22 * wl.z);
+    const float3 gy = cross3(om, Iwo);
+    const float3 rh = make_float3(ta.x - gy.x, ta.y - gy.y, ta.z - gy.z);
+    const float3 ws = make_float3(om.x + (Ixx * rh.x + Ixy * rh.y + Ixz * rh.z) * dt,
+                                  om.y + (Ixy * rh.x + Iyy * rh.y + Iyz * rh.z) * dt,
+                                  om.z + (Ixz * rh.x + Iyz * rh.y + Izz * rh.z) * dt);
+    rec[i] = make_float4(vs.x, vs.y, vs.z, im);
+    rec[Bp + i] = make_float4(ws.x, ws.y, ws.z, Ixx);
+    rec[2 * Bp + i] = make_float4(x.x, x.y, x.z, Iyy);
+    rec[3 * Bp + i] = make_float4(Izz, Ixy, Ixz, Iyz);
+    quat_s[i] = q;
+    acc0[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    acc1[i] = make_float2(0.f, 0.f);
+  }
+  if (TREES) {
+    for (int t = gt; t < T; t += kGT) {
+      const float* Lg = P.tree_L + ((size_t)w * T + t) * 10;
+      float* Ls = tL + 12 * t;
+#pragma unroll
+      for (int k = 0; k < 10; ++k) Ls[k] = Lg[k];
+      float x[4] = {0.f, 0.f, 0.f, 0.f}, qd[4] = {0.f, 0.f, 0.f, 0.f};
+      const float* qv = slab + N_BODY_PLANES * Bp + sc.Qp + t * nd;
+      const float* tau = P.tree_tau + (size_t)w * sc.Q + t * nd;
+      for (int j = 0; j < nd; ++j) { x[j] = tau[j]; qd[j] = qv[j]; }
+      chol_solve(Ls, nd, x);
+      tq[t] = make_float4(qd[0] + x[0] * dt, qd[1] + x[1] * dt, qd[2] + x[2] * dt, qd[3] + x[3] * dt);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) tacc[4 * t + k] = 0.f;
+    }
+  }
+  if (gt < 16) red[gt] = 0.f;
+  group_sync<WPW>(group);
+
+  // ---------------- S2-S6: contacts ----------------
+  // Warp-uniform loop: lane l of warp j handles local contact base + l; base
+  // advances by the group's thread count; the next contact is prefetched.
+  if (base + lane < nloc) {
+    const int j = base + lane;
+    C0 = ld_stream(C0p + j); C1 = ld_stream(C1p + j); C2 = ld_stream(C2p + j); C3 = ld_stream(C3p + j);
+  }
+  for (; base < nloc; base += kGT) {
+    const int j = base + lane;
+    const float4 c0 = C0, c1 = C1, c2 = C2;
+    const int4 c3 = C3;
+    {  // prefetch this lane's next contact (index clamped: no branch)
+      const int jn = min(j + kGT, nloc - 1);
+      C0 = ld_stream(C0p + jn); C1 = ld_stream(C1p + jn); C2 = ld_stream(C2p + jn); C3 = ld_stream(C3p + jn);
+    }
+
+    int ida = c3.x, idb = c3.y;
+    const int cd = c3.w;
+    // ids: free body in [0, B), static -1, chain -(2+t) with J rows; condim in {1,3,4,6}
+    const int lo = TREES ? -1 - T : -1;
+    const bool cd_ok = (unsigned)cd < 8u && ((0x5Au >> (cd & 7)) & 1u);
+    const bool ids_ok = ida >= lo && idb >= lo && ida < B && idb < B && (ida != -1 || idb != -1) &&
+                        (!TREES || P.jrow != nullptr || (ida >= -1 && idb >= -1));
+    const bool in_range = j < nloc;
+    const bool valid = in_range && cd_ok && ids_ok;
+    if (__any_sync(0xffffffffu, in_range && !valid)) {
+      if (in_range && !valid) atomicOr(P.err, cd_ok ? ERR_BODY_RANGE : ERR_CONDIM);
+    }
+    if (!valid) { ida = -1; idb = -1; }
+    const float3 p = make_float3(c0.x, c0.y, c0.z);
+    // S2: relative twist of b w.r.t. a, and the traces of S3
+    float3 vrel = make_float3(0.f, 0.f, 0.f), wrel = make_float3(0.f, 0.f, 0.f);
+    float tr = 0.f;
+    float3 ra = make_float3(0.f, 0.f, 0.f), rb = make_float3(0.f, 0.f, 0.f);
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      const int id = side ? idb : ida;
+      const float sg = side ? 1.f : -1.f;
+      {  // free body (branch-free: a static side reads record 0 and is masked by select)
+        const bool fr = id >= 0;
+        const int ix = fr ? id : 0;
+        const float4 r0 = rec[ix], r1 = rec[Bp + ix], r2 = rec[2 * Bp + ix], r3 = rec[3 * Bp + ix];
+        const float3 r = make_float3(p.x - r2.x, p.y - r2.y, p.z - r2.z);
+        const float3 wxr = cross3(make_float3(r1.x, r1.y, r1.z), r);
+        const float sf = fr ? sg : 0.f;
+        vrel.x += fr ? sg * (r0.x + wxr.x) : 0.f;
+        vrel.y += fr ? sg * (r0.y + wxr.y) : 0.f;
+        vrel.z += fr ? sg * (r0.z + wxr.z) : 0.f;
+        wrel.x += fr ? sf * r1.x : 0.f;
+        wrel.y += fr ? sf * r1.y : 0.f;
+        wrel.z += fr ? sf * r1.z : 0.f;
+        // tr(J M^-1 J^T) of the linear point Jacobian: 3 im + tr(I)|r|^2 - r^T I r
+        const float Ixx = r1.w, Iyy = r2.w, Izz = r3.x, Ixy = r3.y, Ixz = r3.z, Iyz = r3.w;
+        const float3 Ir = make_float3(Ixx * r.x + Ixy * r.y + Ixz * r.z, Ixy * r.x + Iyy * r.y + Iyz * r.z,
+                                      Ixz * r.x + Iyz * r.y + Izz * r.z);
+        const float trs = 3.f * r0.w + (Ixx + Iyy + Izz) * dot3(r, r) - dot3(r, Ir);
+        tr += fr ? trs : 0.f;
+        if (side) rb = r; else ra = r;
+      }
+      if (TREES && id < -1) {
+        const int t = -2 - id;
+        const float4 qd = tq[t];
+        const float* Ls = tL + 12 * t;
+        const float4* jr = P.jrow + (size_t)(side * 6) * P.n_contacts + cbeg + j;
+        float vp[3], wp[3];
+#pragma unroll
+        for (int kk = 0; kk < 3; ++kk) {
+          const float4 jl = ld_stream(jr + (size_t)kk * P.n_contacts);
+          const float4 ja = ld_stream(jr + (size_t)(kk + 3) * P.n_contacts);
+          vp[kk] = dot4(jl, qd);
+          wp[kk] = dot4(ja, qd);
+          tr += chol_quad(Ls, nd, jl);
+        }
+        vrel.x += sg * vp[0]; vrel.y += sg * vp[1]; vrel.z += sg * vp[2];
+        wrel.x += sg * wp[0]; wrel.y += sg * wp[1]; wrel.z += sg * wp[2];
+      }
+    }
+    // S3-S5, computed for every lane (invalid lanes are masked by select at the end)
+    float3 f, tau = make_float3(0.f, 0.f, 0.f);
+    {
+      const float phi = c0.w;
+      const float3 n = make_float3(c1.x, c1.y, c1.z);
+      const float3 t1 = make_float3(c2.x, c2.y, c2.z);
+      const float mu_t = c1.w;
+      const float3 t2 = cross3(n, t1);
+      const float un = dot3(n, vrel);
+      max_pen = fmaxf(max_pen, valid ? -phi : 0.f);
+      // S3: M(phi) (Eq. (12)-(13))
+      const float r = impedance_r<FAST>(P, phi);
+      const float Mc = __fdividef(r, (1.f - r) * tr);
+      // S4: Lambda_f = Mc (A + kappa mu (d . w))_+,  A = -k phi - kappa u_n
+      const float A = -k * phi - kappa * un;
+      float N = 0.f, F1 = 0.f, F2 = 0.f;
+      float* out = nullptr;
+      if (IMP && P.impulses && valid) {
+        const int64_t c = cbeg + j;
+        const int64_t orig = P.perm ? (int64_t)P.perm[c] : c;
+        const int64_t fb = P.foff[orig];
+        const int nf = cd == 1 ? 1 : P.n_t + (cd >= 4 ? 2 : 0) + (cd == 6 ? P.n_rol : 0);
+        if (fb + nf <= P.impulses_cap) out = P.impulses + fb;
+        else atomicOr(P.err, ERR_IMPULSE_CAP);
+      }
+      const float wt1 = dot3(t1, vrel), wt2 = dot3(t2, vrel);
+      int act_t = 0;
+      channel2<FAST ? 4 : 0, IMP>(A, kappa * mu_t, wt1, wt2, P.dir_t, P.n_t, N, F1, F2, act_t,
+                                   cd == 1 ? nullptr : out, Mc);
+      if (cd == 1) {  // normal facet only: one row J_n
+        N = fmaxf(A, 0.f);
+        F1 = 0.f;
+        F2 = 0.f;
+        act_t = N > 0.f;
+        if (IMP && out) out[0] = Mc * N;
+      }
+      n_active += valid ? act_t : 0;
+      if (__any_sync(0xffffffffu, valid && cd >= 4)) {
+        float Mt = 0.f, R1 = 0.f, R2 = 0.f;
+        const float mu_tor = c2.w, mu_rol = __int_as_float(c3.z);
+        if (cd >= 4) {
+          const float wtor = dot3(n, wrel);
+          float Lp, Lm;
+          facet_pair(A, kappa * mu_tor * wtor, Lp, Lm, Mt);
+          N += Lp + Lm;
+          int act = (Lp > 0.f) + (Lm > 0.f);
+          if (IMP && out) { out[P.n_t] = Mc * Lp; out[P.n_t + 1] = Mc * Lm; }
+          if (cd == 6) {
+            const float wr1 = dot3(t1, wrel), wr2 = dot3(t2, wrel);
+            channel2<0, IMP>(A, kappa * mu_rol, wr1, wr2, P.dir_r, P.n_rol, N, R1, R2, act,
+                             out ? out + P.n_t + 2 : nullptr, Mc);
+          }
+          n_active += valid ? act : 0;
+        }
+        // S5 (angular part): tau = -Mc (mu_tor Mt n + mu_rol R . (t1, t2))
+        const float mt = -mu_tor * Mt * Mc, mr1 = -mu_rol * R1 * Mc, mr2 = -mu_rol * R2 * Mc;
+        tau = make_float3(mt * n.x + mr1 * t1.x + mr2 * t2.x, mt * n.y + mr1 * t1.y + mr2 * t2.y,
+                          mt * n.z + mr1 * t1.z + mr2 * t2.z);
+        if (!valid) tau = make_float3(0.f, 0.f, 0.f);
+      }
+      // S5: f = Mc (N n - mu_t F . (t1, t2))
+      const float fn = Mc * N, ft1 = -mu_t * F1 * Mc, ft2 = -mu_t * F2 * Mc;
+      f = make_float3(fn * n.x + ft1 * t1.x + ft2 * t2.x, fn * n.y + ft1 * t1.y + ft2 * t2.y,
+                      fn * n.z + ft1 * t1.z + ft2 * t2.z);
+      if (!valid) f = make_float3(0.f, 0.f, 0.f);
+    }
+    // S6: scatter J^T (f, tau).  Free bodies get (f, r x f + tau) per side: the
+    // warp sums runs of equal body ids (contacts sorted by body pair make them
+    // long), then each run's last lane adds its run total with one 128-bit and
+    // one 64-bit shared-memory CAS.
+#pragma unroll
+    for (int side = 0; side < 2; ++side) {
+      const int id = side ? idb : ida;
+      const float sg = side ? 1.f : -1.f;
+      const float3 m = cross3(side ? rb : ra, f);
+      float v[6] = {sg * f.x, sg * f.y, sg * f.z, sg * (m.x + tau.x), sg * (m.y + tau.y), sg * (m.z + tau.z)};
+      const int key = id >= 0 ? id : -1;
+      const bool tail = seg_sum6(key, v, lane);
+      if (tail && key >= 0) {
+        smem_add4(&acc0[key], v[0], v[1], v[2], v[3]);
+        smem_add2(&acc1[key], v[4], v[5]);
+      }
+    }
+    if (TREES) {
+#pragma unroll
+      for (int side = 0; side < 2; ++side) {
+        const int id = side ? idb : ida;
+        if (id < -1) {  // chain side: J_lin^T f + J_ang^T tau into its DoFs
+          const float sg = side ? 1.f : -1.f;
+          const int t = -2 - id;
+          const float4* jr = P.jrow + (size_t)(side * 6) * P.n_contacts + cbeg + j;
+          float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
+          const float fv[3] = {f.x, f.y, f.z}, tv[3] = {tau.x, tau.y, tau.z};
+#pragma unroll
+          for (int kk = 0; kk < 3; ++kk) {
+            const float4 jl = ld_stream(jr + (size_t)kk * P.n_contacts);
+            const float4 ja = ld_stream(jr + (size_t)(kk + 3) * P.n_contacts);
+            s4.x += jl.x * fv[kk] + ja.x * tv[kk];
+            s4.y += jl.y * fv[kk] + ja.y * tv[kk];
+            s4.z += jl.z * fv[kk] + ja.z * tv[kk];
+            s4.w += jl.w * fv[kk] + ja.w * tv[kk];
+          }
+          const float sv[4] = {s4.x, s4.y, s4.z, s4.w};
+          for (int jj = 0; jj < nd; ++jj) atomicAdd(&tacc[4 * t + jj], sg * sv[jj]);
+        }
+      }
+    }
+  }
+  group_sync<WPW>(group);
+
+  // ---------------- S7: velocity correction + integration (Kernel IV) ----------------
+  float ke = 0.f;
+  bool nonfinite = false;
+  for (int i = gt; i < B; i += kGT) {
+    const float4 r0 = rec[i], r1 = rec[Bp + i], r2 = rec[2 * Bp + i], r3 = rec[3 * Bp + i];
+    const float4 q = quat_s[i];
+    const float4 a0 = acc0[i];
+    const float2 a1 = acc1[i];
+    const float im = r0.w;
+    const float Ixx = r1.w, Iyy = r2.w, Izz = r3.x, Ixy = r3.y, Ixz = r3.z, Iyz = r3.w;
+    const float3 v = make_float3(r0.x + im * a0.x, r0.y + im * a0.y, r0.z + im * a0.z);
+    const float3 om = make_float3(r1.x + Ixx * a0.w + Ixy * a1.x + Ixz * a1.y,
+                                  r1.y + Ixy * a0.w + Iyy * a1.x + Iyz * a1.y,
+                                  r1.z + Ixz * a0.w + Iyz * a1.x + Izz * a1.y);
+    const float3 x = make_float3(r2.x + v.x * dt, r2.y + v.y * dt, r2.z + v.z * dt);
+    // q+ = normalize(exp(omega dt / 2) (x) q), world-frame omega
+    const float3 th = make_float3(om.x * dt, om.y * dt, om.z * dt);
+    const float a2 = dot3(th, th);
+    float s, ch;
+    if (a2 < 0.0625f) {  // |omega dt| < 1/4: sin(h)/(2h), cos(h) by series, h = |omega dt|/2 (error < 1e-10)
+      const float h2 = 0.25f * a2;
+      s = 0.5f * (1.f - h2 * (1.f / 6.f - h2 * (1.f / 120.f - h2 * (1.f / 5040.f))));
+      ch = 1.f - h2 * (0.5f - h2 * (1.f / 24.f - h2 * (1.f / 720.f)));
+    } else {
+      const float ang = sqrtf(a2);
+      float sh;
+      sincosf(0.5f * ang, &sh, &ch);
+      s = sh / ang;
+    }
+    const float ew = ch, ex = s * th.x, ey = s * th.y, ez = s * th.z;
+    float nw = ew * q.x - ex * q.y - ey * q.z - ez * q.w;
+    float nx = ew * q.y + ex * q.x + ey * q.w - ez * q.z;
+    float ny = ew * q.z - ex * q.w + ey * q.x + ez * q.y;
+    float nz = ew * q.w + ex * q.z - ey * q.y + ez * q.x;
+    const float inv = rsqrtf(nw * nw + nx * nx + ny * ny + nz * nz);
+    nw *= inv; nx *= inv; ny *= inv; nz *= inv;
+    slab[0 * Bp + i] = x.x; slab[1 * Bp + i] = x.y; slab[2 * Bp + i] = x.z;
+    slab[3 * Bp + i] = nw; slab[4 * Bp + i] = nx; slab[5 * Bp + i] = ny; slab[6 * Bp + i] = nz;
+    slab[7 * Bp + i] = v.x; slab[8 * Bp + i] = v.y; slab[9 * Bp + i] = v.z;
+    slab[10 * Bp + i] = om.x; slab[11 * Bp + i] = om.y; slab[12 * Bp + i] = om.z;
+    if (P.check_finite) {
+      const float chk = x.x + x.y + x.z + v.x + v.y + v.z + om.x + om.y + om.z + nw + nx + ny + nz;
+      nonfinite |= !isfinite(chk);
+    }
+    if (stats) {
+      // KE = 1/2 m v^2 + 1/2 omega^T Iw(q+) omega
+      const float3 ib = make_float3(sc.inv_inertia[i], sc.inv_inertia[Bp + i], sc.inv_inertia[2 * Bp + i]);
+      const float R00 = 1.f - 2.f * (ny * ny + nz * nz), R01 = 2.f * (nx * ny - nw * nz), R02 = 2.f * (nx * nz + nw * ny);
+      const float R10 = 2.f * (nx * ny + nw * nz), R11 = 1.f - 2.f * (nx * nx + nz * nz), R12 = 2.f * (ny * nz - nw * nx);
+      const float R20 = 2.f * (nx * nz - nw * ny), R21 = 2.f * (ny * nz + nw * nx), R22 = 1.f - 2.f * (nx * nx + ny * ny);
+      const float l0 = R00 * om.x + R10 * om.y + R20 * om.z;
+      const float l1 = R01 * om.x + R11 * om.y + R21 * om.z;
+      const float l2 = R02 * om.x + R12 * om.y + R22 * om.z;
+      ke += 0.5f * ((ib.x > 0.f ? l0 * l0 / ib.x : 0.f) + (ib.y > 0.f ? l1 * l1 / ib.y : 0.f) +
+                    (ib.z > 0.f ? l2 * l2 / ib.z : 0.f));
+      if (im > 0.f) ke += 0.5f * dot3(v, v) / im;
+    }
+  }
+  if (TREES) {
+    for (int t = gt; t < T; t += kGT) {
+      float x[4] = {tacc[4 * t], tacc[4 * t + 1], tacc[4 * t + 2], tacc[4 * t + 3]};
+      const float* Ls = tL + 12 * t;
+      chol_solve(Ls, nd, x);
+      const float4 qs = tq[t];
+      const float qsv[4] = {qs.x, qs.y, qs.z, qs.w};
+      float* qp = slab + N_BODY_PLANES * Bp + t * nd;
+      float* qv = slab + N_BODY_PLANES * Bp + sc.Qp + t * nd;
+      float qdn[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int j = 0; j < nd; ++j) {
+        qdn[j] = qsv[j] + x[j];
+        qv[j] = qdn[j];
+        qp[j] = qp[j] + qdn[j] * dt;
+        if (P.check_finite) nonfinite |= !isfinite(qp[j] + qdn[j]);
+      }
+      if (stats) {  // 1/2 qd^T L L^T qd
+        for (int i2 = 0; i2 < nd; ++i2) {
+          float y = 0.f;
+          for (int j = i2; j < nd; ++j) y += Ls[tri(j, i2)] * qdn[j];
+          ke += 0.5f * y * y;
+        }
+      }
+    }
+  }
+  if (nonfinite) {
+    atomicOr(P.err, ERR_NONFINITE);
+    atomicMin(P.first_bad, (unsigned long long)(P.world_base + w));
+  }
+  if (stats) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      n_active += __shfl_xor_sync(0xffffffffu, n_active, o);
+      max_pen = fmaxf(max_pen, __shfl_xor_sync(0xffffffffu, max_pen, o));
+      ke += __shfl_xor_sync(0xffffffffu, ke, o);
+    }
+    if (lane == 0) {
+      atomicAdd(reinterpret_cast<int*>(&red[0]), n_active);
+      atomicMax(reinterpret_cast<int*>(&red[1]), __float_as_int(fmaxf(max_pen, 0.f)));
+      atomicAdd(&red[2], ke);
+    }
+    group_sync<WPW>(group);
+    if (gt == 0) {
+      comfree_world_stats ws;
+      ws.contacts = nloc;
+      ws.active_facets = *reinterpret_cast<int*>(&red[0]);
+      ws.max_penetration = __int_as_float(*reinterpret_cast<int*>(&red[1]));
+      ws.kinetic_energy = red[2];
+      P.wstats[w] = ws;
+    }
+  }
+}
+
+template <int WPW, bool FAST, bool TREES, bool IMP>
+cudaError_t launch_variant(const StepParams& p, cudaStream_t s) {
+  const int groups = kWarps / WPW;
+  const size_t smem = (size_t)groups * group_layout(p.sc).total * sizeof(float);
+  const unsigned grid = (unsigned)((p.n_worlds + groups - 1) / groups);
+  if (grid == 0) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(k_step<WPW, FAST, TREES, IMP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  k_step<WPW, FAST, TREES, IMP><<<grid, kThreads, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+// FAST = the 4-facet tangential cone with the default power p = 2 (dense piles);
+// every other configuration takes the general facet loop and __powf.
+template <int WPW>
+cudaError_t launch_wpw(const StepParams& p, cudaStream_t s) {
+  const bool trees = p.sc.T > 0, imp = p.impulses != nullptr;
+  if (p.n_t == 4 && p.power_is_2) {
+    if (trees) return imp ? launch_variant<WPW, true, true, true>(p, s) : launch_variant<WPW, true, true, false>(p, s);
+    return imp ? launch_variant<WPW, true, false, true>(p, s) : launch_variant<WPW, true, false, false>(p, s);
+  }
+  if (trees) return imp ? launch_variant<WPW, false, true, true>(p, s) : launch_variant<WPW, false, true, false>(p, s);
+  return imp ? launch_variant<WPW, false, false, true>(p, s) : launch_variant<WPW, false, false, false>(p, s);
+}
+
+}  // namespace cf

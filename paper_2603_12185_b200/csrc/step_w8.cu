@@ -1,0 +1,6 @@
+// Instantiation of the fused step for world groups of 8 warp(s) (parallel build unit).
+#include "step_impl.cuh"
+
+namespace cf {
+cudaError_t launch_step_w8(const StepParams& p, cudaStream_t s) { return launch_wpw<8>(p, s); }
+}  // namespace cf
