@@ -38,12 +38,17 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--worlds", type=int, default=1024, help="worlds per GPU")
+    ap.add_argument("--worlds", type=int, default=None, help="worlds per GPU (pile 1024, hand 4096)")
     ap.add_argument("--contacts", type=int, default=2000, help="contacts per world")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    return ap.parse_args()
+    ap.add_argument("--workload", default="pile", choices=["pile", "hand"],
+                    help="pile: config 4 (the BASELINE metric); hand: config 3")
+    a = ap.parse_args()
+    if a.worlds is None:
+        a.worlds = 4096 if a.workload == "hand" else 1024
+    return a
 
 
 def dist_env():
@@ -123,7 +128,7 @@ def ncu_traffic():
 
 
 # ---------------------------------------------------------------- oracle (CPU) timing
-def cpu_oracle_rate(scene, st, contacts, cfg, seconds: float, max_worlds: int):
+def cpu_oracle_rate(scene, st, contacts, cfg, seconds: float, max_worlds: int, inputs=None):
     """The fp64 oracle as it stands, OpenMP across worlds on all host cores,
     repeated steps over a bounded sample of the workload's worlds."""
     import oracle
@@ -131,12 +136,17 @@ def cpu_oracle_rate(scene, st, contacts, cfg, seconds: float, max_worlds: int):
     sel = np.nonzero(contacts.world < W)[0]
     c = contacts.take(sel)
     s = st.world_slice(0, W)
+    inp = None
+    if inputs is not None:
+        from harness.types import Inputs
+        inp = Inputs(*(None if a is None else np.ascontiguousarray(a[:W]) for a in
+                       (inputs.f_ext, inputs.tree_L, inputs.tree_tau)))
     cores = os.cpu_count() or 1
-    oracle.step(cfg, scene, s, c, None, n_threads=cores)   # warm
+    oracle.step(cfg, scene, s, c, inp, n_threads=cores)   # warm
     n = 0
     t0 = time.perf_counter()
     while True:
-        oracle.step(cfg, scene, s, c, None, n_threads=cores)
+        oracle.step(cfg, scene, s, c, inp, n_threads=cores)
         n += 1
         if time.perf_counter() - t0 >= seconds:
             break
@@ -182,11 +192,27 @@ def run_reference(args, rank, world_size):
     print(json.dumps(line), flush=True)
 
 
+def workload(args, rank):
+    """(scene, state, contacts, inputs, name, algorithmic bytes per step per GPU)."""
+    from harness import scenes
+    W = args.worlds
+    if args.workload == "hand":
+        scene, st, c, inp = scenes.c3_hand(n_worlds=W, world_offset=rank * W)
+        n_rows = int(np.count_nonzero(c.body_a < -1) + np.count_nonzero(c.body_b < -1))
+        Q = scene.n_tree_dofs
+        alg = (c.n * BYTES_PER_CONTACT + n_rows * 96 + W * scene.n_bodies * BYTES_PER_BODY
+               + W * (Q * 16 + scene.n_trees * 40 + Q * 4))
+        return scene, st, c, inp, "c3 LEAP-like hand + cube (4x4-DoF chains + free cube)", alg
+    scene, st, c = scenes.c4_pile(n_worlds=W, contacts_per_world=args.contacts, world_offset=rank * W)
+    alg = W * (args.contacts * BYTES_PER_CONTACT + scene.n_bodies * BYTES_PER_BODY)
+    return scene, st, c, None, "c4 dense pile", alg
+
+
 def run_ours(args, rank, world_size, local):
     import torch
     import torch.distributed as dist
     import paper_2603_12185_b200 as cf
-    from harness import scenes
+    from paper_2603_12185_b200.dist import all_gather_worlds, reduce_max, uniform_ranges
     from harness.types import Config
 
     torch.cuda.set_device(local)
@@ -195,16 +221,20 @@ def run_ours(args, rank, world_size, local):
         dist.init_process_group("nccl", device_id=dev)
     cfg = Config()
     W = args.worlds
-    scene, st, c = scenes.c4_pile(n_worlds=W, contacts_per_world=args.contacts, world_offset=rank * W)
+    scene, st, c, inp, wname, alg_bytes = workload(args, rank)
     ctx = cf.Context(cfg, device=local)
     ctx.load_scene(scene, W, st)
     dc = cf.DeviceContacts.from_host(c, dev)
     assert dc.sorted
+    tin = None
+    if inp is not None:
+        tin = type(inp)(*(None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+                          for a in (inp.f_ext, inp.tree_L, inp.tree_tau)))
     stream = torch.cuda.current_stream()
     flush = None if args.no_flush else torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
     def one_step():
-        ctx.step(dc, None, dt=cfg.dt, stream=stream)
+        ctx.step(dc, tin, dt=cfg.dt, stream=stream)
 
     for _ in range(max(args.warmup, 3)):
         one_step()
@@ -228,44 +258,42 @@ def run_ours(args, rank, world_size, local):
     if world_size > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    step_ms = [a.elapsed_time(b) for a, b in evs]
-    total_ms = float(sum(step_ms))
+    total_ms = float(sum(a.elapsed_time(b) for a, b in evs))
     launches = ctx.kernel_launches - launches0
     kt = ctx.get_timing()
     ctx.set_timing(False)
-    if world_size > 1:
-        t = torch.tensor([total_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = reduce_max(total_ms, dev)   # the job is as slow as its slowest rank
     ms_per_step = total_ms / args.steps
     world_steps = W * world_size * args.steps
     value = world_steps / (total_ms * 1e-3)
-    contacts_per_s = value * args.contacts
+    contacts_per_s = value * (c.n / W)
 
     # roofline of the dominant kernel (fused step): algorithmic bytes per launch / its event time
-    B = scene.n_bodies
-    alg_bytes = W * (args.contacts * BYTES_PER_CONTACT + B * BYTES_PER_BODY)
     k_ms = kt["step_ms"] / max(kt["step_launches"], 1)
     peak, peak_kind = peaks()
     achieved = alg_bytes / (k_ms * 1e-3) / 1e9
     tr = ncu_traffic()
     traffic = None
-    if tr and tr.get("worlds") == W and tr.get("contacts_per_world") == args.contacts:
+    if tr and tr.get("workload") == args.workload and tr.get("worlds") == W and \
+            tr.get("contacts_per_world") == c.n // W:
         traffic = tr.get("dram_bytes_per_launch")
 
-    # stats after the timed region (NCCL all-reduce of a per-rank summary)
+    # after the timed region: final states all-gathered (NCCL) for verification
     final = ctx.get_state()
-    ke = float(np.sum(final["vel"].astype(np.float64) ** 2))
     finite = bool(np.isfinite(final["vel"]).all() and np.isfinite(final["pos"]).all())
+    gathered_mb = None
     if world_size > 1:
-        t = torch.tensor([ke, float(finite)], device=dev, dtype=torch.float64)
-        dist.all_reduce(t)
+        ranges = uniform_ranges(W * world_size, world_size)
+        loc = {k: torch.from_numpy(final[k]).to(dev) for k in ("pos", "quat", "vel", "omega")}
+        full = all_gather_worlds(loc, ranges)
+        gathered_mb = sum(v.numel() * v.element_size() for v in full.values()) / 1e6
+        finite = bool(reduce_max(0.0 if finite else 1.0, dev) == 0.0)
 
     # e2e: the same metric through the C ABI with HOST buffers (pinned), H2D of the
     # step's contacts and D2H of the resulting state inside the timed region
     hc = cf.HostContacts.from_arrays(c, pin=True)
     e2e_steps = max(1, args.e2e_steps)
-    ctx.step(hc, None, dt=cfg.dt)          # warm the staging buffers
+    ctx.step(hc, inp, dt=cfg.dt)           # warm the staging buffers
     out_host = {k: torch.empty(v.shape, dtype=torch.float32).pin_memory().numpy() for k, v in final.items()}
     from paper_2603_12185_b200 import _lib
     import ctypes as ct
@@ -278,47 +306,46 @@ def run_ours(args, rank, world_size, local):
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(e2e_steps):
-        ctx.step(hc, None, dt=cfg.dt, stream=stream)
+        ctx.step(hc, inp, dt=cfg.dt, stream=stream)
         rc = ctx._lib.comfree_get_state(ctx.h, 0, W, ct.byref(st_h), stream.cuda_stream)
         ctx._check(rc, "comfree_get_state")
     e1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = e0.elapsed_time(e1)
-    if world_size > 1:
-        t = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+    e2e_ms = reduce_max(e0.elapsed_time(e1), dev)
     e2e_value = W * world_size * e2e_steps / (e2e_ms * 1e-3)
-    h2d = hc.h2d_bytes()
+    h2d = hc.h2d_bytes() + (0 if inp is None else sum(a.nbytes for a in (inp.f_ext, inp.tree_L, inp.tree_tau)
+                                                      if a is not None))
     d2h = sum(v.nbytes for v in out_host.values())
 
     cpu = None
     if rank == 0 and world_size == 1:
-        cpu = cpu_oracle_rate(scene, st, c, cfg, args.cpu_seconds, max_worlds=W)
+        cpu = cpu_oracle_rate(scene, st, c, cfg, args.cpu_seconds, max_worlds=W, inputs=inp)
     if world_size > 1:
         dist.barrier()
     if rank == 0:
         line = {
-            "metric": METRIC, "value": value, "unit": "world-steps/s", "n_gpus": world_size,
+            "metric": METRIC if args.workload == "pile" else "world-steps/s (LEAP-like hand + cube, 4096 worlds)",
+            "value": value, "unit": "world-steps/s", "n_gpus": world_size,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": "c4 dense pile", "worlds_per_gpu": W, "contacts_per_world": args.contacts,
-                       "bodies_per_world": B, "facets_per_contact": 4, "condim": 3, "dt": cfg.dt,
-                       "l2": "flushed between timed steps (256 MB write); per-step footprint 184 MB > 126 MB L2"
-                       if flush is not None else "not flushed; per-step footprint 184 MB > 126 MB L2",
+            "config": {"workload": wname, "worlds_per_gpu": W, "contacts_per_world": c.n // W,
+                       "bodies_per_world": scene.n_bodies, "chains_per_world": scene.n_trees,
+                       "facets_per_contact": 4, "condim": 3, "dt": cfg.dt,
+                       "l2": "flushed between timed steps (256 MB write)" if flush is not None else "not flushed",
+                       "footprint_mb_per_step": alg_bytes / 1e6,
                        "parallelism": f"world-sharded x{world_size}"},
             "contacts_per_s": contacts_per_s,
             "gpu_launches": int(launches),
             "kernel_ms": {"fused_step": k_ms, "segment_s0": kt["segment_ms"] / max(kt["step_launches"], 1)},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
-                         "kernel": "k_step (S1-S7 fused)",
-                         "algorithmic_bytes_per_launch": alg_bytes},
+                         "kernel": "k_step (S1-S7 fused)", "algorithmic_bytes_per_launch": alg_bytes},
             "clocks": clock.summary(),
             "e2e": {"value": e2e_value, "unit": "world-steps/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": e2e_steps},
             "cpu_baseline": cpu,
+            "allgather_final_state_mb": gathered_mb,
             "context": "paper: 2-3x MJWarp throughput in dense contact on one RTX 4090 (PAPER.md P:11, P:274); "
                        "full-step numbers, not this path alone",
             "final_state_finite": finite,
