@@ -498,9 +498,10 @@ comfree_status comfree_step(comfree_ctx* ctx, const comfree_worlds* wd, const co
   P.check_finite = !(cf_.flags & COMFREE_FLAG_NO_FINITE_CHECK);
   P.deterministic = (cf_.flags & COMFREE_FLAG_DETERMINISTIC) != 0;
   const int wpw = pick_wpw(sc, n, nw);
-  if (cf::step_smem_bytes(sc, wpw) > 227 * 1024)
+  const size_t smem_need = P.deterministic ? cf::step_smem_bytes_det(sc) : cf::step_smem_bytes(sc, wpw);
+  if (smem_need > 227 * 1024)
     return fail(ctx, COMFREE_ERR_CAPACITY, "step: %d bodies per world need %zu B of shared memory (> 227 KB)", sc.B,
-                cf::step_smem_bytes(sc, wpw));
+                smem_need);
   int st_e0 = -1, st_e1 = -1;
   if (ctx->timing) {
     cudaEvent_t e = next_event(ctx, &st_e0);

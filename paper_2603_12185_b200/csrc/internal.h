@@ -68,6 +68,7 @@ struct StepParams {
 // Launchers (return cudaError_t of the launch).
 cudaError_t launch_step(const StepParams& p, int warps_per_world, cudaStream_t s);
 size_t step_smem_bytes(const SceneDev& sc, int warps_per_world);
+size_t step_smem_bytes_det(const SceneDev& sc);
 
 // S0
 cudaError_t launch_offsets_sorted(const int32_t* world, int64_t n, int64_t n_worlds, int64_t* off,

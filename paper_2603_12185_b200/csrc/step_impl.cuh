@@ -33,6 +33,9 @@
 
 namespace cf {
 
+#ifndef CF_MINB
+#define CF_MINB 4
+#endif
 static constexpr int kWarps = 8;
 static constexpr int kThreads = kWarps * 32;
 
@@ -44,7 +47,11 @@ __host__ __device__ inline GroupLayout group_layout(const SceneDev& sc) {
   GroupLayout L;
   int o = 0;
   L.rec = o;  o += 16 * sc.Bp;   // float4 rec[4][Bp]: (v_s,im) (w_s,Ixx) (x,Iyy) (Izz,Ixy,Ixz,Iyz)
+#if !defined(CF_QUAT_GLOBAL)
   L.quat = o; o += 4 * sc.Bp;    // float4 quat[Bp] (step-start orientation)
+#else
+  L.quat = 0;
+#endif
   L.acc0 = o; o += 4 * sc.Bp;    // float4 p[Bp] = (p_lin.xyz, p_ang.x)
   L.acc1 = o; o += 2 * sc.Bp;    // float2 p[Bp] = (p_ang.y, p_ang.z)
   o = (o + 3) & ~3;
@@ -56,11 +63,11 @@ __host__ __device__ inline GroupLayout group_layout(const SceneDev& sc) {
   return L;
 }
 
-template <int WPW>
+template <int WPW, int CW = kWarps>
 __device__ __forceinline__ void group_sync(int group) {
   if (WPW == 1) {
     __syncwarp();
-  } else if (WPW == kWarps) {
+  } else if (WPW == CW) {
     __syncthreads();
   } else {
     asm volatile("bar.sync %0, %1;" ::"r"(group + 1), "r"(WPW * 32) : "memory");
@@ -241,13 +248,36 @@ __device__ __forceinline__ void smem_add2(float2* p, float a, float b) {
   } while (old != assumed);
 }
 
-template <int WPW, bool FAST, bool TREES, bool IMP>
-__global__ void __launch_bounds__(kThreads, 4) k_step(const __grid_constant__ StepParams P) {
+// Deterministic mode (one warp owns the world, so plain read-modify-writes
+// suffice): run totals are applied lane by lane in increasing lane order among
+// lanes with the same body, lanes with different bodies together.
+__device__ __forceinline__ void det_apply(float4* acc0, float2* acc1, bool t, int k, const float v[6], int lane) {
+  const unsigned full = 0xffffffffu;
+  unsigned pend = __ballot_sync(full, t);
+  while (pend) {
+    const unsigned same = __match_any_sync(full, t ? k : -1 - lane);
+    const bool leader = t && ((same & pend & ((1u << lane) - 1u)) == 0u);
+    if (leader) {
+      float4 a = acc0[k];
+      a.x += v[0]; a.y += v[1]; a.z += v[2]; a.w += v[3];
+      acc0[k] = a;
+      float2 b = acc1[k];
+      b.x += v[4]; b.y += v[5];
+      acc1[k] = b;
+      t = false;
+    }
+    __syncwarp();
+    pend = __ballot_sync(full, t);
+  }
+}
+
+template <int CW, int WPW, bool FAST, bool TREES, bool IMP, bool DET>
+__global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : 16) k_step(const __grid_constant__ StepParams P) {
   extern __shared__ float4 smem4[];
   float* smem = reinterpret_cast<float*>(smem4);
   const SceneDev& sc = P.sc;
   const GroupLayout GL = group_layout(sc);
-  constexpr int kGroups = kWarps / WPW;
+  constexpr int kGroups = CW / WPW;
   constexpr int kGT = WPW * 32;
   const int group = threadIdx.x / kGT;
   const int gt = threadIdx.x % kGT;
@@ -332,7 +362,9 @@ __global__ void __launch_bounds__(kThreads, 4) k_step(const __grid_constant__ St
     rec[Bp + i] = make_float4(ws.x, ws.y, ws.z, Ixx);
     rec[2 * Bp + i] = make_float4(x.x, x.y, x.z, Iyy);
     rec[3 * Bp + i] = make_float4(Izz, Ixy, Ixz, Iyz);
+#if !defined(CF_QUAT_GLOBAL)
     quat_s[i] = q;
+#endif
     acc0[i] = make_float4(0.f, 0.f, 0.f, 0.f);
     acc1[i] = make_float2(0.f, 0.f);
   }
@@ -353,7 +385,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_step(const __grid_constant__ St
     }
   }
   if (gt < 16) red[gt] = 0.f;
-  group_sync<WPW>(group);
+  group_sync<WPW, CW>(group);
 
   // ---------------- S2-S6: contacts ----------------
   // Warp-uniform loop: lane l of warp j handles local contact base + l; base
@@ -502,17 +534,48 @@ __global__ void __launch_bounds__(kThreads, 4) k_step(const __grid_constant__ St
     // warp sums runs of equal body ids (contacts sorted by body pair make them
     // long), then each run's last lane adds its run total with one 128-bit and
     // one 64-bit shared-memory CAS.
-#pragma unroll
-    for (int side = 0; side < 2; ++side) {
-      const int id = side ? idb : ida;
-      const float sg = side ? 1.f : -1.f;
-      const float3 m = cross3(side ? rb : ra, f);
-      float v[6] = {sg * f.x, sg * f.y, sg * f.z, sg * (m.x + tau.x), sg * (m.y + tau.y), sg * (m.z + tau.z)};
-      const int key = id >= 0 ? id : -1;
-      const bool tail = seg_sum6(key, v, lane);
-      if (tail && key >= 0) {
-        smem_add4(&acc0[key], v[0], v[1], v[2], v[3]);
-        smem_add2(&acc1[key], v[4], v[5]);
+    if (DET) {
+      const float3 ma = cross3(ra, f), mb = cross3(rb, f);
+      float va[6] = {-f.x, -f.y, -f.z, -(ma.x + tau.x), -(ma.y + tau.y), -(ma.z + tau.z)};
+      float vb[6] = {f.x, f.y, f.z, mb.x + tau.x, mb.y + tau.y, mb.z + tau.z};
+      const int ka = ida >= 0 ? ida : -1, kb = idb >= 0 ? idb : -1;
+      const bool ta = seg_sum6(ka, va, lane) && ka >= 0;
+      det_apply(acc0, acc1, ta, ka, va, lane);
+      const bool tb = seg_sum6(kb, vb, lane) && kb >= 0;
+      det_apply(acc0, acc1, tb, kb, vb, lane);
+    } else {
+      // side a: aggregate, issue the first CAS attempts without waiting
+      const float3 ma = cross3(ra, f);
+      float va[6] = {-f.x, -f.y, -f.z, -(ma.x + tau.x), -(ma.y + tau.y), -(ma.z + tau.z)};
+      const int ka = ida >= 0 ? ida : -1;
+      const bool ta = seg_sum6(ka, va, lane) && ka >= 0;
+      typedef unsigned __int128 u128;
+      typedef unsigned long long u64;
+      u128* pa4 = reinterpret_cast<u128*>(acc0 + (ta ? ka : 0));
+      u64* pa2 = reinterpret_cast<u64*>(acc1 + (ta ? ka : 0));
+      u128 oa4 = 0, ra4 = 0;
+      u64 oa2 = 0, ra2 = 0;
+      if (ta) {
+        oa4 = *pa4; oa2 = *pa2;
+        float4 g = *reinterpret_cast<const float4*>(&oa4);
+        g.x += va[0]; g.y += va[1]; g.z += va[2]; g.w += va[3];
+        float2 h = *reinterpret_cast<const float2*>(&oa2);
+        h.x += va[4]; h.y += va[5];
+        ra4 = atomicCAS(pa4, oa4, *reinterpret_cast<const u128*>(&g));
+        ra2 = atomicCAS(pa2, oa2, *reinterpret_cast<const u64*>(&h));
+      }
+      // side b while side a's CAS is in flight
+      const float3 mb = cross3(rb, f);
+      float vb[6] = {f.x, f.y, f.z, mb.x + tau.x, mb.y + tau.y, mb.z + tau.z};
+      const int kb = idb >= 0 ? idb : -1;
+      const bool tb = seg_sum6(kb, vb, lane) && kb >= 0;
+      if (tb) {
+        smem_add4(&acc0[kb], vb[0], vb[1], vb[2], vb[3]);
+        smem_add2(&acc1[kb], vb[4], vb[5]);
+      }
+      if (ta && (ra4 != oa4 || ra2 != oa2)) {  // lost a race: redo the missing part
+        if (ra4 != oa4) smem_add4(&acc0[ka], va[0], va[1], va[2], va[3]);
+        if (ra2 != oa2) smem_add2(&acc1[ka], va[4], va[5]);
       }
     }
     if (TREES) {
@@ -535,19 +598,31 @@ __global__ void __launch_bounds__(kThreads, 4) k_step(const __grid_constant__ St
             s4.w += jl.w * fv[kk] + ja.w * tv[kk];
           }
           const float sv[4] = {s4.x, s4.y, s4.z, s4.w};
-          for (int jj = 0; jj < nd; ++jj) atomicAdd(&tacc[4 * t + jj], sg * sv[jj]);
+          if (!DET) {
+            for (int jj = 0; jj < nd; ++jj) atomicAdd(&tacc[4 * t + jj], sg * sv[jj]);
+          } else {  // lane order (one warp owns the world)
+            for (int l = 0; l < 32; ++l) {
+              if (l == lane)
+                for (int jj = 0; jj < nd; ++jj) tacc[4 * t + jj] += sg * sv[jj];
+              __syncwarp(__activemask());
+            }
+          }
         }
       }
     }
   }
-  group_sync<WPW>(group);
+  group_sync<WPW, CW>(group);
 
   // ---------------- S7: velocity correction + integration (Kernel IV) ----------------
   float ke = 0.f;
   bool nonfinite = false;
   for (int i = gt; i < B; i += kGT) {
     const float4 r0 = rec[i], r1 = rec[Bp + i], r2 = rec[2 * Bp + i], r3 = rec[3 * Bp + i];
+#if !defined(CF_QUAT_GLOBAL)
     const float4 q = quat_s[i];
+#else
+    const float4 q = make_float4(slab[3 * Bp + i], slab[4 * Bp + i], slab[5 * Bp + i], slab[6 * Bp + i]);
+#endif
     const float4 a0 = acc0[i];
     const float2 a1 = acc1[i];
     const float im = r0.w;
@@ -641,7 +716,7 @@ __global__ void __launch_bounds__(kThreads, 4) k_step(const __grid_constant__ St
       atomicMax(reinterpret_cast<int*>(&red[1]), __float_as_int(fmaxf(max_pen, 0.f)));
       atomicAdd(&red[2], ke);
     }
-    group_sync<WPW>(group);
+    group_sync<WPW, CW>(group);
     if (gt == 0) {
       comfree_world_stats ws;
       ws.contacts = nloc;
@@ -653,30 +728,37 @@ __global__ void __launch_bounds__(kThreads, 4) k_step(const __grid_constant__ St
   }
 }
 
-template <int WPW, bool FAST, bool TREES, bool IMP>
+template <int CW, int WPW, bool FAST, bool TREES, bool IMP, bool DET>
 cudaError_t launch_variant(const StepParams& p, cudaStream_t s) {
-  const int groups = kWarps / WPW;
+  const int groups = CW / WPW;
   const size_t smem = (size_t)groups * group_layout(p.sc).total * sizeof(float);
   const unsigned grid = (unsigned)((p.n_worlds + groups - 1) / groups);
   if (grid == 0) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(k_step<WPW, FAST, TREES, IMP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(k_step<CW, WPW, FAST, TREES, IMP, DET>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_step<WPW, FAST, TREES, IMP><<<grid, kThreads, smem, s>>>(p);
+  k_step<CW, WPW, FAST, TREES, IMP, DET><<<grid, CW * 32, smem, s>>>(p);
   return cudaGetLastError();
 }
 
 // FAST = the 4-facet tangential cone with the default power p = 2 (dense piles);
 // every other configuration takes the general facet loop and __powf.
-template <int WPW>
-cudaError_t launch_wpw(const StepParams& p, cudaStream_t s) {
+template <int CW, int WPW, bool DET>
+cudaError_t launch_cfg(const StepParams& p, cudaStream_t s) {
   const bool trees = p.sc.T > 0, imp = p.impulses != nullptr;
   if (p.n_t == 4 && p.power_is_2) {
-    if (trees) return imp ? launch_variant<WPW, true, true, true>(p, s) : launch_variant<WPW, true, true, false>(p, s);
-    return imp ? launch_variant<WPW, true, false, true>(p, s) : launch_variant<WPW, true, false, false>(p, s);
+    if (trees) return imp ? launch_variant<CW, WPW, true, true, true, DET>(p, s)
+                          : launch_variant<CW, WPW, true, true, false, DET>(p, s);
+    return imp ? launch_variant<CW, WPW, true, false, true, DET>(p, s) : launch_variant<CW, WPW, true, false, false, DET>(p, s);
   }
-  if (trees) return imp ? launch_variant<WPW, false, true, true>(p, s) : launch_variant<WPW, false, true, false>(p, s);
-  return imp ? launch_variant<WPW, false, false, true>(p, s) : launch_variant<WPW, false, false, false>(p, s);
+  if (trees) return imp ? launch_variant<CW, WPW, false, true, true, DET>(p, s)
+                        : launch_variant<CW, WPW, false, true, false, DET>(p, s);
+  return imp ? launch_variant<CW, WPW, false, false, true, DET>(p, s) : launch_variant<CW, WPW, false, false, false, DET>(p, s);
+}
+
+template <int WPW>
+cudaError_t launch_wpw(const StepParams& p, cudaStream_t s) {
+  return launch_cfg<kWarps, WPW, false>(p, s);
 }
 
 }  // namespace cf

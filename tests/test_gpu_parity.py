@@ -259,3 +259,36 @@ def test_trajectory_c2a_incline():
 def test_trajectory_c2b_stack_6d():
     scene, st, geo = scenes.c2b_stack()
     _traj_compare(CFG.with_(n_t=8, n_rol=8), scene, st, geo)
+
+
+# ---------------------------------------------------------------- deterministic mode
+def test_deterministic_mode_bitwise_and_shard_invariant():
+    """COMFREE_FLAG_DETERMINISTIC: one warp owns a world and applies run totals
+    in lane order, so repeated runs and different world batchings give
+    bit-identical states (worlds are independent); parity as usual."""
+    import paper_2603_12185_b200 as cf
+    scene, st, c = scenes.c4_pile(n_worlds=6, contacts_per_world=700)
+    o = oracle.step(CFG, scene, st, c, None)
+    runs = [gpu_step(CFG, scene, st, c, None, flags=cf.FLAG_DETERMINISTIC) for _ in range(3)]
+    for r in runs[1:]:
+        for k in ("pos", "quat", "vel", "omega"):
+            np.testing.assert_array_equal(getattr(r["state"], k), getattr(runs[0]["state"], k))
+        np.testing.assert_array_equal(r["impulses"], runs[0]["impulses"])
+    compare_step(runs[0], o)
+    # worlds 2..3 stepped as their own batch
+    sel = np.nonzero((c.world >= 2) & (c.world < 4))[0]
+    cs = c.take(sel)
+    cs.world = cs.world - 2
+    part = gpu_step(CFG, scene, st.world_slice(2, 4), cs, None, flags=cf.FLAG_DETERMINISTIC, impulses=False)
+    for k in ("pos", "quat", "vel", "omega"):
+        np.testing.assert_array_equal(getattr(part["state"], k), getattr(runs[0]["state"], k)[2:4])
+
+
+def test_deterministic_mode_articulated():
+    import paper_2603_12185_b200 as cf
+    scene, st, c, inp = scenes.c3_hand(n_worlds=8)
+    a = gpu_step(CFG, scene, st, c, inp, flags=cf.FLAG_DETERMINISTIC)
+    b = gpu_step(CFG, scene, st, c, inp, flags=cf.FLAG_DETERMINISTIC)
+    for k in ("pos", "quat", "vel", "omega", "qpos", "qvel"):
+        np.testing.assert_array_equal(getattr(a["state"], k), getattr(b["state"], k))
+    compare_step(a, oracle.step(CFG, scene, st, c, inp))
