@@ -310,18 +310,23 @@ comfree_status comfree_load_scene(comfree_ctx* ctx, const comfree_scene* scene, 
   const size_t slab_bytes = std::max<size_t>(16, (size_t)n_worlds * sc.slab * sizeof(float));
   CUDA_TRY(ctx, cudaMalloc(&ctx->slab, slab_bytes));
   CUDA_TRY(ctx, cudaMalloc(&ctx->inv_mass, sc.Bp * sizeof(float)));
-  CUDA_TRY(ctx, cudaMalloc(&ctx->inv_inertia, 3 * sc.Bp * sizeof(float)));
+  CUDA_TRY(ctx, cudaMalloc(&ctx->inv_inertia, 6 * sc.Bp * sizeof(float)));
   CUDA_TRY(ctx, cudaMalloc(&ctx->wstats, std::max<int64_t>(1, n_worlds) * sizeof(comfree_world_stats)));
-  std::string h(4 * sc.Bp * sizeof(float), '\0');
+  std::string h(7 * sc.Bp * sizeof(float), '\0');
   float* hm = reinterpret_cast<float*>(&h[0]);
   for (int i = 0; i < sc.Bp; ++i) {
     hm[i] = i < sc.B ? scene->inv_mass[i] : 0.f;
-    for (int k = 0; k < 3; ++k) hm[sc.Bp + k * sc.Bp + i] = i < sc.B ? scene->inv_inertia[3 * i + k] : 0.f;
+    for (int k = 0; k < 3; ++k) {
+      const float ib = i < sc.B ? scene->inv_inertia[3 * i + k] : 0.f;
+      hm[sc.Bp + k * sc.Bp + i] = ib;
+      hm[4 * sc.Bp + k * sc.Bp + i] = ib > 0.f ? 1.0f / ib : 0.f;
+    }
   }
   CUDA_TRY(ctx, cudaMemcpy(ctx->inv_mass, hm, sc.Bp * sizeof(float), cudaMemcpyHostToDevice));
-  CUDA_TRY(ctx, cudaMemcpy(ctx->inv_inertia, hm + sc.Bp, 3 * sc.Bp * sizeof(float), cudaMemcpyHostToDevice));
+  CUDA_TRY(ctx, cudaMemcpy(ctx->inv_inertia, hm + sc.Bp, 6 * sc.Bp * sizeof(float), cudaMemcpyHostToDevice));
   sc.inv_mass = ctx->inv_mass;
   sc.inv_inertia = ctx->inv_inertia;
+  sc.inertia = ctx->inv_inertia + 3 * sc.Bp;
   ctx->loaded = true;
   comfree_status st = set_state_impl(ctx, 0, n_worlds, initial, 0);
   if (st != COMFREE_OK) return st;

@@ -28,6 +28,7 @@ struct SceneDev {
   int slab;                     // floats per world
   const float* inv_mass;        // [Bp]
   const float* inv_inertia;     // [3][Bp]
+  const float* inertia;         // [3][Bp] principal I_b (1 / inv_inertia, 0 where locked)
 };
 
 struct StepParams {

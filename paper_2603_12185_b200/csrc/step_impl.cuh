@@ -248,6 +248,39 @@ __device__ __forceinline__ void smem_add2(float2* p, float a, float b) {
   } while (old != assumed);
 }
 
+// Run aggregation and shared-memory CAS for both sides of a contact: side a's
+// first 128-bit and 64-bit CAS are issued, side b is aggregated and added
+// while they are in flight, and side a retries only if it lost a race.
+__device__ __forceinline__ void scatter_cas(float4* acc0, float2* acc1, int ka, float va[6], int kb, float vb[6],
+                                            int lane) {
+  typedef unsigned __int128 u128;
+  typedef unsigned long long u64;
+  const bool ta = seg_sum6(ka, va, lane) && ka >= 0;
+  u128* pa4 = reinterpret_cast<u128*>(acc0 + (ta ? ka : 0));
+  u64* pa2 = reinterpret_cast<u64*>(acc1 + (ta ? ka : 0));
+  u128 oa4 = 0, ra4 = 0;
+  u64 oa2 = 0, ra2 = 0;
+  if (ta) {
+    oa4 = *pa4;
+    oa2 = *pa2;
+    float4 g = *reinterpret_cast<const float4*>(&oa4);
+    g.x += va[0]; g.y += va[1]; g.z += va[2]; g.w += va[3];
+    float2 h = *reinterpret_cast<const float2*>(&oa2);
+    h.x += va[4]; h.y += va[5];
+    ra4 = atomicCAS(pa4, oa4, *reinterpret_cast<const u128*>(&g));
+    ra2 = atomicCAS(pa2, oa2, *reinterpret_cast<const u64*>(&h));
+  }
+  const bool tb = seg_sum6(kb, vb, lane) && kb >= 0;
+  if (tb) {
+    smem_add4(&acc0[kb], vb[0], vb[1], vb[2], vb[3]);
+    smem_add2(&acc1[kb], vb[4], vb[5]);
+  }
+  if (ta && (ra4 != oa4 || ra2 != oa2)) {  // lost a race: redo the missing part
+    if (ra4 != oa4) smem_add4(&acc0[ka], va[0], va[1], va[2], va[3]);
+    if (ra2 != oa2) smem_add2(&acc1[ka], va[4], va[5]);
+  }
+}
+
 // Deterministic mode (one warp owns the world, so plain read-modify-writes
 // suffice): run totals are applied lane by lane in increasing lane order among
 // lanes with the same body, lanes with different bodies together.
@@ -272,7 +305,7 @@ __device__ __forceinline__ void det_apply(float4* acc0, float2* acc1, bool t, in
 }
 
 template <int CW, int WPW, bool FAST, bool TREES, bool IMP, bool DET>
-__global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : 16) k_step(const __grid_constant__ StepParams P) {
+__global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 2 : (CW == 32 ? 1 : 16))) k_step(const __grid_constant__ StepParams P) {
   extern __shared__ float4 smem4[];
   float* smem = reinterpret_cast<float*>(smem4);
   const SceneDev& sc = P.sc;
@@ -348,9 +381,9 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : 16) k_step(c
     // bias c = omega x (Iw omega), Iw = R diag(1/ib) R^T on unlocked axes
     float3 wl = make_float3(R00 * om.x + R10 * om.y + R20 * om.z, R01 * om.x + R11 * om.y + R21 * om.z,
                             R02 * om.x + R12 * om.y + R22 * om.z);
-    wl.x *= ib.x > 0.f ? __frcp_rn(ib.x) : 0.f;
-    wl.y *= ib.y > 0.f ? __frcp_rn(ib.y) : 0.f;
-    wl.z *= ib.z > 0.f ? __frcp_rn(ib.z) : 0.f;
+    wl.x *= sc.inertia[i];            // I_b = 1/I_b^-1, 0 on locked axes (precomputed per scene)
+    wl.y *= sc.inertia[Bp + i];
+    wl.z *= sc.inertia[2 * Bp + i];
     const float3 Iwo = make_float3(R00 * wl.x + R01 * wl.y + R02 * wl.z, R10 * wl.x + R11 * wl.y + R12 * wl.z,
                                    R20 * wl.x + R21 * wl.y + R22 * wl.z);
     const float3 gy = cross3(om, Iwo);
@@ -473,7 +506,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : 16) k_step(c
       const float mu_t = c1.w;
       const float3 t2 = cross3(n, t1);
       const float un = dot3(n, vrel);
-      max_pen = fmaxf(max_pen, valid ? -phi : 0.f);
+      if (stats) max_pen = fmaxf(max_pen, valid ? -phi : 0.f);
       // S3: M(phi) (Eq. (12)-(13))
       const float r = impedance_r<FAST>(P, phi);
       const float Mc = __fdividef(r, (1.f - r) * tr);
@@ -500,7 +533,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : 16) k_step(c
         act_t = N > 0.f;
         if (IMP && out) out[0] = Mc * N;
       }
-      n_active += valid ? act_t : 0;
+      if (stats) n_active += valid ? act_t : 0;
       if (__any_sync(0xffffffffu, valid && cd >= 4)) {
         float Mt = 0.f, R1 = 0.f, R2 = 0.f;
         const float mu_tor = c2.w, mu_rol = __int_as_float(c3.z);
@@ -516,7 +549,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : 16) k_step(c
             channel2<0, IMP>(A, kappa * mu_rol, wr1, wr2, P.dir_r, P.n_rol, N, R1, R2, act,
                              out ? out + P.n_t + 2 : nullptr, Mc);
           }
-          n_active += valid ? act : 0;
+          if (stats) n_active += valid ? act : 0;
         }
         // S5 (angular part): tau = -Mc (mu_tor Mt n + mu_rol R . (t1, t2))
         const float mt = -mu_tor * Mt * Mc, mr1 = -mu_rol * R1 * Mc, mr2 = -mu_rol * R2 * Mc;
@@ -544,39 +577,10 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : 16) k_step(c
       const bool tb = seg_sum6(kb, vb, lane) && kb >= 0;
       det_apply(acc0, acc1, tb, kb, vb, lane);
     } else {
-      // side a: aggregate, issue the first CAS attempts without waiting
-      const float3 ma = cross3(ra, f);
+      const float3 ma = cross3(ra, f), mb = cross3(rb, f);
       float va[6] = {-f.x, -f.y, -f.z, -(ma.x + tau.x), -(ma.y + tau.y), -(ma.z + tau.z)};
-      const int ka = ida >= 0 ? ida : -1;
-      const bool ta = seg_sum6(ka, va, lane) && ka >= 0;
-      typedef unsigned __int128 u128;
-      typedef unsigned long long u64;
-      u128* pa4 = reinterpret_cast<u128*>(acc0 + (ta ? ka : 0));
-      u64* pa2 = reinterpret_cast<u64*>(acc1 + (ta ? ka : 0));
-      u128 oa4 = 0, ra4 = 0;
-      u64 oa2 = 0, ra2 = 0;
-      if (ta) {
-        oa4 = *pa4; oa2 = *pa2;
-        float4 g = *reinterpret_cast<const float4*>(&oa4);
-        g.x += va[0]; g.y += va[1]; g.z += va[2]; g.w += va[3];
-        float2 h = *reinterpret_cast<const float2*>(&oa2);
-        h.x += va[4]; h.y += va[5];
-        ra4 = atomicCAS(pa4, oa4, *reinterpret_cast<const u128*>(&g));
-        ra2 = atomicCAS(pa2, oa2, *reinterpret_cast<const u64*>(&h));
-      }
-      // side b while side a's CAS is in flight
-      const float3 mb = cross3(rb, f);
       float vb[6] = {f.x, f.y, f.z, mb.x + tau.x, mb.y + tau.y, mb.z + tau.z};
-      const int kb = idb >= 0 ? idb : -1;
-      const bool tb = seg_sum6(kb, vb, lane) && kb >= 0;
-      if (tb) {
-        smem_add4(&acc0[kb], vb[0], vb[1], vb[2], vb[3]);
-        smem_add2(&acc1[kb], vb[4], vb[5]);
-      }
-      if (ta && (ra4 != oa4 || ra2 != oa2)) {  // lost a race: redo the missing part
-        if (ra4 != oa4) smem_add4(&acc0[ka], va[0], va[1], va[2], va[3]);
-        if (ra2 != oa2) smem_add2(&acc1[ka], va[4], va[5]);
-      }
+      scatter_cas(acc0, acc1, ida >= 0 ? ida : -1, va, idb >= 0 ? idb : -1, vb, lane);
     }
     if (TREES) {
 #pragma unroll
