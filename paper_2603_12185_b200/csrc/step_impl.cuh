@@ -56,7 +56,7 @@ __host__ __device__ inline GroupLayout group_layout(const SceneDev& sc) {
   L.acc1 = o; o += 2 * sc.Bp;    // float2 p[Bp] = (p_ang.y, p_ang.z)
   o = (o + 3) & ~3;
   L.tq = o;   o += 4 * sc.T;     // float4 qd_s[T]
-  L.tL = o;   o += 12 * sc.T;    // float L[T][12] (10 used)
+  L.tL = o;   o += 16 * sc.T;    // float L[T][16]: 10 packed entries + 4 reciprocal diagonals
   L.tacc = o; o += 4 * sc.T;     // float p_chain[T][4]
   L.red = o;  o += 16;           // reductions
   L.total = (o + 3) & ~3;
@@ -109,7 +109,8 @@ __device__ __forceinline__ float dot3(float3 a, float3 b) { return a.x * b.x + a
 __device__ __forceinline__ float dot4(float4 a, float4 b) { return a.x * b.x + a.y * b.y + a.z * b.z + a.w * b.w; }
 __device__ __forceinline__ int tri(int i, int j) { return i * (i + 1) / 2 + j; }
 
-// x <- (L L^T)^-1 x for a chain of nd <= 4 DoFs (forward then backward substitution)
+// x <- (L L^T)^-1 x for a chain of nd <= 4 DoFs (forward then backward
+// substitution); L[10 + i] holds 1 / L(i,i), precomputed once per step.
 __device__ __forceinline__ void chol_solve(const float* L, int nd, float x[4]) {
   float y[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -118,7 +119,7 @@ __device__ __forceinline__ void chol_solve(const float* L, int nd, float x[4]) {
       float s = x[i];
 #pragma unroll
       for (int j = 0; j < i; ++j) s -= L[tri(i, j)] * y[j];
-      y[i] = s / L[tri(i, i)];
+      y[i] = s * L[10 + i];
     }
   }
 #pragma unroll
@@ -128,7 +129,7 @@ __device__ __forceinline__ void chol_solve(const float* L, int nd, float x[4]) {
 #pragma unroll
       for (int j = i + 1; j < 4; ++j)
         if (j < nd) s -= L[tri(j, i)] * x[j];
-      x[i] = s / L[tri(i, i)];
+      x[i] = s * L[10 + i];
     }
   }
 }
@@ -144,7 +145,7 @@ __device__ __forceinline__ float chol_quad(const float* L, int nd, float4 v4) {
       float s = v[i];
 #pragma unroll
       for (int j = 0; j < i; ++j) s -= L[tri(i, j)] * y[j];
-      y[i] = s / L[tri(i, i)];
+      y[i] = s * L[10 + i];
       acc += y[i] * y[i];
     }
   }
@@ -404,9 +405,11 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
   if (TREES) {
     for (int t = gt; t < T; t += kGT) {
       const float* Lg = P.tree_L + ((size_t)w * T + t) * 10;
-      float* Ls = tL + 12 * t;
+      float* Ls = tL + 16 * t;
 #pragma unroll
       for (int k = 0; k < 10; ++k) Ls[k] = Lg[k];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) Ls[10 + k] = k < nd ? 1.0f / Lg[tri(k, k)] : 0.f;
       float x[4] = {0.f, 0.f, 0.f, 0.f}, qd[4] = {0.f, 0.f, 0.f, 0.f};
       const float* qv = slab + N_BODY_PLANES * Bp + sc.Qp + t * nd;
       const float* tau = P.tree_tau + (size_t)w * sc.Q + t * nd;
@@ -482,7 +485,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
       if (TREES && id < -1) {
         const int t = -2 - id;
         const float4 qd = tq[t];
-        const float* Ls = tL + 12 * t;
+        const float* Ls = tL + 16 * t;
         const float4* jr = P.jrow + (size_t)(side * 6) * P.n_contacts + cbeg + j;
         float vp[3], wp[3];
 #pragma unroll
@@ -682,7 +685,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
   if (TREES) {
     for (int t = gt; t < T; t += kGT) {
       float x[4] = {tacc[4 * t], tacc[4 * t + 1], tacc[4 * t + 2], tacc[4 * t + 3]};
-      const float* Ls = tL + 12 * t;
+      const float* Ls = tL + 16 * t;
       chol_solve(Ls, nd, x);
       const float4 qs = tq[t];
       const float qsv[4] = {qs.x, qs.y, qs.z, qs.w};
