@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo only to exercise the multi-rank path on a single GPU")
     ap.add_argument("--workload", default="pile", choices=["pile", "hand"],
                     help="pile: config 4 (the BASELINE metric); hand: config 3")
     a = ap.parse_args()
@@ -215,10 +217,14 @@ def run_ours(args, rank, world_size, local):
     from paper_2603_12185_b200.dist import all_gather_worlds, reduce_max, uniform_ranges
     from harness.types import Config
 
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world_size > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:                              # plumbing check with several ranks on one GPU
+            dist.init_process_group(args.dist_backend)
     cfg = Config()
     W = args.worlds
     scene, st, c, inp, wname, alg_bytes = workload(args, rank)

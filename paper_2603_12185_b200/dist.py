@@ -45,6 +45,8 @@ def reduce_max(value: float, device=None) -> float:
     import torch.distributed as dist
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
         return float(value)
+    if dist.get_backend() == "gloo":
+        device = "cpu"
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
@@ -59,8 +61,11 @@ def all_gather_worlds(local: Dict[str, "torch.Tensor"], ranges: List[Tuple[int, 
     ws = dist.get_world_size()
     rank = dist.get_rank()
     maxw = max(hi - lo for lo, hi in ranges)
+    cpu = dist.get_backend() == "gloo"
     out = {}
     for k, t in local.items():
+        if cpu:
+            t = t.cpu()
         n_local = ranges[rank][1] - ranges[rank][0]
         assert t.shape[0] == n_local, (k, t.shape, n_local)
         pad = torch.zeros((maxw,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)

@@ -292,3 +292,34 @@ def test_deterministic_mode_articulated():
     for k in ("pos", "quat", "vel", "omega", "qpos", "qvel"):
         np.testing.assert_array_equal(getattr(a["state"], k), getattr(b["state"], k))
     compare_step(a, oracle.step(CFG, scene, st, c, inp))
+
+
+# ---------------------------------------------------------------- CUDA graphs
+def test_step_is_cuda_graph_capturable():
+    """A step (S0 + fused kernel) captured once in a CUDA graph and replayed
+    gives the same states as direct launches (deterministic mode: bitwise)."""
+    import torch
+    import paper_2603_12185_b200 as cf
+    scene, st, c = scenes.c4_pile(n_worlds=8, contacts_per_world=500)
+    outs = []
+    for graph in (False, True):
+        ctx = cf.Context(CFG, flags=cf.FLAG_DETERMINISTIC)
+        ctx.load_scene(scene, 8, st)
+        dc = cf.DeviceContacts.from_host(c)
+        ctx.step(dc, None)                       # allocates scratch outside capture
+        if graph:
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=s):
+                ctx.step(dc, None)
+            for _ in range(5):
+                g.replay()
+        else:
+            for _ in range(5):
+                ctx.step(dc, None)
+        torch.cuda.synchronize()
+        outs.append(ctx.get_state())
+        ctx.close()
+    for k in ("pos", "quat", "vel", "omega"):
+        np.testing.assert_array_equal(outs[0][k], outs[1][k])
