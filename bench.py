@@ -27,9 +27,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "world-steps/s (dense pile, 1024 worlds x 2000 contacts per GPU)"
-BYTES_PER_CONTACT = 64      # c0..c3 float4 streams, read once
+BYTES_PER_CONTACT = 68      # c0..c3 float4 streams (64 B) + the world id read by fused S0
 BYTES_PER_BODY = 104        # 52 B state read + 52 B written
-SEG_BYTES_PER_CONTACT = 4   # S0 reads the world id
 
 
 def parse():
@@ -41,6 +40,7 @@ def parse():
     ap.add_argument("--worlds", type=int, default=None, help="worlds per GPU (pile 1024, hand 4096)")
     ap.add_argument("--contacts", type=int, default=2000, help="contacts per world")
     ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="direct launches instead of CUDA-graph replay")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -194,6 +194,15 @@ def run_reference(args, rank, world_size):
     print(json.dumps(line), flush=True)
 
 
+def kernels_per_step(ctx, dc, tin, cfg):
+    """Kernels one direct step launches (instrumentation counter of the library)."""
+    n0 = ctx.kernel_launches
+    ctx.step(dc, tin, dt=cfg.dt)
+    import torch
+    torch.cuda.synchronize()
+    return ctx.kernel_launches - n0
+
+
 def workload(args, rank):
     """(scene, state, contacts, inputs, name, algorithmic bytes per step per GPU)."""
     from harness import scenes
@@ -245,9 +254,27 @@ def run_ours(args, rank, world_size, local):
     for _ in range(max(args.warmup, 3)):
         one_step()
     torch.cuda.synchronize()
-    launches0 = ctx.kernel_launches
-    ctx.get_timing()                       # clear
+    # direct launches with the library's own event timing around the fused kernel
+    ctx.get_timing()
     ctx.set_timing(True)
+    for _ in range(min(args.steps, 20)):
+        if flush is not None:
+            flush.zero_()
+        one_step()
+    kt = ctx.get_timing()
+    ctx.set_timing(False)
+    k_ms_direct = kt["step_ms"] / max(kt["step_launches"], 1)
+    # one step captured in a CUDA graph (no host launch path inside the timed region)
+    graph = None
+    if not args.no_graph:
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(stream)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=side):
+            ctx.step(dc, tin, dt=cfg.dt, stream=side)
+        stream.wait_stream(side)
+        torch.cuda.synchronize()
+    launches0 = ctx.kernel_launches
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     if world_size > 1:
         dist.barrier()
@@ -258,24 +285,29 @@ def run_ours(args, rank, world_size, local):
             if flush is not None:
                 flush.zero_()              # evict L2 between timed steps (untimed)
             evs[i][0].record(stream)
-            one_step()
+            if graph is not None:
+                graph.replay()
+            else:
+                one_step()
             evs[i][1].record(stream)
         torch.cuda.synchronize()
     if world_size > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    total_ms = float(sum(a.elapsed_time(b) for a, b in evs))
-    launches = ctx.kernel_launches - launches0
-    kt = ctx.get_timing()
-    ctx.set_timing(False)
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = float(sum(step_ms))
+    # kernels per step: one fused kernel (S0 fused for sorted ids); counted by the
+    # library for direct launches, the same for each graph replay
+    launches = (ctx.kernel_launches - launches0) if graph is None else args.steps * kernels_per_step(ctx, dc, tin, cfg)
     total_ms = reduce_max(total_ms, dev)   # the job is as slow as its slowest rank
     ms_per_step = total_ms / args.steps
     world_steps = W * world_size * args.steps
     value = world_steps / (total_ms * 1e-3)
     contacts_per_s = value * (c.n / W)
 
-    # roofline of the dominant kernel (fused step): algorithmic bytes per launch / its event time
-    k_ms = kt["step_ms"] / max(kt["step_launches"], 1)
+    # roofline of the dominant kernel: with one kernel per step the per-step CUDA
+    # events around the graph replay bracket exactly that kernel
+    k_ms = (total_ms / args.steps) if graph is not None else k_ms_direct
     peak, peak_kind = peaks()
     achieved = alg_bytes / (k_ms * 1e-3) / 1e9
     tr = ncu_traffic()
@@ -343,7 +375,9 @@ def run_ours(args, rank, world_size, local):
                        "parallelism": f"world-sharded x{world_size}"},
             "contacts_per_s": contacts_per_s,
             "gpu_launches": int(launches),
-            "kernel_ms": {"fused_step": k_ms, "segment_s0": kt["segment_ms"] / max(kt["step_launches"], 1)},
+            "kernel_ms": {"fused_step": k_ms, "fused_step_direct_launch": k_ms_direct,
+                          "segment_s0_separate": kt["segment_ms"] / max(kt["step_launches"], 1)},
+            "cuda_graph": graph is not None,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
                          "kernel": "k_step (S1-S7 fused)", "algorithmic_bytes_per_launch": alg_bytes},

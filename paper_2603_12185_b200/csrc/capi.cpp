@@ -388,8 +388,9 @@ comfree_status comfree_step(comfree_ctx* ctx, const comfree_worlds* wd, const co
   const float4 *k0 = (const float4*)c0, *k1 = (const float4*)c1, *k2 = (const float4*)c2, *kj = (const float4*)jrow;
   const int4* k3 = (const int4*)c3;
   ctx->last_sorted_copy = false;
+  const int32_t* fused_world = nullptr;
   int seg_e0 = -1, seg_e1 = -1;
-  if (!off && ctx->timing) {
+  if (!off && ctx->timing && !(c->flags & COMFREE_CONTACTS_SORTED)) {
     cudaEvent_t e = next_event(ctx, &seg_e0);
     if (e) cudaEventRecord(e, s);
   }
@@ -397,8 +398,8 @@ comfree_status comfree_step(comfree_ctx* ctx, const comfree_worlds* wd, const co
     CUDA_TRY(ctx, ensure(ctx->off, (size_t)(nw + 1) * sizeof(int64_t)));
     int64_t* doff = static_cast<int64_t*>(ctx->off.p);
     if (c->flags & COMFREE_CONTACTS_SORTED) {
-      CUDA_TRY(ctx, cf::launch_offsets_sorted(world, n, nw, doff, ctx->d_err, s));
-      ctx->launches += 1;
+      // fused S0: the step kernel locates each world's range and verifies the ids
+      fused_world = world;
     } else {
       CUDA_TRY(ctx, ensure(ctx->keys, std::max<size_t>(1, n) * sizeof(int32_t)));
       CUDA_TRY(ctx, ensure(ctx->perm, std::max<size_t>(1, n) * sizeof(int32_t)));
@@ -490,6 +491,8 @@ comfree_status comfree_step(comfree_ctx* ctx, const comfree_worlds* wd, const co
   P.tree_L = tL;
   P.tree_tau = ttau;
   P.off = off;
+  P.world_sorted = fused_world;
+  P.off_out = fused_world ? const_cast<int64_t*>(off) : nullptr;
   P.c0 = k0; P.c1 = k1; P.c2 = k2; P.c3 = k3; P.jrow = kj;
   P.n_contacts = n;
   P.perm = perm;

@@ -48,6 +48,8 @@ struct StepParams {
   const float* tree_tau;        // [n_worlds][Q]
   // contacts, grouped by world (possibly a permuted copy)
   const int64_t* off;           // [n_worlds + 1]
+  const int32_t* world_sorted;  // fused S0: sorted world ids (then off is computed in-kernel), or null
+  int64_t* off_out;             // fused S0: receives off[n_worlds + 1]
   const float4* c0;
   const float4* c1;
   const float4* c2;

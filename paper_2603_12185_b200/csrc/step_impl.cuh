@@ -249,6 +249,45 @@ __device__ __forceinline__ void smem_add2(float2* p, float a, float b) {
   } while (old != assumed);
 }
 
+// S0 fused into the step for sorted input: one warp finds the first index with
+// world id >= key0 and >= key1 in the sorted id array by 32-way search (each
+// round one coalesced probe per lane; both searches advance together).
+__device__ __forceinline__ int ld_id(const int32_t* p) {
+  int r;
+  asm volatile("ld.global.nc.s32 %0, [%1];" : "=r"(r) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void lower_bound2(const int32_t* a, int64_t n, int64_t key0, int64_t key1, int lane,
+                                             int64_t& r0, int64_t& r1) {
+  const unsigned full = 0xffffffffu;
+  int64_t lo0 = 0, hi0 = n, lo1 = 0, hi1 = n;  // answers in [lo, hi]
+  while (hi0 - lo0 > 32 || hi1 - lo1 > 32) {
+    const int64_t st0 = hi0 - lo0 > 32 ? (hi0 - lo0 + 31) / 32 : 1;
+    const int64_t st1 = hi1 - lo1 > 32 ? (hi1 - lo1 + 31) / 32 : 1;
+    const int64_t p0 = lo0 + lane * st0, p1 = lo1 + lane * st1;
+    const bool q0 = p0 < hi0 && ld_id(a + p0) < key0;
+    const bool q1 = p1 < hi1 && ld_id(a + p1) < key1;
+    const int k0 = __popc(__ballot_sync(full, q0)), k1 = __popc(__ballot_sync(full, q1));
+    if (hi0 - lo0 > 32) {
+      const int64_t nlo = k0 ? lo0 + (k0 - 1) * st0 + 1 : lo0;
+      const int64_t pk = lo0 + k0 * st0;
+      hi0 = k0 == 0 ? lo0 : (k0 < 32 && pk < hi0 ? pk : hi0);
+      lo0 = nlo;
+    }
+    if (hi1 - lo1 > 32) {
+      const int64_t nlo = k1 ? lo1 + (k1 - 1) * st1 + 1 : lo1;
+      const int64_t pk = lo1 + k1 * st1;
+      hi1 = k1 == 0 ? lo1 : (k1 < 32 && pk < hi1 ? pk : hi1);
+      lo1 = nlo;
+    }
+  }
+  const int64_t p0 = lo0 + lane, p1 = lo1 + lane;
+  const bool q0 = p0 < hi0 && ld_id(a + p0) < key0;
+  const bool q1 = p1 < hi1 && ld_id(a + p1) < key1;
+  r0 = lo0 + __popc(__ballot_sync(full, q0));
+  r1 = lo1 + __popc(__ballot_sync(full, q1));
+}
+
 // Run aggregation and shared-memory CAS for both sides of a contact: side a's
 // first 128-bit and 64-bit CAS are issued, side b is aggregated and added
 // while they are in flight, and side a retries only if it lost a race.
@@ -333,13 +372,25 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
   const float dt = P.dt;
   const bool stats = P.wstats != nullptr;
 
-  // Contact range of this world.
-  const int64_t cbeg = P.off[w];
-  const int nloc = (int)(P.off[w + 1] - cbeg);
-  const float4* C0p = P.c0 + cbeg;
-  const float4* C1p = P.c1 + cbeg;
-  const float4* C2p = P.c2 + cbeg;
-  const int4* C3p = P.c3 + cbeg;
+  // S0 (sorted input, fused): the first warp of the group locates this world's
+  // contact range while the others start on S1.
+  int64_t* rng = reinterpret_cast<int64_t*>(red + 12);
+  if (P.world_sorted && gt < 32) {
+    int64_t b0, b1;
+    lower_bound2(P.world_sorted, P.n_contacts, w, w + 1, lane, b0, b1);
+    if (lane == 0) {
+      rng[0] = b0;
+      rng[1] = b1;
+      P.off_out[w] = b0;
+      if (w == P.n_worlds - 1) P.off_out[w + 1] = b1;
+      // coverage: ids below 0 precede world 0, ids >= n_worlds follow the last world
+      if ((w == 0 && b0 != 0) || (w == P.n_worlds - 1 && b1 != P.n_contacts)) atomicOr(P.err, ERR_WORLD_RANGE);
+      if (b1 < b0) {  // only possible when the ids are not sorted
+        atomicOr(P.err, ERR_UNSORTED);
+        rng[1] = b0;
+      }
+    }
+  }
   const float k = P.k, kappa = P.kappa;
   int n_active = 0;
   float max_pen = 0.f;
@@ -420,23 +471,36 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
       for (int k = 0; k < 4; ++k) tacc[4 * t + k] = 0.f;
     }
   }
-  if (gt < 16) red[gt] = 0.f;
+  if (gt < 8) red[gt] = 0.f;
   group_sync<WPW, CW>(group);
+
+  // Contact range of this world.
+  const int64_t cbeg = P.world_sorted ? rng[0] : P.off[w];
+  const int nloc = (int)((P.world_sorted ? rng[1] : P.off[w + 1]) - cbeg);
+  const float4* C0p = P.c0 + cbeg;
+  const float4* C1p = P.c1 + cbeg;
+  const float4* C2p = P.c2 + cbeg;
+  const int4* C3p = P.c3 + cbeg;
+  const int32_t* Wp = P.world_sorted ? P.world_sorted + cbeg : nullptr;
 
   // ---------------- S2-S6: contacts ----------------
   // Warp-uniform loop: lane l of warp j handles local contact base + l; base
   // advances by the group's thread count; the next contact is prefetched.
+  int WID = (int)w;  // world id of the prefetched contact (fused S0 check)
   if (base + lane < nloc) {
     const int j = base + lane;
     C0 = ld_stream(C0p + j); C1 = ld_stream(C1p + j); C2 = ld_stream(C2p + j); C3 = ld_stream(C3p + j);
+    if (Wp) WID = ld_id(Wp + j);
   }
   for (; base < nloc; base += kGT) {
     const int j = base + lane;
     const float4 c0 = C0, c1 = C1, c2 = C2;
     const int4 c3 = C3;
+    const int wid = WID;
     {  // prefetch this lane's next contact (index clamped: no branch)
       const int jn = min(j + kGT, nloc - 1);
       C0 = ld_stream(C0p + jn); C1 = ld_stream(C1p + jn); C2 = ld_stream(C2p + jn); C3 = ld_stream(C3p + jn);
+      if (Wp) WID = ld_id(Wp + jn);
     }
 
     int ida = c3.x, idb = c3.y;
@@ -447,6 +511,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
     const bool ids_ok = ida >= lo && idb >= lo && ida < B && idb < B && (ida != -1 || idb != -1) &&
                         (!TREES || P.jrow != nullptr || (ida >= -1 && idb >= -1));
     const bool in_range = j < nloc;
+    if (in_range && wid != (int)w) atomicOr(P.err, ERR_UNSORTED);  // fused S0 check
     const bool valid = in_range && cd_ok && ids_ok;
     if (__any_sync(0xffffffffu, in_range && !valid)) {
       if (in_range && !valid) atomicOr(P.err, cd_ok ? ERR_BODY_RANGE : ERR_CONDIM);
