@@ -1,0 +1,25 @@
+"""Small workload for compute-sanitizer runs (tests/test_sanitizer.py): every
+kernel variant once on tiny inputs."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+
+import numpy as np  # noqa: E402
+
+import paper_2603_12185_b200 as cf  # noqa: E402
+from _gpu import gpu_step  # noqa: E402
+from harness import scenes  # noqa: E402
+from harness.types import Config  # noqa: E402
+
+cfg = Config()
+scene, st, c, inp = scenes.random_instance(11, n_worlds=3, n_bodies=5, contacts_per_world=[7, 0, 40])
+gpu_step(cfg, scene, st, scenes.shuffle_contacts(c, 1), inp)                     # unsorted S0 + impulses
+gpu_step(cfg.with_(n_t=8, n_rol=6), scene, st, c, inp, impulses=False)          # sorted, fused S0, generic facets
+gpu_step(cfg, scene, st, c, inp, flags=cf.FLAG_DETERMINISTIC | cf.FLAG_STATS)   # deterministic + stats
+scene, st, c, inp = scenes.random_instance(12, n_worlds=2, n_bodies=3, contacts_per_world=[9, 33], n_trees=2, tree_ndof=3)
+gpu_step(cfg, scene, st, c, inp)                                                 # articulated chains
+scene, st, c = scenes.c4_pile(n_worlds=2, contacts_per_world=300, lattice=(5, 5, 2))
+gpu_step(cfg, scene, st, c, None, host=True)                                     # host buffers, big-world CTA path
+print("sanitize run ok")

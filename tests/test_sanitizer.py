@@ -1,0 +1,31 @@
+"""compute-sanitizer (memcheck, racecheck, synccheck, initcheck) over every
+kernel variant on tiny inputs (race detection)."""
+import os
+import shutil
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck", "initcheck"])
+def test_compute_sanitizer_clean(tool):
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    exe = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(exe):
+        pytest.skip("compute-sanitizer not found")
+    cmd = [exe, "--tool", tool, "--error-exitcode", "3", "--target-processes", "all"]
+    if tool == "racecheck":
+        cmd += ["--racecheck-report", "all"]
+    cmd += [sys.executable, os.path.join(HERE, "_sanitize_run.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    tail = (r.stdout + r.stderr)[-3000:]
+    assert r.returncode == 0, tail
+    assert "sanitize run ok" in r.stdout, tail
+    out = r.stdout + r.stderr
+    assert "ERROR SUMMARY: 0 errors" in out or "(0 errors, 0 warnings)" in out, tail
