@@ -257,10 +257,36 @@ __device__ __forceinline__ int ld_id(const int32_t* p) {
   asm volatile("ld.global.nc.s32 %0, [%1];" : "=r"(r) : "l"(p));
   return r;
 }
-__device__ __forceinline__ void lower_bound2(const int32_t* a, int64_t n, int64_t key0, int64_t key1, int lane,
-                                             int64_t& r0, int64_t& r1) {
+__device__ __forceinline__ void lower_bound2(const int32_t* a, int64_t n, int64_t n_keys, int64_t key0, int64_t key1,
+                                             int lane, int64_t& r0, int64_t& r1) {
   const unsigned full = 0xffffffffu;
   int64_t lo0 = 0, hi0 = n, lo1 = 0, hi1 = n;  // answers in [lo, hi]
+  {  // first round: 16 lanes per key probe a window around the uniform guess k n / n_keys
+    const int64_t avg = n_keys > 0 ? n / n_keys : n;
+    const int64_t hw = 2 * avg + 32;
+    const int half = lane >> 4, l = lane & 15;
+    const int64_t key = half ? key1 : key0;
+    int64_t g = (n_keys > 0 ? key * n / n_keys : 0) - hw;
+    g = g < 0 ? 0 : (g > n ? n : g);
+    const int64_t width = (2 * hw < n - g) ? 2 * hw : n - g;
+    const int64_t step = (width + 15) / 16 > 0 ? (width + 15) / 16 : 1;
+    const int64_t pp = g + l * step;
+    const bool q = pp < n && ld_id(a + pp) < key;
+    const unsigned b = __ballot_sync(full, q);
+    const int k0 = __popc(b & 0xffffu), k1 = __popc(b >> 16);
+    const int64_t g0 = __shfl_sync(full, g, 0), s0 = __shfl_sync(full, step, 0);
+    const int64_t g1 = __shfl_sync(full, g, 16), s1 = __shfl_sync(full, step, 16);
+    if (k0 == 0) { lo0 = 0; hi0 = g0; }
+    else if (k0 < 16) { lo0 = g0 + (k0 - 1) * s0 + 1; hi0 = g0 + k0 * s0; }
+    else { lo0 = g0 + 15 * s0 + 1; hi0 = n; }
+    if (k1 == 0) { lo1 = 0; hi1 = g1; }
+    else if (k1 < 16) { lo1 = g1 + (k1 - 1) * s1 + 1; hi1 = g1 + k1 * s1; }
+    else { lo1 = g1 + 15 * s1 + 1; hi1 = n; }
+    if (lo0 > n) lo0 = n;
+    if (hi0 > n) hi0 = n;
+    if (lo1 > n) lo1 = n;
+    if (hi1 > n) hi1 = n;
+  }
   while (hi0 - lo0 > 32 || hi1 - lo1 > 32) {
     const int64_t st0 = hi0 - lo0 > 32 ? (hi0 - lo0 + 31) / 32 : 1;
     const int64_t st1 = hi1 - lo1 > 32 ? (hi1 - lo1 + 31) / 32 : 1;
@@ -377,7 +403,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
   int64_t* rng = reinterpret_cast<int64_t*>(red + 12);
   if (P.world_sorted && gt < 32) {
     int64_t b0, b1;
-    lower_bound2(P.world_sorted, P.n_contacts, w, w + 1, lane, b0, b1);
+    lower_bound2(P.world_sorted, P.n_contacts, P.n_worlds, w, w + 1, lane, b0, b1);
     if (lane == 0) {
       rng[0] = b0;
       rng[1] = b1;

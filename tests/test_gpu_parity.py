@@ -323,3 +323,15 @@ def test_step_is_cuda_graph_capturable():
         ctx.close()
     for k in ("pos", "quat", "vel", "omega"):
         np.testing.assert_array_equal(outs[0][k], outs[1][k])
+
+
+def test_fused_segmentation_uneven_worlds():
+    """Sorted world ids with very uneven counts (the in-kernel range search
+    starts from a uniform guess and must fall back): off bit-exact and parity."""
+    cpw = [0, 0, 900, 1, 0, 3, 2500, 0, 17, 0]
+    scene, st, c, inp = scenes.random_instance(950, n_worlds=len(cpw), n_bodies=4, contacts_per_world=cpw)
+    g = gpu_step(CFG, scene, st, c, inp, sorted_hint=True)
+    off_g, _ = g["ctx"].segment_info(len(cpw), c.n)
+    off_o, _, _ = oracle.segment(c, len(cpw), CFG)
+    np.testing.assert_array_equal(off_g, off_o)
+    compare_step(g, oracle.step(CFG, scene, st, c, inp))
