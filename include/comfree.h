@@ -61,7 +61,7 @@ typedef enum {
   COMFREE_ERR_INVALID_ARGUMENT = 1, /* NULL / out-of-range argument */
   COMFREE_ERR_VALIDATION = 2,       /* config or scene violates a documented invariant */
   COMFREE_ERR_CAPACITY = 3,         /* allocation failed or size limit exceeded */
-  COMFREE_ERR_NONFINITE = 4,        /* a world produced a non-finite state */
+  COMFREE_ERR_NONFINITE = 4,        /* a world produced a non-finite state (or overflowed S6) */
   COMFREE_ERR_CUDA = 5,             /* CUDA runtime error */
   COMFREE_ERR_STATE = 6             /* call out of order (e.g. step before load_scene) */
 } comfree_status;
@@ -72,7 +72,8 @@ enum { COMFREE_MEM_DEVICE = 0, COMFREE_MEM_HOST = 1 };
 /* comfree_config.flags */
 enum {
   COMFREE_FLAG_STATS = 1u << 0,         /* per-world statistics every step */
-  COMFREE_FLAG_DETERMINISTIC = 1u << 1, /* run-to-run bitwise identical scatter order */
+  COMFREE_FLAG_DETERMINISTIC = 1u << 1, /* accepted, no effect: every step is bitwise deterministic
+                                           (fixed-point accumulation, see comfree_step) */
   COMFREE_FLAG_NO_FINITE_CHECK = 1u << 2
 };
 
@@ -218,7 +219,14 @@ comfree_status comfree_load_scene(comfree_ctx* ctx, const comfree_scene* scene, 
                                   const comfree_state* initial);
 
 /* One step of duration dt > 0 for the worlds in *worlds with contacts *c.
- * Asynchronous on `stream` when every buffer is on the device. */
+ * Asynchronous on `stream` when every buffer is on the device.
+ * Deterministic: the J^T lambda scatter (S6) accumulates each body's
+ * generalized impulse in 64-bit fixed point (scale 2^(exponent(m^-1)+33)
+ * linear, 2^(exponent(max diag I_w^-1)+33) angular, i.e. a velocity
+ * resolution near 1e-10) with integer atomics, so the result is bitwise
+ * identical run to run for the same input (contact order included).  A
+ * velocity change beyond ~2^28 in one step exceeds the range and is reported
+ * as COMFREE_ERR_NONFINITE. */
 comfree_status comfree_step(comfree_ctx* ctx, const comfree_worlds* worlds,
                             const comfree_contacts* c, float dt, void* stream);
 

@@ -504,9 +504,8 @@ comfree_status comfree_step(comfree_ctx* ctx, const comfree_worlds* wd, const co
   P.first_bad = ctx->d_first_bad;
   P.world_base = first;
   P.check_finite = !(cf_.flags & COMFREE_FLAG_NO_FINITE_CHECK);
-  P.deterministic = (cf_.flags & COMFREE_FLAG_DETERMINISTIC) != 0;
   const int wpw = pick_wpw(sc, n, nw);
-  const size_t smem_need = P.deterministic ? cf::step_smem_bytes_det(sc) : cf::step_smem_bytes(sc, wpw);
+  const size_t smem_need = cf::step_smem_bytes(sc, wpw);
   if (smem_need > 227 * 1024)
     return fail(ctx, COMFREE_ERR_CAPACITY, "step: %d bodies per world need %zu B of shared memory (> 227 KB)", sc.B,
                 smem_need);

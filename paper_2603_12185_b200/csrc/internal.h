@@ -65,13 +65,11 @@ struct StepParams {
   unsigned long long* first_bad;// min world id with a non-finite state
   int64_t world_base;           // absolute id of world 0 of the range (error reporting)
   int check_finite;
-  int deterministic;
 };
 
 // Launchers (return cudaError_t of the launch).
 cudaError_t launch_step(const StepParams& p, int warps_per_world, cudaStream_t s);
 size_t step_smem_bytes(const SceneDev& sc, int warps_per_world);
-size_t step_smem_bytes_det(const SceneDev& sc);
 
 // S0
 cudaError_t launch_offsets_sorted(const int32_t* world, int64_t n, int64_t n_worlds, int64_t* off,

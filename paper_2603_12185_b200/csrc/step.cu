@@ -7,16 +7,12 @@ cudaError_t launch_step_w1(const StepParams& p, cudaStream_t s);
 cudaError_t launch_step_w2(const StepParams& p, cudaStream_t s);
 cudaError_t launch_step_w4(const StepParams& p, cudaStream_t s);
 cudaError_t launch_step_w8(const StepParams& p, cudaStream_t s);
-cudaError_t launch_step_det(const StepParams& p, cudaStream_t s);
 
 size_t step_smem_bytes(const SceneDev& sc, int wpw) {
   return (size_t)(kWarps / wpw) * group_layout(sc).total * sizeof(float);
 }
 
-size_t step_smem_bytes_det(const SceneDev& sc) { return (size_t)group_layout(sc).total * sizeof(float); }
-
 cudaError_t launch_step(const StepParams& p, int wpw, cudaStream_t s) {
-  if (p.deterministic) return launch_step_det(p, s);
   switch (wpw) {
     case 1: return launch_step_w1(p, s);
     case 2: return launch_step_w2(p, s);

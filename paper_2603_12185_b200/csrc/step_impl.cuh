@@ -40,25 +40,21 @@ static constexpr int kWarps = 8;
 static constexpr int kThreads = kWarps * 32;
 
 struct GroupLayout {  // float offsets inside one group's shared-memory window
-  int rec, quat, acc0, acc1, tq, tL, tacc, red, total;
+  int rec, accl, acch, tq, tL, tacl, tach, red, total;
 };
 
 __host__ __device__ inline GroupLayout group_layout(const SceneDev& sc) {
   GroupLayout L;
   int o = 0;
   L.rec = o;  o += 16 * sc.Bp;   // float4 rec[4][Bp]: (v_s,im) (w_s,Ixx) (x,Iyy) (Izz,Ixy,Ixz,Iyz)
-#if !defined(CF_QUAT_GLOBAL)
-  L.quat = o; o += 4 * sc.Bp;    // float4 quat[Bp] (step-start orientation)
-#else
-  L.quat = 0;
-#endif
-  L.acc0 = o; o += 4 * sc.Bp;    // float4 p[Bp] = (p_lin.xyz, p_ang.x)
-  L.acc1 = o; o += 2 * sc.Bp;    // float2 p[Bp] = (p_ang.y, p_ang.z)
+  L.accl = o; o += 6 * sc.Bp;    // uint32 lo[6][Bp] \ generalized impulse p (lin, ang) as 64-bit
+  L.acch = o; o += 6 * sc.Bp;    // int32  hi[6][Bp] /  fixed point, per-body scale
   o = (o + 3) & ~3;
   L.tq = o;   o += 4 * sc.T;     // float4 qd_s[T]
-  L.tL = o;   o += 16 * sc.T;    // float L[T][16]: 10 packed entries + 4 reciprocal diagonals
-  L.tacc = o; o += 4 * sc.T;     // float p_chain[T][4]
-  L.red = o;  o += 16;           // reductions
+  L.tL = o;   o += 16 * sc.T;    // float L[T][16]: 10 packed, 4 reciprocal diagonals, scale, -
+  L.tacl = o; o += 4 * sc.T;     // uint32 chain impulse lo[T][4]
+  L.tach = o; o += 4 * sc.T;     // int32  chain impulse hi[T][4]
+  L.red = o;  o += 16;           // reductions / contact range
   L.total = (o + 3) & ~3;
   return L;
 }
@@ -226,27 +222,30 @@ __device__ __forceinline__ bool seg_sum6(int key, float v[6], int lane) {
   return tail;
 }
 
-// Shared-memory float accumulation by 128-bit / 64-bit compare-and-swap
-// (sm_100a has no native shared-memory float add; one CAS covers 4 / 2 floats).
-__device__ __forceinline__ void smem_add4(float4* p, float a, float b, float c, float d) {
-  unsigned __int128* q = reinterpret_cast<unsigned __int128*>(p);
-  unsigned __int128 old = *q, assumed;
-  do {
-    assumed = old;
-    float4 f = *reinterpret_cast<const float4*>(&assumed);
-    f.x += a; f.y += b; f.z += c; f.w += d;
-    old = atomicCAS(q, assumed, *reinterpret_cast<const unsigned __int128*>(&f));
-  } while (old != assumed);
+// ---- S6 accumulation: 64-bit fixed point in shared memory ----------------
+// sm_100a has no native shared-memory fp32 add (atomicAdd compiles to a CAS
+// loop), but native 32-bit integer atomics.  Each accumulator is a 64-bit
+// two's-complement integer split in lo (uint32) and hi (int32) planes; a value
+// is added as round(v * 2^e) with an explicit carry from the lo word.  Integer
+// addition is associative, so the result does not depend on the order in which
+// warps arrive: the step is bitwise deterministic.  The scale 2^e is per body
+// and per component group: e = exponent(m^-1) + 33 for the linear part,
+// exponent(max diag I_w^-1) + 33 for the angular part, i.e. a velocity
+// resolution of about 2^-33 (1.2e-10) with a range of about 2^30 in velocity.
+__device__ __forceinline__ int fx_exp(float inv) {
+  const int e = inv > 0.f ? ((__float_as_int(inv) >> 23) & 0xff) - 127 : 0;
+  return max(-90, min(90, e + 33));
 }
-__device__ __forceinline__ void smem_add2(float2* p, float a, float b) {
-  unsigned long long* q = reinterpret_cast<unsigned long long*>(p);
-  unsigned long long old = *q, assumed;
-  do {
-    assumed = old;
-    float2 f = *reinterpret_cast<const float2*>(&assumed);
-    f.x += a; f.y += b;
-    old = atomicCAS(q, assumed, *reinterpret_cast<const unsigned long long*>(&f));
-  } while (old != assumed);
+__device__ __forceinline__ float fx_pow2(int e) { return __int_as_float((e + 127) << 23); }
+__device__ __forceinline__ void fx_add(unsigned* lo, int* hi, float v, float scale) {
+  const long long x = __float2ll_rn(v * scale);
+  const unsigned xl = (unsigned)x;
+  const unsigned old = atomicAdd(lo, xl);
+  atomicAdd(hi, (int)(x >> 32) + (int)((unsigned)(old + xl) < xl));
+}
+__device__ __forceinline__ float fx_get(unsigned lo, int hi, float inv_scale) {
+  const long long x = (long long)(((unsigned long long)(unsigned)hi << 32) | (unsigned long long)lo);
+  return __ll2float_rn(x) * inv_scale;
 }
 
 // S0 fused into the step for sorted input: one warp finds the first index with
@@ -314,63 +313,22 @@ __device__ __forceinline__ void lower_bound2(const int32_t* a, int64_t n, int64_
   r1 = lo1 + __popc(__ballot_sync(full, q1));
 }
 
-// Run aggregation and shared-memory CAS for both sides of a contact: side a's
-// first 128-bit and 64-bit CAS are issued, side b is aggregated and added
-// while they are in flight, and side a retries only if it lost a race.
-__device__ __forceinline__ void scatter_cas(float4* acc0, float2* acc1, int ka, float va[6], int kb, float vb[6],
-                                            int lane) {
-  typedef unsigned __int128 u128;
-  typedef unsigned long long u64;
-  const bool ta = seg_sum6(ka, va, lane) && ka >= 0;
-  u128* pa4 = reinterpret_cast<u128*>(acc0 + (ta ? ka : 0));
-  u64* pa2 = reinterpret_cast<u64*>(acc1 + (ta ? ka : 0));
-  u128 oa4 = 0, ra4 = 0;
-  u64 oa2 = 0, ra2 = 0;
-  if (ta) {
-    oa4 = *pa4;
-    oa2 = *pa2;
-    float4 g = *reinterpret_cast<const float4*>(&oa4);
-    g.x += va[0]; g.y += va[1]; g.z += va[2]; g.w += va[3];
-    float2 h = *reinterpret_cast<const float2*>(&oa2);
-    h.x += va[4]; h.y += va[5];
-    ra4 = atomicCAS(pa4, oa4, *reinterpret_cast<const u128*>(&g));
-    ra2 = atomicCAS(pa2, oa2, *reinterpret_cast<const u64*>(&h));
-  }
-  const bool tb = seg_sum6(kb, vb, lane) && kb >= 0;
-  if (tb) {
-    smem_add4(&acc0[kb], vb[0], vb[1], vb[2], vb[3]);
-    smem_add2(&acc1[kb], vb[4], vb[5]);
-  }
-  if (ta && (ra4 != oa4 || ra2 != oa2)) {  // lost a race: redo the missing part
-    if (ra4 != oa4) smem_add4(&acc0[ka], va[0], va[1], va[2], va[3]);
-    if (ra2 != oa2) smem_add2(&acc1[ka], va[4], va[5]);
+// S6 for one side: run aggregation inside the warp, then the run's last lane
+// adds its total (6 values) to the body's fixed-point accumulators.
+__device__ __forceinline__ void scatter_side(unsigned* accl, int* acch, const float4* rec, int Bp, int key, float v[6],
+                                             int lane) {
+  const bool tail = seg_sum6(key, v, lane) && key >= 0;
+  if (tail) {
+    const float* r = reinterpret_cast<const float*>(rec);
+    const float im = r[4 * key + 3];
+    const float dmax = fmaxf(fmaxf(r[4 * (Bp + key) + 3], r[4 * (2 * Bp + key) + 3]), r[4 * (3 * Bp + key)]);
+    const float sl = fx_pow2(fx_exp(im)), sa = fx_pow2(fx_exp(dmax));
+#pragma unroll
+    for (int q = 0; q < 6; ++q) fx_add(accl + q * Bp + key, acch + q * Bp + key, v[q], q < 3 ? sl : sa);
   }
 }
 
-// Deterministic mode (one warp owns the world, so plain read-modify-writes
-// suffice): run totals are applied lane by lane in increasing lane order among
-// lanes with the same body, lanes with different bodies together.
-__device__ __forceinline__ void det_apply(float4* acc0, float2* acc1, bool t, int k, const float v[6], int lane) {
-  const unsigned full = 0xffffffffu;
-  unsigned pend = __ballot_sync(full, t);
-  while (pend) {
-    const unsigned same = __match_any_sync(full, t ? k : -1 - lane);
-    const bool leader = t && ((same & pend & ((1u << lane) - 1u)) == 0u);
-    if (leader) {
-      float4 a = acc0[k];
-      a.x += v[0]; a.y += v[1]; a.z += v[2]; a.w += v[3];
-      acc0[k] = a;
-      float2 b = acc1[k];
-      b.x += v[4]; b.y += v[5];
-      acc1[k] = b;
-      t = false;
-    }
-    __syncwarp();
-    pend = __ballot_sync(full, t);
-  }
-}
-
-template <int CW, int WPW, bool FAST, bool TREES, bool IMP, bool DET>
+template <int CW, int WPW, bool FAST, bool TREES, bool IMP>
 __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 2 : (CW == 32 ? 1 : 16))) k_step(const __grid_constant__ StepParams P) {
   extern __shared__ float4 smem4[];
   float* smem = reinterpret_cast<float*>(smem4);
@@ -386,12 +344,12 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
 
   float* G = smem + (size_t)group * GL.total;
   float4* rec = reinterpret_cast<float4*>(G + GL.rec);
-  float4* quat_s = reinterpret_cast<float4*>(G + GL.quat);
-  float4* acc0 = reinterpret_cast<float4*>(G + GL.acc0);
-  float2* acc1 = reinterpret_cast<float2*>(G + GL.acc1);
+  unsigned* accl = reinterpret_cast<unsigned*>(G + GL.accl);
+  int* acch = reinterpret_cast<int*>(G + GL.acch);
   float4* tq = reinterpret_cast<float4*>(G + GL.tq);
   float* tL = G + GL.tL;
-  float* tacc = G + GL.tacc;
+  unsigned* tacl = reinterpret_cast<unsigned*>(G + GL.tacl);
+  int* tach = reinterpret_cast<int*>(G + GL.tach);
   float* red = G + GL.red;
   const int B = sc.B, Bp = sc.Bp, T = sc.T, nd = sc.nd;
   float* slab = P.slab + (size_t)w * sc.slab;
@@ -473,11 +431,8 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
     rec[Bp + i] = make_float4(ws.x, ws.y, ws.z, Ixx);
     rec[2 * Bp + i] = make_float4(x.x, x.y, x.z, Iyy);
     rec[3 * Bp + i] = make_float4(Izz, Ixy, Ixz, Iyz);
-#if !defined(CF_QUAT_GLOBAL)
-    quat_s[i] = q;
-#endif
-    acc0[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-    acc1[i] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int q6 = 0; q6 < 6; ++q6) { accl[q6 * Bp + i] = 0u; acch[q6 * Bp + i] = 0; }
   }
   if (TREES) {
     for (int t = gt; t < T; t += kGT) {
@@ -485,8 +440,13 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
       float* Ls = tL + 16 * t;
 #pragma unroll
       for (int k = 0; k < 10; ++k) Ls[k] = Lg[k];
+      float dmax = 0.f;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) Ls[10 + k] = k < nd ? 1.0f / Lg[tri(k, k)] : 0.f;
+      for (int k = 0; k < 4; ++k) {
+        Ls[10 + k] = k < nd ? 1.0f / Lg[tri(k, k)] : 0.f;
+        dmax = fmaxf(dmax, Ls[10 + k] * Ls[10 + k]);
+      }
+      Ls[14] = __int_as_float(fx_exp(dmax));  // fixed-point exponent of this chain's impulses
       float x[4] = {0.f, 0.f, 0.f, 0.f}, qd[4] = {0.f, 0.f, 0.f, 0.f};
       const float* qv = slab + N_BODY_PLANES * Bp + sc.Qp + t * nd;
       const float* tau = P.tree_tau + (size_t)w * sc.Q + t * nd;
@@ -494,7 +454,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
       chol_solve(Ls, nd, x);
       tq[t] = make_float4(qd[0] + x[0] * dt, qd[1] + x[1] * dt, qd[2] + x[2] * dt, qd[3] + x[3] * dt);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) tacc[4 * t + k] = 0.f;
+      for (int k = 0; k < 4; ++k) { tacl[4 * t + k] = 0u; tach[4 * t + k] = 0; }
     }
   }
   if (gt < 8) red[gt] = 0.f;
@@ -657,24 +617,15 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
                       fn * n.z + ft1 * t1.z + ft2 * t2.z);
       if (!valid) f = make_float3(0.f, 0.f, 0.f);
     }
-    // S6: scatter J^T (f, tau).  Free bodies get (f, r x f + tau) per side: the
-    // warp sums runs of equal body ids (contacts sorted by body pair make them
-    // long), then each run's last lane adds its run total with one 128-bit and
-    // one 64-bit shared-memory CAS.
-    if (DET) {
+    // S6: scatter J^T (f, tau).  Free bodies get (f, r x f + tau) per side:
+    // the warp sums runs of equal body ids (contacts sorted by body pair make
+    // them long), then each run's last lane adds the total in fixed point.
+    {
       const float3 ma = cross3(ra, f), mb = cross3(rb, f);
       float va[6] = {-f.x, -f.y, -f.z, -(ma.x + tau.x), -(ma.y + tau.y), -(ma.z + tau.z)};
+      scatter_side(accl, acch, rec, Bp, ida >= 0 ? ida : -1, va, lane);
       float vb[6] = {f.x, f.y, f.z, mb.x + tau.x, mb.y + tau.y, mb.z + tau.z};
-      const int ka = ida >= 0 ? ida : -1, kb = idb >= 0 ? idb : -1;
-      const bool ta = seg_sum6(ka, va, lane) && ka >= 0;
-      det_apply(acc0, acc1, ta, ka, va, lane);
-      const bool tb = seg_sum6(kb, vb, lane) && kb >= 0;
-      det_apply(acc0, acc1, tb, kb, vb, lane);
-    } else {
-      const float3 ma = cross3(ra, f), mb = cross3(rb, f);
-      float va[6] = {-f.x, -f.y, -f.z, -(ma.x + tau.x), -(ma.y + tau.y), -(ma.z + tau.z)};
-      float vb[6] = {f.x, f.y, f.z, mb.x + tau.x, mb.y + tau.y, mb.z + tau.z};
-      scatter_cas(acc0, acc1, ida >= 0 ? ida : -1, va, idb >= 0 ? idb : -1, vb, lane);
+      scatter_side(accl, acch, rec, Bp, idb >= 0 ? idb : -1, vb, lane);
     }
     if (TREES) {
 #pragma unroll
@@ -696,15 +647,8 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
             s4.w += jl.w * fv[kk] + ja.w * tv[kk];
           }
           const float sv[4] = {s4.x, s4.y, s4.z, s4.w};
-          if (!DET) {
-            for (int jj = 0; jj < nd; ++jj) atomicAdd(&tacc[4 * t + jj], sg * sv[jj]);
-          } else {  // lane order (one warp owns the world)
-            for (int l = 0; l < 32; ++l) {
-              if (l == lane)
-                for (int jj = 0; jj < nd; ++jj) tacc[4 * t + jj] += sg * sv[jj];
-              __syncwarp(__activemask());
-            }
-          }
+          const float scl = fx_pow2(__float_as_int(tL[16 * t + 14]));
+          for (int jj = 0; jj < nd; ++jj) fx_add(tacl + 4 * t + jj, tach + 4 * t + jj, sg * sv[jj], scl);
         }
       }
     }
@@ -716,15 +660,21 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
   bool nonfinite = false;
   for (int i = gt; i < B; i += kGT) {
     const float4 r0 = rec[i], r1 = rec[Bp + i], r2 = rec[2 * Bp + i], r3 = rec[3 * Bp + i];
-#if !defined(CF_QUAT_GLOBAL)
-    const float4 q = quat_s[i];
-#else
     const float4 q = make_float4(slab[3 * Bp + i], slab[4 * Bp + i], slab[5 * Bp + i], slab[6 * Bp + i]);
-#endif
-    const float4 a0 = acc0[i];
-    const float2 a1 = acc1[i];
     const float im = r0.w;
     const float Ixx = r1.w, Iyy = r2.w, Izz = r3.x, Ixy = r3.y, Ixz = r3.z, Iyz = r3.w;
+    const float isl = fx_pow2(-fx_exp(im)), isa = fx_pow2(-fx_exp(fmaxf(fmaxf(Ixx, Iyy), Izz)));
+    int hi[6];
+    unsigned range = 0u;
+#pragma unroll
+    for (int q6 = 0; q6 < 6; ++q6) {
+      hi[q6] = acch[q6 * Bp + i];
+      range |= (unsigned)hi[q6] + (1u << 30);  // bit 31 set: |sum| >= 2^62, fixed-point range exceeded
+    }
+    if (P.check_finite) nonfinite |= (range >> 31) != 0u;
+    const float4 a0 = make_float4(fx_get(accl[i], hi[0], isl), fx_get(accl[Bp + i], hi[1], isl),
+                                  fx_get(accl[2 * Bp + i], hi[2], isl), fx_get(accl[3 * Bp + i], hi[3], isa));
+    const float2 a1 = make_float2(fx_get(accl[4 * Bp + i], hi[4], isa), fx_get(accl[5 * Bp + i], hi[5], isa));
     const float3 v = make_float3(r0.x + im * a0.x, r0.y + im * a0.y, r0.z + im * a0.z);
     const float3 om = make_float3(r1.x + Ixx * a0.w + Ixy * a1.x + Ixz * a1.y,
                                   r1.y + Ixy * a0.w + Iyy * a1.x + Iyz * a1.y,
@@ -775,8 +725,11 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
   }
   if (TREES) {
     for (int t = gt; t < T; t += kGT) {
-      float x[4] = {tacc[4 * t], tacc[4 * t + 1], tacc[4 * t + 2], tacc[4 * t + 3]};
       const float* Ls = tL + 16 * t;
+      const float isc = fx_pow2(-__float_as_int(Ls[14]));
+      float x[4];
+#pragma unroll
+      for (int k4 = 0; k4 < 4; ++k4) x[k4] = fx_get(tacl[4 * t + k4], tach[4 * t + k4], isc);
       chol_solve(Ls, nd, x);
       const float4 qs = tq[t];
       const float qsv[4] = {qs.x, qs.y, qs.z, qs.w};
@@ -809,10 +762,10 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
       max_pen = fmaxf(max_pen, __shfl_xor_sync(0xffffffffu, max_pen, o));
       ke += __shfl_xor_sync(0xffffffffu, ke, o);
     }
-    if (lane == 0) {
+    if (lane == 0) {  // integer counters are order-free; energy is summed in warp order below
       atomicAdd(reinterpret_cast<int*>(&red[0]), n_active);
       atomicMax(reinterpret_cast<int*>(&red[1]), __float_as_int(fmaxf(max_pen, 0.f)));
-      atomicAdd(&red[2], ke);
+      red[8 + (gt >> 5)] = ke;
     }
     group_sync<WPW, CW>(group);
     if (gt == 0) {
@@ -820,43 +773,43 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
       ws.contacts = nloc;
       ws.active_facets = *reinterpret_cast<int*>(&red[0]);
       ws.max_penetration = __int_as_float(*reinterpret_cast<int*>(&red[1]));
-      ws.kinetic_energy = red[2];
+      float kes = 0.f;
+      for (int q8 = 0; q8 < WPW; ++q8) kes += red[8 + q8];
+      ws.kinetic_energy = kes;
       P.wstats[w] = ws;
     }
   }
 }
 
-template <int CW, int WPW, bool FAST, bool TREES, bool IMP, bool DET>
+template <int CW, int WPW, bool FAST, bool TREES, bool IMP>
 cudaError_t launch_variant(const StepParams& p, cudaStream_t s) {
   const int groups = CW / WPW;
   const size_t smem = (size_t)groups * group_layout(p.sc).total * sizeof(float);
   const unsigned grid = (unsigned)((p.n_worlds + groups - 1) / groups);
   if (grid == 0) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(k_step<CW, WPW, FAST, TREES, IMP, DET>,
+  cudaError_t e = cudaFuncSetAttribute(k_step<CW, WPW, FAST, TREES, IMP>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_step<CW, WPW, FAST, TREES, IMP, DET><<<grid, CW * 32, smem, s>>>(p);
+  k_step<CW, WPW, FAST, TREES, IMP><<<grid, CW * 32, smem, s>>>(p);
   return cudaGetLastError();
 }
 
 // FAST = the 4-facet tangential cone with the default power p = 2 (dense piles);
 // every other configuration takes the general facet loop and __powf.
-template <int CW, int WPW, bool DET>
+template <int CW, int WPW>
 cudaError_t launch_cfg(const StepParams& p, cudaStream_t s) {
   const bool trees = p.sc.T > 0, imp = p.impulses != nullptr;
   if (p.n_t == 4 && p.power_is_2) {
-    if (trees) return imp ? launch_variant<CW, WPW, true, true, true, DET>(p, s)
-                          : launch_variant<CW, WPW, true, true, false, DET>(p, s);
-    return imp ? launch_variant<CW, WPW, true, false, true, DET>(p, s) : launch_variant<CW, WPW, true, false, false, DET>(p, s);
+    if (trees) return imp ? launch_variant<CW, WPW, true, true, true>(p, s) : launch_variant<CW, WPW, true, true, false>(p, s);
+    return imp ? launch_variant<CW, WPW, true, false, true>(p, s) : launch_variant<CW, WPW, true, false, false>(p, s);
   }
-  if (trees) return imp ? launch_variant<CW, WPW, false, true, true, DET>(p, s)
-                        : launch_variant<CW, WPW, false, true, false, DET>(p, s);
-  return imp ? launch_variant<CW, WPW, false, false, true, DET>(p, s) : launch_variant<CW, WPW, false, false, false, DET>(p, s);
+  if (trees) return imp ? launch_variant<CW, WPW, false, true, true>(p, s) : launch_variant<CW, WPW, false, true, false>(p, s);
+  return imp ? launch_variant<CW, WPW, false, false, true>(p, s) : launch_variant<CW, WPW, false, false, false>(p, s);
 }
 
 template <int WPW>
 cudaError_t launch_wpw(const StepParams& p, cudaStream_t s) {
-  return launch_cfg<kWarps, WPW, false>(p, s);
+  return launch_cfg<kWarps, WPW>(p, s);
 }
 
 }  // namespace cf
