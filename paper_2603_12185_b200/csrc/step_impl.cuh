@@ -40,7 +40,7 @@ static constexpr int kWarps = 8;
 static constexpr int kThreads = kWarps * 32;
 
 struct GroupLayout {  // float offsets inside one group's shared-memory window
-  int rec, accl, acch, tq, tL, tacl, tach, red, total;
+  int rec, accl, acch, tq, tqp, tL, tacl, tach, red, total;
 };
 
 __host__ __device__ inline GroupLayout group_layout(const SceneDev& sc) {
@@ -51,6 +51,7 @@ __host__ __device__ inline GroupLayout group_layout(const SceneDev& sc) {
   L.acch = o; o += 6 * sc.Bp;    // int32  hi[6][Bp] /  fixed point, per-body scale
   o = (o + 3) & ~3;
   L.tq = o;   o += 4 * sc.T;     // float4 qd_s[T]
+  L.tqp = o;  o += 4 * sc.T;     // float4 q[T] (step-start chain positions, read in S1)
   L.tL = o;   o += 16 * sc.T;    // float L[T][16]: 10 packed, 4 reciprocal diagonals, scale, -
   L.tacl = o; o += 4 * sc.T;     // uint32 chain impulse lo[T][4]
   L.tach = o; o += 4 * sc.T;     // int32  chain impulse hi[T][4]
@@ -347,6 +348,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
   unsigned* accl = reinterpret_cast<unsigned*>(G + GL.accl);
   int* acch = reinterpret_cast<int*>(G + GL.acch);
   float4* tq = reinterpret_cast<float4*>(G + GL.tq);
+  float4* tqp = reinterpret_cast<float4*>(G + GL.tqp);
   float* tL = G + GL.tL;
   unsigned* tacl = reinterpret_cast<unsigned*>(G + GL.tacl);
   int* tach = reinterpret_cast<int*>(G + GL.tach);
@@ -450,7 +452,11 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
       float x[4] = {0.f, 0.f, 0.f, 0.f}, qd[4] = {0.f, 0.f, 0.f, 0.f};
       const float* qv = slab + N_BODY_PLANES * Bp + sc.Qp + t * nd;
       const float* tau = P.tree_tau + (size_t)w * sc.Q + t * nd;
-      for (int j = 0; j < nd; ++j) { x[j] = tau[j]; qd[j] = qv[j]; }
+      float qq[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (j < nd) { x[j] = tau[j]; qd[j] = qv[j]; qq[j] = qv[j - sc.Qp]; }
+      tqp[t] = make_float4(qq[0], qq[1], qq[2], qq[3]);
       chol_solve(Ls, nd, x);
       tq[t] = make_float4(qd[0] + x[0] * dt, qd[1] + x[1] * dt, qd[2] + x[2] * dt, qd[3] + x[3] * dt);
 #pragma unroll
@@ -648,7 +654,9 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
           }
           const float sv[4] = {s4.x, s4.y, s4.z, s4.w};
           const float scl = fx_pow2(__float_as_int(tL[16 * t + 14]));
-          for (int jj = 0; jj < nd; ++jj) fx_add(tacl + 4 * t + jj, tach + 4 * t + jj, sg * sv[jj], scl);
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj)
+            if (jj < nd) fx_add(tacl + 4 * t + jj, tach + 4 * t + jj, sg * sv[jj], scl);
         }
       }
     }
@@ -731,22 +739,28 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
 #pragma unroll
       for (int k4 = 0; k4 < 4; ++k4) x[k4] = fx_get(tacl[4 * t + k4], tach[4 * t + k4], isc);
       chol_solve(Ls, nd, x);
-      const float4 qs = tq[t];
-      const float qsv[4] = {qs.x, qs.y, qs.z, qs.w};
+      const float4 qs = tq[t], q0 = tqp[t];
+      const float qsv[4] = {qs.x, qs.y, qs.z, qs.w}, q0v[4] = {q0.x, q0.y, q0.z, q0.w};
       float* qp = slab + N_BODY_PLANES * Bp + t * nd;
       float* qv = slab + N_BODY_PLANES * Bp + sc.Qp + t * nd;
       float qdn[4] = {0.f, 0.f, 0.f, 0.f};
-      for (int j = 0; j < nd; ++j) {
-        qdn[j] = qsv[j] + x[j];
-        qv[j] = qdn[j];
-        qp[j] = qp[j] + qdn[j] * dt;
-        if (P.check_finite) nonfinite |= !isfinite(qp[j] + qdn[j]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (j < nd) {
+          qdn[j] = qsv[j] + x[j];
+          qv[j] = qdn[j];
+          const float qn = q0v[j] + qdn[j] * dt;
+          qp[j] = qn;
+          if (P.check_finite) nonfinite |= !isfinite(qn + qdn[j]);
+        }
       }
       if (stats) {  // 1/2 qd^T L L^T qd
-        for (int i2 = 0; i2 < nd; ++i2) {
+#pragma unroll
+        for (int i2 = 0; i2 < 4; ++i2) {
           float y = 0.f;
-          for (int j = i2; j < nd; ++j) y += Ls[tri(j, i2)] * qdn[j];
-          ke += 0.5f * y * y;
+#pragma unroll
+          for (int j = i2; j < 4; ++j) y += j < nd ? Ls[tri(j, i2)] * qdn[j] : 0.f;
+          ke += i2 < nd ? 0.5f * y * y : 0.f;
         }
       }
     }

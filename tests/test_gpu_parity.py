@@ -195,6 +195,23 @@ def test_nonfinite_state_reported_with_world():
     assert ei.value.status == 4 and "world 2" in str(ei.value)
 
 
+def test_fixed_point_range_exceeded_is_reported():
+    """S6 accumulates in 64-bit fixed point (~2^28 m/s of velocity change per
+    step, include/comfree.h): an impulse beyond that range is reported as
+    COMFREE_ERR_NONFINITE for its world instead of wrapping silently."""
+    import paper_2603_12185_b200 as cf
+    scene, st, c = scenes.c4_pile(n_worlds=4, contacts_per_world=50)
+    i = int(np.nonzero((c.world == 1) & (c.body_b >= 0))[0][0])
+    b = int(c.body_b[i])
+    st.vel[1, b] = -1e12 * c.c1[i, :3]          # approach along the normal at 1e12 m/s
+    ctx = cf.Context(CFG)
+    ctx.load_scene(scene, 4, st)
+    ctx.step(cf.DeviceContacts.from_host(c), None)
+    with pytest.raises(cf.ComfreeError) as ei:
+        ctx.get_state()
+    assert ei.value.status == 4 and "world 1" in str(ei.value)
+
+
 def test_invalid_body_id_and_unsorted_lie_are_validation_errors():
     import paper_2603_12185_b200 as cf
     scene, st, c = scenes.c4_pile(n_worlds=3, contacts_per_world=40)
