@@ -10,6 +10,11 @@ and L2 is additionally flushed between timed steps.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
     torchrun --nproc-per-node N bench.py --gpus N   (weak scaling: 1024 worlds per GPU)
+
+Other workloads (reported, not the BASELINE metric): --workload hand (config 3,
+4096 worlds per GPU) and --workload mixed (config 5: 65536 worlds in total,
+half hand / half pile-lite, sharded over the GPUs -- strong scaling; the two
+world kinds are two library contexts stepped concurrently on two streams).
 """
 from __future__ import annotations
 
@@ -45,12 +50,17 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to exercise the multi-rank path on a single GPU")
-    ap.add_argument("--workload", default="pile", choices=["pile", "hand"],
-                    help="pile: config 4 (the BASELINE metric); hand: config 3")
+    ap.add_argument("--workload", default="pile", choices=["pile", "hand", "mixed"],
+                    help="pile: config 4 (the BASELINE metric); hand: config 3; mixed: config 5")
     a = ap.parse_args()
     if a.worlds is None:
-        a.worlds = 4096 if a.workload == "hand" else 1024
+        a.worlds = {"hand": 4096, "mixed": 65536}.get(a.workload, 1024)
     return a
+
+
+METRICS = {"pile": METRIC,
+           "hand": "world-steps/s (LEAP-like hand + cube, 4096 worlds per GPU)",
+           "mixed": "world-steps/s (mixed hand + pile-lite, 65536 worlds in total)"}
 
 
 def dist_env():
@@ -129,100 +139,129 @@ def ncu_traffic():
         return None
 
 
+# ---------------------------------------------------------------- workloads
+class Part:
+    """One homogeneous batch of worlds (one library context)."""
+
+    def __init__(self, name, scene, st, c, inp, alg_bytes):
+        self.name, self.scene, self.st, self.c, self.inp, self.alg_bytes = name, scene, st, c, inp, alg_bytes
+        self.W = st.n_worlds
+
+
+def _hand_bytes(scene, c, W):
+    n_rows = int(np.count_nonzero(c.body_a < -1) + np.count_nonzero(c.body_b < -1))
+    Q = scene.n_tree_dofs
+    return (c.n * BYTES_PER_CONTACT + n_rows * 96 + W * scene.n_bodies * BYTES_PER_BODY
+            + W * (Q * 16 + scene.n_trees * 40 + Q * 4))
+
+
+def workload(args, rank, world_size):
+    """(parts, workload name, worlds per rank) -- parts are homogeneous batches."""
+    from harness import scenes
+    if args.workload == "hand":
+        W = args.worlds
+        scene, st, c, inp = scenes.c3_hand(n_worlds=W, world_offset=rank * W)
+        return [Part("hand", scene, st, c, inp, _hand_bytes(scene, c, W))], \
+            "c3 LEAP-like hand + cube (4x4-DoF chains + free cube)", W
+    if args.workload == "mixed":
+        n = args.worlds // world_size                # strong scaling: the total is fixed
+        d = scenes.c5_mixed(n_worlds=n, world_offset=rank * n)
+        sh, sth, ch, ih = d["hand"]
+        sp, stp, cp = d["pile"]
+        parts = [Part("pile-lite", sp, stp, cp, None,
+                      cp.n * BYTES_PER_CONTACT + stp.n_worlds * sp.n_bodies * BYTES_PER_BODY),
+                 Part("hand", sh, sth, ch, ih, _hand_bytes(sh, ch, sth.n_worlds))]
+        return parts, "c5 mixed: half c3 hand, half pile-lite (100 bodies, 400 contacts)", n
+    W = args.worlds
+    scene, st, c = scenes.c4_pile(n_worlds=W, contacts_per_world=args.contacts, world_offset=rank * W)
+    return [Part("pile", scene, st, c, None, W * (args.contacts * BYTES_PER_CONTACT + scene.n_bodies * BYTES_PER_BODY))], \
+        "c4 dense pile", W
+
+
 # ---------------------------------------------------------------- oracle (CPU) timing
-def cpu_oracle_rate(scene, st, contacts, cfg, seconds: float, max_worlds: int, inputs=None):
-    """The fp64 oracle as it stands, OpenMP across worlds on all host cores,
-    repeated steps over a bounded sample of the workload's worlds."""
-    import oracle
-    W = min(max_worlds, st.n_worlds)
-    sel = np.nonzero(contacts.world < W)[0]
-    c = contacts.take(sel)
-    s = st.world_slice(0, W)
+def _sample(part, max_worlds):
+    from harness.types import Inputs
+    W = min(max_worlds, part.W)
+    c = part.c.take(np.nonzero(part.c.world < W)[0])
+    st = part.st.world_slice(0, W)
     inp = None
-    if inputs is not None:
-        from harness.types import Inputs
+    if part.inp is not None:
         inp = Inputs(*(None if a is None else np.ascontiguousarray(a[:W]) for a in
-                       (inputs.f_ext, inputs.tree_L, inputs.tree_tau)))
+                       (part.inp.f_ext, part.inp.tree_L, part.inp.tree_tau)))
+    return W, st, c, inp
+
+
+def cpu_oracle_rate(parts, cfg, seconds: float, max_worlds: int):
+    """The fp64 oracle as it stands, OpenMP across worlds on all host cores,
+    repeated steps over a bounded sample of each part's worlds."""
+    import oracle
     cores = os.cpu_count() or 1
-    oracle.step(cfg, scene, s, c, inp, n_threads=cores)   # warm
+    samples = [(p, _sample(p, max_worlds)) for p in parts]
+    for p, (W, st, c, inp) in samples:
+        oracle.step(cfg, p.scene, st, c, inp, n_threads=cores)   # warm
     n = 0
     t0 = time.perf_counter()
     while True:
-        oracle.step(cfg, scene, s, c, inp, n_threads=cores)
+        for p, (W, st, c, inp) in samples:
+            oracle.step(cfg, p.scene, st, c, inp, n_threads=cores)
         n += 1
         if time.perf_counter() - t0 >= seconds:
             break
     dt = time.perf_counter() - t0
-    return dict(value=n * W / dt, unit="world-steps/s", cores=cores, kind="oracle",
-                sample=f"{n} oracle steps x {W} worlds of the same workload ({c.n} contacts), fp64, "
+    Ws = sum(x[1][0] for x in samples)
+    nc = sum(x[1][2].n for x in samples)
+    return dict(value=n * Ws / dt, unit="world-steps/s", cores=cores, kind="oracle",
+                sample=f"{n} oracle steps x {Ws} worlds of the same workload ({nc} contacts), fp64, "
                        f"{dt:.1f} s, OpenMP over worlds")
 
 
 # ---------------------------------------------------------------- main arms
 def run_reference(args, rank, world_size):
-    from harness import scenes
+    """--impl reference: the fp64 oracle as it stands on the host cores, each
+    step a bounded sample of the same workload (rank 0 only)."""
     from harness.types import Config
     if rank != 0:
         return
-    cfg = Config()
-    W = args.worlds
-    scene, st, c = scenes.c4_pile(n_worlds=W, contacts_per_world=args.contacts)
     import oracle
+    cfg = Config()
+    parts, wname, n_local = workload(args, 0, world_size)
     cores = os.cpu_count() or 1
-    # each step: a bounded sample of the workload (64 worlds) so K steps finish in minutes
-    Ws = min(64, W)
-    sel = np.nonzero(c.world < Ws)[0]
-    cs = c.take(sel)
-    ss = st.world_slice(0, Ws)
+    Wcap = 64 if args.workload == "pile" else 256
+    samples = [(p, _sample(p, Wcap)) for p in parts]
+    states = [x[1][1] for x in samples]
+
+    def one():
+        for i, (p, (W, st, c, inp)) in enumerate(samples):
+            states[i] = oracle.step(cfg, p.scene, states[i], c, inp, n_threads=cores)["state"].astype(np.float32)
+
     for _ in range(args.warmup):
-        ss = oracle.step(cfg, scene, ss, cs, None, n_threads=cores)["state"].astype(np.float32)
+        one()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        ss = oracle.step(cfg, scene, ss, cs, None, n_threads=cores)["state"].astype(np.float32)
+        one()
     dt = time.perf_counter() - t0
+    Ws = sum(x[1][0] for x in samples)
     v = args.steps * Ws / dt
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "world-steps/s",
+    line = {"impl": "reference", "metric": METRICS[args.workload], "value": v, "unit": "world-steps/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "strong" if args.workload == "mixed" else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "c4 dense pile", "worlds_per_gpu": W, "contacts_per_world": args.contacts,
-                       "bodies_per_world": 500, "facets_per_contact": 4, "dt": cfg.dt,
-                       "sample_worlds_per_step": Ws},
+            "config": {"workload": wname, "worlds_per_gpu": n_local,
+                       "contacts_per_world": sum(p.c.n for p in parts) // max(n_local, 1),
+                       "facets_per_contact": 4, "dt": cfg.dt, "sample_worlds_per_step": Ws},
             "cpu_baseline": {"value": v, "unit": "world-steps/s", "cores": cores, "kind": "oracle",
-                             "sample": f"{args.steps} steps x {Ws} of {W} worlds, fp64 oracle, OpenMP over worlds"},
+                             "sample": f"{args.steps} steps x {Ws} of {n_local} worlds, fp64 oracle, OpenMP over worlds"},
             "e2e": {"value": v, "unit": "world-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def kernels_per_step(ctx, dc, tin, cfg):
-    """Kernels one direct step launches (instrumentation counter of the library)."""
-    n0 = ctx.kernel_launches
-    ctx.step(dc, tin, dt=cfg.dt)
-    import torch
-    torch.cuda.synchronize()
-    return ctx.kernel_launches - n0
-
-
-def workload(args, rank):
-    """(scene, state, contacts, inputs, name, algorithmic bytes per step per GPU)."""
-    from harness import scenes
-    W = args.worlds
-    if args.workload == "hand":
-        scene, st, c, inp = scenes.c3_hand(n_worlds=W, world_offset=rank * W)
-        n_rows = int(np.count_nonzero(c.body_a < -1) + np.count_nonzero(c.body_b < -1))
-        Q = scene.n_tree_dofs
-        alg = (c.n * BYTES_PER_CONTACT + n_rows * 96 + W * scene.n_bodies * BYTES_PER_BODY
-               + W * (Q * 16 + scene.n_trees * 40 + Q * 4))
-        return scene, st, c, inp, "c3 LEAP-like hand + cube (4x4-DoF chains + free cube)", alg
-    scene, st, c = scenes.c4_pile(n_worlds=W, contacts_per_world=args.contacts, world_offset=rank * W)
-    alg = W * (args.contacts * BYTES_PER_CONTACT + scene.n_bodies * BYTES_PER_BODY)
-    return scene, st, c, None, "c4 dense pile", alg
-
-
 def run_ours(args, rank, world_size, local):
+    import ctypes as ct
     import torch
     import torch.distributed as dist
     import paper_2603_12185_b200 as cf
+    from paper_2603_12185_b200 import _lib
     from paper_2603_12185_b200.dist import all_gather_worlds, reduce_max, uniform_ranges
     from harness.types import Config
 
@@ -235,35 +274,47 @@ def run_ours(args, rank, world_size, local):
         else:                              # plumbing check with several ranks on one GPU
             dist.init_process_group(args.dist_backend)
     cfg = Config()
-    W = args.worlds
-    scene, st, c, inp, wname, alg_bytes = workload(args, rank)
-    ctx = cf.Context(cfg, device=local)
-    ctx.load_scene(scene, W, st)
-    dc = cf.DeviceContacts.from_host(c, dev)
-    assert dc.sorted
-    tin = None
-    if inp is not None:
-        tin = type(inp)(*(None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(dev)
-                          for a in (inp.f_ext, inp.tree_L, inp.tree_tau)))
+    parts, wname, n_local = workload(args, rank, world_size)
     stream = torch.cuda.current_stream()
+    for i, p in enumerate(parts):
+        p.ctx = cf.Context(cfg, device=local)
+        p.ctx.load_scene(p.scene, p.W, p.st)
+        p.dc = cf.DeviceContacts.from_host(p.c, dev)
+        assert p.dc.sorted
+        p.tin = None
+        if p.inp is not None:
+            p.tin = type(p.inp)(*(None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+                                  for a in (p.inp.f_ext, p.inp.tree_L, p.inp.tree_tau)))
+        # part 0 on the caller's stream, the others on their own streams (fork / join)
+        p.stream = stream if i == 0 else torch.cuda.Stream(device=dev)
     flush = None if args.no_flush else torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
-    def one_step():
-        ctx.step(dc, tin, dt=cfg.dt, stream=stream)
+    def one_step(s0):
+        """One step of every part: part 0 on s0, the rest forked from s0 and joined back."""
+        for i, p in enumerate(parts):
+            if i == 0:
+                p.ctx.step(p.dc, p.tin, dt=cfg.dt, stream=s0)
+            else:
+                p.stream.wait_stream(s0)
+                p.ctx.step(p.dc, p.tin, dt=cfg.dt, stream=p.stream)
+        for p in parts[1:]:
+            s0.wait_stream(p.stream)
 
     for _ in range(max(args.warmup, 3)):
-        one_step()
+        one_step(stream)
     torch.cuda.synchronize()
-    # direct launches with the library's own event timing around the fused kernel
-    ctx.get_timing()
-    ctx.set_timing(True)
+    # direct launches with the library's own event timing around each fused kernel
+    for p in parts:
+        p.ctx.get_timing()
+        p.ctx.set_timing(True)
     for _ in range(min(args.steps, 20)):
         if flush is not None:
             flush.zero_()
-        one_step()
-    kt = ctx.get_timing()
-    ctx.set_timing(False)
-    k_ms_direct = kt["step_ms"] / max(kt["step_launches"], 1)
+        one_step(stream)
+    for p in parts:
+        p.kt = p.ctx.get_timing()
+        p.ctx.set_timing(False)
+        p.k_ms_direct = p.kt["step_ms"] / max(p.kt["step_launches"], 1)
     # one step captured in a CUDA graph (no host launch path inside the timed region)
     graph = None
     if not args.no_graph:
@@ -271,10 +322,10 @@ def run_ours(args, rank, world_size, local):
         side.wait_stream(stream)
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph, stream=side):
-            ctx.step(dc, tin, dt=cfg.dt, stream=side)
+            one_step(side)
         stream.wait_stream(side)
         torch.cuda.synchronize()
-    launches0 = ctx.kernel_launches
+    launches0 = sum(p.ctx.kernel_launches for p in parts)
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     if world_size > 1:
         dist.barrier()
@@ -288,7 +339,7 @@ def run_ours(args, rank, world_size, local):
             if graph is not None:
                 graph.replay()
             else:
-                one_step()
+                one_step(stream)
             evs[i][1].record(stream)
         torch.cuda.synchronize()
     if world_size > 1:
@@ -296,47 +347,64 @@ def run_ours(args, rank, world_size, local):
     torch.cuda.synchronize()
     step_ms = [a.elapsed_time(b) for a, b in evs]
     total_ms = float(sum(step_ms))
-    # kernels per step: one fused kernel (S0 fused for sorted ids); counted by the
-    # library for direct launches, the same for each graph replay
-    launches = (ctx.kernel_launches - launches0) if graph is None else args.steps * kernels_per_step(ctx, dc, tin, cfg)
+    # kernels per step: one fused kernel per part (S0 fused for sorted ids); counted
+    # by the library for direct launches, the same for each graph replay
+    if graph is None:
+        launches = sum(p.ctx.kernel_launches for p in parts) - launches0
+    else:
+        n0 = sum(p.ctx.kernel_launches for p in parts)
+        one_step(stream)
+        torch.cuda.synchronize()
+        launches = args.steps * (sum(p.ctx.kernel_launches for p in parts) - n0)
     total_ms = reduce_max(total_ms, dev)   # the job is as slow as its slowest rank
     ms_per_step = total_ms / args.steps
-    world_steps = W * world_size * args.steps
+    world_steps = n_local * world_size * args.steps
     value = world_steps / (total_ms * 1e-3)
-    contacts_per_s = value * (c.n / W)
+    n_contacts = sum(p.c.n for p in parts)
+    contacts_per_s = value * (n_contacts / n_local)
 
-    # roofline of the dominant kernel: with one kernel per step the per-step CUDA
-    # events around the graph replay bracket exactly that kernel
-    k_ms = (total_ms / args.steps) if graph is not None else k_ms_direct
+    # roofline of the dominant kernel (part 0: the pile / pile-lite k_step).  With
+    # one part and one kernel per step the per-step CUDA events around the graph
+    # replay bracket exactly that kernel; with several parts the kernel's own
+    # events (library timing, direct launches, parts running concurrently) are used.
+    dom = parts[0]
+    k_ms = (total_ms / args.steps) if (graph is not None and len(parts) == 1) else dom.k_ms_direct
     peak, peak_kind = peaks()
-    achieved = alg_bytes / (k_ms * 1e-3) / 1e9
+    achieved = dom.alg_bytes / (k_ms * 1e-3) / 1e9
     tr = ncu_traffic()
     traffic = None
-    if tr and tr.get("workload") == args.workload and tr.get("worlds") == W and \
-            tr.get("contacts_per_world") == c.n // W:
+    if tr and tr.get("workload") == args.workload and tr.get("worlds") == dom.W and \
+            tr.get("contacts_per_world") == dom.c.n // dom.W:
         traffic = tr.get("dram_bytes_per_launch")
 
     # after the timed region: final states all-gathered (NCCL) for verification
-    final = ctx.get_state()
-    finite = bool(np.isfinite(final["vel"]).all() and np.isfinite(final["pos"]).all())
+    finite = True
     gathered_mb = None
+    for p in parts:
+        p.final = p.ctx.get_state()
+        finite &= bool(np.isfinite(p.final["vel"]).all() and np.isfinite(p.final["pos"]).all())
     if world_size > 1:
-        ranges = uniform_ranges(W * world_size, world_size)
-        loc = {k: torch.from_numpy(final[k]).to(dev) for k in ("pos", "quat", "vel", "omega")}
-        full = all_gather_worlds(loc, ranges)
-        gathered_mb = sum(v.numel() * v.element_size() for v in full.values()) / 1e6
+        gathered_mb = 0.0
+        for p in parts:
+            ranges = uniform_ranges(p.W * world_size, world_size)
+            loc = {k: torch.from_numpy(p.final[k]).to(dev) for k in ("pos", "quat", "vel", "omega")}
+            full = all_gather_worlds(loc, ranges)
+            gathered_mb += sum(v.numel() * v.element_size() for v in full.values()) / 1e6
         finite = bool(reduce_max(0.0 if finite else 1.0, dev) == 0.0)
 
     # e2e: the same metric through the C ABI with HOST buffers (pinned), H2D of the
     # step's contacts and D2H of the resulting state inside the timed region
-    hc = cf.HostContacts.from_arrays(c, pin=True)
     e2e_steps = max(1, args.e2e_steps)
-    ctx.step(hc, inp, dt=cfg.dt)           # warm the staging buffers
-    out_host = {k: torch.empty(v.shape, dtype=torch.float32).pin_memory().numpy() for k, v in final.items()}
-    from paper_2603_12185_b200 import _lib
-    import ctypes as ct
-    st_h = _lib.comfree_state(*[out_host[k].ctypes.data if out_host[k].size else None
-                                for k in ("pos", "quat", "vel", "omega", "qpos", "qvel")], _lib.MEM_HOST)
+    h2d = d2h = 0
+    for p in parts:
+        p.hc = cf.HostContacts.from_arrays(p.c, pin=True)
+        p.ctx.step(p.hc, p.inp, dt=cfg.dt)           # warm the staging buffers
+        p.out_host = {k: torch.empty(v.shape, dtype=torch.float32).pin_memory().numpy() for k, v in p.final.items()}
+        p.st_h = _lib.comfree_state(*[p.out_host[k].ctypes.data if p.out_host[k].size else None
+                                      for k in ("pos", "quat", "vel", "omega", "qpos", "qvel")], _lib.MEM_HOST)
+        h2d += p.hc.h2d_bytes() + (0 if p.inp is None else sum(a.nbytes for a in (p.inp.f_ext, p.inp.tree_L, p.inp.tree_tau)
+                                                                if a is not None))
+        d2h += sum(v.nbytes for v in p.out_host.values())
     if world_size > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -344,43 +412,46 @@ def run_ours(args, rank, world_size, local):
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(e2e_steps):
-        ctx.step(hc, inp, dt=cfg.dt, stream=stream)
-        rc = ctx._lib.comfree_get_state(ctx.h, 0, W, ct.byref(st_h), stream.cuda_stream)
-        ctx._check(rc, "comfree_get_state")
+        for p in parts:
+            p.ctx.step(p.hc, p.inp, dt=cfg.dt, stream=stream)
+            rc = p.ctx._lib.comfree_get_state(p.ctx.h, 0, p.W, ct.byref(p.st_h), stream.cuda_stream)
+            p.ctx._check(rc, "comfree_get_state")
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = reduce_max(e0.elapsed_time(e1), dev)
-    e2e_value = W * world_size * e2e_steps / (e2e_ms * 1e-3)
-    h2d = hc.h2d_bytes() + (0 if inp is None else sum(a.nbytes for a in (inp.f_ext, inp.tree_L, inp.tree_tau)
-                                                      if a is not None))
-    d2h = sum(v.nbytes for v in out_host.values())
+    e2e_value = n_local * world_size * e2e_steps / (e2e_ms * 1e-3)
 
     cpu = None
     if rank == 0 and world_size == 1:
-        cpu = cpu_oracle_rate(scene, st, c, cfg, args.cpu_seconds, max_worlds=W, inputs=inp)
+        cpu = cpu_oracle_rate(parts, cfg, args.cpu_seconds, max_worlds=(parts[0].W if args.workload != "mixed" else 256))
     if world_size > 1:
         dist.barrier()
     if rank == 0:
+        alg_total = sum(p.alg_bytes for p in parts)
         line = {
-            "metric": METRIC if args.workload == "pile" else "world-steps/s (LEAP-like hand + cube, 4096 worlds)",
+            "metric": METRICS[args.workload],
             "value": value, "unit": "world-steps/s", "n_gpus": world_size,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic",
-            "config": {"workload": wname, "worlds_per_gpu": W, "contacts_per_world": c.n // W,
-                       "bodies_per_world": scene.n_bodies, "chains_per_world": scene.n_trees,
+            "higher_is_better": True, "scaling": "strong" if args.workload == "mixed" else "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": wname, "worlds_per_gpu": n_local,
+                       "contacts_per_world": n_contacts // n_local,
+                       "parts": {p.name: {"worlds": p.W, "contacts_per_world": p.c.n // p.W,
+                                          "bodies_per_world": p.scene.n_bodies, "chains_per_world": p.scene.n_trees}
+                                 for p in parts},
                        "facets_per_contact": 4, "condim": 3, "dt": cfg.dt,
                        "l2": "flushed between timed steps (256 MB write)" if flush is not None else "not flushed",
-                       "footprint_mb_per_step": alg_bytes / 1e6,
+                       "footprint_mb_per_step": alg_total / 1e6,
                        "parallelism": f"world-sharded x{world_size}"},
             "contacts_per_s": contacts_per_s,
             "gpu_launches": int(launches),
-            "kernel_ms": {"fused_step": k_ms, "fused_step_direct_launch": k_ms_direct,
-                          "segment_s0_separate": kt["segment_ms"] / max(kt["step_launches"], 1)},
+            "kernel_ms": {**{f"fused_step[{p.name}]_direct_launch": p.k_ms_direct for p in parts},
+                          "step_graph": total_ms / args.steps,
+                          "segment_s0_separate": sum(p.kt["segment_ms"] / max(p.kt["step_launches"], 1) for p in parts)},
             "cuda_graph": graph is not None,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
-                         "kernel": "k_step (S1-S7 fused)", "algorithmic_bytes_per_launch": alg_bytes},
+                         "kernel": f"k_step (S1-S7 fused) [{dom.name}]", "algorithmic_bytes_per_launch": dom.alg_bytes},
             "clocks": clock.summary(),
             "e2e": {"value": e2e_value, "unit": "world-steps/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": e2e_steps},
@@ -391,7 +462,8 @@ def run_ours(args, rank, world_size, local):
             "final_state_finite": finite,
         }
         print(json.dumps(line), flush=True)
-    ctx.close()
+    for p in parts:
+        p.ctx.close()
     if world_size > 1:
         dist.destroy_process_group()
 

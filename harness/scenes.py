@@ -488,3 +488,43 @@ def c3_hand(n_worlds=4096, seed=0, world_offset=0):
                         np.full(C, 1e-4, np.float32), np.full(C, 3, np.int32),
                         jr.reshape(C, 2, 6, 4))
     return scene, st, contacts, Inputs(None, Ls, tau)
+
+
+# ---------------------------------------------------------------- C5 mixed
+def tile_worlds(st: State, c: Contacts, inp, n_worlds: int):
+    """Repeat a batch of U worlds cyclically to n_worlds worlds (world w is a
+    copy of world w mod U; contacts stay grouped and sorted by world).  Used
+    to build large batches quickly: every copy is still stepped, the bytes are
+    only not unique."""
+    U = st.n_worlds
+    src = np.arange(n_worlds) % U
+    st2 = State(*(np.ascontiguousarray(a[src]) for a in (st.pos, st.quat, st.vel, st.omega, st.qpos, st.qvel)))
+    off = np.zeros(U + 1, np.int64)
+    np.cumsum(np.bincount(c.world, minlength=U), out=off[1:])
+    counts = off[1:] - off[:-1]
+    idx = np.concatenate([np.arange(off[s], off[s + 1]) for s in src]) if n_worlds else np.zeros(0, np.int64)
+    c2 = c.take(idx)
+    c2.world = np.repeat(np.arange(n_worlds, dtype=np.int32), counts[src])
+    inp2 = None
+    if inp is not None:
+        inp2 = Inputs(*(None if a is None else np.ascontiguousarray(a[src]) for a in
+                        (inp.f_ext, inp.tree_L, inp.tree_tau)))
+    return st2, c2, inp2
+
+
+def c5_mixed(n_worlds=65536, seed=0, world_offset=0, unique_hand=1024, unique_pile=4096):
+    """Config 5: n_worlds // 2 C3 hand worlds plus n_worlds - n_worlds // 2
+    "pile-lite" worlds (5x5x4 lattice = 100 bodies, 400 contacts), as two
+    homogeneous batches (one library context each, stepped concurrently).
+    At most unique_hand / unique_pile distinct worlds are generated per call
+    (seeded by world_offset) and tiled to the requested counts.
+    Returns {"hand": (scene, state, contacts, inputs), "pile": (scene, state, contacts)}."""
+    nh = n_worlds // 2
+    npl = n_worlds - nh
+    uh, up = max(1, min(nh, unique_hand)), max(1, min(npl, unique_pile))
+    sh, sth, ch, ih = c3_hand(n_worlds=uh, seed=seed + 5, world_offset=world_offset)
+    sp, stp, cp = c4_pile(n_worlds=up, contacts_per_world=400, lattice=(5, 5, 4), seed=seed + 5,
+                          world_offset=world_offset)
+    sth, ch, ih = tile_worlds(sth, ch, ih, nh)
+    stp, cp, _ = tile_worlds(stp, cp, None, npl)
+    return {"hand": (sh, sth, ch, ih), "pile": (sp, stp, cp)}

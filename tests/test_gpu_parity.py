@@ -278,6 +278,37 @@ def test_trajectory_c2b_stack_6d():
     _traj_compare(CFG.with_(n_t=8, n_rol=8), scene, st, geo)
 
 
+# ---------------------------------------------------------------- C5 mixed
+def test_c5_mixed_two_contexts_concurrent_streams():
+    """Config 5: hand and pile-lite worlds as two contexts stepped concurrently
+    on two CUDA streams (as bench.py --workload mixed does); each part matches
+    the oracle, and the concurrent result equals stepping each part alone."""
+    import torch
+    import paper_2603_12185_b200 as cf
+    d = scenes.c5_mixed(n_worlds=48, unique_hand=6, unique_pile=5)
+    sh, sth, ch, ih = d["hand"]
+    sp, stp, cp = d["pile"]
+    s0, s1 = torch.cuda.Stream(), torch.cuda.Stream()
+    cp_ctx, ch_ctx = cf.Context(CFG), cf.Context(CFG)
+    cp_ctx.load_scene(sp, stp.n_worlds, stp)
+    ch_ctx.load_scene(sh, sth.n_worlds, sth)
+    dcp, dch = cf.DeviceContacts.from_host(cp), cf.DeviceContacts.from_host(ch)
+    tin = type(ih)(*(None if a is None else torch.from_numpy(np.ascontiguousarray(a)).cuda()
+                     for a in (ih.f_ext, ih.tree_L, ih.tree_tau)))
+    torch.cuda.synchronize()
+    cp_ctx.step(dcp, None, stream=s0)
+    ch_ctx.step(dch, tin, stream=s1)
+    torch.cuda.synchronize()
+    gp, gh = cp_ctx.get_state(), ch_ctx.get_state()
+    op, oh = oracle.step(CFG, sp, stp, cp, None), oracle.step(CFG, sh, sth, ch, ih)
+    compare_step({"state": type(stp)(**{k: gp[k] for k in gp})}, op)
+    compare_step({"state": type(sth)(**{k: gh[k] for k in gh})}, oh)
+    alone = gpu_step(CFG, sp, stp, cp, None, impulses=False)
+    for k in ("pos", "quat", "vel", "omega"):
+        np.testing.assert_array_equal(gp[k], getattr(alone["state"], k))
+    cp_ctx.close(); ch_ctx.close()
+
+
 # ---------------------------------------------------------------- determinism
 def test_step_is_bitwise_deterministic_and_shard_invariant():
     """S6 accumulates in 64-bit fixed point with integer atomics (order-free),
