@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -335,10 +336,21 @@ comfree_status comfree_load_scene(comfree_ctx* ctx, const comfree_scene* scene, 
   return COMFREE_OK;
 }
 
+// Warps per world.  An SM holds 32 warps of the step kernel (64 registers) and
+// as many worlds as fit its 228 KB of shared memory; the world group gets the
+// warps the SM can spare per resident world (rounded up to a power of two),
+// but no more than its work needs (about one lane per contact or body).
+// Measured on B200 (profiles/r01_wpw_sweep.txt): B = 500 -> 8 at every contact
+// count, pile-lite (B = 100, 400 contacts) -> 2, hand (20 contacts) -> 1.
 static int pick_wpw(const cf::SceneDev& sc, int64_t n_contacts, int64_t n_worlds) {
   const int64_t avgc = n_worlds ? n_contacts / n_worlds : 0;
   const int64_t work = std::max<int64_t>(sc.B + sc.T, avgc);
-  int wpw = work <= 64 ? 1 : work <= 256 ? 2 : work <= 768 ? 4 : 8;
+  const int cap = work <= 32 ? 1 : work <= 64 ? 2 : work <= 128 ? 4 : 8;
+  const size_t world_smem = cf::step_smem_bytes(sc, 8) + 256;   // one group per CTA at 8 warps
+  const int64_t worlds_per_sm = std::max<int64_t>(1, (int64_t)(228 * 1024 / world_smem));
+  int want = 1;
+  while (want < 8 && want * worlds_per_sm < 32) want *= 2;
+  int wpw = std::min(want, cap);
   while (wpw < 8 && cf::step_smem_bytes(sc, wpw) > 200 * 1024) wpw *= 2;
   return wpw;
 }
@@ -504,7 +516,11 @@ comfree_status comfree_step(comfree_ctx* ctx, const comfree_worlds* wd, const co
   P.first_bad = ctx->d_first_bad;
   P.world_base = first;
   P.check_finite = !(cf_.flags & COMFREE_FLAG_NO_FINITE_CHECK);
-  const int wpw = pick_wpw(sc, n, nw);
+  int wpw = pick_wpw(sc, n, nw);
+  if (const char* e = getenv("COMFREE_WPW")) {  // tuning override (1, 2, 4 or 8 warps per world)
+    const int v = atoi(e);
+    if (v == 1 || v == 2 || v == 4 || v == 8) wpw = v;
+  }
   const size_t smem_need = cf::step_smem_bytes(sc, wpw);
   if (smem_need > 227 * 1024)
     return fail(ctx, COMFREE_ERR_CAPACITY, "step: %d bodies per world need %zu B of shared memory (> 227 KB)", sc.B,
