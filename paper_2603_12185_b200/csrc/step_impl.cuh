@@ -242,7 +242,10 @@ __device__ __forceinline__ void fx_add(unsigned* lo, int* hi, float v, float sca
   const long long x = __float2ll_rn(v * scale);
   const unsigned xl = (unsigned)x;
   const unsigned old = atomicAdd(lo, xl);
-  atomicAdd(hi, (int)(x >> 32) + (int)((unsigned)(old + xl) < xl));
+  int h;  // hi word + carry out of (old + xl): two instructions with the carry flag
+  asm("{\n\t.reg .u32 t;\n\tadd.cc.u32 t, %1, %2;\n\taddc.s32 %0, %3, 0;\n\t}"
+      : "=r"(h) : "r"(old), "r"(xl), "r"((int)(x >> 32)));
+  atomicAdd(hi, h);
 }
 __device__ __forceinline__ float fx_get(unsigned lo, int hi, float inv_scale) {
   const long long x = (long long)(((unsigned long long)(unsigned)hi << 32) | (unsigned long long)lo);
@@ -433,8 +436,10 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
     rec[Bp + i] = make_float4(ws.x, ws.y, ws.z, Ixx);
     rec[2 * Bp + i] = make_float4(x.x, x.y, x.z, Iyy);
     rec[3 * Bp + i] = make_float4(Izz, Ixy, Ixz, Iyz);
-#pragma unroll
-    for (int q6 = 0; q6 < 6; ++q6) { accl[q6 * Bp + i] = 0u; acch[q6 * Bp + i] = 0; }
+  }
+  {  // zero the accumulators (lo and hi planes are contiguous: 12 Bp words = 3 Bp uint4)
+    uint4* z = reinterpret_cast<uint4*>(accl);
+    for (int q = gt; q < 3 * Bp; q += kGT) z[q] = make_uint4(0u, 0u, 0u, 0u);
   }
   if (TREES) {
     for (int t = gt; t < T; t += kGT) {
