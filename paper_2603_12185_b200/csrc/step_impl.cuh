@@ -199,17 +199,24 @@ __device__ __forceinline__ void channel2(float A, float kmu, float w1, float w2,
   }
 }
 
-// Inclusive segmented sum of v[6] over runs of equal `key` in consecutive lanes
-// (Hillis-Steele inside each run, bounded by the longest run of the warp).
-// Returns true on the last lane of each run, which then holds the run total.
+// S6 run aggregation.  Lanes hold (body key, 6 values); runs of equal keys in
+// consecutive lanes are summed (Hillis-Steele inside each run, bounded by the
+// longest run of the warp) and only each run's last lane then adds to shared
+// memory.  When the warp's keys are mostly distinct (at least CF_DIRECT_RUNS
+// runs of 32) the shuffles cost more than they save and every lane adds its own
+// values directly (same-address lanes are serialised by the atomic unit).
+// Returns true on the lanes that must add.
+#ifndef CF_DIRECT_RUNS
+#define CF_DIRECT_RUNS 16
+#endif
 __device__ __forceinline__ bool seg_sum6(int key, float v[6], int lane) {
   const unsigned full = 0xffffffffu;
   const int prev = __shfl_up_sync(full, key, 1);
-  const int next = __shfl_down_sync(full, key, 1);
   const bool head = lane == 0 || prev != key;
-  const bool tail = lane == 31 || next != key;
   const unsigned heads = __ballot_sync(full, head);
-  if (heads == full) return tail;  // every run has length one (warp-uniform)
+  if (__popc(heads) >= CF_DIRECT_RUNS) return true;  // warp-uniform: direct adds
+  const int next = __shfl_down_sync(full, key, 1);
+  const bool tail = lane == 31 || next != key;
   const int start = 31 - __clz(heads & (full >> (31 - lane)));
   const int pos = lane - start;
   const int maxpos = (int)__reduce_max_sync(full, (unsigned)pos);
@@ -319,9 +326,10 @@ __device__ __forceinline__ void lower_bound2(const int32_t* a, int64_t n, int64_
 
 // S6 for one side: run aggregation inside the warp, then the run's last lane
 // adds its total (6 values) to the body's fixed-point accumulators.
+template <bool RUNS>
 __device__ __forceinline__ void scatter_side(unsigned* accl, int* acch, const float4* rec, int Bp, int key, float v[6],
                                              int lane) {
-  const bool tail = seg_sum6(key, v, lane) && key >= 0;
+  const bool tail = (!RUNS || seg_sum6(key, v, lane)) && key >= 0;
   if (tail) {
     const float* r = reinterpret_cast<const float*>(rec);
     const float im = r[4 * key + 3];
@@ -634,9 +642,9 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
     {
       const float3 ma = cross3(ra, f), mb = cross3(rb, f);
       float va[6] = {-f.x, -f.y, -f.z, -(ma.x + tau.x), -(ma.y + tau.y), -(ma.z + tau.z)};
-      scatter_side(accl, acch, rec, Bp, ida >= 0 ? ida : -1, va, lane);
+      scatter_side<true>(accl, acch, rec, Bp, ida >= 0 ? ida : -1, va, lane);
       float vb[6] = {f.x, f.y, f.z, mb.x + tau.x, mb.y + tau.y, mb.z + tau.z};
-      scatter_side(accl, acch, rec, Bp, idb >= 0 ? idb : -1, vb, lane);
+      scatter_side<false>(accl, acch, rec, Bp, idb >= 0 ? idb : -1, vb, lane);
     }
     if (TREES) {
 #pragma unroll
