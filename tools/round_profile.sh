@@ -5,10 +5,12 @@ TAG=${1:-r01}
 mkdir -p gpurun_out
 timeout 600 python bench.py > gpurun_out/${TAG}_bench_pile.json 2> gpurun_out/${TAG}_bench_pile.err
 timeout 600 python bench.py --workload hand --cpu-seconds 5 > gpurun_out/${TAG}_bench_hand.json 2> gpurun_out/${TAG}_bench_hand.err
+timeout 900 python bench.py --workload mixed --cpu-seconds 5 --steps 100 > gpurun_out/${TAG}_bench_mixed.json 2> gpurun_out/${TAG}_bench_mixed.err
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches_pile.csv \
     python bench.py --steps 4 --warmup 3 --cpu-seconds 0.1 --e2e-steps 1 > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_step -s 3 -c 1 -o gpurun_out/${TAG}_prof_pile \
     python bench.py --steps 2 --warmup 3 --cpu-seconds 0.1 --e2e-steps 1 > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_step -s 3 -c 1 -o gpurun_out/${TAG}_prof_hand \
     python bench.py --workload hand --steps 2 --warmup 3 --cpu-seconds 0.1 --e2e-steps 1 > /dev/null 2>&1
+bash tools/sweep_contacts.sh ${TAG} > gpurun_out/${TAG}_c4_sweep.txt 2>&1
 ls -la gpurun_out | grep $TAG
