@@ -128,6 +128,65 @@ def test_c4_full_size_sampled_worlds():
         compare_step(dict(state=gst), o)
 
 
+def test_c3_full_size_sampled_worlds():
+    """BASELINE config 3 at full size (4096 hand worlds) in the bench's launch
+    configuration (one warp per world); sampled worlds against the oracle."""
+    import torch
+    import paper_2603_12185_b200 as cf
+    from harness.types import Inputs
+    scene, st, c, inp = scenes.c3_hand(n_worlds=4096)
+    ctx = cf.Context(CFG)
+    ctx.load_scene(scene, 4096, st)
+    tin = Inputs(*(None if a is None else torch.from_numpy(np.ascontiguousarray(a)).cuda()
+                   for a in (inp.f_ext, inp.tree_L, inp.tree_tau)))
+    ctx.step(cf.DeviceContacts.from_host(c), tin, dt=CFG.dt)
+    out = ctx.get_state()
+    for w in (0, 1, 1000, 2047, 4095):
+        sel = np.nonzero(c.world == w)[0]
+        cw = c.take(sel)
+        cw.world = np.zeros(len(sel), np.int32)
+        iw = Inputs(None, inp.tree_L[w:w + 1], inp.tree_tau[w:w + 1])
+        o = oracle.step(CFG, scene, st.world_slice(w, w + 1), cw, iw)
+        gst = State(*(out[k][w:w + 1] for k in ("pos", "quat", "vel", "omega", "qpos", "qvel")))
+        compare_step(dict(state=gst), o)
+
+
+def test_c5_full_size_sampled_worlds():
+    """BASELINE config 5 at full size on one GPU (65536 worlds: 32768 hand +
+    32768 pile-lite as two contexts on two streams, as bench.py times it);
+    sampled worlds of each part against the oracle."""
+    import torch
+    import paper_2603_12185_b200 as cf
+    from harness.types import Inputs
+    d = scenes.c5_mixed(n_worlds=65536)
+    sh, sth, ch, ih = d["hand"]
+    sp, stp, cp = d["pile"]
+    s1 = torch.cuda.Stream()
+    cpx, chx = cf.Context(CFG), cf.Context(CFG)
+    cpx.load_scene(sp, stp.n_worlds, stp)
+    chx.load_scene(sh, sth.n_worlds, sth)
+    tin = Inputs(*(None if a is None else torch.from_numpy(np.ascontiguousarray(a)).cuda()
+                   for a in (ih.f_ext, ih.tree_L, ih.tree_tau)))
+    dcp, dch = cf.DeviceContacts.from_host(cp), cf.DeviceContacts.from_host(ch)
+    torch.cuda.synchronize()
+    cpx.step(dcp, None, dt=CFG.dt)
+    s1.wait_stream(torch.cuda.current_stream())
+    chx.step(dch, tin, dt=CFG.dt, stream=s1)
+    torch.cuda.synchronize()
+    for ctx, scene, st, c, inp, ws in ((cpx, sp, stp, cp, None, (0, 4095, 4096, 32767)),
+                                       (chx, sh, sth, ch, ih, (0, 1023, 1024, 32767))):
+        out = ctx.get_state()
+        for w in ws:
+            sel = np.nonzero(c.world == w)[0]
+            cw = c.take(sel)
+            cw.world = np.zeros(len(sel), np.int32)
+            iw = None if inp is None else Inputs(None, inp.tree_L[w:w + 1], inp.tree_tau[w:w + 1])
+            o = oracle.step(CFG, scene, st.world_slice(w, w + 1), cw, iw)
+            gst = State(*(out[k][w:w + 1] for k in ("pos", "quat", "vel", "omega", "qpos", "qvel")))
+            compare_step(dict(state=gst), o)
+        ctx.close()
+
+
 # ---------------------------------------------------------------- S0 integer outputs
 @pytest.mark.parametrize("seed", range(3))
 def test_segmentation_bit_exact(seed):
