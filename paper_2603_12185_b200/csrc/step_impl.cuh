@@ -328,12 +328,27 @@ __device__ __forceinline__ void lower_bound2(const int32_t* a, int64_t n, int64_
 // adds its total (6 values) to the body's fixed-point accumulators.
 template <bool RUNS>
 __device__ __forceinline__ void scatter_side(unsigned* accl, int* acch, const float4* rec, int Bp, int key, float v[6],
-                                             int lane) {
+                                             int lane, float im_own, float dm_own) {
   const bool tail = (!RUNS || seg_sum6(key, v, lane)) && key >= 0;
   if (tail) {
+#if defined(CF_SA_REG)
+    const float im = im_own, dmax = dm_own;  // the run's last lane has the run's body as its side a
+#else
     const float* r = reinterpret_cast<const float*>(rec);
     const float im = r[4 * key + 3];
     const float dmax = fmaxf(fmaxf(r[4 * (Bp + key) + 3], r[4 * (2 * Bp + key) + 3]), r[4 * (3 * Bp + key)]);
+#endif
+    const float sl = fx_pow2(fx_exp(im)), sa = fx_pow2(fx_exp(dmax));
+#pragma unroll
+    for (int q = 0; q < 6; ++q) fx_add(accl + q * Bp + key, acch + q * Bp + key, v[q], q < 3 ? sl : sa);
+  }
+}
+
+// S6 for a side whose body record is still in registers (direct adds, no runs):
+// the scales come from the lane's own m^-1 and max diag I_w^-1.
+__device__ __forceinline__ void scatter_own(unsigned* accl, int* acch, int Bp, int key, const float v[6], float im,
+                                            float dmax) {
+  if (key >= 0) {
     const float sl = fx_pow2(fx_exp(im)), sa = fx_pow2(fx_exp(dmax));
 #pragma unroll
     for (int q = 0; q < 6; ++q) fx_add(accl + q * Bp + key, acch + q * Bp + key, v[q], q < 3 ? sl : sa);
@@ -504,8 +519,12 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
     const int wid = WID;
     {  // prefetch this lane's next contact (index clamped: no branch)
       const int jn = min(j + kGT, nloc - 1);
-      C0 = ld_stream(C0p + jn); C1 = ld_stream(C1p + jn); C2 = ld_stream(C2p + jn); C3 = ld_stream(C3p + jn);
-      if (Wp) WID = ld_id(Wp + jn);
+      // global index made opaque so the stream addresses are formed from the
+      // kernel parameters each time (no per-stream 64-bit pointers held live)
+      int64_t g = cbeg + jn;
+      asm volatile("" : "+l"(g));
+      C0 = ld_stream(P.c0 + g); C1 = ld_stream(P.c1 + g); C2 = ld_stream(P.c2 + g); C3 = ld_stream(P.c3 + g);
+      if (P.world_sorted) WID = ld_id(P.world_sorted + g);
     }
 
     int ida = c3.x, idb = c3.y;
@@ -527,6 +546,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
     float3 vrel = make_float3(0.f, 0.f, 0.f), wrel = make_float3(0.f, 0.f, 0.f);
     float tr = 0.f;
     float3 ra = make_float3(0.f, 0.f, 0.f), rb = make_float3(0.f, 0.f, 0.f);
+    float ima = 0.f, dma = 0.f, imb = 0.f, dmb = 0.f;  // m^-1 and max diag I_w^-1 per side (S6 scales)
 #pragma unroll
     for (int side = 0; side < 2; ++side) {
       const int id = side ? idb : ida;
@@ -550,7 +570,8 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
                                       Ixz * r.x + Iyz * r.y + Izz * r.z);
         const float trs = 3.f * r0.w + (Ixx + Iyy + Izz) * dot3(r, r) - dot3(r, Ir);
         tr += fr ? trs : 0.f;
-        if (side) rb = r; else ra = r;
+        const float dm = fmaxf(fmaxf(Ixx, Iyy), Izz);
+        if (side) { rb = r; imb = r0.w; dmb = dm; } else { ra = r; ima = r0.w; dma = dm; }
       }
       if (TREES && id < -1) {
         const int t = -2 - id;
@@ -642,9 +663,9 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
     {
       const float3 ma = cross3(ra, f), mb = cross3(rb, f);
       float va[6] = {-f.x, -f.y, -f.z, -(ma.x + tau.x), -(ma.y + tau.y), -(ma.z + tau.z)};
-      scatter_side<true>(accl, acch, rec, Bp, ida >= 0 ? ida : -1, va, lane);
+      scatter_side<true>(accl, acch, rec, Bp, ida >= 0 ? ida : -1, va, lane, ima, dma);
       float vb[6] = {f.x, f.y, f.z, mb.x + tau.x, mb.y + tau.y, mb.z + tau.z};
-      scatter_side<false>(accl, acch, rec, Bp, idb >= 0 ? idb : -1, vb, lane);
+      scatter_own(accl, acch, Bp, idb >= 0 ? idb : -1, vb, imb, dmb);
     }
     if (TREES) {
 #pragma unroll
