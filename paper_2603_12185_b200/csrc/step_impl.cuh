@@ -411,12 +411,16 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
   int base = gt & ~31;
   // ---------------- S1: smooth prediction (Kernel I) ----------------
   for (int i = gt; i < B; i += kGT) {
-    const float3 x = make_float3(slab[0 * Bp + i], slab[1 * Bp + i], slab[2 * Bp + i]);
-    const float4 q = make_float4(slab[3 * Bp + i], slab[4 * Bp + i], slab[5 * Bp + i], slab[6 * Bp + i]);
-    const float3 v = make_float3(slab[7 * Bp + i], slab[8 * Bp + i], slab[9 * Bp + i]);
-    const float3 om = make_float3(slab[10 * Bp + i], slab[11 * Bp + i], slab[12 * Bp + i]);
+    // plane k of body i at sp + k * pb (64-bit pointer + uniform 64-bit stride)
+    const float* sp = slab + i;
+    const size_t pb = (size_t)Bp;
+    const float3 x = make_float3(sp[0 * pb], sp[1 * pb], sp[2 * pb]);
+    const float4 q = make_float4(sp[3 * pb], sp[4 * pb], sp[5 * pb], sp[6 * pb]);
+    const float3 v = make_float3(sp[7 * pb], sp[8 * pb], sp[9 * pb]);
+    const float3 om = make_float3(sp[10 * pb], sp[11 * pb], sp[12 * pb]);
     const float im = sc.inv_mass[i];
-    const float3 ib = make_float3(sc.inv_inertia[i], sc.inv_inertia[Bp + i], sc.inv_inertia[2 * Bp + i]);
+    const float* ip = sc.inv_inertia + i;
+    const float3 ib = make_float3(ip[0], ip[pb], ip[2 * pb]);
     // rotation of the normalised quaternion (reading R15)
     const float qn = rsqrtf(q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w);
     const float qw = q.x * qn, qx = q.y * qn, qy = q.z * qn, qz = q.w * qn;
@@ -445,9 +449,10 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
     // bias c = omega x (Iw omega), Iw = R diag(1/ib) R^T on unlocked axes
     float3 wl = make_float3(R00 * om.x + R10 * om.y + R20 * om.z, R01 * om.x + R11 * om.y + R21 * om.z,
                             R02 * om.x + R12 * om.y + R22 * om.z);
-    wl.x *= sc.inertia[i];            // I_b = 1/I_b^-1, 0 on locked axes (precomputed per scene)
-    wl.y *= sc.inertia[Bp + i];
-    wl.z *= sc.inertia[2 * Bp + i];
+    const float* ipi = sc.inertia + i;  // I_b = 1/I_b^-1, 0 on locked axes (precomputed per scene)
+    wl.x *= ipi[0];
+    wl.y *= ipi[pb];
+    wl.z *= ipi[2 * pb];
     const float3 Iwo = make_float3(R00 * wl.x + R01 * wl.y + R02 * wl.z, R10 * wl.x + R11 * wl.y + R12 * wl.z,
                                    R20 * wl.x + R21 * wl.y + R22 * wl.z);
     const float3 gy = cross3(om, Iwo);
@@ -702,7 +707,9 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
   bool nonfinite = false;
   for (int i = gt; i < B; i += kGT) {
     const float4 r0 = rec[i], r1 = rec[Bp + i], r2 = rec[2 * Bp + i], r3 = rec[3 * Bp + i];
-    const float4 q = make_float4(slab[3 * Bp + i], slab[4 * Bp + i], slab[5 * Bp + i], slab[6 * Bp + i]);
+    float* sp = slab + i;
+    const size_t pb = (size_t)Bp;
+    const float4 q = make_float4(sp[3 * pb], sp[4 * pb], sp[5 * pb], sp[6 * pb]);
     const float im = r0.w;
     const float Ixx = r1.w, Iyy = r2.w, Izz = r3.x, Ixy = r3.y, Ixz = r3.z, Iyz = r3.w;
     const float isl = fx_pow2(-fx_exp(im)), isa = fx_pow2(-fx_exp(fmaxf(fmaxf(Ixx, Iyy), Izz)));
@@ -743,10 +750,10 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
     float nz = ew * q.w + ex * q.z - ey * q.y + ez * q.x;
     const float inv = rsqrtf(nw * nw + nx * nx + ny * ny + nz * nz);
     nw *= inv; nx *= inv; ny *= inv; nz *= inv;
-    slab[0 * Bp + i] = x.x; slab[1 * Bp + i] = x.y; slab[2 * Bp + i] = x.z;
-    slab[3 * Bp + i] = nw; slab[4 * Bp + i] = nx; slab[5 * Bp + i] = ny; slab[6 * Bp + i] = nz;
-    slab[7 * Bp + i] = v.x; slab[8 * Bp + i] = v.y; slab[9 * Bp + i] = v.z;
-    slab[10 * Bp + i] = om.x; slab[11 * Bp + i] = om.y; slab[12 * Bp + i] = om.z;
+    sp[0 * pb] = x.x; sp[1 * pb] = x.y; sp[2 * pb] = x.z;
+    sp[3 * pb] = nw; sp[4 * pb] = nx; sp[5 * pb] = ny; sp[6 * pb] = nz;
+    sp[7 * pb] = v.x; sp[8 * pb] = v.y; sp[9 * pb] = v.z;
+    sp[10 * pb] = om.x; sp[11 * pb] = om.y; sp[12 * pb] = om.z;
     if (P.check_finite) {
       const float chk = x.x + x.y + x.z + v.x + v.y + v.z + om.x + om.y + om.z + nw + nx + ny + nz;
       nonfinite |= !isfinite(chk);
