@@ -301,7 +301,7 @@ comfree_status comfree_load_scene(comfree_ctx* ctx, const comfree_scene* scene, 
   ctx->loaded = false;
   cf::SceneDev& sc = ctx->sc;
   sc.B = scene->n_bodies;
-  sc.Bp = (int)round4(std::max(1, scene->n_bodies));
+  sc.Bp = (int)round4(scene->n_bodies + 1);  // + the all-zero body record the step reads for static sides
   sc.T = scene->n_trees;
   sc.nd = scene->n_trees ? scene->tree_ndof : 0;
   sc.Q = sc.T * sc.nd;

@@ -20,7 +20,8 @@ enum : int {
 
 // State slab: per world, 13 planes of Bp floats (px py pz qw qx qy qz vx vy vz
 // wx wy wz) followed by 2 planes of Qp floats (qpos, qvel).  Bp, Qp are
-// multiples of 4 so each plane is 16-byte aligned.
+// multiples of 4 so each plane is 16-byte aligned; Bp >= B + 1 (body record B
+// of the step's shared memory is the all-zero record of static sides).
 enum { PL_PX = 0, PL_QW = 3, PL_VX = 7, PL_WX = 10, N_BODY_PLANES = 13 };
 
 struct SceneDev {

@@ -410,6 +410,8 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
   int4 C3 = make_int4(-1, -1, 0, 0);
   int base = gt & ~31;
   // ---------------- S1: smooth prediction (Kernel I) ----------------
+  // record B (Bp >= B + 1) stays all zero: static and chain sides read it in S2
+  if (gt < 4) rec[gt * Bp + B] = make_float4(0.f, 0.f, 0.f, 0.f);
   for (int i = gt; i < B; i += kGT) {
     // plane k of body i at sp + k * pb (64-bit pointer + uniform 64-bit stride)
     const float* sp = slab + i;
@@ -556,25 +558,24 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
     for (int side = 0; side < 2; ++side) {
       const int id = side ? idb : ida;
       const float sg = side ? 1.f : -1.f;
-      {  // free body (branch-free: a static side reads record 0 and is masked by select)
-        const bool fr = id >= 0;
-        const int ix = fr ? id : 0;
+      {  // free body (branch-free: a static or chain side reads the all-zero record B,
+         // whose velocity, inverse mass and inverse inertia contribute exactly 0)
+        const int ix = id >= 0 ? id : B;
         const float4 r0 = rec[ix], r1 = rec[Bp + ix], r2 = rec[2 * Bp + ix], r3 = rec[3 * Bp + ix];
         const float3 r = make_float3(p.x - r2.x, p.y - r2.y, p.z - r2.z);
         const float3 wxr = cross3(make_float3(r1.x, r1.y, r1.z), r);
-        const float sf = fr ? sg : 0.f;
-        vrel.x += fr ? sg * (r0.x + wxr.x) : 0.f;
-        vrel.y += fr ? sg * (r0.y + wxr.y) : 0.f;
-        vrel.z += fr ? sg * (r0.z + wxr.z) : 0.f;
-        wrel.x += fr ? sf * r1.x : 0.f;
-        wrel.y += fr ? sf * r1.y : 0.f;
-        wrel.z += fr ? sf * r1.z : 0.f;
+        vrel.x += sg * (r0.x + wxr.x);
+        vrel.y += sg * (r0.y + wxr.y);
+        vrel.z += sg * (r0.z + wxr.z);
+        wrel.x += sg * r1.x;
+        wrel.y += sg * r1.y;
+        wrel.z += sg * r1.z;
         // tr(J M^-1 J^T) of the linear point Jacobian: 3 im + tr(I)|r|^2 - r^T I r
         const float Ixx = r1.w, Iyy = r2.w, Izz = r3.x, Ixy = r3.y, Ixz = r3.z, Iyz = r3.w;
         const float3 Ir = make_float3(Ixx * r.x + Ixy * r.y + Ixz * r.z, Ixy * r.x + Iyy * r.y + Iyz * r.z,
                                       Ixz * r.x + Iyz * r.y + Izz * r.z);
         const float trs = 3.f * r0.w + (Ixx + Iyy + Izz) * dot3(r, r) - dot3(r, Ir);
-        tr += fr ? trs : 0.f;
+        tr += trs;
         const float dm = fmaxf(fmaxf(Ixx, Iyy), Izz);
         if (side) { rb = r; imb = r0.w; dmb = dm; } else { ra = r; ima = r0.w; dma = dm; }
       }
