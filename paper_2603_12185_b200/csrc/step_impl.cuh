@@ -47,8 +47,8 @@ __host__ __device__ inline GroupLayout group_layout(const SceneDev& sc) {
   GroupLayout L;
   int o = 0;
   L.rec = o;  o += 16 * sc.Bp;   // float4 rec[4][Bp]: (v_s,im) (w_s,Ixx) (x,Iyy) (Izz,Ixy,Ixz,Iyz)
-  L.accl = o; o += 6 * sc.Bp;    // uint32 lo[6][Bp] \ generalized impulse p (lin, ang) as 64-bit
-  L.acch = o; o += 6 * sc.Bp;    // int32  hi[6][Bp] /  fixed point, per-body scale
+  L.accl = o; o += 6 * sc.Bp;    // (uint32 lo, int32 hi)[6][Bp]: generalized impulse p (lin, ang) as
+  L.acch = o; o += 6 * sc.Bp;    //   64-bit fixed point, per-body scale (S6); 12 Bp words from accl
   o = (o + 3) & ~3;
   L.tq = o;   o += 4 * sc.T;     // float4 qd_s[T]
   L.tqp = o;  o += 4 * sc.T;     // float4 q[T] (step-start chain positions, read in S1)
@@ -326,32 +326,35 @@ __device__ __forceinline__ void lower_bound2(const int32_t* a, int64_t n, int64_
 
 // S6 for one side: run aggregation inside the warp, then the run's last lane
 // adds its total (6 values) to the body's fixed-point accumulators.
+// Accumulator of component q of body k: (lo, hi) words adjacent, so one
+// address serves both atomics (planes of Bp uint2 per component).
+#define ACC_LO(q, k) (accl + 2 * ((q) * Bp + (k)))
+#define ACC_HI(q, k) (reinterpret_cast<int*>(accl) + 2 * ((q) * Bp + (k)) + 1)
+
 template <bool RUNS>
-__device__ __forceinline__ void scatter_side(unsigned* accl, int* acch, const float4* rec, int Bp, int key, float v[6],
-                                             int lane, float im_own, float dm_own) {
+__device__ __forceinline__ void scatter_side(unsigned* accl, const float4* rec, int Bp, int key, float v[6],
+                                             int lane, float, float) {
   const bool tail = (!RUNS || seg_sum6(key, v, lane)) && key >= 0;
   if (tail) {
-#if defined(CF_SA_REG)
-    const float im = im_own, dmax = dm_own;  // the run's last lane has the run's body as its side a
-#else
+    // scales from the body record in shared memory (keeping side a's values in
+    // registers across S3-S5 spills at 64 registers)
     const float* r = reinterpret_cast<const float*>(rec);
     const float im = r[4 * key + 3];
     const float dmax = fmaxf(fmaxf(r[4 * (Bp + key) + 3], r[4 * (2 * Bp + key) + 3]), r[4 * (3 * Bp + key)]);
-#endif
     const float sl = fx_pow2(fx_exp(im)), sa = fx_pow2(fx_exp(dmax));
 #pragma unroll
-    for (int q = 0; q < 6; ++q) fx_add(accl + q * Bp + key, acch + q * Bp + key, v[q], q < 3 ? sl : sa);
+    for (int q = 0; q < 6; ++q) fx_add(ACC_LO(q, key), ACC_HI(q, key), v[q], q < 3 ? sl : sa);
   }
 }
 
 // S6 for a side whose body record is still in registers (direct adds, no runs):
 // the scales come from the lane's own m^-1 and max diag I_w^-1.
-__device__ __forceinline__ void scatter_own(unsigned* accl, int* acch, int Bp, int key, const float v[6], float im,
+__device__ __forceinline__ void scatter_own(unsigned* accl, int Bp, int key, const float v[6], float im,
                                             float dmax) {
   if (key >= 0) {
     const float sl = fx_pow2(fx_exp(im)), sa = fx_pow2(fx_exp(dmax));
 #pragma unroll
-    for (int q = 0; q < 6; ++q) fx_add(accl + q * Bp + key, acch + q * Bp + key, v[q], q < 3 ? sl : sa);
+    for (int q = 0; q < 6; ++q) fx_add(ACC_LO(q, key), ACC_HI(q, key), v[q], q < 3 ? sl : sa);
   }
 }
 
@@ -372,7 +375,6 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
   float* G = smem + (size_t)group * GL.total;
   float4* rec = reinterpret_cast<float4*>(G + GL.rec);
   unsigned* accl = reinterpret_cast<unsigned*>(G + GL.accl);
-  int* acch = reinterpret_cast<int*>(G + GL.acch);
   float4* tq = reinterpret_cast<float4*>(G + GL.tq);
   float4* tqp = reinterpret_cast<float4*>(G + GL.tqp);
   float* tL = G + GL.tL;
@@ -467,7 +469,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
     rec[2 * Bp + i] = make_float4(x.x, x.y, x.z, Iyy);
     rec[3 * Bp + i] = make_float4(Izz, Ixy, Ixz, Iyz);
   }
-  {  // zero the accumulators (lo and hi planes are contiguous: 12 Bp words = 3 Bp uint4)
+  {  // zero the accumulators (12 Bp words = 3 Bp uint4)
     uint4* z = reinterpret_cast<uint4*>(accl);
     for (int q = gt; q < 3 * Bp; q += kGT) z[q] = make_uint4(0u, 0u, 0u, 0u);
   }
@@ -669,9 +671,9 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
     {
       const float3 ma = cross3(ra, f), mb = cross3(rb, f);
       float va[6] = {-f.x, -f.y, -f.z, -(ma.x + tau.x), -(ma.y + tau.y), -(ma.z + tau.z)};
-      scatter_side<true>(accl, acch, rec, Bp, ida >= 0 ? ida : -1, va, lane, ima, dma);
+      scatter_side<true>(accl, rec, Bp, ida >= 0 ? ida : -1, va, lane, ima, dma);
       float vb[6] = {f.x, f.y, f.z, mb.x + tau.x, mb.y + tau.y, mb.z + tau.z};
-      scatter_own(accl, acch, Bp, idb >= 0 ? idb : -1, vb, imb, dmb);
+      scatter_own(accl, Bp, idb >= 0 ? idb : -1, vb, imb, dmb);
     }
     if (TREES) {
 #pragma unroll
@@ -718,13 +720,13 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
     unsigned range = 0u;
 #pragma unroll
     for (int q6 = 0; q6 < 6; ++q6) {
-      hi[q6] = acch[q6 * Bp + i];
+      hi[q6] = *ACC_HI(q6, i);
       range |= (unsigned)hi[q6] + (1u << 30);  // bit 31 set: |sum| >= 2^62, fixed-point range exceeded
     }
     if (P.check_finite) nonfinite |= (range >> 31) != 0u;
-    const float4 a0 = make_float4(fx_get(accl[i], hi[0], isl), fx_get(accl[Bp + i], hi[1], isl),
-                                  fx_get(accl[2 * Bp + i], hi[2], isl), fx_get(accl[3 * Bp + i], hi[3], isa));
-    const float2 a1 = make_float2(fx_get(accl[4 * Bp + i], hi[4], isa), fx_get(accl[5 * Bp + i], hi[5], isa));
+    const float4 a0 = make_float4(fx_get(*ACC_LO(0, i), hi[0], isl), fx_get(*ACC_LO(1, i), hi[1], isl),
+                                  fx_get(*ACC_LO(2, i), hi[2], isl), fx_get(*ACC_LO(3, i), hi[3], isa));
+    const float2 a1 = make_float2(fx_get(*ACC_LO(4, i), hi[4], isa), fx_get(*ACC_LO(5, i), hi[5], isa));
     const float3 v = make_float3(r0.x + im * a0.x, r0.y + im * a0.y, r0.z + im * a0.z);
     const float3 om = make_float3(r1.x + Ixx * a0.w + Ixy * a1.x + Ixz * a1.y,
                                   r1.y + Ixy * a0.w + Iyy * a1.x + Iyz * a1.y,
