@@ -16,15 +16,16 @@
 //                 = sum_f J~_f^T Lambda_f in contact space; symmetric facet
 //                 pairs are differenced exactly (2a when both are active)
 //             S6  J^T (f_c, tau_c) scattered into per-world shared-memory
-//                 accumulators (Alg. 1 Kernel III): a warp first sums
-//                 runs of equal body ids, then one 128-bit + one 64-bit
-//                 shared-memory CAS per run and side — no global atomics
+//                 accumulators (Alg. 1 Kernel III) as 64-bit fixed
+//                 point with native int32 atomics (deterministic): side a sums
+//                 runs of equal body ids in the warp first, side b adds directly
+//                 — no global atomics
 //   epilogue  S7  v+ = v_s + M^-1 p (Eq. (10), Alg. 1 Kernel IV), semi-implicit
 //                 Euler with the exp-map quaternion update; chains q+ = q + qd+ dt;
 //                 finite check and per-world statistics.
 // WPW = 8: one 256-thread CTA per world (dense piles); WPW = 1: eight worlds per
-// CTA, one warp each (hand + cube).  TREES / IMP compile the articulated sides
-// and the per-facet impulse output in or out.
+// CTA, one warp each (hand + cube); pick_wpw (capi.cpp) chooses.  TREES / IMP
+// compile the articulated sides and the per-facet impulse output in or out.
 #pragma once
 #include <cuda_runtime.h>
 #include <math.h>
