@@ -44,6 +44,23 @@ def test_random_mixed_step(seed, cfg):
     compare_step(g, o)
 
 
+def test_largest_world_that_fits_shared_memory():
+    """Maximum size: 2070 bodies per world (the step's per-world shared memory,
+    28 words per body, just under the 227 KB a CTA may use; one world per SM,
+    8 warps) matches the oracle; one more step of the same kind with 2100
+    bodies is refused with COMFREE_ERR_CAPACITY instead of launching."""
+    import paper_2603_12185_b200 as cf
+    scene, st, c, inp = scenes.random_instance(777, n_worlds=3, n_bodies=2070, contacts_per_world=[4000, 17, 2500],
+                                               condims=(3, 4, 6))
+    compare_step(gpu_step(CFG, scene, st, c, inp), oracle.step(CFG, scene, st, c, inp))
+    scene2, st2, c2, inp2 = scenes.random_instance(778, n_worlds=2, n_bodies=2100, contacts_per_world=50)
+    ctx = cf.Context(CFG)
+    ctx.load_scene(scene2, 2, st2)
+    with pytest.raises(cf.ComfreeError) as ei:
+        ctx.step(cf.DeviceContacts.from_host(c2), None)
+    assert ei.value.status == 3 and "shared memory" in str(ei.value)
+
+
 @pytest.mark.parametrize("seed", range(4))
 def test_random_articulated_step(seed):
     """Chains (S8): tree sides with J rows, Cholesky M^-1, mixed with free bodies."""
