@@ -104,6 +104,7 @@ class Contacts:
     condim: np.ndarray                       # (C,) int32
     jrow: Optional[np.ndarray] = None        # (C,2,6,4) f32
     meta: dict = field(default_factory=dict)
+    kd: Optional[np.ndarray] = None          # (C,2) f32 per-contact (k_user, d_user), or None
 
     @property
     def n(self) -> int:
@@ -113,7 +114,7 @@ class Contacts:
         return Contacts(self.world[idx], self.c0[idx], self.c1[idx], self.c2[idx],
                         self.body_a[idx], self.body_b[idx], self.mu_rol[idx],
                         self.condim[idx], None if self.jrow is None else self.jrow[idx],
-                        dict(self.meta))
+                        dict(self.meta), None if self.kd is None else self.kd[idx])
 
     @staticmethod
     def empty(with_jrow: bool = False) -> "Contacts":
@@ -130,6 +131,9 @@ class Contacts:
         if any(p.jrow is not None for p in parts):
             jr = np.concatenate([p.jrow if p.jrow is not None else
                                  np.zeros((p.n, 2, 6, 4), np.float32) for p in parts])
+        kd = None
+        if any(p.kd is not None for p in parts):
+            raise ValueError("concat of contacts with per-contact impedance is not supported")
         return Contacts(*(np.concatenate([getattr(p, k) for p in parts]) for k in
                           ("world", "c0", "c1", "c2", "body_a", "body_b", "mu_rol", "condim")),
-                        jr)
+                        jr, {}, kd)

@@ -62,7 +62,7 @@ def _load():
         lib.orc_step.restype = ct.c_int
         lib.orc_step.argtypes = [ct.POINTER(_Cfg), ct.POINTER(_Scene), ct.c_int64,
                                  P, P, P, P, P, P, P, P, P, ct.c_int64, P, P, P, P, P, P, P, P, P,
-                                 P, P, P, ct.c_int]
+                                 P, P, P, P, ct.c_int]
         lib.orc_segment.restype = ct.c_int
         lib.orc_segment.argtypes = [ct.c_int64, P, ct.c_int64, P, ct.c_int32, ct.c_int32, P, P, P]
         lib.orc_gamma.restype = ct.c_double
@@ -161,11 +161,12 @@ def step(cfg: Config, scene: Scene, state: State, contacts: Contacts,
     ba, bb = _i(contacts.body_a), _i(contacts.body_b)
     mr, cd, wd = _d(contacts.mu_rol), _i(contacts.condim), _i(contacts.world)
     jr = _d(contacts.jrow)
+    kd = _d(getattr(contacts, "kd", None))
     fe, tl, tt = _d(inputs.f_ext), _d(inputs.tree_L), _d(inputs.tree_tau)
     rc = _load().orc_step(ct.byref(c), ct.byref(sc), W,
                           _p(s.pos), _p(s.quat), _p(s.vel), _p(s.omega), _p(s.qpos), _p(s.qvel),
                           _p(fe), _p(tl), _p(tt), n, _p(wd), _p(c0), _p(c1), _p(c2),
-                          _p(ba), _p(bb), _p(mr), _p(cd), _p(jr), _p(imp), _p(wr), _p(st),
+                          _p(ba), _p(bb), _p(mr), _p(cd), _p(jr), _p(kd), _p(imp), _p(wr), _p(st),
                           int(n_threads))
     if rc == 1 or (strict and rc != 0):
         raise OracleError(f"orc_step failed rc={rc}")

@@ -146,7 +146,9 @@ def dense_world_step(cfg: Config, scene: Scene, state: State, contacts: Contacts
         x = min(abs(phi) / cfg.width, 1.0)
         r = cfg.r_min + (cfg.r_max - cfg.r_min) * _gamma(x, cfg.midpoint, cfg.power)
         Mphi = r / (1 - r) / tr
-        K, D = cfg.k_user * Mphi / dt, cfg.d_user * Mphi / dt   # Eq. (12)
+        ku, du = (cfg.k_user, cfg.d_user) if getattr(contacts, "kd", None) is None else \
+            (float(contacts.kd[c, 0]), float(contacts.kd[c, 1]))   # per-contact pair
+        K, D = ku * Mphi / dt, du * Mphi / dt                       # Eq. (12)
         for row in facet_rows(cfg, n, t1, float(contacts.c1[c, 3]), float(contacts.c2[c, 3]),
                               float(contacts.mu_rol[c]), int(contacts.condim[c]), Jc):
             s = row @ v_s

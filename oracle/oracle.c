@@ -249,6 +249,7 @@ static int step_world(const orc_config* cfg, const orc_scene* sc, int64_t w,
                       const double* c0, const double* c1, const double* c2,
                       const int32_t* body_a, const int32_t* body_b,
                       const double* mu_rol, const int32_t* condim, const double* jrow,
+                      const double* kd,
                       const int64_t* foff, double* impulses, double* wrench, double* stats) {
   const int B = sc->n_bodies, T = sc->n_trees, nd = sc->tree_ndof, Q = T * nd;
   const double dt = cfg->dt;
@@ -327,7 +328,9 @@ static int step_world(const orc_config* cfg, const orc_scene* sc, int64_t w,
               + side_trace(b, p, pos_w, sc->inv_mass, bw, L_w, nd, Jb);
     double r = orc_r(phi, cfg);
     double Mphi = r / (1.0 - r) / tr;
-    double K = k * Mphi / dt, D = d * Mphi / dt;
+    /* per-contact (k_user, d_user) when given, else the global pair */
+    const double kc = kd ? kd[2 * c] : k, dc = kd ? kd[2 * c + 1] : d;
+    double K = kc * Mphi / dt, D = dc * Mphi / dt;
 
     /* Eq. (7)-(8): facets. Each facet row J~_f acts on the contact twist through
      * g_f = (g_lin, g_ang):  J~_f v = g_lin . v_c + g_ang . omega_c           */
@@ -442,10 +445,14 @@ int orc_step(const orc_config* cfg, const orc_scene* sc, int64_t n_worlds,
              const double* c0, const double* c1, const double* c2,
              const int32_t* body_a, const int32_t* body_b,
              const double* mu_rol, const int32_t* condim, const double* jrow,
+             const double* kd,
              double* impulses, double* wrench, double* stats, int n_threads) {
   if (!cfg || !sc || n_worlds < 0 || n < 0 || !(cfg->dt > 0)) return ORC_EINVAL;
   if (sc->n_trees > 0 && (sc->tree_ndof < 1 || sc->tree_ndof > 4 || !tree_L || !tree_tau)) return ORC_EINVAL;
   for (int64_t c = 0; c < n; ++c) {
+    /* per-contact impedance: finite and non-negative, like the global pair */
+    if (kd && !(kd[2 * c] >= 0.0 && kd[2 * c + 1] >= 0.0 && kd[2 * c] < HUGE_VAL && kd[2 * c + 1] < HUGE_VAL))
+      return ORC_EINVAL;
     int32_t ids[2] = {body_a[c], body_b[c]};
     for (int s = 0; s < 2; ++s) {
       int32_t id = ids[s];
@@ -466,7 +473,7 @@ int orc_step(const orc_config* cfg, const orc_scene* sc, int64_t n_worlds,
 #endif
   for (int64_t w = 0; w < n_worlds; ++w) {
     int s = step_world(cfg, sc, w, pos, quat, vel, omega, qpos, qvel, f_ext, tree_L, tree_tau,
-                       off[w], off[w + 1], perm, c0, c1, c2, body_a, body_b, mu_rol, condim, jrow,
+                       off[w], off[w + 1], perm, c0, c1, c2, body_a, body_b, mu_rol, condim, jrow, kd,
                        foff, impulses, wrench, stats);
     if (s != ORC_OK) {
 #ifdef _OPENMP

@@ -58,6 +58,8 @@ int orc_facets_per_contact(int32_t condim, int32_t n_t, int32_t n_rol);
  * wrench:   [n][6] per-contact (f_c, tau_c) on body b, or NULL.
  * stats:    [n_worlds][5] (contacts, active facets, max penetration, KE,
  *           non-finite flag), or NULL.
+ * kd:       [n][2] per-contact (k_user, d_user) replacing the global pair in
+ *           Eq. (12) (user-set or learned impedance), or NULL.
  * n_threads > 1 parallelises across worlds only (timing driver).       */
 int orc_step(const orc_config* cfg, const orc_scene* scene, int64_t n_worlds,
              double* pos, double* quat, double* vel, double* omega,
@@ -67,6 +69,7 @@ int orc_step(const orc_config* cfg, const orc_scene* scene, int64_t n_worlds,
              const double* c0, const double* c1, const double* c2,
              const int32_t* body_a, const int32_t* body_b,
              const double* mu_rol, const int32_t* condim, const double* jrow,
+             const double* kd,
              double* impulses, double* wrench, double* stats, int n_threads);
 
 /* Pieces exposed for the pins (same code the step uses). */
