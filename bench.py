@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to exercise the multi-rank path on a single GPU")
+    ap.add_argument("--kd", action="store_true",
+                    help="per-contact (k_user, d_user) impedance arrays (learned-impedance variant, P:206-208)")
     ap.add_argument("--workload", default="pile", choices=["pile", "hand", "mixed"],
                     help="pile: config 4 (the BASELINE metric); hand: config 3; mixed: config 5")
     a = ap.parse_args()
@@ -157,6 +159,17 @@ def _hand_bytes(scene, c, W):
 
 def workload(args, rank, world_size):
     """(parts, workload name, worlds per rank) -- parts are homogeneous batches."""
+    parts, name, n = _workload(args, rank, world_size)
+    if args.kd:                      # per-contact impedance: 8 more bytes per contact
+        for p in parts:
+            rng = np.random.default_rng([260312185, 11, rank])
+            p.c.kd = np.stack([rng.uniform(0.05, 0.3, p.c.n), rng.uniform(0.0, 0.002, p.c.n)], 1).astype(np.float32)
+            p.alg_bytes += 8 * p.c.n
+        name += " + per-contact impedance"
+    return parts, name, n
+
+
+def _workload(args, rank, world_size):
     from harness import scenes
     if args.workload == "hand":
         W = args.worlds

@@ -54,7 +54,7 @@
 extern "C" {
 #endif
 
-#define COMFREE_ABI_VERSION 1
+#define COMFREE_ABI_VERSION 2  /* 2: comfree_contacts.kd */
 
 typedef enum {
   COMFREE_OK = 0,
@@ -147,6 +147,10 @@ typedef struct {
  *   jrow [12][n][4]: stream s = side*6 + row (side 0 = a, 1 = b): rows 0-2
  *       linear velocity of the contact point, rows 3-5 angular velocity, of
  *       an articulated side, one column per chain DoF; NULL if no chains.
+ *   kd [n][2] (optional, NULL = use the config's pair): per-contact
+ *       (k_user, d_user) replacing the global pair of Eq. (12), for
+ *       user-set or learned impedance; finite and >= 0
+ *       (checked on the device, reported as COMFREE_ERR_VALIDATION).
  * Segmentation (S0): if off != NULL contacts are grouped by world and
  * off[n_worlds + 1] is their CSR (no S0 work).  Otherwise world[n] (relative
  * to first_world) is used; with COMFREE_CONTACTS_SORTED it must be
@@ -164,6 +168,7 @@ typedef struct {
   const float* c2;
   const int32_t* c3;
   const float* jrow;
+  const float* kd;
   float* impulses;
   int64_t* foff;
   int64_t impulses_capacity; /* elements available at impulses (checked) */

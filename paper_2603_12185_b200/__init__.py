@@ -114,6 +114,7 @@ class HostContacts:
     c3: object
     jrow: object
     sorted: bool
+    kd: object = None
 
     @staticmethod
     def from_arrays(contacts, pin: bool = True) -> "HostContacts":
@@ -132,11 +133,12 @@ class HostContacts:
                             host(pack_c3(contacts.body_a, contacts.body_b, contacts.mu_rol,
                                          contacts.condim), np.int32),
                             None if contacts.jrow is None else host(pack_jrow(contacts.jrow), np.float32),
-                            srt)
+                            srt,
+                            None if getattr(contacts, "kd", None) is None else host(contacts.kd, np.float32))
 
     def h2d_bytes(self) -> int:
         tot = 0
-        for a in (self.world, self.c0, self.c1, self.c2, self.c3, self.jrow):
+        for a in (self.world, self.c0, self.c1, self.c2, self.c3, self.jrow, self.kd):
             if a is not None:
                 tot += a.nbytes if isinstance(a, np.ndarray) else a.numel() * a.element_size()
         return tot
@@ -153,6 +155,7 @@ class DeviceContacts:
     c3: object
     jrow: object
     sorted: bool
+    kd: object = None                      # (C, 2) per-contact (k_user, d_user) or None
 
     @staticmethod
     def from_host(contacts, device=None) -> "DeviceContacts":
@@ -168,7 +171,8 @@ class DeviceContacts:
                               d(pack_c3(contacts.body_a, contacts.body_b, contacts.mu_rol,
                                         contacts.condim), np.int32),
                               None if contacts.jrow is None else d(pack_jrow(contacts.jrow), np.float32),
-                              srt)
+                              srt,
+                              None if getattr(contacts, "kd", None) is None else d(contacts.kd, np.float32))
 
     def nbytes(self) -> int:
         return sum(t.numel() * t.element_size() for t in (self.c0, self.c1, self.c2, self.c3)) + \
@@ -244,7 +248,8 @@ class Context:
             cap = impulses.size if isinstance(impulses, np.ndarray) else impulses.numel()
         c = _lib.comfree_contacts(int(contacts.n), _ptr(contacts.world) if contacts.n else None,
                                   _ptr(off), _ptr(contacts.c0), _ptr(contacts.c1), _ptr(contacts.c2),
-                                  _ptr(contacts.c3), _ptr(contacts.jrow), _ptr(impulses), _ptr(foff),
+                                  _ptr(contacts.c3), _ptr(contacts.jrow), _ptr(getattr(contacts, "kd", None)),
+                                  _ptr(impulses), _ptr(foff),
                                   int(cap), CONTACTS_SORTED if srt else 0, loc)
         wloc = MEM_DEVICE
         fe = tl = tt = None

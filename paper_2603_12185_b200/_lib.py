@@ -47,7 +47,7 @@ class comfree_worlds(ct.Structure):
 class comfree_contacts(ct.Structure):
     _fields_ = [("n_contacts", ct.c_int64), ("world", ct.c_void_p), ("off", ct.c_void_p),
                 ("c0", ct.c_void_p), ("c1", ct.c_void_p), ("c2", ct.c_void_p), ("c3", ct.c_void_p),
-                ("jrow", ct.c_void_p), ("impulses", ct.c_void_p), ("foff", ct.c_void_p),
+                ("jrow", ct.c_void_p), ("kd", ct.c_void_p), ("impulses", ct.c_void_p), ("foff", ct.c_void_p),
                 ("impulses_capacity", ct.c_int64), ("flags", ct.c_uint32), ("location", ct.c_int32)]
 
 

@@ -58,9 +58,9 @@ struct comfree_ctx {
   int* d_err = nullptr;
   unsigned long long* d_first_bad = nullptr;
   // S0 scratch
-  DevBuf off, keys, perm, iota, s0, s1, s2, s3, sj, nf, foff, cub_tmp;
+  DevBuf off, keys, perm, iota, s0, s1, s2, s3, sj, skd, nf, foff, cub_tmp;
   // host-input staging
-  DevBuf in_world, in_off, in_c0, in_c1, in_c2, in_c3, in_jrow, in_fext, in_L, in_tau, imp;
+  DevBuf in_world, in_off, in_c0, in_c1, in_c2, in_c3, in_jrow, in_kd, in_fext, in_L, in_tau, imp;
   DevBuf st_tmp;
   int64_t launches = 0;
   int64_t last_first = 0, last_nw = 0, last_nc = 0;
@@ -124,13 +124,15 @@ comfree_status check_latched(comfree_ctx* ctx, cudaStream_t s) {
   const unsigned long long none = ~0ull;
   CUDA_TRY(ctx, cudaMemcpy(ctx->d_err, &zero, sizeof zero, cudaMemcpyHostToDevice));
   CUDA_TRY(ctx, cudaMemcpy(ctx->d_first_bad, &none, sizeof none, cudaMemcpyHostToDevice));
-  if (e & (cf::ERR_UNSORTED | cf::ERR_WORLD_RANGE | cf::ERR_BODY_RANGE | cf::ERR_CONDIM | cf::ERR_IMPULSE_CAP))
-    return fail(ctx, COMFREE_ERR_VALIDATION, "device validation failed (flags 0x%x):%s%s%s%s%s", e,
+  if (e & (cf::ERR_UNSORTED | cf::ERR_WORLD_RANGE | cf::ERR_BODY_RANGE | cf::ERR_CONDIM | cf::ERR_IMPULSE_CAP |
+           cf::ERR_IMPEDANCE))
+    return fail(ctx, COMFREE_ERR_VALIDATION, "device validation failed (flags 0x%x):%s%s%s%s%s%s", e,
                 (e & cf::ERR_UNSORTED) ? " contacts not sorted by world;" : "",
                 (e & cf::ERR_WORLD_RANGE) ? " world id out of range;" : "",
                 (e & cf::ERR_BODY_RANGE) ? " body id out of range or chain side without J rows;" : "",
                 (e & cf::ERR_CONDIM) ? " condim not in {1,3,4,6};" : "",
-                (e & cf::ERR_IMPULSE_CAP) ? " impulses buffer too small;" : "");
+                (e & cf::ERR_IMPULSE_CAP) ? " impulses buffer too small;" : "",
+                (e & cf::ERR_IMPEDANCE) ? " per-contact impedance negative or non-finite;" : "");
   return fail(ctx, COMFREE_ERR_NONFINITE, "non-finite state in world %lld", (long long)bad);
 }
 
@@ -388,6 +390,8 @@ comfree_status comfree_step(comfree_ctx* ctx, const comfree_worlds* wd, const co
   if ((st = stage(ctx, ctx->in_c2, c->c2, (size_t)n * 4, loc, s, &c2)) != COMFREE_OK) return st;
   if ((st = stage(ctx, ctx->in_c3, c->c3, (size_t)n * 4, loc, s, &c3)) != COMFREE_OK) return st;
   if ((st = stage(ctx, ctx->in_jrow, c->jrow, (size_t)n * 48, loc, s, &jrow)) != COMFREE_OK) return st;
+  const float* kdp = nullptr;
+  if ((st = stage(ctx, ctx->in_kd, c->kd, (size_t)n * 2, loc, s, &kdp)) != COMFREE_OK) return st;
   const float *fext = nullptr, *tL = nullptr, *ttau = nullptr;
   const int wloc = wd->location;
   if ((st = stage(ctx, ctx->in_fext, wd->f_ext, (size_t)nw * sc.B * 6, wloc, s, &fext)) != COMFREE_OK) return st;
@@ -398,6 +402,7 @@ comfree_status comfree_step(comfree_ctx* ctx, const comfree_worlds* wd, const co
   const int64_t* off = off_in;
   const int32_t* perm = nullptr;
   const float4 *k0 = (const float4*)c0, *k1 = (const float4*)c1, *k2 = (const float4*)c2, *kj = (const float4*)jrow;
+  const float2* kk = (const float2*)kdp;
   const int4* k3 = (const int4*)c3;
   ctx->last_sorted_copy = false;
   const int32_t* fused_world = nullptr;
@@ -431,12 +436,15 @@ comfree_status comfree_step(comfree_ctx* ctx, const comfree_worlds* wd, const co
       CUDA_TRY(ctx, ensure(ctx->s2, std::max<size_t>(1, n) * 16));
       CUDA_TRY(ctx, ensure(ctx->s3, std::max<size_t>(1, n) * 16));
       if (jrow) CUDA_TRY(ctx, ensure(ctx->sj, std::max<size_t>(1, n) * 16 * 12));
-      CUDA_TRY(ctx, cf::launch_gather_contacts(static_cast<int32_t*>(ctx->perm.p), n, k0, k1, k2, k3, kj,
+      if (kk) CUDA_TRY(ctx, ensure(ctx->skd, std::max<size_t>(1, n) * 8));
+      CUDA_TRY(ctx, cf::launch_gather_contacts(static_cast<int32_t*>(ctx->perm.p), n, k0, k1, k2, k3, kj, kk,
                                                (float4*)ctx->s0.p, (float4*)ctx->s1.p, (float4*)ctx->s2.p,
-                                               (int4*)ctx->s3.p, jrow ? (float4*)ctx->sj.p : nullptr, s));
+                                               (int4*)ctx->s3.p, jrow ? (float4*)ctx->sj.p : nullptr,
+                                               kk ? (float2*)ctx->skd.p : nullptr, s));
       ctx->launches += 5;
       k0 = (const float4*)ctx->s0.p; k1 = (const float4*)ctx->s1.p; k2 = (const float4*)ctx->s2.p;
       k3 = (const int4*)ctx->s3.p; kj = jrow ? (const float4*)ctx->sj.p : nullptr;
+      kk = kk ? (const float2*)ctx->skd.p : nullptr;
       perm = static_cast<int32_t*>(ctx->perm.p);
       ctx->last_sorted_copy = true;
     }
@@ -505,7 +513,7 @@ comfree_status comfree_step(comfree_ctx* ctx, const comfree_worlds* wd, const co
   P.off = off;
   P.world_sorted = fused_world;
   P.off_out = fused_world ? const_cast<int64_t*>(off) : nullptr;
-  P.c0 = k0; P.c1 = k1; P.c2 = k2; P.c3 = k3; P.jrow = kj;
+  P.c0 = k0; P.c1 = k1; P.c2 = k2; P.c3 = k3; P.jrow = kj; P.kd = kk;
   P.n_contacts = n;
   P.perm = perm;
   P.foff = foff;
@@ -691,8 +699,8 @@ void comfree_destroy(comfree_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaDeviceSynchronize();
   DevBuf* bufs[] = {&ctx->off, &ctx->keys, &ctx->perm, &ctx->iota, &ctx->s0, &ctx->s1, &ctx->s2, &ctx->s3,
-                    &ctx->sj, &ctx->nf, &ctx->foff, &ctx->cub_tmp, &ctx->in_world, &ctx->in_off, &ctx->in_c0,
-                    &ctx->in_c1, &ctx->in_c2, &ctx->in_c3, &ctx->in_jrow, &ctx->in_fext, &ctx->in_L,
+                    &ctx->sj, &ctx->skd, &ctx->nf, &ctx->foff, &ctx->cub_tmp, &ctx->in_world, &ctx->in_off, &ctx->in_c0,
+                    &ctx->in_c1, &ctx->in_c2, &ctx->in_c3, &ctx->in_jrow, &ctx->in_kd, &ctx->in_fext, &ctx->in_L,
                     &ctx->in_tau, &ctx->imp, &ctx->st_tmp};
   for (DevBuf* b : bufs) release(*b);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);

@@ -15,7 +15,8 @@ enum : int {
   ERR_WORLD_RANGE = 4,  // world id outside [0, n_worlds)
   ERR_BODY_RANGE = 8,   // body id out of range / tree side without J rows
   ERR_CONDIM = 16,      // condim not in {1,3,4,6}
-  ERR_IMPULSE_CAP = 32  // impulses buffer too small
+  ERR_IMPULSE_CAP = 32, // impulses buffer too small
+  ERR_IMPEDANCE = 64    // per-contact (k_user, d_user) negative or non-finite
 };
 
 // State slab: per world, 13 planes of Bp floats (px py pz qw qx qy qz vx vy vz
@@ -56,6 +57,7 @@ struct StepParams {
   const float4* c2;
   const int4* c3;
   const float4* jrow;           // [12][n_contacts] or null
+  const float2* kd;             // [n_contacts] per-contact (k_user, d_user) or null
   int64_t n_contacts;
   const int32_t* perm;          // sorted position -> input index, or null (identity)
   const int64_t* foff;          // [n_contacts + 1] facet offsets (input order) or null
@@ -81,8 +83,9 @@ cudaError_t sort_by_world(const int32_t* world, int64_t n, int64_t n_worlds, int
                           int32_t* perm_out, int32_t* iota_tmp, void* temp, size_t* temp_bytes,
                           cudaStream_t s);
 cudaError_t launch_gather_contacts(const int32_t* perm, int64_t n, const float4* c0, const float4* c1,
-                                   const float4* c2, const int4* c3, const float4* jrow, float4* o0,
-                                   float4* o1, float4* o2, int4* o3, float4* ojrow, cudaStream_t s);
+                                   const float4* c2, const int4* c3, const float4* jrow, const float2* kd,
+                                   float4* o0, float4* o1, float4* o2, int4* o3, float4* ojrow, float2* okd,
+                                   cudaStream_t s);
 cudaError_t facet_offsets(const int4* c3, int64_t n, int n_t, int n_rol, int32_t* nf_tmp,
                           int64_t* foff, void* temp, size_t* temp_bytes, int* err, cudaStream_t s);
 cudaError_t launch_iota(int32_t* out, int64_t n, cudaStream_t s);

@@ -72,8 +72,9 @@ __global__ void k_iota(int32_t* out, int64_t n) {
 __global__ void k_gather(const int32_t* __restrict__ perm, int64_t n, const float4* __restrict__ c0,
                          const float4* __restrict__ c1, const float4* __restrict__ c2,
                          const int4* __restrict__ c3, const float4* __restrict__ jrow,
+                         const float2* __restrict__ kd,
                          float4* __restrict__ o0, float4* __restrict__ o1, float4* __restrict__ o2,
-                         int4* __restrict__ o3, float4* __restrict__ oj) {
+                         int4* __restrict__ o3, float4* __restrict__ oj, float2* __restrict__ okd) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int64_t src = perm[i];
@@ -83,6 +84,7 @@ __global__ void k_gather(const int32_t* __restrict__ perm, int64_t n, const floa
   o3[i] = c3[src];
   if (jrow)
     for (int s = 0; s < 12; ++s) oj[(size_t)s * n + i] = jrow[(size_t)s * n + src];
+  if (kd) okd[i] = kd[src];
 }
 
 // facets per contact (condim -> 1 / n_t / n_t + 2 / n_t + 2 + n_rol); the
@@ -138,10 +140,11 @@ cudaError_t sort_by_world(const int32_t* world, int64_t n, int64_t W, int32_t* k
 }
 
 cudaError_t launch_gather_contacts(const int32_t* perm, int64_t n, const float4* c0, const float4* c1,
-                                   const float4* c2, const int4* c3, const float4* jrow, float4* o0,
-                                   float4* o1, float4* o2, int4* o3, float4* oj, cudaStream_t s) {
+                                   const float4* c2, const int4* c3, const float4* jrow, const float2* kd,
+                                   float4* o0, float4* o1, float4* o2, int4* o3, float4* oj, float2* okd,
+                                   cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  k_gather<<<blocks_for(n), 256, 0, s>>>(perm, n, c0, c1, c2, c3, jrow, o0, o1, o2, o3, oj);
+  k_gather<<<blocks_for(n), 256, 0, s>>>(perm, n, c0, c1, c2, c3, jrow, kd, o0, o1, o2, o3, oj, okd);
   return cudaGetLastError();
 }
 

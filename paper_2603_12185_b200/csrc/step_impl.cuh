@@ -406,7 +406,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
       }
     }
   }
-  const float k = P.k, kappa = P.kappa;
+  const float k = P.k, kappa_g = P.kappa;
   int n_active = 0;
   float max_pen = 0.f;
   float4 C0 = make_float4(0.f, 0.f, 0.f, 0.f), C1 = C0, C2 = C0;
@@ -613,8 +613,17 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
       // S3: M(phi) (Eq. (12)-(13))
       const float r = impedance_r<FAST>(P, phi);
       const float Mc = __fdividef(r, (1.f - r) * tr);
-      // S4: Lambda_f = Mc (A + kappa mu (d . w))_+,  A = -k phi - kappa u_n
-      const float A = -k * phi - kappa * un;
+      // S4: Lambda_f = Mc (A + kappa mu (d . w))_+,  A = -k phi - kappa u_n,
+      // with the contact's own (k_user, d_user) when given
+      float kc = k, kappa = kappa_g;
+      if (IMP && P.kd) {
+        const float2 kd = P.kd[cbeg + min(j, max(nloc - 1, 0))];
+        if (valid && !(kd.x >= 0.f && kd.y >= 0.f && kd.x < INFINITY && kd.y < INFINITY))
+          atomicOr(P.err, ERR_IMPEDANCE);
+        kc = kd.x;
+        kappa = kd.x * P.dt + kd.y;
+      }
+      const float A = -kc * phi - kappa * un;
       float N = 0.f, F1 = 0.f, F2 = 0.f;
       float* out = nullptr;
       if (IMP && P.impulses && valid) {
@@ -857,7 +866,7 @@ cudaError_t launch_variant(const StepParams& p, cudaStream_t s) {
 // every other configuration takes the general facet loop and __powf.
 template <int CW, int WPW>
 cudaError_t launch_cfg(const StepParams& p, cudaStream_t s) {
-  const bool trees = p.sc.T > 0, imp = p.impulses != nullptr;
+  const bool trees = p.sc.T > 0, imp = p.impulses != nullptr || p.kd != nullptr;  // IMP: optional per-contact I/O
   if (p.n_t == 4 && p.power_is_2) {
     if (trees) return imp ? launch_variant<CW, WPW, true, true, true>(p, s) : launch_variant<CW, WPW, true, true, false>(p, s);
     return imp ? launch_variant<CW, WPW, true, false, true>(p, s) : launch_variant<CW, WPW, true, false, false>(p, s);

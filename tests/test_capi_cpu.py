@@ -56,7 +56,7 @@ def test_struct_layouts_match_c(tmp_path):
 
 
 def test_abi_version_and_status_strings(lib):
-    assert lib.comfree_abi_version() == 1
+    assert lib.comfree_abi_version() == 2
     for s in range(7):
         assert lib.comfree_status_string(s)
 

@@ -354,6 +354,50 @@ def test_trajectory_c2b_stack_6d():
     _traj_compare(CFG.with_(n_t=8, n_rol=8), scene, st, geo)
 
 
+# ---------------------------------------------------------------- per-contact impedance
+def _kd(c, seed, lo=0.02, hi=0.6):
+    rng = np.random.default_rng(seed)
+    c2 = c.take(np.arange(c.n))
+    c2.kd = np.stack([rng.uniform(lo, hi, c.n), rng.uniform(0.0, 0.01, c.n)], 1).astype(np.float32)
+    return c2
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_per_contact_impedance_random(seed):
+    """Per-contact (k_user, d_user) on mixed instances,
+    unsorted ids (the pairs are permuted with the contacts), chains."""
+    scene, st, c, inp = scenes.random_instance(1100 + seed, n_worlds=5, n_bodies=6, contacts_per_world=[9, 0, 33, 70, 2],
+                                               n_trees=2 if seed else 0)
+    c = _kd(scenes.shuffle_contacts(c, seed), seed)
+    compare_step(gpu_step(CFG, scene, st, c, inp), oracle.step(CFG, scene, st, c, inp))
+
+
+def test_per_contact_impedance_pile_and_identity():
+    """C4-shaped pile with per-contact pairs (sorted ids, fused S0); pairs equal
+    to the config's globals reproduce the plain step."""
+    scene, st, c = scenes.c4_pile(n_worlds=6, contacts_per_world=700)
+    ck = _kd(c, 7)
+    compare_step(gpu_step(CFG, scene, st, ck, None), oracle.step(CFG, scene, st, ck, None))
+    cg = c.take(np.arange(c.n))
+    cg.kd = np.tile(np.array([CFG.k_user, CFG.d_user], np.float32), (c.n, 1))
+    a, b = gpu_step(CFG, scene, st, cg, None), gpu_step(CFG, scene, st, c, None)
+    for k in ("pos", "quat", "vel", "omega"):
+        np.testing.assert_allclose(getattr(a["state"], k), getattr(b["state"], k), rtol=1e-6, atol=1e-7)
+
+
+def test_per_contact_impedance_invalid_is_validation_error():
+    import paper_2603_12185_b200 as cf
+    scene, st, c = scenes.c4_pile(n_worlds=3, contacts_per_world=40)
+    ck = _kd(c, 3)
+    ck.kd[17] = (-0.1, 0.0)
+    ctx = cf.Context(CFG)
+    ctx.load_scene(scene, 3, st)
+    ctx.step(cf.DeviceContacts.from_host(ck), None)
+    with pytest.raises(cf.ComfreeError) as ei:
+        ctx.get_state()
+    assert ei.value.status == 2 and "impedance" in str(ei.value)
+
+
 # ---------------------------------------------------------------- C5 mixed
 def test_c5_mixed_two_contexts_concurrent_streams():
     """Config 5: hand and pile-lite worlds as two contexts stepped concurrently
