@@ -616,7 +616,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
       // S4: Lambda_f = Mc (A + kappa mu (d . w))_+,  A = -k phi - kappa u_n,
       // with the contact's own (k_user, d_user) when given
       float kc = k, kappa = kappa_g;
-      if (IMP && P.kd) {
+      if (P.kd) {  // warp-uniform
         const float2 kd = P.kd[cbeg + min(j, max(nloc - 1, 0))];
         if (valid && !(kd.x >= 0.f && kd.y >= 0.f && kd.x < INFINITY && kd.y < INFINITY))
           atomicOr(P.err, ERR_IMPEDANCE);
@@ -866,7 +866,7 @@ cudaError_t launch_variant(const StepParams& p, cudaStream_t s) {
 // every other configuration takes the general facet loop and __powf.
 template <int CW, int WPW>
 cudaError_t launch_cfg(const StepParams& p, cudaStream_t s) {
-  const bool trees = p.sc.T > 0, imp = p.impulses != nullptr || p.kd != nullptr;  // IMP: optional per-contact I/O
+  const bool trees = p.sc.T > 0, imp = p.impulses != nullptr;
   if (p.n_t == 4 && p.power_is_2) {
     if (trees) return imp ? launch_variant<CW, WPW, true, true, true>(p, s) : launch_variant<CW, WPW, true, true, false>(p, s);
     return imp ? launch_variant<CW, WPW, true, false, true>(p, s) : launch_variant<CW, WPW, true, false, false>(p, s);
