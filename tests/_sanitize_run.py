@@ -22,4 +22,11 @@ scene, st, c, inp = scenes.random_instance(12, n_worlds=2, n_bodies=3, contacts_
 gpu_step(cfg, scene, st, c, inp)                                                 # articulated chains
 scene, st, c = scenes.c4_pile(n_worlds=2, contacts_per_world=300, lattice=(5, 5, 2))
 gpu_step(cfg, scene, st, c, None, host=True)                                     # host buffers, big-world CTA path
+ck = c.take(np.arange(c.n))
+ck.kd = np.tile(np.array([0.2, 0.001], np.float32), (c.n, 1))
+gpu_step(cfg, scene, st, ck, None)                                               # per-contact impedance, fused S0
+scene, st, c, inp = scenes.random_instance(13, n_worlds=3, n_bodies=4, contacts_per_world=[5, 20, 0])
+c = scenes.shuffle_contacts(c, 2)
+c.kd = np.tile(np.array([0.3, 0.002], np.float32), (c.n, 1))
+gpu_step(cfg, scene, st, c, inp)                                                 # per-contact impedance, sort + gather
 print("sanitize run ok")
