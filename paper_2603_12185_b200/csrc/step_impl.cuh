@@ -88,18 +88,6 @@ __device__ __forceinline__ int4 ld_stream(const int4* p) {
   return r;
 }
 
-// TMA bulk prefetch of [p, p + bytes) into L2 (16-byte aligned, multiple of 16);
-// issued in pieces of at most 64 KB.
-__device__ __forceinline__ void bulk_prefetch_l2(const void* p, uint32_t bytes) {
-  const char* c = static_cast<const char*>(p);
-  while (bytes > 0) {
-    const uint32_t n = bytes > 65536u ? 65536u : bytes;
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(c), "r"(n) : "memory");
-    c += n;
-    bytes -= n;
-  }
-}
-
 __device__ __forceinline__ float3 cross3(float3 a, float3 b) {
   return make_float3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
 }
@@ -334,7 +322,7 @@ __device__ __forceinline__ void lower_bound2(const int32_t* a, int64_t n, int64_
 
 template <bool RUNS>
 __device__ __forceinline__ void scatter_side(unsigned* accl, const float4* rec, int Bp, int key, float v[6],
-                                             int lane, float, float) {
+                                             int lane) {
   const bool tail = (!RUNS || seg_sum6(key, v, lane)) && key >= 0;
   if (tail) {
     // scales from the body record in shared memory (keeping side a's values in
@@ -556,7 +544,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
     float3 vrel = make_float3(0.f, 0.f, 0.f), wrel = make_float3(0.f, 0.f, 0.f);
     float tr = 0.f;
     float3 ra = make_float3(0.f, 0.f, 0.f), rb = make_float3(0.f, 0.f, 0.f);
-    float ima = 0.f, dma = 0.f, imb = 0.f, dmb = 0.f;  // m^-1 and max diag I_w^-1 per side (S6 scales)
+    float imb = 0.f, dmb = 0.f;  // side b's m^-1 and max diag I_w^-1 (S6 scales)
 #pragma unroll
     for (int side = 0; side < 2; ++side) {
       const int id = side ? idb : ida;
@@ -579,8 +567,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
                                       Ixz * r.x + Iyz * r.y + Izz * r.z);
         const float trs = 3.f * r0.w + (Ixx + Iyy + Izz) * dot3(r, r) - dot3(r, Ir);
         tr += trs;
-        const float dm = fmaxf(fmaxf(Ixx, Iyy), Izz);
-        if (side) { rb = r; imb = r0.w; dmb = dm; } else { ra = r; ima = r0.w; dma = dm; }
+        if (side) { rb = r; imb = r0.w; dmb = fmaxf(fmaxf(Ixx, Iyy), Izz); } else { ra = r; }
       }
       if (TREES && id < -1) {
         const int t = -2 - id;
@@ -681,7 +668,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
     {
       const float3 ma = cross3(ra, f), mb = cross3(rb, f);
       float va[6] = {-f.x, -f.y, -f.z, -(ma.x + tau.x), -(ma.y + tau.y), -(ma.z + tau.z)};
-      scatter_side<true>(accl, rec, Bp, ida >= 0 ? ida : -1, va, lane, ima, dma);
+      scatter_side<true>(accl, rec, Bp, ida >= 0 ? ida : -1, va, lane);
       float vb[6] = {f.x, f.y, f.z, mb.x + tau.x, mb.y + tau.y, mb.z + tau.z};
       scatter_own(accl, Bp, idb >= 0 ? idb : -1, vb, imb, dmb);
     }
