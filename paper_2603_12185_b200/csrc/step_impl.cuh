@@ -512,10 +512,14 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
   }
   for (; base < nloc; base += kGT) {
     const int j = base + lane;
+    // Next-contact prefetch: free-body variants load it once this contact's
+    // fields are dead (after S5), so the loads reuse the same registers (no
+    // copies); chain variants load it here, at the top of the iteration.
+    constexpr bool kLatePrefetch = !TREES;
     const float4 c0 = C0, c1 = C1, c2 = C2;
     const int4 c3 = C3;
     const int wid = WID;
-    {  // prefetch this lane's next contact (index clamped: no branch)
+    auto prefetch_next = [&]() {  // index clamped: no branch
       const int jn = min(j + kGT, nloc - 1);
       // global index made opaque so the stream addresses are formed from the
       // kernel parameters each time (no per-stream 64-bit pointers held live)
@@ -523,7 +527,8 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
       asm volatile("" : "+l"(g));
       C0 = ld_stream(P.c0 + g); C1 = ld_stream(P.c1 + g); C2 = ld_stream(P.c2 + g); C3 = ld_stream(P.c3 + g);
       if (P.world_sorted) WID = ld_id(P.world_sorted + g);
-    }
+    };
+    if (!kLatePrefetch) prefetch_next();
 
     int ida = c3.x, idb = c3.y;
     const int cd = c3.w;
@@ -662,6 +667,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
                       fn * n.z + ft1 * t1.z + ft2 * t2.z);
       if (!valid) f = make_float3(0.f, 0.f, 0.f);
     }
+    if (kLatePrefetch) prefetch_next();
     // S6: scatter J^T (f, tau).  Free bodies get (f, r x f + tau) per side:
     // the warp sums runs of equal body ids (contacts sorted by body pair make
     // them long), then each run's last lane adds the total in fixed point.
