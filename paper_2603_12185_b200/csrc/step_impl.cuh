@@ -320,16 +320,20 @@ __device__ __forceinline__ void lower_bound2(const int32_t* a, int64_t n, int64_
 #define ACC_LO(q, k) (accl + 2 * ((q) * Bp + (k)))
 #define ACC_HI(q, k) (reinterpret_cast<int*>(accl) + 2 * ((q) * Bp + (k)) + 1)
 
-template <bool RUNS>
-__device__ __forceinline__ void scatter_side(unsigned* accl, const float4* rec, int Bp, int key, float v[6],
-                                             int lane) {
+template <bool RUNS, bool OWN>
+__device__ __forceinline__ void scatter_side(unsigned* accl, const float4* rec, int Bp, int key, float v[6], int lane,
+                                             float im_own, float dm_own) {
   const bool tail = (!RUNS || seg_sum6(key, v, lane)) && key >= 0;
   if (tail) {
-    // scales from the body record in shared memory (keeping side a's values in
-    // registers across S3-S5 spills at 64 registers)
-    const float* r = reinterpret_cast<const float*>(rec);
-    const float im = r[4 * key + 3];
-    const float dmax = fmaxf(fmaxf(r[4 * (Bp + key) + 3], r[4 * (2 * Bp + key) + 3]), r[4 * (3 * Bp + key)]);
+    // scales: OWN = from the run's last lane's own side-a record (registers of
+    // S2; that lane's body is the run's body), else reloaded from shared memory
+    // (chain variants, where the extra live registers cost more)
+    float im = im_own, dmax = dm_own;
+    if (!OWN) {
+      const float* r = reinterpret_cast<const float*>(rec);
+      im = r[4 * key + 3];
+      dmax = fmaxf(fmaxf(r[4 * (Bp + key) + 3], r[4 * (2 * Bp + key) + 3]), r[4 * (3 * Bp + key)]);
+    }
     const float sl = fx_pow2(fx_exp(im)), sa = fx_pow2(fx_exp(dmax));
 #pragma unroll
     for (int q = 0; q < 6; ++q) fx_add(ACC_LO(q, key), ACC_HI(q, key), v[q], q < 3 ? sl : sa);
@@ -549,7 +553,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
     float3 vrel = make_float3(0.f, 0.f, 0.f), wrel = make_float3(0.f, 0.f, 0.f);
     float tr = 0.f;
     float3 ra = make_float3(0.f, 0.f, 0.f), rb = make_float3(0.f, 0.f, 0.f);
-    float imb = 0.f, dmb = 0.f;  // side b's m^-1 and max diag I_w^-1 (S6 scales)
+    float ima = 0.f, dma = 0.f, imb = 0.f, dmb = 0.f;  // m^-1 and max diag I_w^-1 per side (S6 scales)
 #pragma unroll
     for (int side = 0; side < 2; ++side) {
       const int id = side ? idb : ida;
@@ -572,7 +576,8 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
                                       Ixz * r.x + Iyz * r.y + Izz * r.z);
         const float trs = 3.f * r0.w + (Ixx + Iyy + Izz) * dot3(r, r) - dot3(r, Ir);
         tr += trs;
-        if (side) { rb = r; imb = r0.w; dmb = fmaxf(fmaxf(Ixx, Iyy), Izz); } else { ra = r; }
+        const float dm = fmaxf(fmaxf(Ixx, Iyy), Izz);
+        if (side) { rb = r; imb = r0.w; dmb = dm; } else { ra = r; ima = r0.w; dma = dm; }
       }
       if (TREES && id < -1) {
         const int t = -2 - id;
@@ -674,7 +679,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
     {
       const float3 ma = cross3(ra, f), mb = cross3(rb, f);
       float va[6] = {-f.x, -f.y, -f.z, -(ma.x + tau.x), -(ma.y + tau.y), -(ma.z + tau.z)};
-      scatter_side<true>(accl, rec, Bp, ida >= 0 ? ida : -1, va, lane);
+      scatter_side<true, !TREES>(accl, rec, Bp, ida >= 0 ? ida : -1, va, lane, ima, dma);
       float vb[6] = {f.x, f.y, f.z, mb.x + tau.x, mb.y + tau.y, mb.z + tau.z};
       scatter_own(accl, Bp, idb >= 0 ? idb : -1, vb, imb, dmb);
     }
