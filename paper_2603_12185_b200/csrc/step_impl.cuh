@@ -25,7 +25,8 @@
 //                 finite check and per-world statistics.
 // WPW = 8: one 256-thread CTA per world (dense piles); WPW = 1: eight worlds per
 // CTA, one warp each (hand + cube); pick_wpw (capi.cpp) chooses.  TREES / IMP
-// compile the articulated sides and the per-facet impulse output in or out.
+// compile the articulated sides and the optional outputs (per-facet impulses,
+// per-world statistics) in or out.
 #pragma once
 #include <cuda_runtime.h>
 #include <math.h>
@@ -377,7 +378,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
   const int B = sc.B, Bp = sc.Bp, T = sc.T, nd = sc.nd;
   float* slab = P.slab + (size_t)w * sc.slab;
   const float dt = P.dt;
-  const bool stats = P.wstats != nullptr;
+  const bool stats = IMP && P.wstats != nullptr;  // IMP: per-facet impulses and/or statistics requested
 
   // S0 (sorted input, fused): the first warp of the group locates this world's
   // contact range while the others start on S1.
@@ -864,7 +865,7 @@ cudaError_t launch_variant(const StepParams& p, cudaStream_t s) {
 // every other configuration takes the general facet loop and __powf.
 template <int CW, int WPW>
 cudaError_t launch_cfg(const StepParams& p, cudaStream_t s) {
-  const bool trees = p.sc.T > 0, imp = p.impulses != nullptr;
+    const bool trees = p.sc.T > 0, imp = p.impulses != nullptr || p.wstats != nullptr;
   if (p.n_t == 4 && p.power_is_2) {
     if (trees) return imp ? launch_variant<CW, WPW, true, true, true>(p, s) : launch_variant<CW, WPW, true, true, false>(p, s);
     return imp ? launch_variant<CW, WPW, true, false, true>(p, s) : launch_variant<CW, WPW, true, false, false>(p, s);
