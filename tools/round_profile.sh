@@ -14,3 +14,4 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_st
     python bench.py --workload hand --steps 2 --warmup 3 --cpu-seconds 0.1 --e2e-steps 1 > /dev/null 2>&1
 bash tools/sweep_contacts.sh ${TAG} > gpurun_out/${TAG}_c4_sweep.txt 2>&1
 ls -la gpurun_out | grep $TAG
+timeout 600 python bench.py --kd --cpu-seconds 0.5 > gpurun_out/${TAG}_bench_pile_kd.json 2> gpurun_out/${TAG}_bench_pile_kd.err
