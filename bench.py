@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to exercise the multi-rank path on a single GPU")
+    ap.add_argument("--condim", type=int, default=3, choices=[1, 3, 4, 6],
+                    help="pile contact dimensionality (3: the BASELINE config; 6: the 6D variant, n_t = n_rol = 4)")
     ap.add_argument("--kd", action="store_true",
                     help="per-contact (k_user, d_user) impedance arrays (learned-impedance variant, P:206-208)")
     ap.add_argument("--workload", default="pile", choices=["pile", "hand", "mixed"],
@@ -186,9 +188,10 @@ def _workload(args, rank, world_size):
                  Part("hand", sh, sth, ch, ih, _hand_bytes(sh, ch, sth.n_worlds))]
         return parts, "c5 mixed: half c3 hand, half pile-lite (100 bodies, 400 contacts)", n
     W = args.worlds
-    scene, st, c = scenes.c4_pile(n_worlds=W, contacts_per_world=args.contacts, world_offset=rank * W)
+    scene, st, c = scenes.c4_pile(n_worlds=W, contacts_per_world=args.contacts, world_offset=rank * W,
+                                  condim=args.condim)
     return [Part("pile", scene, st, c, None, W * (args.contacts * BYTES_PER_CONTACT + scene.n_bodies * BYTES_PER_BODY))], \
-        "c4 dense pile", W
+        "c4 dense pile" + ("" if args.condim == 3 else f" (condim {args.condim})"), W
 
 
 # ---------------------------------------------------------------- oracle (CPU) timing
@@ -452,7 +455,8 @@ def run_ours(args, rank, world_size, local):
                        "parts": {p.name: {"worlds": p.W, "contacts_per_world": p.c.n // p.W,
                                           "bodies_per_world": p.scene.n_bodies, "chains_per_world": p.scene.n_trees}
                                  for p in parts},
-                       "facets_per_contact": 4, "condim": 3, "dt": cfg.dt,
+                       "facets_per_contact": {1: 1, 3: 4, 4: 6, 6: 10}[args.condim], "condim": args.condim,
+                       "dt": cfg.dt,
                        "l2": "flushed between timed steps (256 MB write)" if flush is not None else "not flushed",
                        "footprint_mb_per_step": alg_total / 1e6,
                        "parallelism": f"world-sharded x{world_size}"},
