@@ -12,6 +12,9 @@ import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libcomfree.so")
+# tuning experiments only: a variant build of the same sources (build.py --variant)
+if os.environ.get("COMFREE_LIB"):
+    LIB_PATH = os.path.abspath(os.environ["COMFREE_LIB"])
 
 COMFREE_OK = 0
 STATUS_NAMES = {0: "OK", 1: "ERR_INVALID_ARGUMENT", 2: "ERR_VALIDATION", 3: "ERR_CAPACITY",

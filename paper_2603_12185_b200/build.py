@@ -28,18 +28,23 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    os.makedirs(OBJDIR, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, defines=(), tag: str = "") -> str:
+    """Build libcomfree.so; with `tag`, a variant (extra -D `defines`) into
+    _build_<tag>/libcomfree_<tag>.so for tuning experiments (COMFREE_LIB)."""
+    objdir = OBJDIR + ("_" + tag if tag else "")
+    lib = os.path.join(objdir, f"libcomfree_{tag}.so") if tag else LIB
+    dflags = [f"-D{d}" for d in defines]
+    os.makedirs(objdir, exist_ok=True)
     headers = [os.path.join(CSRC, "internal.h"), os.path.join(CSRC, "step_impl.cuh"),
                os.path.join(INCLUDE, "comfree.h")]
     objs = []
     jobs = []
     for src in CU_SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(OBJDIR, src + ".o")
+        o = os.path.join(objdir, src + ".o")
         objs.append(o)
         if force or _stale(o, [s] + headers):
-            jobs.append([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+            jobs.append([NVCC, *ARCH, *dflags, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                          "-Xptxas", "-v" if verbose else "-O3", "-I", INCLUDE, "-I", CSRC, "-c", s, "-o", o])
     from concurrent.futures import ThreadPoolExecutor
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
@@ -48,16 +53,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 raise subprocess.CalledProcessError(rc, "nvcc")
     for src in CPP_SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(OBJDIR, src + ".o")
+        o = os.path.join(objdir, src + ".o")
         objs.append(o)
         if force or _stale(o, [s] + headers):
-            cmd = [NVCC, "-x", "cu", *ARCH, "-O2", "-std=c++17", "-Xcompiler", "-fPIC,-Wall",
+            cmd = [NVCC, "-x", "cu", *ARCH, *dflags, "-O2", "-std=c++17", "-Xcompiler", "-fPIC,-Wall",
                    "-I", INCLUDE, "-I", CSRC, "-c", s, "-o", o]
             subprocess.check_call(cmd)
-    if force or _stale(LIB, objs):
-        subprocess.check_call([NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-cudart", "static"])
-    return LIB
+    if force or _stale(lib, objs):
+        subprocess.check_call([NVCC, *ARCH, "-shared", "-o", lib, *objs, "-cudart", "static"])
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--force", action="store_true")
+    ap.add_argument("-v", action="store_true")
+    ap.add_argument("--variant", default="", help="tag of a tuning variant build")
+    ap.add_argument("-D", action="append", default=[], help="extra preprocessor define (variant builds)")
+    a = ap.parse_args()
+    print(build(force=a.force, verbose=a.v, defines=a.D, tag=a.variant))

@@ -125,14 +125,15 @@ comfree_status check_latched(comfree_ctx* ctx, cudaStream_t s) {
   CUDA_TRY(ctx, cudaMemcpy(ctx->d_err, &zero, sizeof zero, cudaMemcpyHostToDevice));
   CUDA_TRY(ctx, cudaMemcpy(ctx->d_first_bad, &none, sizeof none, cudaMemcpyHostToDevice));
   if (e & (cf::ERR_UNSORTED | cf::ERR_WORLD_RANGE | cf::ERR_BODY_RANGE | cf::ERR_CONDIM | cf::ERR_IMPULSE_CAP |
-           cf::ERR_IMPEDANCE))
-    return fail(ctx, COMFREE_ERR_VALIDATION, "device validation failed (flags 0x%x):%s%s%s%s%s%s", e,
+           cf::ERR_IMPEDANCE | cf::ERR_WORLD_CONTACTS))
+    return fail(ctx, COMFREE_ERR_VALIDATION, "device validation failed (flags 0x%x):%s%s%s%s%s%s%s", e,
                 (e & cf::ERR_UNSORTED) ? " contacts not sorted by world;" : "",
                 (e & cf::ERR_WORLD_RANGE) ? " world id out of range;" : "",
                 (e & cf::ERR_BODY_RANGE) ? " body id out of range or chain side without J rows;" : "",
                 (e & cf::ERR_CONDIM) ? " condim not in {1,3,4,6};" : "",
                 (e & cf::ERR_IMPULSE_CAP) ? " impulses buffer too small;" : "",
-                (e & cf::ERR_IMPEDANCE) ? " per-contact impedance negative or non-finite;" : "");
+                (e & cf::ERR_IMPEDANCE) ? " per-contact impedance negative or non-finite;" : "",
+                (e & cf::ERR_WORLD_CONTACTS) ? " more than 65536 contacts in one world;" : "");
   return fail(ctx, COMFREE_ERR_NONFINITE, "non-finite state in world %lld", (long long)bad);
 }
 
@@ -161,6 +162,19 @@ cudaEvent_t next_event(comfree_ctx* ctx, int* idx) {
 }
 
 }  // namespace
+
+#ifdef CF_TIMELINE
+// Tuning builds only: per-CTA phase timestamps of the last step launch.
+static unsigned* g_tl = nullptr;
+static unsigned* cf_debug_timeline_buf() {
+  if (!g_tl) cudaMalloc(&g_tl, sizeof(unsigned) * 8 * (1 << 20));
+  return g_tl;
+}
+extern "C" int comfree_debug_timeline(unsigned* host, int64_t n_ctas) {
+  if (!g_tl) return -1;
+  return (int)cudaMemcpy(host, g_tl, sizeof(unsigned) * 8 * n_ctas, cudaMemcpyDeviceToHost);
+}
+#endif
 
 extern "C" {
 
@@ -524,6 +538,9 @@ comfree_status comfree_step(comfree_ctx* ctx, const comfree_worlds* wd, const co
   P.first_bad = ctx->d_first_bad;
   P.world_base = first;
   P.check_finite = !(cf_.flags & COMFREE_FLAG_NO_FINITE_CHECK);
+#ifdef CF_TIMELINE
+  P.timeline = cf_debug_timeline_buf();
+#endif
   int wpw = pick_wpw(sc, n, nw);
   if (const char* e = getenv("COMFREE_WPW")) {  // tuning override (1, 2, 4 or 8 warps per world)
     const int v = atoi(e);

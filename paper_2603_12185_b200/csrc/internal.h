@@ -16,7 +16,8 @@ enum : int {
   ERR_BODY_RANGE = 8,   // body id out of range / tree side without J rows
   ERR_CONDIM = 16,      // condim not in {1,3,4,6}
   ERR_IMPULSE_CAP = 32, // impulses buffer too small
-  ERR_IMPEDANCE = 64    // per-contact (k_user, d_user) negative or non-finite
+  ERR_IMPEDANCE = 64,   // per-contact (k_user, d_user) negative or non-finite
+  ERR_WORLD_CONTACTS = 128  // more contacts in one world than the S6 fixed-point bound (65536)
 };
 
 // State slab: per world, 13 planes of Bp floats (px py pz qw qx qy qz vx vy vz
@@ -68,6 +69,7 @@ struct StepParams {
   unsigned long long* first_bad;// min world id with a non-finite state
   int64_t world_base;           // absolute id of world 0 of the range (error reporting)
   int check_finite;
+  unsigned* timeline;           // CF_TIMELINE builds only: per CTA (smid, t0, t1, t2, t3) globaltimer ns
 };
 
 // Launchers (return cudaError_t of the launch).

@@ -35,9 +35,16 @@
 
 namespace cf {
 
+#ifndef CF_HI_ALWAYS
+#define CF_HI_ALWAYS 1
+#endif
 #ifndef CF_MINB
 #define CF_MINB 4
 #endif
+#ifndef CF_S1_UNROLL
+#define CF_S1_UNROLL 1
+#endif
+static constexpr int kS1Unroll = CF_S1_UNROLL;  // S1 bodies per thread in flight (unstaged S1)
 static constexpr int kWarps = 8;
 static constexpr int kThreads = kWarps * 32;
 
@@ -94,6 +101,21 @@ __device__ __forceinline__ float3 cross3(float3 a, float3 b) {
 }
 __device__ __forceinline__ float dot3(float3 a, float3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
 __device__ __forceinline__ float dot4(float4 a, float4 b) { return a.x * b.x + a.y * b.y + a.z * b.z + a.w * b.w; }
+#ifdef CF_TIMELINE
+__device__ __forceinline__ unsigned tl_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return (unsigned)t;
+}
+#define TL_MARK(k)                                                                     \
+  if (P.timeline && threadIdx.x == 0) {                                                \
+    unsigned* tlp = P.timeline + 8 * (size_t)blockIdx.x;                               \
+    if ((k) == 0) { unsigned sm; asm volatile("mov.u32 %0, %smid;" : "=r"(sm)); tlp[0] = sm; } \
+    tlp[1 + (k)] = tl_now();                                                           \
+  }
+#else
+#define TL_MARK(k)
+#endif
 __device__ __forceinline__ int tri(int i, int j) { return i * (i + 1) / 2 + j; }
 
 // x <- (L L^T)^-1 x for a chain of nd <= 4 DoFs (forward then backward
@@ -222,14 +244,22 @@ __device__ __forceinline__ bool seg_sum6(int key, float v[6], int lane) {
 
 // ---- S6 accumulation: 64-bit fixed point in shared memory ----------------
 // sm_100a has no native shared-memory fp32 add (atomicAdd compiles to a CAS
-// loop), but native 32-bit integer atomics.  Each accumulator is a 64-bit
-// two's-complement integer split in lo (uint32) and hi (int32) planes; a value
-// is added as round(v * 2^e) with an explicit carry from the lo word.  Integer
-// addition is associative, so the result does not depend on the order in which
-// warps arrive: the step is bitwise deterministic.  The scale 2^e is per body
-// and per component group: e = exponent(m^-1) + 33 for the linear part,
-// exponent(max diag I_w^-1) + 33 for the angular part, i.e. a velocity
-// resolution of about 2^-33 (1.2e-10) with a range of about 2^30 in velocity.
+// loop), but native 32-bit integer atomics.  Each value is added as the 64-bit
+// integer x = round(v * 2^e); integer addition is associative, so the result
+// does not depend on the order in which warps arrive: the step is bitwise
+// deterministic.  The scale 2^e is per body and per component group:
+// e = exponent(m^-1) + 33 for the linear part, exponent(max diag I_w^-1) + 33
+// for the angular part, i.e. a velocity resolution of about 2^-33 (1.2e-10).
+// Split form (default): the lo plane receives the low 16 bits of x (unsigned)
+// and the hi plane x >> 16, so neither atomic needs the other's result (no
+// carry, no returned value); the sum is hi * 2^16 + lo exactly while a world
+// has at most 65536 contacts (lo < 2^32) and |x| < 2^47 per add (checked,
+// ~16000 m/s of velocity change per contact).  CF_FX_SPLIT=0: lo/hi words of
+// one 64-bit integer with an explicit carry (the previous form).
+#ifndef CF_FX_SPLIT
+#define CF_FX_SPLIT 0  // split: measured neutral on C4 (61.6 us both), kept as a variant
+#endif
+static constexpr int kMaxWorldContacts = CF_FX_SPLIT ? 65536 : 0x7fffffff;
 __device__ __forceinline__ int fx_exp(float inv) {
   const int e = inv > 0.f ? ((__float_as_int(inv) >> 23) & 0xff) - 127 : 0;
   return max(-90, min(90, e + 33));
@@ -237,15 +267,28 @@ __device__ __forceinline__ int fx_exp(float inv) {
 __device__ __forceinline__ float fx_pow2(int e) { return __int_as_float((e + 127) << 23); }
 __device__ __forceinline__ void fx_add(unsigned* lo, int* hi, float v, float scale) {
   const long long x = __float2ll_rn(v * scale);
+#if CF_FX_SPLIT
+  atomicAdd(lo, (unsigned)x & 0xffffu);
+  atomicAdd(hi, (int)(x >> 16));
+#else
   const unsigned xl = (unsigned)x;
   const unsigned old = atomicAdd(lo, xl);
   int h;  // hi word + carry out of (old + xl): two instructions with the carry flag
   asm("{\n\t.reg .u32 t;\n\tadd.cc.u32 t, %1, %2;\n\taddc.s32 %0, %3, 0;\n\t}"
       : "=r"(h) : "r"(old), "r"(xl), "r"((int)(x >> 32)));
   atomicAdd(hi, h);
+#endif
+}
+// per-add range of the split form: |v| * scale < 2^47 (max over a group of values)
+__device__ __forceinline__ bool fx_over(float vmax_abs, float scale) {
+  return CF_FX_SPLIT && !(vmax_abs * scale < 1.40737488e14f);  // 2^47; NaN counts as over
 }
 __device__ __forceinline__ float fx_get(unsigned lo, int hi, float inv_scale) {
+#if CF_FX_SPLIT
+  const long long x = ((long long)hi << 16) + (long long)lo;
+#else
   const long long x = (long long)(((unsigned long long)(unsigned)hi << 32) | (unsigned long long)lo);
+#endif
   return __ll2float_rn(x) * inv_scale;
 }
 
@@ -261,6 +304,29 @@ __device__ __forceinline__ void lower_bound2(const int32_t* a, int64_t n, int64_
                                              int lane, int64_t& r0, int64_t& r1) {
   const unsigned full = 0xffffffffu;
   int64_t lo0 = 0, hi0 = n, lo1 = 0, hi1 = n;  // answers in [lo, hi]
+  {  // exact-guess round: 16 lanes per key read a[g - 8, g + 8) around the uniform
+     // guess g = key n / n_keys; worlds of equal size resolve here (one access)
+    const int half = lane >> 4, l = lane & 15;
+    const int64_t key = half ? key1 : key0;
+    int64_t g = (n_keys > 0 ? key * n / n_keys : 0) - 8;
+    const int64_t pp = g + l;
+    const bool q = pp < 0 || (pp < n && ld_id(a + pp) < key);  // a[-1] = -inf, a[n] = +inf
+    const unsigned b = __ballot_sync(full, q);
+    const unsigned b0 = b & 0xffffu, b1 = b >> 16;
+    const int64_t g0 = (n_keys > 0 ? key0 * n / n_keys : 0) - 8, g1 = (n_keys > 0 ? key1 * n / n_keys : 0) - 8;
+    // resolved when the window holds both a "< key" and a ">= key" position, or
+    // touches an end of the array on the matching side
+    const bool ok0 = (b0 & 1u) && !(b0 >> 15);
+    const bool ok1 = (b1 & 1u) && !(b1 >> 15);
+    if (ok0) lo0 = hi0 = g0 + __popc(b0);  // a resolved key keeps this answer in every later
+    if (ok1) lo1 = hi1 = g1 + __popc(b1);  // round (adjacent worlds agree even on unsorted ids)
+    if (ok0 && ok1) {
+      r0 = lo0;
+      r1 = lo1;
+      return;
+    }
+  }
+  const bool done0 = lo0 == hi0, done1 = lo1 == hi1;
   {  // first round: 16 lanes per key probe a window around the uniform guess k n / n_keys
     const int64_t avg = n_keys > 0 ? n / n_keys : n;
     const int64_t hw = 2 * avg + 32;
@@ -276,16 +342,20 @@ __device__ __forceinline__ void lower_bound2(const int32_t* a, int64_t n, int64_
     const int k0 = __popc(b & 0xffffu), k1 = __popc(b >> 16);
     const int64_t g0 = __shfl_sync(full, g, 0), s0 = __shfl_sync(full, step, 0);
     const int64_t g1 = __shfl_sync(full, g, 16), s1 = __shfl_sync(full, step, 16);
-    if (k0 == 0) { lo0 = 0; hi0 = g0; }
-    else if (k0 < 16) { lo0 = g0 + (k0 - 1) * s0 + 1; hi0 = g0 + k0 * s0; }
-    else { lo0 = g0 + 15 * s0 + 1; hi0 = n; }
-    if (k1 == 0) { lo1 = 0; hi1 = g1; }
-    else if (k1 < 16) { lo1 = g1 + (k1 - 1) * s1 + 1; hi1 = g1 + k1 * s1; }
-    else { lo1 = g1 + 15 * s1 + 1; hi1 = n; }
-    if (lo0 > n) lo0 = n;
-    if (hi0 > n) hi0 = n;
-    if (lo1 > n) lo1 = n;
-    if (hi1 > n) hi1 = n;
+    if (!done0) {
+      if (k0 == 0) { lo0 = 0; hi0 = g0; }
+      else if (k0 < 16) { lo0 = g0 + (k0 - 1) * s0 + 1; hi0 = g0 + k0 * s0; }
+      else { lo0 = g0 + 15 * s0 + 1; hi0 = n; }
+      if (lo0 > n) lo0 = n;
+      if (hi0 > n) hi0 = n;
+    }
+    if (!done1) {
+      if (k1 == 0) { lo1 = 0; hi1 = g1; }
+      else if (k1 < 16) { lo1 = g1 + (k1 - 1) * s1 + 1; hi1 = g1 + k1 * s1; }
+      else { lo1 = g1 + 15 * s1 + 1; hi1 = n; }
+      if (lo1 > n) lo1 = n;
+      if (hi1 > n) hi1 = n;
+    }
   }
   while (hi0 - lo0 > 32 || hi1 - lo1 > 32) {
     const int64_t st0 = hi0 - lo0 > 32 ? (hi0 - lo0 + 31) / 32 : 1;
@@ -323,7 +393,7 @@ __device__ __forceinline__ void lower_bound2(const int32_t* a, int64_t n, int64_
 
 template <bool RUNS, bool OWN>
 __device__ __forceinline__ void scatter_side(unsigned* accl, const float4* rec, int Bp, int key, float v[6], int lane,
-                                             float im_own, float dm_own) {
+                                             float im_own, float dm_own, bool& ovf) {
   const bool tail = (!RUNS || seg_sum6(key, v, lane)) && key >= 0;
   if (tail) {
     // scales: OWN = from the run's last lane's own side-a record (registers of
@@ -336,6 +406,8 @@ __device__ __forceinline__ void scatter_side(unsigned* accl, const float4* rec, 
       dmax = fmaxf(fmaxf(r[4 * (Bp + key) + 3], r[4 * (2 * Bp + key) + 3]), r[4 * (3 * Bp + key)]);
     }
     const float sl = fx_pow2(fx_exp(im)), sa = fx_pow2(fx_exp(dmax));
+    ovf |= fx_over(fmaxf(fmaxf(fabsf(v[0]), fabsf(v[1])), fabsf(v[2])), sl) |
+           fx_over(fmaxf(fmaxf(fabsf(v[3]), fabsf(v[4])), fabsf(v[5])), sa);
 #pragma unroll
     for (int q = 0; q < 6; ++q) fx_add(ACC_LO(q, key), ACC_HI(q, key), v[q], q < 3 ? sl : sa);
   }
@@ -344,9 +416,11 @@ __device__ __forceinline__ void scatter_side(unsigned* accl, const float4* rec, 
 // S6 for a side whose body record is still in registers (direct adds, no runs):
 // the scales come from the lane's own m^-1 and max diag I_w^-1.
 __device__ __forceinline__ void scatter_own(unsigned* accl, int Bp, int key, const float v[6], float im,
-                                            float dmax) {
+                                            float dmax, bool& ovf) {
   if (key >= 0) {
     const float sl = fx_pow2(fx_exp(im)), sa = fx_pow2(fx_exp(dmax));
+    ovf |= fx_over(fmaxf(fmaxf(fabsf(v[0]), fabsf(v[1])), fabsf(v[2])), sl) |
+           fx_over(fmaxf(fmaxf(fabsf(v[3]), fabsf(v[4])), fabsf(v[5])), sa);
 #pragma unroll
     for (int q = 0; q < 6; ++q) fx_add(ACC_LO(q, key), ACC_HI(q, key), v[q], q < 3 ? sl : sa);
   }
@@ -366,6 +440,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
   const int64_t w = (int64_t)blockIdx.x * kGroups + group;
   if (w >= P.n_worlds) return;  // whole group leaves together
 
+  TL_MARK(0);
   float* G = smem + (size_t)group * GL.total;
   float4* rec = reinterpret_cast<float4*>(G + GL.rec);
   unsigned* accl = reinterpret_cast<unsigned*>(G + GL.accl);
@@ -386,6 +461,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
   if (P.world_sorted && gt < 32) {
     int64_t b0, b1;
     lower_bound2(P.world_sorted, P.n_contacts, P.n_worlds, w, w + 1, lane, b0, b1);
+    TL_MARK(4);
     if (lane == 0) {
       rng[0] = b0;
       rng[1] = b1;
@@ -408,17 +484,17 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
   // ---------------- S1: smooth prediction (Kernel I) ----------------
   // record B (Bp >= B + 1) stays all zero: static and chain sides read it in S2
   if (gt < 4) rec[gt * Bp + B] = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int i = gt; i < B; i += kGT) {
-    // plane k of body i at sp + k * pb (64-bit pointer + uniform 64-bit stride)
-    const float* sp = slab + i;
+  // body i: x, q, v, omega from the slab planes (from `stg` instead of the slab
+  // for planes 0-11 when given), omega_z and the scene parameters passed in.
+  // (Staging planes 0-11 with cp.async into the accumulator region before S1
+  // was measured neutral on C4 and slower on C3.)
+  auto s1_body = [&](int i, const float* stg, float omz, float im, float3 ib, float3 ibi) {
+    const float* sp = stg ? stg + i : slab + i;
     const size_t pb = (size_t)Bp;
     const float3 x = make_float3(sp[0 * pb], sp[1 * pb], sp[2 * pb]);
     const float4 q = make_float4(sp[3 * pb], sp[4 * pb], sp[5 * pb], sp[6 * pb]);
     const float3 v = make_float3(sp[7 * pb], sp[8 * pb], sp[9 * pb]);
-    const float3 om = make_float3(sp[10 * pb], sp[11 * pb], sp[12 * pb]);
-    const float im = sc.inv_mass[i];
-    const float* ip = sc.inv_inertia + i;
-    const float3 ib = make_float3(ip[0], ip[pb], ip[2 * pb]);
+    const float3 om = make_float3(sp[10 * pb], sp[11 * pb], omz);
     // rotation of the normalised quaternion (reading R15)
     const float qn = rsqrtf(q.x * q.x + q.y * q.y + q.z * q.z + q.w * q.w);
     const float qw = q.x * qn, qx = q.y * qn, qy = q.z * qn, qz = q.w * qn;
@@ -445,12 +521,12 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
       vs.z += (im * fl.z + P.g[2]) * dt;
     }
     // bias c = omega x (Iw omega), Iw = R diag(1/ib) R^T on unlocked axes
+    // (ibi = I_b = 1/I_b^-1, 0 on locked axes, precomputed per scene)
     float3 wl = make_float3(R00 * om.x + R10 * om.y + R20 * om.z, R01 * om.x + R11 * om.y + R21 * om.z,
                             R02 * om.x + R12 * om.y + R22 * om.z);
-    const float* ipi = sc.inertia + i;  // I_b = 1/I_b^-1, 0 on locked axes (precomputed per scene)
-    wl.x *= ipi[0];
-    wl.y *= ipi[pb];
-    wl.z *= ipi[2 * pb];
+    wl.x *= ibi.x;
+    wl.y *= ibi.y;
+    wl.z *= ibi.z;
     const float3 Iwo = make_float3(R00 * wl.x + R01 * wl.y + R02 * wl.z, R10 * wl.x + R11 * wl.y + R12 * wl.z,
                                    R20 * wl.x + R21 * wl.y + R22 * wl.z);
     const float3 gy = cross3(om, Iwo);
@@ -462,7 +538,22 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
     rec[Bp + i] = make_float4(ws.x, ws.y, ws.z, Ixx);
     rec[2 * Bp + i] = make_float4(x.x, x.y, x.z, Iyy);
     rec[3 * Bp + i] = make_float4(Izz, Ixy, Ixz, Iyz);
+  };
+  auto s1_params = [&](int i, float& omz, float& im, float3& ib, float3& ibi) {
+    const size_t pb = (size_t)Bp;
+    omz = slab[12 * pb + i];
+    im = sc.inv_mass[i];
+    ib = make_float3(sc.inv_inertia[i], sc.inv_inertia[pb + i], sc.inv_inertia[2 * pb + i]);
+    ibi = make_float3(sc.inertia[i], sc.inertia[pb + i], sc.inertia[2 * pb + i]);
+  };
+#pragma unroll kS1Unroll
+  for (int i = gt; i < B; i += kGT) {
+    float omz, im;
+    float3 ib, ibi;
+    s1_params(i, omz, im, ib, ibi);
+    s1_body(i, nullptr, omz, im, ib, ibi);
   }
+  TL_MARK(5);
   {  // zero the accumulators (12 Bp words = 3 Bp uint4)
     uint4* z = reinterpret_cast<uint4*>(accl);
     for (int q = gt; q < 3 * Bp; q += kGT) z[q] = make_uint4(0u, 0u, 0u, 0u);
@@ -496,6 +587,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
   }
   if (gt < 8) red[gt] = 0.f;
   group_sync<WPW, CW>(group);
+  TL_MARK(1);
 
   // Contact range of this world.
   const int64_t cbeg = P.world_sorted ? rng[0] : P.off[w];
@@ -504,6 +596,8 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
   const float4* C1p = P.c1 + cbeg;
   const float4* C2p = P.c2 + cbeg;
   const int4* C3p = P.c3 + cbeg;
+  if (nloc > kMaxWorldContacts && gt == 0) atomicOr(P.err, ERR_WORLD_CONTACTS);  // S6 lo-plane bound
+  bool fx_ovf = false;  // S6 per-add fixed-point range exceeded (reported as non-finite)
   const int32_t* Wp = P.world_sorted ? P.world_sorted + cbeg : nullptr;
 
   // ---------------- S2-S6: contacts ----------------
@@ -680,9 +774,9 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
     {
       const float3 ma = cross3(ra, f), mb = cross3(rb, f);
       float va[6] = {-f.x, -f.y, -f.z, -(ma.x + tau.x), -(ma.y + tau.y), -(ma.z + tau.z)};
-      scatter_side<true, !TREES>(accl, rec, Bp, ida >= 0 ? ida : -1, va, lane, ima, dma);
+      scatter_side<true, !TREES>(accl, rec, Bp, ida >= 0 ? ida : -1, va, lane, ima, dma, fx_ovf);
       float vb[6] = {f.x, f.y, f.z, mb.x + tau.x, mb.y + tau.y, mb.z + tau.z};
-      scatter_own(accl, Bp, idb >= 0 ? idb : -1, vb, imb, dmb);
+      scatter_own(accl, Bp, idb >= 0 ? idb : -1, vb, imb, dmb, fx_ovf);
     }
     if (TREES) {
 #pragma unroll
@@ -705,6 +799,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
           }
           const float sv[4] = {s4.x, s4.y, s4.z, s4.w};
           const float scl = fx_pow2(__float_as_int(tL[16 * t + 14]));
+          fx_ovf |= fx_over(fmaxf(fmaxf(fabsf(s4.x), fabsf(s4.y)), fmaxf(fabsf(s4.z), fabsf(s4.w))), scl);
 #pragma unroll
           for (int jj = 0; jj < 4; ++jj)
             if (jj < nd) fx_add(tacl + 4 * t + jj, tach + 4 * t + jj, sg * sv[jj], scl);
@@ -713,10 +808,11 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
     }
   }
   group_sync<WPW, CW>(group);
+  TL_MARK(2);
 
   // ---------------- S7: velocity correction + integration (Kernel IV) ----------------
   float ke = 0.f;
-  bool nonfinite = false;
+  bool nonfinite = P.check_finite && fx_ovf;
   for (int i = gt; i < B; i += kGT) {
     const float4 r0 = rec[i], r1 = rec[Bp + i], r2 = rec[2 * Bp + i], r3 = rec[3 * Bp + i];
     float* sp = slab + i;
@@ -730,7 +826,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
 #pragma unroll
     for (int q6 = 0; q6 < 6; ++q6) {
       hi[q6] = *ACC_HI(q6, i);
-      range |= (unsigned)hi[q6] + (1u << 30);  // bit 31 set: |sum| >= 2^62, fixed-point range exceeded
+      range |= (unsigned)hi[q6] + (1u << 30);  // bit 31 set: |hi| >= 2^30, fixed-point range exceeded
     }
     if (P.check_finite) nonfinite |= (range >> 31) != 0u;
     const float4 a0 = make_float4(fx_get(*ACC_LO(0, i), hi[0], isl), fx_get(*ACC_LO(1, i), hi[1], isl),
@@ -818,6 +914,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
       }
     }
   }
+  TL_MARK(3);
   if (nonfinite) {
     atomicOr(P.err, ERR_NONFINITE);
     atomicMin(P.first_bad, (unsigned long long)(P.world_base + w));
