@@ -45,6 +45,9 @@ def parse():
     ap.add_argument("--worlds", type=int, default=None, help="worlds per GPU (pile 1024, hand 4096)")
     ap.add_argument("--contacts", type=int, default=2000, help="contacts per world")
     ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--flush-mode", default="write+read", choices=["write", "write+read"],
+                    help="L2 flush between timed steps: write 256 MB (leaves L2 full of dirty lines whose "
+                         "write-back the next step pays), or write then read it back (cold, clean L2)")
     ap.add_argument("--no-graph", action="store_true", help="direct launches instead of CUDA-graph replay")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -304,6 +307,15 @@ def run_ours(args, rank, world_size, local):
         # part 0 on the caller's stream, the others on their own streams (fork / join)
         p.stream = stream if i == 0 else torch.cuda.Stream(device=dev)
     flush = None if args.no_flush else torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    flush_sink = torch.empty(1, dtype=torch.float32, device=dev)
+
+    def flush_l2():
+        """Evict L2 between timed steps (untimed): write a 256 MB buffer (> the
+        126 MB L2); in write+read mode read it back so the lines left in L2 are
+        clean (the dirty lines' write-back happens here, not in the next step)."""
+        flush.zero_()
+        if args.flush_mode == "write+read":
+            torch.sum(flush, dim=0, keepdim=True, out=flush_sink)
 
     def one_step(s0):
         """One step of every part: part 0 on s0, the rest forked from s0 and joined back."""
@@ -325,7 +337,7 @@ def run_ours(args, rank, world_size, local):
         p.ctx.set_timing(True)
     for _ in range(min(args.steps, 20)):
         if flush is not None:
-            flush.zero_()
+            flush_l2()
         one_step(stream)
     for p in parts:
         p.kt = p.ctx.get_timing()
@@ -350,7 +362,7 @@ def run_ours(args, rank, world_size, local):
     with clock:
         for i in range(args.steps):
             if flush is not None:
-                flush.zero_()              # evict L2 between timed steps (untimed)
+                flush_l2()                 # evict L2 between timed steps (untimed)
             evs[i][0].record(stream)
             if graph is not None:
                 graph.replay()
@@ -457,7 +469,9 @@ def run_ours(args, rank, world_size, local):
                                  for p in parts},
                        "facets_per_contact": {1: 1, 3: 4, 4: 6, 6: 10}[args.condim], "condim": args.condim,
                        "dt": cfg.dt,
-                       "l2": "flushed between timed steps (256 MB write)" if flush is not None else "not flushed",
+                       "l2": (("flushed between timed steps (256 MB write, then read back: cold clean L2)"
+                               if args.flush_mode == "write+read" else "flushed between timed steps (256 MB write)")
+                              if flush is not None else "not flushed"),
                        "footprint_mb_per_step": alg_total / 1e6,
                        "parallelism": f"world-sharded x{world_size}"},
             "contacts_per_s": contacts_per_s,

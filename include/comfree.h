@@ -101,8 +101,9 @@ typedef struct {
 } comfree_config;
 
 /* Per-scene body parameters shared by every world (HOST pointers, copied).
- * inv_mass[i] >= 0 and inv_inertia[i][0..2] >= 0 (principal body-frame
- * inverse inertia; 0 locks that DoF).  Articulated chains: n_trees chains of
+ * 0 <= inv_mass[i] <= 1e27 and 0 <= inv_inertia[i][0..2] <= 1e27 (principal
+ * body-frame inverse inertia; 0 locks that DoF; the upper bound keeps the S6
+ * fixed-point scales normal floats).  Articulated chains: n_trees chains of
  * tree_ndof in 1..4 DoFs each; their inertia comes per step as Cholesky
  * factors in comfree_worlds (the upstream CRBA is not part of this step). */
 typedef struct {

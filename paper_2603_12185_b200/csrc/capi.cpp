@@ -223,15 +223,19 @@ comfree_status comfree_validate_config(const comfree_config* c) {
   return ok ? COMFREE_OK : COMFREE_ERR_VALIDATION;
 }
 
+static constexpr float kMaxInv = 1e27f;
+
 comfree_status comfree_validate_scene(const comfree_scene* s) {
   if (!s) return COMFREE_ERR_INVALID_ARGUMENT;
   if (s->n_bodies < 0 || s->n_trees < 0) return COMFREE_ERR_VALIDATION;
   if (s->n_bodies > 0 && (!s->inv_mass || !s->inv_inertia)) return COMFREE_ERR_INVALID_ARGUMENT;
   if (s->n_trees > 0 && (s->tree_ndof < 1 || s->tree_ndof > 4)) return COMFREE_ERR_VALIDATION;
   for (int i = 0; i < s->n_bodies; ++i) {
-    if (!(finite(s->inv_mass[i]) && s->inv_mass[i] >= 0)) return COMFREE_ERR_VALIDATION;
+    // finite, >= 0 and <= kMaxInv (the S6 fixed-point scale 2^(exponent + 33) stays a normal float)
+    if (!(finite(s->inv_mass[i]) && s->inv_mass[i] >= 0 && s->inv_mass[i] <= kMaxInv)) return COMFREE_ERR_VALIDATION;
     for (int k = 0; k < 3; ++k)
-      if (!(finite(s->inv_inertia[3 * i + k]) && s->inv_inertia[3 * i + k] >= 0)) return COMFREE_ERR_VALIDATION;
+      if (!(finite(s->inv_inertia[3 * i + k]) && s->inv_inertia[3 * i + k] >= 0 && s->inv_inertia[3 * i + k] <= kMaxInv))
+        return COMFREE_ERR_VALIDATION;
   }
   return COMFREE_OK;
 }
