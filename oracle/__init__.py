@@ -44,7 +44,8 @@ class _Cfg(ct.Structure):
                 ("r_min", ct.c_double), ("r_max", ct.c_double), ("width", ct.c_double),
                 ("midpoint", ct.c_double), ("power", ct.c_double),
                 ("n_t", ct.c_int32), ("n_rol", ct.c_int32),
-                ("gravity", ct.c_double * 3), ("dt", ct.c_double)]
+                ("gravity", ct.c_double * 3), ("dt", ct.c_double),
+                ("exact_diagonal", ct.c_int32)]
 
 
 class _Scene(ct.Structure):
@@ -90,6 +91,7 @@ def _cfg(cfg: Config) -> _Cfg:
     for i in range(3):
         c.gravity[i] = cfg.gravity[i]
     c.dt = cfg.dt
+    c.exact_diagonal = 1 if getattr(cfg, "impedance", "heuristic") == "exact_diagonal" else 0
     return c
 
 

@@ -152,11 +152,17 @@ def dense_world_step(cfg: Config, scene: Scene, state: State, contacts: Contacts
         for row in facet_rows(cfg, n, t1, float(contacts.c1[c, 3]), float(contacts.c2[c, 3]),
                               float(contacts.mu_rol[c]), int(contacts.condim[c]), Jc):
             s = row @ v_s
+            Kf, Df = K, D
+            if getattr(cfg, "impedance", "heuristic") == "exact_diagonal":
+                # Eq. (11): the diagonal entry J~_f M^-1 J~_f^T of this facet
+                A = float(row @ np.linalg.solve(M, row))
+                Mf = r / (1 - r) / A
+                Kf, Df = ku * Mf / dt, du * Mf / dt
             rows.append(row)
             phis.append(phi)
-            Ks.append(K)
-            Ds.append(D)
-            a_list.append(-K * (s * dt + phi) - D * s)           # Eq. (9) before the clamp
+            Ks.append(Kf)
+            Ds.append(Df)
+            a_list.append(-Kf * (s * dt + phi) - Df * s)         # Eq. (9) before the clamp
     if rows:
         Jt = np.stack(rows)
         lam = np.maximum(np.asarray(a_list), 0.0)

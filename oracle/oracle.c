@@ -216,6 +216,35 @@ static double side_trace(int32_t id, const double* p, const double* pos_w, const
   return tr;
 }
 
+/* g J_x M_x^-1 J_x^T g^T for a facet row g = (gl, ga) acting on the contact
+ * twist, restricted to side x (its contribution to the diagonal entry
+ * J~_f M^-1 J~_f^T of Eq. (11); a side's sign drops out). */
+static double side_quad(int32_t id, const double* p, const double* pos_w, const double* inv_mass,
+                        const body_work* bw, const double* Lw, int nd, const double* J,
+                        const double gl[3], const double ga[3]) {
+  if (id == -1) return 0.0;
+  if (id >= 0) {
+    /* J_x^T g = (gl, r x gl + ga) for a free body; M_x^-1 = diag(inv_m I_3, Iw^-1) */
+    const double* x = pos_w + 3 * id;
+    double r[3] = {p[0] - x[0], p[1] - x[1], p[2] - x[2]}, u[3], Iu[3];
+    cross3(r, gl, u);
+    for (int k = 0; k < 3; ++k) u[k] += ga[k];
+    matvec3(bw[id].Iw_inv, u, Iu);
+    return inv_mass[id] * dot3(gl, gl) + dot3(u, Iu);
+  }
+  /* tree: y = J_lin^T gl + J_ang^T ga over the chain's DoFs; y^T (L L^T)^-1 y */
+  int t = -2 - id;
+  double y[4] = {0, 0, 0, 0}, z[4] = {0, 0, 0, 0};
+  for (int j = 0; j < nd; ++j) {
+    for (int k = 0; k < 3; ++k) y[j] += J[k*4 + j] * gl[k] + J[(3+k)*4 + j] * ga[k];
+    z[j] = y[j];
+  }
+  tree_minv(Lw + 10 * t, nd, z);
+  double q = 0.0;
+  for (int j = 0; j < nd; ++j) q += y[j] * z[j];
+  return q;
+}
+
 /* apply J_x^T (f, tau) * sign to side x's generalized impulse */
 static void side_scatter(int32_t id, double sign, const double* p, const double* pos_w,
                          body_work* bw, double* p_tree, int nd, const double* J,
@@ -353,7 +382,15 @@ static int step_world(const orc_config* cfg, const orc_scene* sc, int64_t w,
         }
       }
       double s = dot3(gl, vc) + dot3(ga, wc);                 /* s = J~ v_s */
-      double lam = orc_facet_lambda(K, D, s, phi, dt);        /* Eq. (9) */
+      double Kf = K, Df = D;
+      if (cfg->exact_diagonal) {  /* Eq. (11): this facet's own J~_f M^-1 J~_f^T (reading R24) */
+        double A = side_quad(a, p, pos_w, sc->inv_mass, bw, L_w, nd, Ja, gl, ga)
+                 + side_quad(b, p, pos_w, sc->inv_mass, bw, L_w, nd, Jb, gl, ga);
+        double Mf = r / (1.0 - r) / A;
+        Kf = kc * Mf / dt;
+        Df = dc * Mf / dt;
+      }
+      double lam = orc_facet_lambda(Kf, Df, s, phi, dt);      /* Eq. (9) */
       double Lam = lam * dt;                                  /* impulse, Eq. (10) */
       if (Lam > 0.0) n_active++;
       if (impulses) impulses[foff[c] + f] = Lam;

@@ -29,6 +29,10 @@ typedef struct {
   int32_t n_t, n_rol;                            /* Eq. (7) facet counts */
   double gravity[3];
   double dt;
+  int32_t exact_diagonal;   /* 0: M(phi) of Eq. (12) (trace heuristic);
+                               1: Eq. (11) diagonal, reading R24 in DESIGN.md:
+                               per facet M_f = r/(1-r) / (J~_f M^-1 J~_f^T),
+                               K_f = k M_f/dt, D_f = d M_f/dt               */
 } orc_config;
 
 typedef struct {
