@@ -57,6 +57,8 @@ def parse():
                     help="pile contact dimensionality (3: the BASELINE config; 6: the 6D variant, n_t = n_rol = 4)")
     ap.add_argument("--kd", action="store_true",
                     help="per-contact (k_user, d_user) impedance arrays (learned-impedance variant, P:206-208)")
+    ap.add_argument("--impedance", default="heuristic", choices=["heuristic", "exact_diagonal"],
+                    help="exact_diagonal: Eq. (11) per facet (reading R24) instead of the trace heuristic")
     ap.add_argument("--workload", default="pile", choices=["pile", "hand", "mixed"],
                     help="pile: config 4 (the BASELINE metric); hand: config 3; mixed: config 5")
     a = ap.parse_args()
@@ -171,6 +173,8 @@ def workload(args, rank, world_size):
             p.c.kd = np.stack([rng.uniform(0.05, 0.3, p.c.n), rng.uniform(0.0, 0.002, p.c.n)], 1).astype(np.float32)
             p.alg_bytes += 8 * p.c.n
         name += " + per-contact impedance"
+    if args.impedance == "exact_diagonal":
+        name += " + exact-diagonal impedance (Eq. 11)"
     return parts, name, n
 
 
@@ -242,7 +246,7 @@ def run_reference(args, rank, world_size):
     if rank != 0:
         return
     import oracle
-    cfg = Config()
+    cfg = Config(impedance=args.impedance)
     parts, wname, n_local = workload(args, 0, world_size)
     cores = os.cpu_count() or 1
     Wcap = 64 if args.workload == "pile" else 256
@@ -292,7 +296,7 @@ def run_ours(args, rank, world_size, local):
             dist.init_process_group("nccl", device_id=dev)
         else:                              # plumbing check with several ranks on one GPU
             dist.init_process_group(args.dist_backend)
-    cfg = Config()
+    cfg = Config(impedance=args.impedance)
     parts, wname, n_local = workload(args, rank, world_size)
     stream = torch.cuda.current_stream()
     for i, p in enumerate(parts):

@@ -74,7 +74,12 @@ enum {
   COMFREE_FLAG_STATS = 1u << 0,         /* per-world statistics every step */
   COMFREE_FLAG_DETERMINISTIC = 1u << 1, /* accepted, no effect: every step is bitwise deterministic
                                            (fixed-point accumulation, see comfree_step) */
-  COMFREE_FLAG_NO_FINITE_CHECK = 1u << 2
+  COMFREE_FLAG_NO_FINITE_CHECK = 1u << 2,
+  /* Eq. (11) instead of the trace heuristic of Eq. (12): every
+   * facet f uses its own diagonal entry, M_f = r/(1-r) / (J~_f M^-1 J~_f^T),
+   * K_f = k M_f/dt, D_f = d M_f/dt (reading R24).  Costs one
+   * quadratic form per facet and side (general kernel variant). */
+  COMFREE_FLAG_EXACT_DIAGONAL = 1u << 3
 };
 
 /* comfree_contacts.flags */

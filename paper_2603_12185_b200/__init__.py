@@ -57,6 +57,11 @@ def make_config(cfg=None, flags: int = 0, **kw) -> _lib.comfree_config:
             if hasattr(cfg, name):
                 src[name] = getattr(cfg, name)
     src.update(kw)
+    impedance = src.pop("impedance", getattr(cfg, "impedance", "heuristic"))
+    if impedance == "exact_diagonal":      # Eq. (11) per facet (reading R24)
+        flags |= _lib.FLAG_EXACT_DIAGONAL
+    elif impedance != "heuristic":
+        raise ValueError(f"impedance must be 'heuristic' or 'exact_diagonal', not {impedance!r}")
     for k, v in src.items():
         if k == "gravity":
             for i in range(3):

@@ -20,7 +20,7 @@ COMFREE_OK = 0
 STATUS_NAMES = {0: "OK", 1: "ERR_INVALID_ARGUMENT", 2: "ERR_VALIDATION", 3: "ERR_CAPACITY",
                 4: "ERR_NONFINITE", 5: "ERR_CUDA", 6: "ERR_STATE"}
 MEM_DEVICE, MEM_HOST = 0, 1
-FLAG_STATS, FLAG_DETERMINISTIC, FLAG_NO_FINITE_CHECK = 1, 2, 4
+FLAG_STATS, FLAG_DETERMINISTIC, FLAG_NO_FINITE_CHECK, FLAG_EXACT_DIAGONAL = 1, 2, 4, 8
 CONTACTS_SORTED = 1
 
 

@@ -432,9 +432,12 @@ comfree_status comfree_step(comfree_ctx* ctx, const comfree_worlds* wd, const co
   if (!off) {
     CUDA_TRY(ctx, ensure(ctx->off, (size_t)(nw + 1) * sizeof(int64_t)));
     int64_t* doff = static_cast<int64_t*>(ctx->off.p);
-    if (c->flags & COMFREE_CONTACTS_SORTED) {
+    if ((c->flags & COMFREE_CONTACTS_SORTED) && n > 0) {
       // fused S0: the step kernel locates each world's range and verifies the ids
       fused_world = world;
+    } else if (c->flags & COMFREE_CONTACTS_SORTED) {
+      // no contacts (world[] may be null): every offset is 0
+      CUDA_TRY(ctx, cf::launch_offsets_sorted(world, 0, nw, doff, ctx->d_err, s));
     } else {
       CUDA_TRY(ctx, ensure(ctx->keys, std::max<size_t>(1, n) * sizeof(int32_t)));
       CUDA_TRY(ctx, ensure(ctx->perm, std::max<size_t>(1, n) * sizeof(int32_t)));
@@ -542,6 +545,7 @@ comfree_status comfree_step(comfree_ctx* ctx, const comfree_worlds* wd, const co
   P.first_bad = ctx->d_first_bad;
   P.world_base = first;
   P.check_finite = !(cf_.flags & COMFREE_FLAG_NO_FINITE_CHECK);
+  P.exact_diag = (cf_.flags & COMFREE_FLAG_EXACT_DIAGONAL) != 0;
 #ifdef CF_TIMELINE
   P.timeline = cf_debug_timeline_buf();
 #endif

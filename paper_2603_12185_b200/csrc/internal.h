@@ -69,6 +69,7 @@ struct StepParams {
   unsigned long long* first_bad;// min world id with a non-finite state
   int64_t world_base;           // absolute id of world 0 of the range (error reporting)
   int check_finite;
+  int exact_diag;               // Eq. (11) per-facet impedance (COMFREE_FLAG_EXACT_DIAGONAL), general variants only
   unsigned* timeline;           // CF_TIMELINE builds only: per CTA (smid, t0, t1, t2, t3) globaltimer ns
 };
 

@@ -405,6 +405,35 @@ __device__ __forceinline__ void lower_bound2(const int32_t* a, int64_t n, int64_
   r1 = lo1 + __popc(__ballot_sync(full, q1));
 }
 
+// Exact-diagonal impedance (Eq. (11), reading R24): one side's share of the
+// facet's diagonal entry J~_f M^-1 J~_f^T for a facet row g = (gl, ga) acting on
+// the contact twist.  Free body (record ix; static sides read the all-zero
+// record): J_x^T g = (gl, r x gl + ga), M_x^-1 = diag(m^-1 I, I_w^-1).
+__device__ __forceinline__ float side_quad_free(const float4* rec, int Bp, int ix, float3 r, float3 gl, float3 ga) {
+  const float4 r0 = rec[ix], r1 = rec[Bp + ix], r2 = rec[2 * Bp + ix], r3 = rec[3 * Bp + ix];
+  const float3 c = cross3(r, gl);
+  const float3 u = make_float3(c.x + ga.x, c.y + ga.y, c.z + ga.z);
+  const float Ixx = r1.w, Iyy = r2.w, Izz = r3.x, Ixy = r3.y, Ixz = r3.z, Iyz = r3.w;
+  const float3 Iu = make_float3(Ixx * u.x + Ixy * u.y + Ixz * u.z, Ixy * u.x + Iyy * u.y + Iyz * u.z,
+                                Ixz * u.x + Iyz * u.y + Izz * u.z);
+  return r0.w * dot3(gl, gl) + dot3(u, Iu);
+}
+// Chain side: y = J_lin^T gl + J_ang^T ga over the chain's DoFs, y^T (L L^T)^-1 y.
+__device__ __forceinline__ float side_quad_tree(const float4* jr, int64_t stride, const float* Ls, int nd, float3 gl,
+                                                float3 ga) {
+  const float gv[3] = {gl.x, gl.y, gl.z}, av[3] = {ga.x, ga.y, ga.z};
+  float4 y = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int kk = 0; kk < 3; ++kk) {
+    const float4 jl = jr[(size_t)kk * stride], ja = jr[(size_t)(kk + 3) * stride];
+    y.x += jl.x * gv[kk] + ja.x * av[kk];
+    y.y += jl.y * gv[kk] + ja.y * av[kk];
+    y.z += jl.z * gv[kk] + ja.z * av[kk];
+    y.w += jl.w * gv[kk] + ja.w * av[kk];
+  }
+  return chol_quad(Ls, nd, y);
+}
+
 // S6 for one side: run aggregation inside the warp, then the run's last lane
 // adds its total (6 values) to the body's fixed-point accumulators.
 // Accumulator of component q of body k: (lo, hi) words adjacent, so one
@@ -783,6 +812,54 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
         if (IMP && out) out[0] = Mc * N;
       }
       if (stats) n_active += valid ? act_t : 0;
+      if (!FAST && P.exact_diag) {  // warp-uniform: Eq. (11) per facet (reading R24)
+        // every facet f: row g_f = (gl, ga), s_f = g_f . (v_rel, w_rel),
+        // M_f = r/(1-r) / (J~_f M^-1 J~_f^T), Lambda_f = M_f (-k phi - kappa s_f)_+;
+        // the contact wrench is (sum Lambda_f gl, sum Lambda_f ga)
+        const float rho = r * rcp_approx(1.f - r);
+        const float mu_tor = c2.w, mu_rol = __int_as_float(c3.z);
+        const int nf = cd == 1 ? 1 : P.n_t + (cd >= 4 ? 2 : 0) + (cd == 6 ? P.n_rol : 0);
+        const int ixa = ida >= 0 ? ida : B, ixb = idb >= 0 ? idb : B;
+        float3 fs = make_float3(0.f, 0.f, 0.f), ts = make_float3(0.f, 0.f, 0.f);
+        int act = 0;
+        for (int fi = 0; fi < nf; ++fi) {
+          float3 gl = n, ga = make_float3(0.f, 0.f, 0.f);
+          if (cd != 1) {
+            if (fi < P.n_t) {
+              const float2 d = P.dir_t[fi];
+              gl = make_float3(n.x - mu_t * (d.x * t1.x + d.y * t2.x), n.y - mu_t * (d.x * t1.y + d.y * t2.y),
+                               n.z - mu_t * (d.x * t1.z + d.y * t2.z));
+            } else if (fi < P.n_t + 2) {
+              const float sg = fi == P.n_t ? -mu_tor : mu_tor;
+              ga = make_float3(sg * n.x, sg * n.y, sg * n.z);
+            } else {
+              const float2 d = P.dir_r[fi - P.n_t - 2];
+              ga = make_float3(-mu_rol * (d.x * t1.x + d.y * t2.x), -mu_rol * (d.x * t1.y + d.y * t2.y),
+                               -mu_rol * (d.x * t1.z + d.y * t2.z));
+            }
+          }
+          const float sf = dot3(gl, vrel) + dot3(ga, wrel);
+          float Af = side_quad_free(rec, Bp, ixa, ra, gl, ga) + side_quad_free(rec, Bp, ixb, rb, gl, ga);
+          if (TREES) {
+#pragma unroll
+            for (int side = 0; side < 2; ++side) {
+              const int id = side ? idb : ida;
+              if (id < -1) {
+                const float4* jr = P.jrow + (size_t)(side * 6) * P.n_contacts + cbeg + j;
+                Af += side_quad_tree(jr, P.n_contacts, tL + 16 * (-2 - id), nd, gl, ga);
+              }
+            }
+          }
+          const float Lf = rho * rcp_approx(Af) * fmaxf(-kc * phi - kappa * sf, 0.f);
+          fs = make_float3(fs.x + Lf * gl.x, fs.y + Lf * gl.y, fs.z + Lf * gl.z);
+          ts = make_float3(ts.x + Lf * ga.x, ts.y + Lf * ga.y, ts.z + Lf * ga.z);
+          act += Lf > 0.f;
+          if (IMP && out) out[fi] = Lf;
+        }
+        if (stats) n_active += valid ? act - act_t : 0;
+        f = valid ? fs : make_float3(0.f, 0.f, 0.f);
+        tau = valid ? ts : make_float3(0.f, 0.f, 0.f);
+      } else {
       if (__any_sync(0xffffffffu, valid && cd >= 4)) {
         float Mt = 0.f, R1 = 0.f, R2 = 0.f;
         const float mu_tor = c2.w, mu_rol = __int_as_float(c3.z);
@@ -811,6 +888,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
       f = make_float3(fn * n.x + ft1 * t1.x + ft2 * t2.x, fn * n.y + ft1 * t1.y + ft2 * t2.y,
                       fn * n.z + ft1 * t1.z + ft2 * t2.z);
       if (!valid) f = make_float3(0.f, 0.f, 0.f);
+      }
     }
     if (kLatePrefetch) prefetch_next();
     // S6: scatter J^T (f, tau).  Free bodies get (f, r x f + tau) per side:
@@ -1008,7 +1086,7 @@ cudaError_t launch_variant(const StepParams& p, cudaStream_t s) {
 template <int CW, int WPW>
 cudaError_t launch_cfg(const StepParams& p, cudaStream_t s) {
     const bool trees = p.sc.T > 0, imp = p.impulses != nullptr || p.wstats != nullptr;
-  if (p.n_t == 4 && p.power_is_2) {
+  if (p.n_t == 4 && p.power_is_2 && !p.exact_diag) {
     if (trees) return imp ? launch_variant<CW, WPW, true, true, true>(p, s) : launch_variant<CW, WPW, true, true, false>(p, s);
     return imp ? launch_variant<CW, WPW, true, false, true>(p, s) : launch_variant<CW, WPW, true, false, false>(p, s);
   }
