@@ -22,7 +22,7 @@ import math
 import numpy as np
 
 from .collide import Friction, Geom, Plane, WorldGeometry, quat_R
-from .types import Config, Contacts, Inputs, Scene, State
+from .types import Articulation, Config, Contacts, Inputs, Scene, State
 
 BASE_SEED = 260312185
 
@@ -359,6 +359,22 @@ def c4_pile(n_worlds=1024, contacts_per_world=2000, lattice=(10, 10, 5), seed=0,
 
 
 # ---------------------------------------------------------------- C3 hand
+def hand_articulation() -> Articulation:
+    """The synthetic LEAP-like hand of config 3 as an Articulation: 4 chains x
+    4 hinges (first about the base z axis, then three about the link y axis),
+    link lengths (0.045, 0.035, 0.03, 0.03) m, masses (0.04, 0.03, 0.02,
+    0.015) kg, isotropic link inertia m l^2 / 12, armature 2e-4."""
+    T, nd = 4, 4
+    lens = np.array([0.045, 0.035, 0.03, 0.03])
+    lmass = np.array([0.04, 0.03, 0.02, 0.015])
+    bases = np.array([[0.04, -0.045, 0.0], [0.04, 0.0, 0.0], [0.04, 0.045, 0.0], [-0.02, -0.06, 0.0]])
+    axis = np.zeros((T, nd, 3))
+    axis[:, 0] = (0, 0, 1.0)
+    axis[:, 1:] = (0, 1.0, 0)
+    return Articulation(bases, axis, np.tile(lens, (T, 1)), np.tile(lmass, (T, 1)),
+                        np.tile(lmass * lens ** 2 / 12, (T, 1)), np.full((T, nd), 2e-4))
+
+
 def c3_hand(n_worlds=4096, seed=0, world_offset=0):
     """Config 3: LEAP-like hand, 4 hinge chains x 4 DoF (nv = 16 + 6) plus a
     free cube (0.06 m, 0.1 kg).  Per world, from q ~ U(joint range): link

@@ -61,6 +61,31 @@ class Scene:
 
 
 @dataclass
+class Articulation:
+    """Serial hinge chains shared by every world.  Chain t
+    starts at base[t] with the world frame's orientation; joint j rotates about
+    axis[t, j] given in the frame of the link before it (the base frame for
+    j = 0); link j extends length[t, j] along its local +z, carries mass[t, j]
+    with its centre of mass at mid-length and isotropic rotational inertia
+    inertia[t, j] about it; armature[t, j] adds to the joint-space inertia's
+    diagonal.  Data only (see oracle/articulation.py and include/comfree.h)."""
+    base: np.ndarray                         # (T,3)
+    axis: np.ndarray                         # (T,nd,3) unit, parent-link frame
+    length: np.ndarray                       # (T,nd)
+    mass: np.ndarray                         # (T,nd)
+    inertia: np.ndarray                      # (T,nd) isotropic, about the link COM
+    armature: np.ndarray                     # (T,nd)
+
+    @property
+    def n_trees(self) -> int:
+        return int(self.base.shape[0])
+
+    @property
+    def tree_ndof(self) -> int:
+        return int(self.length.shape[1])
+
+
+@dataclass
 class State:
     pos: np.ndarray
     quat: np.ndarray
