@@ -59,6 +59,9 @@ def parse():
                     help="per-contact (k_user, d_user) impedance arrays (learned-impedance variant, P:206-208)")
     ap.add_argument("--impedance", default="heuristic", choices=["heuristic", "exact_diagonal"],
                     help="exact_diagonal: Eq. (11) per facet (reading R24) instead of the trace heuristic")
+    ap.add_argument("--upstream", action="store_true",
+                    help="hand / mixed: run the articulated upstream (FK, M(q), Cholesky, c(q,v), chain J rows) "
+                         "on the GPU every step before the contact resolution (SURVEY 8(f) rank 2)")
     ap.add_argument("--workload", default="pile", choices=["pile", "hand", "mixed"],
                     help="pile: config 4 (the BASELINE metric); hand: config 3; mixed: config 5")
     a = ap.parse_args()
@@ -175,6 +178,8 @@ def workload(args, rank, world_size):
         name += " + per-contact impedance"
     if args.impedance == "exact_diagonal":
         name += " + exact-diagonal impedance (Eq. 11)"
+    if args.upstream:
+        name += " + articulated upstream on the GPU every step"
     return parts, name, n
 
 
@@ -310,6 +315,15 @@ def run_ours(args, rank, world_size, local):
                                   for a in (p.inp.f_ext, p.inp.tree_L, p.inp.tree_tau)))
         # part 0 on the caller's stream, the others on their own streams (fork / join)
         p.stream = stream if i == 0 else torch.cuda.Stream(device=dev)
+        p.up = None
+        if args.upstream and p.scene.n_trees > 0:     # articulated upstream every step
+            from harness import scenes as _sc
+            p.ctx.load_articulation(_sc.hand_articulation())
+            p.up = (torch.from_numpy(np.ascontiguousarray(p.c.meta["link"], np.int32)).to(dev),
+                    p.tin.tree_tau.clone())          # applied joint torques; tree_tau receives tau - c
+    alg_up = sum(p.W * p.scene.n_trees * (2 * 4 * p.scene.tree_ndof + 4 * 10 + 4 * p.scene.tree_ndof)
+                 + int(np.count_nonzero(p.c.body_a < -1) + np.count_nonzero(p.c.body_b < -1)) * (16 + 4 + 96)
+                 for p in parts if p.up is not None)
     flush = None if args.no_flush else torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     flush_sink = torch.empty(1, dtype=torch.float32, device=dev)
 
@@ -324,11 +338,12 @@ def run_ours(args, rank, world_size, local):
     def one_step(s0):
         """One step of every part: part 0 on s0, the rest forked from s0 and joined back."""
         for i, p in enumerate(parts):
-            if i == 0:
-                p.ctx.step(p.dc, p.tin, dt=cfg.dt, stream=s0)
-            else:
+            if i != 0:
                 p.stream.wait_stream(s0)
-                p.ctx.step(p.dc, p.tin, dt=cfg.dt, stream=p.stream)
+            ps = s0 if i == 0 else p.stream
+            if p.up is not None:
+                p.ctx.articulation_update(p.tin.tree_L, p.tin.tree_tau, p.dc, p.up[0], tau_ext=p.up[1], stream=ps)
+            p.ctx.step(p.dc, p.tin, dt=cfg.dt, stream=ps)
         for p in parts[1:]:
             s0.wait_stream(p.stream)
 
@@ -400,7 +415,7 @@ def run_ours(args, rank, world_size, local):
     # replay bracket exactly that kernel; with several parts the kernel's own
     # events (library timing, direct launches, parts running concurrently) are used.
     dom = parts[0]
-    k_ms = (total_ms / args.steps) if (graph is not None and len(parts) == 1) else dom.k_ms_direct
+    k_ms = (total_ms / args.steps) if (graph is not None and len(parts) == 1 and dom.up is None) else dom.k_ms_direct
     peak, peak_kind = peaks()
     achieved = dom.alg_bytes / (k_ms * 1e-3) / 1e9
     tr = ncu_traffic()
@@ -477,6 +492,8 @@ def run_ours(args, rank, world_size, local):
                                if args.flush_mode == "write+read" else "flushed between timed steps (256 MB write)")
                               if flush is not None else "not flushed"),
                        "footprint_mb_per_step": alg_total / 1e6,
+                       "articulated_upstream": bool(args.upstream),
+                       "upstream_mb_per_step": alg_up / 1e6,
                        "parallelism": f"world-sharded x{world_size}"},
             "contacts_per_s": contacts_per_s,
             "gpu_launches": int(launches),

@@ -406,6 +406,7 @@ def c3_hand(n_worlds=4096, seed=0, world_offset=0):
     ba = np.zeros((W, Cw), np.int32)
     bb = np.zeros((W, Cw), np.int32)
     jr = np.zeros((W, Cw, 2, 6, 4), np.float32)
+    lk = np.zeros((W, Cw, 2), np.int32)       # link index of each chain side (articulated upstream)
     bases = np.array([[0.04, -0.045, 0.0], [0.04, 0.0, 0.0], [0.04, 0.045, 0.0],
                       [-0.02, -0.06, 0.0]])
     for wi in range(W):
@@ -471,6 +472,7 @@ def c3_hand(n_worlds=4096, seed=0, world_offset=0):
                 n /= np.linalg.norm(n)
                 ba[wi, k], bb[wi, k] = -2 - t, 0
                 jr[wi, k, 0] = link_jac(t, l, p)
+                lk[wi, k, 0] = l
                 c0[wi, k] = (*p, rng.uniform(-2e-3, 5e-4))
                 c1[wi, k, :3] = n
                 k += 1
@@ -485,6 +487,7 @@ def c3_hand(n_worlds=4096, seed=0, world_offset=0):
             p = link_pts[t][3].copy()
             ba[wi, k], bb[wi, k] = -1, -2 - t
             jr[wi, k, 1] = link_jac(t, 3, p)
+            lk[wi, k, 1] = 3
             c0[wi, k] = (*p, rng.uniform(-2e-3, 5e-4))
             c1[wi, k, :3] = (0, 0, 1.0)
             k += 1
@@ -503,6 +506,7 @@ def c3_hand(n_worlds=4096, seed=0, world_offset=0):
                         c1.reshape(C, 4), c2.reshape(C, 4), ba.reshape(C), bb.reshape(C),
                         np.full(C, 1e-4, np.float32), np.full(C, 3, np.int32),
                         jr.reshape(C, 2, 6, 4))
+    contacts.meta["link"] = lk.reshape(C, 2)
     return scene, st, contacts, Inputs(None, Ls, tau)
 
 

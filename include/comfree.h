@@ -252,6 +252,51 @@ comfree_status comfree_get_state(comfree_ctx* ctx, int64_t first_world, int64_t 
 comfree_status comfree_set_state(comfree_ctx* ctx, int64_t first_world, int64_t n_worlds,
                                   const comfree_state* in, void* stream);
 
+/* ---- Articulated upstream ----------------------------
+ * The step takes each chain's Cholesky factor of M(q), tau - c(q, v) and the
+ * J rows of chain-side contacts as inputs (Eq. (1)-(2), P:80-97;
+ * Eq. (4)-(5)).  For serial hinge chains these can be computed on
+ * the device from the state with the two calls below.
+ *
+ * Chain t starts at base[t] with the world frame's orientation; joint j
+ * rotates about axis[t][j] (unit, in the frame of the link before it; the
+ * base frame for j = 0); link j extends length[t][j] along its local +z,
+ * has mass[t][j] at mid-length and isotropic rotational inertia inertia[t][j]
+ * about its centre of mass; armature[t][j] adds to M's diagonal:
+ *   M(q) = diag(armature) + sum_l m_l Jv_l^T Jv_l + I_l Jw_l^T Jw_l,
+ *   c(q, v) = the Coriolis/centrifugal/gravity bias (gravity from the config).
+ * HOST arrays, copied; n_trees / tree_ndof must equal the loaded scene's. */
+typedef struct {
+  int32_t n_trees, tree_ndof;
+  const float* base;      /* [T][3] */
+  const float* axis;      /* [T][nd][3] */
+  const float* length;    /* [T][nd] */
+  const float* mass;      /* [T][nd] */
+  const float* inertia;   /* [T][nd] */
+  const float* armature;  /* [T][nd] */
+} comfree_articulation;
+
+/* Validate and copy the chain model to the device (after load_scene).
+ * COMFREE_ERR_VALIDATION on a size mismatch, a non-unit axis or a negative
+ * link parameter. */
+comfree_status comfree_load_articulation(comfree_ctx* ctx, const comfree_articulation* art);
+
+/* For worlds [first_world, first_world + n_worlds), from the current state's
+ * chain q, v (the step-start pose, reading R17): tree_L[n_worlds][T][10]
+ * (packed Cholesky factor of M(q)) and tree_tau[n_worlds][Q] = tau_ext - c
+ * (tau_ext [n_worlds][Q] or NULL).  For the n contacts (world ids world[n],
+ * absolute; c0[n][4] points; c3[n][4] body ids as in comfree_contacts; link
+ * [n][2] link index of each side, read for chain sides only): the chain-side
+ * J rows at the contact point into jrow[12][n][4] (the comfree_contacts.jrow
+ * layout; rows of other sides are not written).  All pointers DEVICE,
+ * asynchronous on `stream`; errors (M not positive definite, bad chain or
+ * link id) are reported by the next synchronising call as
+ * COMFREE_ERR_VALIDATION. */
+comfree_status comfree_articulation_update(comfree_ctx* ctx, int64_t first_world, int64_t n_worlds,
+                                           const float* tau_ext, float* tree_L, float* tree_tau,
+                                           int64_t n_contacts, const int32_t* world, const float* c0,
+                                           const int32_t* c3, const int32_t* link, float* jrow, void* stream);
+
 /* Aggregate statistics of the last step (requires COMFREE_FLAG_STATS for
  * contacts / facets / penetration / energy; the non-finite check is always
  * on unless COMFREE_FLAG_NO_FINITE_CHECK).  Synchronises. */

@@ -238,6 +238,31 @@ class Context:
         self.scene = scene
         return self
 
+    def load_articulation(self, art):
+        """comfree_load_articulation from a harness.types.Articulation (host arrays)."""
+        arrs = [np.ascontiguousarray(getattr(art, k), np.float32)
+                for k in ("base", "axis", "length", "mass", "inertia", "armature")]
+        a = _lib.comfree_articulation(int(art.n_trees), int(art.tree_ndof), *[x.ctypes.data for x in arrs])
+        self._check(self._lib.comfree_load_articulation(self.h, ct.byref(a)), "comfree_load_articulation")
+        return self
+
+    def articulation_update(self, tree_L, tree_tau, contacts=None, link=None, tau_ext=None,
+                            first_world: int = 0, n_worlds: Optional[int] = None, stream=None):
+        """comfree_articulation_update: device tensors tree_L (W,T,10) and
+        tree_tau (W,Q) receive the chain factors and tau - c; with
+        ``contacts`` (DeviceContacts, jrow allocated) and ``link`` (device
+        int32 (C,2)), the chain-side J rows are written into contacts.jrow."""
+        nw = self.n_worlds - first_world if n_worlds is None else int(n_worlds)
+        n = 0 if contacts is None else int(contacts.n)
+        if n and (link is None or contacts.jrow is None):
+            raise ValueError("articulation_update: contacts need link ids and a jrow buffer")
+        s = _stream_handle(stream)
+        st = self._lib.comfree_articulation_update(
+            self.h, int(first_world), nw, _ptr(tau_ext), _ptr(tree_L), _ptr(tree_tau), n,
+            _ptr(contacts.world) if n else None, _ptr(contacts.c0) if n else None,
+            _ptr(contacts.c3) if n else None, _ptr(link) if n else None, _ptr(contacts.jrow) if n else None, s)
+        self._check(st, "comfree_articulation_update")
+
     def step(self, contacts, inputs=None, dt: Optional[float] = None, first_world: int = 0,
              n_worlds: Optional[int] = None, stream=None, impulses=None, foff=None,
              off=None, sorted_hint: Optional[bool] = None):

@@ -42,6 +42,12 @@ class comfree_state(ct.Structure):
                 ("location", ct.c_int32)]
 
 
+class comfree_articulation(ct.Structure):
+    _fields_ = [("n_trees", ct.c_int32), ("tree_ndof", ct.c_int32), ("base", ct.c_void_p), ("axis", ct.c_void_p),
+                ("length", ct.c_void_p), ("mass", ct.c_void_p), ("inertia", ct.c_void_p),
+                ("armature", ct.c_void_p)]
+
+
 class comfree_worlds(ct.Structure):
     _fields_ = [("first_world", ct.c_int64), ("n_worlds", ct.c_int64), ("f_ext", ct.c_void_p),
                 ("tree_L", ct.c_void_p), ("tree_tau", ct.c_void_p), ("location", ct.c_int32)]
@@ -80,6 +86,8 @@ SIGNATURES = {
     "comfree_get_state": (ct.c_int, [P, ct.c_int64, ct.c_int64, ct.POINTER(comfree_state), P]),
     "comfree_set_state": (ct.c_int, [P, ct.c_int64, ct.c_int64, ct.POINTER(comfree_state), P]),
     "comfree_get_stats": (ct.c_int, [P, ct.POINTER(comfree_stats), P]),
+    "comfree_load_articulation": (ct.c_int, [P, ct.POINTER(comfree_articulation)]),
+    "comfree_articulation_update": (ct.c_int, [P, ct.c_int64, ct.c_int64, P, P, P, ct.c_int64, P, P, P, P, P, P]),
     "comfree_get_world_stats": (ct.c_int, [P, ct.c_int64, ct.c_int64, P, ct.c_int32, P]),
     "comfree_segment_info": (ct.c_int, [P, P, P, P]),
     "comfree_set_timing": (ct.c_int, [P, ct.c_int]),

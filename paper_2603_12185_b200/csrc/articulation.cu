@@ -1,0 +1,231 @@
+// articulation.cu — the articulated upstream of the step on the GPU (SURVEY
+// §8(f) rank 2): for serial hinge chains (comfree_articulation), per world and
+// chain, from the step-start joint positions and velocities in the state slab:
+//   forward kinematics, joint-space inertia M(q) = armature + sum_l m_l Jv_l^T Jv_l
+//   + I_l Jw_l^T Jw_l, its Cholesky factor (packed, the step's tree_L), and the
+//   bias c(q, v) (Coriolis/centrifugal/gravity, Eq. (1)-(2))
+//   by a Newton-Euler forward pass at zero acceleration -> tree_tau = tau - c;
+// and per contact, the 6 x nd rows of a chain side (point velocity and angular
+// velocity of link l at the contact point, Eq. (4)-(5)) written in
+// the step's [12][n][4] jrow layout.
+// One thread per (world, chain) and one per contact; everything in registers
+// (nd <= 4).  HBM-bound on the slab reads and the factor / row writes.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "internal.h"
+
+namespace cf {
+
+namespace {
+
+struct V3 {
+  float x, y, z;
+};
+__device__ __forceinline__ V3 v3(float x, float y, float z) { return V3{x, y, z}; }
+__device__ __forceinline__ V3 add(V3 a, V3 b) { return v3(a.x + b.x, a.y + b.y, a.z + b.z); }
+__device__ __forceinline__ V3 sub(V3 a, V3 b) { return v3(a.x - b.x, a.y - b.y, a.z - b.z); }
+__device__ __forceinline__ V3 mul(float s, V3 a) { return v3(s * a.x, s * a.y, s * a.z); }
+__device__ __forceinline__ float dot(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ V3 cross(V3 a, V3 b) {
+  return v3(a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x);
+}
+
+// Forward kinematics of chain t (model in `art`: per chain base[3], then per
+// joint axis[3], length, mass, inertia, armature -> 3 + 7 nd floats) at q:
+// world joint axes a[j], joint origins o[j], link directions d[j] (link j's +z).
+__device__ __forceinline__ void chain_fk(const float* m, int nd, const float q[4], V3 a[4], V3 o[4], V3 d[4]) {
+  float R[9] = {1.f, 0.f, 0.f, 0.f, 1.f, 0.f, 0.f, 0.f, 1.f};
+  V3 org = v3(m[0], m[1], m[2]);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    if (j < nd) {
+      const float* mj = m + 3 + 7 * j;
+      const V3 al = v3(mj[0], mj[1], mj[2]);
+      const V3 ax = v3(R[0] * al.x + R[1] * al.y + R[2] * al.z, R[3] * al.x + R[4] * al.y + R[5] * al.z,
+                       R[6] * al.x + R[7] * al.y + R[8] * al.z);
+      // R <- Rot(ax, q_j) R  (Rodrigues: I + s K + (1 - c) K^2)
+      float s, c;
+      sincosf(q[j], &s, &c);
+      const float oc = 1.f - c;
+      const float Q[9] = {c + oc * ax.x * ax.x, oc * ax.x * ax.y - s * ax.z, oc * ax.x * ax.z + s * ax.y,
+                          oc * ax.x * ax.y + s * ax.z, c + oc * ax.y * ax.y, oc * ax.y * ax.z - s * ax.x,
+                          oc * ax.x * ax.z - s * ax.y, oc * ax.y * ax.z + s * ax.x, c + oc * ax.z * ax.z};
+      float N[9];
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) N[3 * r + k] = Q[3 * r] * R[k] + Q[3 * r + 1] * R[3 + k] + Q[3 * r + 2] * R[6 + k];
+#pragma unroll
+      for (int k = 0; k < 9; ++k) R[k] = N[k];
+      a[j] = ax;
+      o[j] = org;
+      d[j] = v3(R[2], R[5], R[8]);
+      org = add(org, mul(mj[3], d[j]));
+    }
+  }
+}
+
+// One thread per (world, chain): M, its Cholesky factor, tau - c.
+__global__ void k_chain_dynamics(const float* __restrict__ model, int T, int nd, const float* __restrict__ slab,
+                                 int slab_stride, int qoff, int Qp, int64_t n_worlds, const float* __restrict__ tau_ext,
+                                 float gx, float gy, float gz, float* __restrict__ L_out, float* __restrict__ tau_out,
+                                 int* __restrict__ err) {
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= n_worlds * T) return;
+  const int64_t w = id / T;
+  const int t = (int)(id - w * T);
+  const float* m = model + (size_t)t * (3 + 7 * nd);
+  const float* sq = slab + (size_t)w * slab_stride + qoff + t * nd;  // qpos, then qvel at + Qp
+  float q[4] = {0.f, 0.f, 0.f, 0.f}, v[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    if (j < nd) { q[j] = sq[j]; v[j] = sq[Qp + j]; }
+  V3 a[4], o[4], d[4];
+  chain_fk(m, nd, q, a, o, d);
+  // M = armature + sum_l m_l Jv_l^T Jv_l + I_l Jw_l^T Jw_l, with
+  // Jv_l[:, i] = a_i x (com_l - o_i), Jw_l[:, i] = a_i (i <= l)
+  float M[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) M[i][k] = (i == k && i < nd) ? m[3 + 7 * i + 6] : 0.f;
+  // bias by Newton-Euler at zero acceleration: link angular velocity w, angular
+  // acceleration al, joint-origin acceleration ao; c_i = sum_l Jv_l[:, i] . F_l + Jw_l[:, i] . N_l
+  float c[4] = {0.f, 0.f, 0.f, 0.f};
+  V3 w3 = v3(0.f, 0.f, 0.f), al = w3, ao = w3;
+  const V3 g = v3(gx, gy, gz);
+#pragma unroll
+  for (int l = 0; l < 4; ++l) {
+    if (l < nd) {
+      const float* ml = m + 3 + 7 * l;
+      const float len = ml[3], mass = ml[4], inert = ml[5];
+      const V3 com = add(o[l], mul(0.5f * len, d[l]));
+      V3 jv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) jv[i] = (i <= l && i < nd) ? cross(a[i], sub(com, o[i])) : v3(0.f, 0.f, 0.f);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (i <= l && k <= l) M[i][k] += mass * dot(jv[i], jv[k]) + inert * dot(a[i], a[k]);
+      const V3 aq = mul(v[l], a[l]);
+      const V3 wl = add(w3, aq);
+      const V3 all = add(al, cross(w3, aq));
+      const V3 r = sub(com, o[l]);
+      const V3 acom = add(add(ao, cross(all, r)), cross(wl, cross(wl, r)));
+      const V3 F = mul(mass, sub(acom, g));
+      const V3 N = mul(inert, all);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (i <= l) c[i] += dot(jv[i], F) + dot(a[i], N);
+      const V3 re = mul(2.f, r);  // joint l+1's origin: the link's far end
+      ao = add(add(ao, cross(all, re)), cross(wl, cross(wl, re)));
+      w3 = wl;
+      al = all;
+    }
+  }
+  // Cholesky M = L L^T (packed row-major lower triangle, L[i(i+1)/2 + j])
+  float Lp[10];
+#pragma unroll
+  for (int k = 0; k < 10; ++k) Lp[k] = 0.f;
+  bool ok = true;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (i < nd) {
+#pragma unroll
+      for (int j = 0; j <= i; ++j) {
+        float s = M[i][j];
+#pragma unroll
+        for (int k = 0; k < j; ++k) s -= Lp[i * (i + 1) / 2 + k] * Lp[j * (j + 1) / 2 + k];
+        if (j == i) {
+          ok &= s > 0.f;
+          Lp[i * (i + 1) / 2 + i] = sqrtf(fmaxf(s, 0.f));
+        } else {
+          Lp[i * (i + 1) / 2 + j] = s / Lp[j * (j + 1) / 2 + j];
+        }
+      }
+    }
+  }
+  if (!ok) atomicOr(err, ERR_ARTICULATION);
+  float* Lo = L_out + (size_t)id * 10;
+#pragma unroll
+  for (int k = 0; k < 10; ++k) Lo[k] = Lp[k];
+  float* to = tau_out + (size_t)w * T * nd + t * nd;
+  const float* te = tau_ext ? tau_ext + (size_t)w * T * nd + t * nd : nullptr;
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+    if (j < nd) to[j] = (te ? te[j] : 0.f) - c[j];
+}
+
+// One thread per contact: J rows of its chain sides (side s is chain -(2+t),
+// link[2c + s] in [0, nd)) at the contact point, in the [12][n][4] layout;
+// rows of free / static sides are left untouched (the step ignores them).
+__global__ void k_contact_rows(const float* __restrict__ model, int T, int nd, const float* __restrict__ slab,
+                               int slab_stride, int qoff, int64_t first_world, int64_t n_worlds, int64_t n,
+                               const int32_t* __restrict__ world, const float4* __restrict__ c0,
+                               const int4* __restrict__ c3, const int32_t* __restrict__ link,
+                               float4* __restrict__ jrow, int* __restrict__ err) {
+  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const int4 ids = c3[c];
+  const int64_t w = (int64_t)world[c] - first_world;
+  const float4 pc = c0[c];
+  const V3 p = v3(pc.x, pc.y, pc.z);
+#pragma unroll
+  for (int side = 0; side < 2; ++side) {
+    const int id = side ? ids.y : ids.x;
+    if (id >= -1) continue;
+    const int t = -2 - id;
+    const int l = link[2 * c + side];
+    if (t >= T || l < 0 || l >= nd || w < 0 || w >= n_worlds) {
+      atomicOr(err, ERR_ARTICULATION);
+      continue;
+    }
+    const float* sq = slab + (size_t)w * slab_stride + qoff + t * nd;
+    float q[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (j < nd) q[j] = sq[j];
+    V3 a[4], o[4], d[4];
+    chain_fk(model + (size_t)t * (3 + 7 * nd), nd, q, a, o, d);
+    float rows[6][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const bool on = i <= l && i < nd;
+      const V3 jl = on ? cross(a[i], sub(p, o[i])) : v3(0.f, 0.f, 0.f);
+      const V3 ja = on ? a[i] : v3(0.f, 0.f, 0.f);
+      rows[0][i] = jl.x; rows[1][i] = jl.y; rows[2][i] = jl.z;
+      rows[3][i] = ja.x; rows[4][i] = ja.y; rows[5][i] = ja.z;
+    }
+#pragma unroll
+    for (int r = 0; r < 6; ++r)
+      jrow[(size_t)(side * 6 + r) * n + c] = make_float4(rows[r][0], rows[r][1], rows[r][2], rows[r][3]);
+  }
+}
+
+int blocks(int64_t n, int bs) { return (int)((n + bs - 1) / bs); }
+
+}  // namespace
+
+cudaError_t launch_chain_dynamics(const float* model, const SceneDev& sc, const float* slab, int64_t n_worlds,
+                                  const float* tau_ext, const float g[3], float* L_out, float* tau_out, int* err,
+                                  cudaStream_t s) {
+  const int64_t n = n_worlds * sc.T;
+  if (n == 0) return cudaSuccess;
+  k_chain_dynamics<<<blocks(n, 128), 128, 0, s>>>(model, sc.T, sc.nd, slab, sc.slab, N_BODY_PLANES * sc.Bp, sc.Qp,
+                                                  n_worlds, tau_ext, g[0], g[1], g[2], L_out, tau_out, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_contact_rows(const float* model, const SceneDev& sc, const float* slab, int64_t first_world,
+                                int64_t n_worlds, int64_t n, const int32_t* world, const float4* c0, const int4* c3,
+                                const int32_t* link, float4* jrow, int* err, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  k_contact_rows<<<blocks(n, 128), 128, 0, s>>>(model, sc.T, sc.nd, slab, sc.slab, N_BODY_PLANES * sc.Bp,
+                                                first_world, n_worlds, n, world, c0, c3, link, jrow, err);
+  return cudaGetLastError();
+}
+
+}  // namespace cf

@@ -62,6 +62,9 @@ struct comfree_ctx {
   // host-input staging
   DevBuf in_world, in_off, in_c0, in_c1, in_c2, in_c3, in_jrow, in_kd, in_fext, in_L, in_tau, imp;
   DevBuf st_tmp;
+  // articulated upstream: device copy of the chain model (comfree_load_articulation)
+  DevBuf art;
+  bool art_loaded = false;
   int64_t launches = 0;
   int64_t last_first = 0, last_nw = 0, last_nc = 0;
   bool last_sorted_copy = false;
@@ -125,15 +128,16 @@ comfree_status check_latched(comfree_ctx* ctx, cudaStream_t s) {
   CUDA_TRY(ctx, cudaMemcpy(ctx->d_err, &zero, sizeof zero, cudaMemcpyHostToDevice));
   CUDA_TRY(ctx, cudaMemcpy(ctx->d_first_bad, &none, sizeof none, cudaMemcpyHostToDevice));
   if (e & (cf::ERR_UNSORTED | cf::ERR_WORLD_RANGE | cf::ERR_BODY_RANGE | cf::ERR_CONDIM | cf::ERR_IMPULSE_CAP |
-           cf::ERR_IMPEDANCE | cf::ERR_WORLD_CONTACTS))
-    return fail(ctx, COMFREE_ERR_VALIDATION, "device validation failed (flags 0x%x):%s%s%s%s%s%s%s", e,
+           cf::ERR_IMPEDANCE | cf::ERR_WORLD_CONTACTS | cf::ERR_ARTICULATION))
+    return fail(ctx, COMFREE_ERR_VALIDATION, "device validation failed (flags 0x%x):%s%s%s%s%s%s%s%s", e,
                 (e & cf::ERR_UNSORTED) ? " contacts not sorted by world;" : "",
                 (e & cf::ERR_WORLD_RANGE) ? " world id out of range;" : "",
                 (e & cf::ERR_BODY_RANGE) ? " body id out of range or chain side without J rows;" : "",
                 (e & cf::ERR_CONDIM) ? " condim not in {1,3,4,6};" : "",
                 (e & cf::ERR_IMPULSE_CAP) ? " impulses buffer too small;" : "",
                 (e & cf::ERR_IMPEDANCE) ? " per-contact impedance negative or non-finite;" : "",
-                (e & cf::ERR_WORLD_CONTACTS) ? " more than 65536 contacts in one world;" : "");
+                (e & cf::ERR_WORLD_CONTACTS) ? " more than 65536 contacts in one world;" : "",
+                (e & cf::ERR_ARTICULATION) ? " articulation: M(q) not positive definite or bad chain/link id;" : "");
   return fail(ctx, COMFREE_ERR_NONFINITE, "non-finite state in world %lld", (long long)bad);
 }
 
@@ -625,6 +629,63 @@ comfree_status comfree_get_state(comfree_ctx* ctx, int64_t first, int64_t nw, co
   return check_latched(ctx, s);
 }
 
+comfree_status comfree_load_articulation(comfree_ctx* ctx, const comfree_articulation* a) {
+  if (!ctx || !a) return COMFREE_ERR_INVALID_ARGUMENT;
+  if (!ctx->loaded) return fail(ctx, COMFREE_ERR_STATE, "load_articulation before load_scene");
+  const cf::SceneDev& sc = ctx->sc;
+  if (a->n_trees != sc.T || a->tree_ndof != sc.nd || sc.T == 0)
+    return fail(ctx, COMFREE_ERR_VALIDATION, "load_articulation: %d chains x %d DoFs, the scene has %d x %d",
+                a->n_trees, a->tree_ndof, sc.T, sc.nd);
+  if (!a->base || !a->axis || !a->length || !a->mass || !a->inertia || !a->armature)
+    return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "load_articulation: null array");
+  const int T = sc.T, nd = sc.nd, per = 3 + 7 * nd;
+  std::vector<float> h((size_t)T * per);
+  for (int t = 0; t < T; ++t) {
+    float* m = h.data() + (size_t)t * per;
+    for (int k = 0; k < 3; ++k) m[k] = a->base[3 * t + k];
+    for (int j = 0; j < nd; ++j) {
+      const int tj = t * nd + j;
+      float* mj = m + 3 + 7 * j;
+      const float ax = a->axis[3 * tj], ay = a->axis[3 * tj + 1], az = a->axis[3 * tj + 2];
+      const float nrm = std::sqrt(ax * ax + ay * ay + az * az);
+      if (!(std::fabs(nrm - 1.f) < 1e-3f)) return fail(ctx, COMFREE_ERR_VALIDATION, "load_articulation: axis not unit");
+      mj[0] = ax / nrm; mj[1] = ay / nrm; mj[2] = az / nrm;
+      mj[3] = a->length[tj]; mj[4] = a->mass[tj]; mj[5] = a->inertia[tj]; mj[6] = a->armature[tj];
+      for (int k = 3; k < 7; ++k)
+        if (!(finite(mj[k]) && mj[k] >= 0.f)) return fail(ctx, COMFREE_ERR_VALIDATION, "load_articulation: negative or non-finite link parameter");
+    }
+  }
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  CUDA_TRY(ctx, ensure(ctx->art, h.size() * sizeof(float)));
+  CUDA_TRY(ctx, cudaMemcpy(ctx->art.p, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice));
+  ctx->art_loaded = true;
+  return COMFREE_OK;
+}
+
+comfree_status comfree_articulation_update(comfree_ctx* ctx, int64_t first, int64_t nw, const float* tau_ext,
+                                           float* tree_L, float* tree_tau, int64_t n, const int32_t* world,
+                                           const float* c0, const int32_t* c3, const int32_t* link, float* jrow,
+                                           void* stream) {
+  if (!ctx) return COMFREE_ERR_INVALID_ARGUMENT;
+  if (!ctx->art_loaded) return fail(ctx, COMFREE_ERR_STATE, "articulation_update before load_articulation");
+  if (first < 0 || nw < 0 || first + nw > ctx->W) return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "articulation_update: world range");
+  if (nw > 0 && (!tree_L || !tree_tau)) return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "articulation_update: tree_L / tree_tau required");
+  if (n < 0 || n > INT32_MAX) return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "articulation_update: n_contacts");
+  if (n > 0 && (!world || !c0 || !c3 || !link || !jrow))
+    return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "articulation_update: contact arrays required");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  const cf::SceneDev& sc = ctx->sc;
+  const float* slab = ctx->slab + (size_t)first * sc.slab;
+  const float* model = static_cast<const float*>(ctx->art.p);
+  CUDA_TRY(ctx, cf::launch_chain_dynamics(model, sc, slab, nw, tau_ext, ctx->cfg.gravity, tree_L, tree_tau, ctx->d_err, s));
+  CUDA_TRY(ctx, cf::launch_contact_rows(model, sc, slab, first, nw, n, world, reinterpret_cast<const float4*>(c0),
+                                        reinterpret_cast<const int4*>(c3), link, reinterpret_cast<float4*>(jrow),
+                                        ctx->d_err, s));
+  ctx->launches += (nw > 0) + (n > 0);
+  return COMFREE_OK;
+}
+
 comfree_status comfree_set_state(comfree_ctx* ctx, int64_t first, int64_t nw, const comfree_state* in, void* stream) {
   if (!ctx || !in) return COMFREE_ERR_INVALID_ARGUMENT;
   if (!ctx->loaded) return fail(ctx, COMFREE_ERR_STATE, "set_state before load_scene");
@@ -726,7 +787,7 @@ void comfree_destroy(comfree_ctx* ctx) {
   DevBuf* bufs[] = {&ctx->off, &ctx->keys, &ctx->perm, &ctx->iota, &ctx->s0, &ctx->s1, &ctx->s2, &ctx->s3,
                     &ctx->sj, &ctx->skd, &ctx->nf, &ctx->foff, &ctx->cub_tmp, &ctx->in_world, &ctx->in_off, &ctx->in_c0,
                     &ctx->in_c1, &ctx->in_c2, &ctx->in_c3, &ctx->in_jrow, &ctx->in_kd, &ctx->in_fext, &ctx->in_L,
-                    &ctx->in_tau, &ctx->imp, &ctx->st_tmp};
+                    &ctx->in_tau, &ctx->imp, &ctx->st_tmp, &ctx->art};
   for (DevBuf* b : bufs) release(*b);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->slab) cudaFree(ctx->slab);

@@ -17,7 +17,8 @@ enum : int {
   ERR_CONDIM = 16,      // condim not in {1,3,4,6}
   ERR_IMPULSE_CAP = 32, // impulses buffer too small
   ERR_IMPEDANCE = 64,   // per-contact (k_user, d_user) negative or non-finite
-  ERR_WORLD_CONTACTS = 128  // more contacts in one world than the S6 fixed-point bound (65536)
+  ERR_WORLD_CONTACTS = 128, // more contacts in one world than the S6 fixed-point bound (65536)
+  ERR_ARTICULATION = 256    // articulated upstream: M(q) not positive definite, or a bad chain/link id
 };
 
 // State slab: per world, 13 planes of Bp floats (px py pz qw qx qy qz vx vy vz
@@ -92,6 +93,15 @@ cudaError_t launch_gather_contacts(const int32_t* perm, int64_t n, const float4*
 cudaError_t facet_offsets(const int4* c3, int64_t n, int n_t, int n_rol, int32_t* nf_tmp,
                           int64_t* foff, void* temp, size_t* temp_bytes, int* err, cudaStream_t s);
 cudaError_t launch_iota(int32_t* out, int64_t n, cudaStream_t s);
+
+// articulated upstream (articulation.cu); model: per chain base[3] + per joint
+// (axis[3], length, mass, inertia, armature), slab: world 0 of the range
+cudaError_t launch_chain_dynamics(const float* model, const SceneDev& sc, const float* slab, int64_t n_worlds,
+                                  const float* tau_ext, const float g[3], float* L_out, float* tau_out, int* err,
+                                  cudaStream_t s);
+cudaError_t launch_contact_rows(const float* model, const SceneDev& sc, const float* slab, int64_t first_world,
+                                int64_t n_worlds, int64_t n, const int32_t* world, const float4* c0, const int4* c3,
+                                const int32_t* link, float4* jrow, int* err, cudaStream_t s);
 
 // state layout conversion
 cudaError_t launch_public_to_slab(const float* pos, const float* quat, const float* vel,
