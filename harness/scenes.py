@@ -375,6 +375,31 @@ def hand_articulation() -> Articulation:
                         np.tile(lmass * lens ** 2 / 12, (T, 1)), np.full((T, nd), 2e-4))
 
 
+def hand_geometry(margin=0.001, tip_radius=0.008, cube_half=0.03):
+    """Collision geometry of the config-3 hand for the GPU front-end: the palm
+    plane z = 0, the cube (free body 0, box), and a sphere at the far end of
+    every finger link.  Candidate pairs: every link sphere with the cube
+    (normal from the finger to the cube), the palm with every link sphere but
+    the first of each finger, and the palm with the cube."""
+    from .types import Geometry
+    art = hand_articulation()
+    T, nd = art.n_trees, art.tree_ndof
+    kind, body, link, size, local = [2, 1], [-1, 0], [0, 0], [(0, 0, 1.0), (cube_half,) * 3], [(0.0, 0, 0), (0, 0, 0)]
+    for t in range(T):
+        for l in range(nd):
+            kind.append(0)
+            body.append(-2 - t)
+            link.append(l)
+            size.append((tip_radius, 0, 0))
+            local.append((0, 0, float(art.length[t, l])))
+    pairs = [(2 + t * nd + l, 1) for t in range(T) for l in range(nd)]
+    pairs += [(0, 2 + t * nd + l) for t in range(T) for l in range(1, nd)]
+    pairs += [(0, 1)]
+    return Geometry(np.array(kind, np.int32), np.array(body, np.int32), np.array(link, np.int32),
+                    np.array(size, np.float64), np.array(local, np.float64), np.array(pairs, np.int32),
+                    margin=margin)
+
+
 def c3_hand(n_worlds=4096, seed=0, world_offset=0):
     """Config 3: LEAP-like hand, 4 hinge chains x 4 DoF (nv = 16 + 6) plus a
     free cube (0.06 m, 0.1 kg).  Per world, from q ~ U(joint range): link

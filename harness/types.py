@@ -86,6 +86,26 @@ class Articulation:
 
 
 @dataclass
+class Geometry:
+    """Collision geometry shared by every world (the front-end of SURVEY §8(f)
+    rank 1).  Geom g is attached to body[g] (>= 0 free body, -1 static/world,
+    -(2+t) chain t, link link[g]) at position local[g] in that frame; kind 0
+    sphere (size[g, 0] = radius), 1 box (size = half extents, axes = the frame's),
+    2 plane (static; size = unit normal, local[g, 0] = offset: n . x = offset).
+    pairs (P,2) lists candidate geom pairs (g1, g2) tested in every world; the
+    contact normal points from g1 to g2 (body_a = body of g1).  Data only."""
+    kind: np.ndarray                         # (G,) int32
+    body: np.ndarray                         # (G,) int32
+    link: np.ndarray                         # (G,) int32
+    size: np.ndarray                         # (G,3)
+    local: np.ndarray                        # (G,3)
+    pairs: np.ndarray                        # (P,2) int32
+    margin: float = 0.001
+    mu: tuple = (1.0, 0.005, 0.0001)         # (mu_t, mu_tor, mu_rol) of every contact
+    condim: int = 3
+
+
+@dataclass
 class State:
     pos: np.ndarray
     quat: np.ndarray

@@ -4,8 +4,15 @@
 TAG=${1:-r01}
 mkdir -p gpurun_out
 timeout 600 python bench.py > gpurun_out/${TAG}_bench_pile.json 2> gpurun_out/${TAG}_bench_pile.err
+timeout 600 python bench.py --flush-mode write --cpu-seconds 1 > gpurun_out/${TAG}_bench_pile_writeflush.json 2> /dev/null
 timeout 600 python bench.py --workload hand --cpu-seconds 5 > gpurun_out/${TAG}_bench_hand.json 2> gpurun_out/${TAG}_bench_hand.err
+timeout 600 python bench.py --workload hand --upstream --cpu-seconds 2 > gpurun_out/${TAG}_bench_hand_upstream.json 2> /dev/null
 timeout 900 python bench.py --workload mixed --cpu-seconds 5 --steps 100 > gpurun_out/${TAG}_bench_mixed.json 2> gpurun_out/${TAG}_bench_mixed.err
+timeout 600 python bench.py --kd --cpu-seconds 0.5 > gpurun_out/${TAG}_bench_pile_kd.json 2> /dev/null
+timeout 600 python bench.py --impedance exact_diagonal --cpu-seconds 0.5 > gpurun_out/${TAG}_bench_pile_exact_diag.json 2> /dev/null
+for cd in 1 4 6; do
+  timeout 600 python bench.py --condim $cd --cpu-seconds 0.5 > gpurun_out/${TAG}_bench_pile_condim$cd.json 2> /dev/null
+done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_launches_pile.csv \
     python bench.py --steps 4 --warmup 3 --cpu-seconds 0.1 --e2e-steps 1 > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_step -s 3 -c 1 -o gpurun_out/${TAG}_prof_pile \
@@ -13,5 +20,5 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_st
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_step -s 3 -c 1 -o gpurun_out/${TAG}_prof_hand \
     python bench.py --workload hand --steps 2 --warmup 3 --cpu-seconds 0.1 --e2e-steps 1 > /dev/null 2>&1
 bash tools/sweep_contacts.sh ${TAG} > gpurun_out/${TAG}_c4_sweep.txt 2>&1
+bash tools/sweep_worlds.sh ${TAG} > gpurun_out/${TAG}_worlds_sweep.txt 2>&1
 ls -la gpurun_out | grep $TAG
-timeout 600 python bench.py --kd --cpu-seconds 0.5 > gpurun_out/${TAG}_bench_pile_kd.json 2> gpurun_out/${TAG}_bench_pile_kd.err
