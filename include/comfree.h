@@ -297,6 +297,50 @@ comfree_status comfree_articulation_update(comfree_ctx* ctx, int64_t first_world
                                            int64_t n_contacts, const int32_t* world, const float* c0,
                                            const int32_t* c3, const int32_t* link, float* jrow, void* stream);
 
+/* ---- Collision front-end -------------------------------
+ * Primitive narrowphase over a candidate pair list shared by every world,
+ * emitting the step's contact records (the paper takes them from MJWarp's
+ * collision; records as PAPER.md P:244-246).  Geom k: kind[k] 0 sphere
+ * (size[k][0] = radius), 1 box (size = half extents along the frame's axes),
+ * 2 plane (static; size = unit normal, local[k][0] = offset, n . x = offset);
+ * attached to body[k] (>= 0 free body, -1 world, -(2+t) chain t at link[k],
+ * which needs comfree_load_articulation) at local[k] in that frame.  Pair p =
+ * (pairs[2p], pairs[2p+1]) = (g1, g2) in {sphere-sphere, plane-sphere,
+ * plane-box, sphere-box, box-sphere}; the contact normal points from g1 to g2
+ * (body_a = body of g1), phi is the signed surface distance, the point the
+ * midpoint of the two surface points, t1 the branch-free basis of Duff et al.
+ * (2017); a pair emits when phi < margin (plane-box: every corner below).
+ * Every contact carries mu[0..2] = (mu_t, mu_tor, mu_rol) and condim.
+ * HOST arrays, copied. */
+typedef struct {
+  int32_t n_geoms, n_pairs;
+  const int32_t* kind;    /* [G] */
+  const int32_t* body;    /* [G] */
+  const int32_t* link;    /* [G] (chain geoms) */
+  const float* size;      /* [G][3] */
+  const float* local;     /* [G][3] */
+  const int32_t* pairs;   /* [P][2] */
+  float margin;
+  float mu[3];
+  int32_t condim;
+} comfree_geometry;
+
+/* Validate and copy the geometry (after load_scene, and load_articulation
+ * when chain geoms are present).  COMFREE_ERR_VALIDATION on bad kinds, bodies,
+ * links, sizes, unsupported pair kinds, margin / friction / condim. */
+comfree_status comfree_load_geometry(comfree_ctx* ctx, const comfree_geometry* geo);
+
+/* Contacts of worlds [first_world, first_world + n_worlds) at the current
+ * state into DEVICE arrays of `capacity` records: world[n] (absolute ids,
+ * sorted), c0/c1/c2 [n][4], c3 [n][4] (the comfree_contacts streams) and
+ * link [n][2] (link index of chain sides, for comfree_articulation_update);
+ * world-major, candidate-pair order within a world (deterministic).
+ * Synchronises `stream` once to read the count into *n_contacts;
+ * COMFREE_ERR_CAPACITY (with *n_contacts set) when it exceeds capacity. */
+comfree_status comfree_collide(comfree_ctx* ctx, int64_t first_world, int64_t n_worlds, int64_t capacity,
+                               int32_t* world, float* c0, float* c1, float* c2, int32_t* c3, int32_t* link,
+                               int64_t* n_contacts, void* stream);
+
 /* Aggregate statistics of the last step (requires COMFREE_FLAG_STATS for
  * contacts / facets / penetration / energy; the non-finite check is always
  * on unless COMFREE_FLAG_NO_FINITE_CHECK).  Synchronises. */

@@ -199,6 +199,7 @@ class Context:
         self.device = device
         self.n_worlds = 0
         self.scene = None
+        self._col = None
 
     # ---------------------------------------------------------------- helpers
     def _check(self, st: int, what: str):
@@ -245,6 +246,46 @@ class Context:
         a = _lib.comfree_articulation(int(art.n_trees), int(art.tree_ndof), *[x.ctypes.data for x in arrs])
         self._check(self._lib.comfree_load_articulation(self.h, ct.byref(a)), "comfree_load_articulation")
         return self
+
+    def load_geometry(self, geo):
+        """comfree_load_geometry from a harness.types.Geometry."""
+        arrs = [np.ascontiguousarray(geo.kind, np.int32), np.ascontiguousarray(geo.body, np.int32),
+                np.ascontiguousarray(geo.link, np.int32), np.ascontiguousarray(geo.size, np.float32),
+                np.ascontiguousarray(geo.local, np.float32), np.ascontiguousarray(geo.pairs, np.int32)]
+        g = _lib.comfree_geometry(int(arrs[0].shape[0]), int(arrs[5].shape[0]), *[a.ctypes.data for a in arrs],
+                                  float(geo.margin), (ct.c_float * 3)(*[float(m) for m in geo.mu]), int(geo.condim))
+        self._check(self._lib.comfree_load_geometry(self.h, ct.byref(g)), "comfree_load_geometry")
+        self._col = None
+        return self
+
+    def collide(self, capacity: int, first_world: int = 0, n_worlds: Optional[int] = None, stream=None):
+        """comfree_collide into device buffers of ``capacity`` records (kept by
+        the context and reused).  Returns (DeviceContacts, link (n,2) int32);
+        the contacts carry a zero J-row buffer when the scene has chains (for
+        articulation_update)."""
+        torch = _torch()
+        nw = self.n_worlds - first_world if n_worlds is None else int(n_worlds)
+        dev = torch.device("cuda", self.device)
+        if self._col is None or self._col["cap"] < capacity:
+            cap = max(int(capacity), 1)
+            self._col = dict(cap=cap, world=torch.empty(cap, dtype=torch.int32, device=dev),
+                             c0=torch.empty((cap, 4), device=dev), c1=torch.empty((cap, 4), device=dev),
+                             c2=torch.empty((cap, 4), device=dev),
+                             c3=torch.empty((cap, 4), dtype=torch.int32, device=dev),
+                             link=torch.empty((cap, 2), dtype=torch.int32, device=dev))
+        b = self._col
+        n = ct.c_int64(0)
+        st = self._lib.comfree_collide(self.h, int(first_world), nw, int(capacity), _ptr(b["world"]), _ptr(b["c0"]),
+                                       _ptr(b["c1"]), _ptr(b["c2"]), _ptr(b["c3"]), _ptr(b["link"]), ct.byref(n),
+                                       _stream_handle(stream))
+        self._check(st, "comfree_collide")
+        k = int(n.value)
+        jrow = None
+        if self.scene is not None and self.scene.n_trees > 0:
+            jrow = torch.zeros((12, max(k, 1), 4), device=dev)[:, :k]
+        dc = DeviceContacts(k, b["world"][:k], b["c0"][:k], b["c1"][:k], b["c2"][:k], b["c3"][:k],
+                            None if jrow is None else jrow.contiguous(), True)
+        return dc, b["link"][:k]
 
     def articulation_update(self, tree_L, tree_tau, contacts=None, link=None, tau_ext=None,
                             first_world: int = 0, n_worlds: Optional[int] = None, stream=None):

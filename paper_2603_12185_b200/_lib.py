@@ -48,6 +48,12 @@ class comfree_articulation(ct.Structure):
                 ("armature", ct.c_void_p)]
 
 
+class comfree_geometry(ct.Structure):
+    _fields_ = [("n_geoms", ct.c_int32), ("n_pairs", ct.c_int32), ("kind", ct.c_void_p), ("body", ct.c_void_p),
+                ("link", ct.c_void_p), ("size", ct.c_void_p), ("local", ct.c_void_p), ("pairs", ct.c_void_p),
+                ("margin", ct.c_float), ("mu", ct.c_float * 3), ("condim", ct.c_int32)]
+
+
 class comfree_worlds(ct.Structure):
     _fields_ = [("first_world", ct.c_int64), ("n_worlds", ct.c_int64), ("f_ext", ct.c_void_p),
                 ("tree_L", ct.c_void_p), ("tree_tau", ct.c_void_p), ("location", ct.c_int32)]
@@ -87,6 +93,8 @@ SIGNATURES = {
     "comfree_set_state": (ct.c_int, [P, ct.c_int64, ct.c_int64, ct.POINTER(comfree_state), P]),
     "comfree_get_stats": (ct.c_int, [P, ct.POINTER(comfree_stats), P]),
     "comfree_load_articulation": (ct.c_int, [P, ct.POINTER(comfree_articulation)]),
+    "comfree_load_geometry": (ct.c_int, [P, ct.POINTER(comfree_geometry)]),
+    "comfree_collide": (ct.c_int, [P, ct.c_int64, ct.c_int64, ct.c_int64, P, P, P, P, P, P, ct.POINTER(ct.c_int64), P]),
     "comfree_articulation_update": (ct.c_int, [P, ct.c_int64, ct.c_int64, P, P, P, ct.c_int64, P, P, P, P, P, P]),
     "comfree_get_world_stats": (ct.c_int, [P, ct.c_int64, ct.c_int64, P, ct.c_int32, P]),
     "comfree_segment_info": (ct.c_int, [P, P, P, P]),

@@ -17,7 +17,7 @@ OBJDIR = os.path.join(HERE, "_build")
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["step.cu", "step_w1.cu", "step_w2.cu", "step_w4.cu", "step_w8.cu", "segment.cu", "state.cu", "articulation.cu"]
+CU_SOURCES = ["step.cu", "step_w1.cu", "step_w2.cu", "step_w4.cu", "step_w8.cu", "segment.cu", "state.cu", "articulation.cu", "collide.cu"]
 CPP_SOURCES = ["capi.cpp"]
 
 
@@ -35,7 +35,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), tag: str = "")
     lib = os.path.join(objdir, f"libcomfree_{tag}.so") if tag else LIB
     dflags = [f"-D{d}" for d in defines]
     os.makedirs(objdir, exist_ok=True)
-    headers = [os.path.join(CSRC, "internal.h"), os.path.join(CSRC, "step_impl.cuh"),
+    headers = [os.path.join(CSRC, "internal.h"), os.path.join(CSRC, "step_impl.cuh"), os.path.join(CSRC, "chain.cuh"),
                os.path.join(INCLUDE, "comfree.h")]
     objs = []
     jobs = []

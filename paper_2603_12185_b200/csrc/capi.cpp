@@ -65,6 +65,12 @@ struct comfree_ctx {
   // articulated upstream: device copy of the chain model (comfree_load_articulation)
   DevBuf art;
   bool art_loaded = false;
+  // collision front-end: device geometry (comfree_load_geometry) and scan scratch
+  DevBuf geo, col_counts, col_offs, col_tmp;
+  int32_t n_geoms = 0, n_pairs = 0;
+  float col_margin = 0.f, col_mu[3] = {0.f, 0.f, 0.f};
+  int32_t col_condim = 3;
+  bool geo_loaded = false;
   int64_t launches = 0;
   int64_t last_first = 0, last_nw = 0, last_nc = 0;
   bool last_sorted_copy = false;
@@ -686,6 +692,124 @@ comfree_status comfree_articulation_update(comfree_ctx* ctx, int64_t first, int6
   return COMFREE_OK;
 }
 
+comfree_status comfree_load_geometry(comfree_ctx* ctx, const comfree_geometry* g) {
+  if (!ctx || !g) return COMFREE_ERR_INVALID_ARGUMENT;
+  if (!ctx->loaded) return fail(ctx, COMFREE_ERR_STATE, "load_geometry before load_scene");
+  const int G = g->n_geoms, P = g->n_pairs;
+  if (G < 0 || P < 0 || (G > 0 && (!g->kind || !g->body || !g->link || !g->size || !g->local)) || (P > 0 && !g->pairs))
+    return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "load_geometry: arrays");
+  if (!(g->margin >= 0.f && finite(g->margin)) || !(g->mu[0] >= 0.f && g->mu[1] >= 0.f && g->mu[2] >= 0.f) ||
+      !(g->condim == 1 || g->condim == 3 || g->condim == 4 || g->condim == 6))
+    return fail(ctx, COMFREE_ERR_VALIDATION, "load_geometry: margin, friction or condim");
+  const cf::SceneDev& sc = ctx->sc;
+  std::vector<int4> gi(G > 0 ? G : 1);
+  std::vector<float4> gs(G > 0 ? G : 1), gl(G > 0 ? G : 1);
+  bool chains = false;
+  for (int k = 0; k < G; ++k) {
+    const int kind = g->kind[k], body = g->body[k], link = g->link[k];
+    if (kind < 0 || kind > 2 || body >= sc.B || body < -1 - sc.T) return fail(ctx, COMFREE_ERR_VALIDATION, "load_geometry: geom %d kind/body", k);
+    if (body < -1 && (link < 0 || link >= sc.nd)) return fail(ctx, COMFREE_ERR_VALIDATION, "load_geometry: geom %d link", k);
+    if (kind == 2 && body != -1) return fail(ctx, COMFREE_ERR_VALIDATION, "load_geometry: planes must be static");
+    chains |= body < -1;
+    const float* sz = g->size + 3 * k;
+    const float* lc = g->local + 3 * k;
+    if (kind == 2) {
+      const float nrm = std::sqrt(sz[0] * sz[0] + sz[1] * sz[1] + sz[2] * sz[2]);
+      if (!(std::fabs(nrm - 1.f) < 1e-3f)) return fail(ctx, COMFREE_ERR_VALIDATION, "load_geometry: plane normal not unit");
+    } else if (!(sz[0] > 0.f && (kind == 0 || (sz[1] > 0.f && sz[2] > 0.f)))) {
+      return fail(ctx, COMFREE_ERR_VALIDATION, "load_geometry: geom %d size", k);
+    }
+    gi[k] = make_int4(kind, body, link, 0);
+    gs[k] = make_float4(sz[0], sz[1], sz[2], 0.f);
+    gl[k] = make_float4(lc[0], lc[1], lc[2], 0.f);
+  }
+  std::vector<int2> pr(P > 0 ? P : 1);
+  for (int k = 0; k < P; ++k) {
+    const int a = g->pairs[2 * k], b = g->pairs[2 * k + 1];
+    if (a < 0 || a >= G || b < 0 || b >= G) return fail(ctx, COMFREE_ERR_VALIDATION, "load_geometry: pair %d index", k);
+    const int ka = g->kind[a], kb = g->kind[b];
+    const bool ok = (ka == 0 && kb == 0) || (ka == 2 && (kb == 0 || kb == 1)) || (ka == 0 && kb == 1) || (ka == 1 && kb == 0);
+    if (!ok) return fail(ctx, COMFREE_ERR_VALIDATION, "load_geometry: pair %d kinds %d-%d not supported", k, ka, kb);
+    if (g->body[a] == g->body[b] && g->body[a] >= 0)
+      return fail(ctx, COMFREE_ERR_VALIDATION, "load_geometry: pair %d on one body", k);
+    pr[k] = make_int2(a, b);
+  }
+  if (chains && !ctx->art_loaded) return fail(ctx, COMFREE_ERR_STATE, "load_geometry: chain geoms need load_articulation first");
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  const size_t bytes = (size_t)gi.size() * (sizeof(int4) + 2 * sizeof(float4)) + pr.size() * sizeof(int2);
+  CUDA_TRY(ctx, ensure(ctx->geo, bytes));
+  char* base = static_cast<char*>(ctx->geo.p);
+  CUDA_TRY(ctx, cudaMemcpy(base, gi.data(), gi.size() * sizeof(int4), cudaMemcpyHostToDevice));
+  CUDA_TRY(ctx, cudaMemcpy(base + gi.size() * sizeof(int4), gs.data(), gs.size() * sizeof(float4), cudaMemcpyHostToDevice));
+  CUDA_TRY(ctx, cudaMemcpy(base + gi.size() * (sizeof(int4) + sizeof(float4)), gl.data(), gl.size() * sizeof(float4),
+                           cudaMemcpyHostToDevice));
+  CUDA_TRY(ctx, cudaMemcpy(base + gi.size() * (sizeof(int4) + 2 * sizeof(float4)), pr.data(), pr.size() * sizeof(int2),
+                           cudaMemcpyHostToDevice));
+  ctx->n_geoms = G;
+  ctx->n_pairs = P;
+  ctx->col_margin = g->margin;
+  for (int k = 0; k < 3; ++k) ctx->col_mu[k] = g->mu[k];
+  ctx->col_condim = g->condim;
+  ctx->geo_loaded = true;
+  return COMFREE_OK;
+}
+
+comfree_status comfree_collide(comfree_ctx* ctx, int64_t first, int64_t nw, int64_t capacity, int32_t* world,
+                               float* c0, float* c1, float* c2, int32_t* c3, int32_t* link, int64_t* n_out,
+                               void* stream) {
+  if (!ctx || !n_out) return COMFREE_ERR_INVALID_ARGUMENT;
+  *n_out = 0;
+  if (!ctx->geo_loaded) return fail(ctx, COMFREE_ERR_STATE, "collide before load_geometry");
+  if (first < 0 || nw < 0 || first + nw > ctx->W) return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "collide: world range");
+  if (capacity < 0 || (capacity > 0 && (!world || !c0 || !c1 || !c2 || !c3 || !link)))
+    return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "collide: output arrays");
+  if (nw * (int64_t)ctx->n_pairs * 8 >= INT32_MAX) return fail(ctx, COMFREE_ERR_CAPACITY, "collide: too many candidate pairs");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  cf::CollideParams P{};
+  P.sc = ctx->sc;
+  P.slab = ctx->slab + (size_t)first * ctx->sc.slab;
+  P.model = static_cast<const float*>(ctx->art.p);
+  const size_t G = ctx->n_geoms > 0 ? ctx->n_geoms : 1;
+  char* base = static_cast<char*>(ctx->geo.p);
+  P.geom = reinterpret_cast<const int4*>(base);
+  P.size = reinterpret_cast<const float4*>(base + G * sizeof(int4));
+  P.local = reinterpret_cast<const float4*>(base + G * (sizeof(int4) + sizeof(float4)));
+  P.pairs = reinterpret_cast<const int2*>(base + G * (sizeof(int4) + 2 * sizeof(float4)));
+  P.n_pairs = ctx->n_pairs;
+  P.n_worlds = nw;
+  P.first_world = first;
+  P.margin = ctx->col_margin;
+  P.mu_t = ctx->col_mu[0];
+  P.mu_tor = ctx->col_mu[1];
+  P.mu_rol = ctx->col_mu[2];
+  P.condim = ctx->col_condim;
+  P.c0 = reinterpret_cast<float4*>(c0);
+  P.c1 = reinterpret_cast<float4*>(c1);
+  P.c2 = reinterpret_cast<float4*>(c2);
+  P.c3 = reinterpret_cast<int4*>(c3);
+  P.world = world;
+  P.link = reinterpret_cast<int2*>(link);
+  const size_t m = (size_t)nw * ctx->n_pairs + 1;
+  CUDA_TRY(ctx, ensure(ctx->col_counts, m * sizeof(int32_t)));
+  CUDA_TRY(ctx, ensure(ctx->col_offs, m * sizeof(int32_t)));
+  size_t tb = 0;
+  CUDA_TRY(ctx, cf::collide_count_scan(P, nullptr, nullptr, nullptr, &tb, s));
+  CUDA_TRY(ctx, ensure(ctx->col_tmp, tb > 0 ? tb : 1));
+  tb = ctx->col_tmp.cap;
+  int32_t* offs = static_cast<int32_t*>(ctx->col_offs.p);
+  CUDA_TRY(ctx, cf::collide_count_scan(P, static_cast<int32_t*>(ctx->col_counts.p), offs, ctx->col_tmp.p, &tb, s));
+  int32_t total = 0;
+  CUDA_TRY(ctx, cudaMemcpyAsync(&total, offs + (m - 1), sizeof total, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  *n_out = total;
+  ctx->launches += 2;
+  if (total > capacity) return fail(ctx, COMFREE_ERR_CAPACITY, "collide: %d contacts, capacity %lld", total, (long long)capacity);
+  CUDA_TRY(ctx, cf::collide_emit(P, offs, capacity, s));
+  ctx->launches += 1;
+  return COMFREE_OK;
+}
+
 comfree_status comfree_set_state(comfree_ctx* ctx, int64_t first, int64_t nw, const comfree_state* in, void* stream) {
   if (!ctx || !in) return COMFREE_ERR_INVALID_ARGUMENT;
   if (!ctx->loaded) return fail(ctx, COMFREE_ERR_STATE, "set_state before load_scene");
@@ -787,7 +911,8 @@ void comfree_destroy(comfree_ctx* ctx) {
   DevBuf* bufs[] = {&ctx->off, &ctx->keys, &ctx->perm, &ctx->iota, &ctx->s0, &ctx->s1, &ctx->s2, &ctx->s3,
                     &ctx->sj, &ctx->skd, &ctx->nf, &ctx->foff, &ctx->cub_tmp, &ctx->in_world, &ctx->in_off, &ctx->in_c0,
                     &ctx->in_c1, &ctx->in_c2, &ctx->in_c3, &ctx->in_jrow, &ctx->in_kd, &ctx->in_fext, &ctx->in_L,
-                    &ctx->in_tau, &ctx->imp, &ctx->st_tmp, &ctx->art};
+                    &ctx->in_tau, &ctx->imp, &ctx->st_tmp, &ctx->art, &ctx->geo, &ctx->col_counts,
+                    &ctx->col_offs, &ctx->col_tmp};
   for (DevBuf* b : bufs) release(*b);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->slab) cudaFree(ctx->slab);

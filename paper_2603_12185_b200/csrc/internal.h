@@ -103,6 +103,30 @@ cudaError_t launch_contact_rows(const float* model, const SceneDev& sc, const fl
                                 int64_t n_worlds, int64_t n, const int32_t* world, const float4* c0, const int4* c3,
                                 const int32_t* link, float4* jrow, int* err, cudaStream_t s);
 
+// collision front-end (collide.cu)
+struct CollideParams {
+  SceneDev sc;
+  const float* slab;          // world 0 of the range
+  const float* model;         // articulation model (chain-link geoms) or null
+  const int4* geom;           // [G] (kind, body, link, 0)
+  const float4* size;         // [G]
+  const float4* local;        // [G]
+  const int2* pairs;          // [P]
+  int n_pairs;
+  int64_t n_worlds, first_world;
+  float margin, mu_t, mu_tor, mu_rol;
+  int condim;
+  float4* c0;
+  float4* c1;
+  float4* c2;
+  int4* c3;
+  int32_t* world;
+  int2* link;
+};
+cudaError_t collide_count_scan(const CollideParams& P, int32_t* counts, int32_t* offs, void* temp,
+                               size_t* temp_bytes, cudaStream_t s);
+cudaError_t collide_emit(const CollideParams& P, const int32_t* offs, int64_t capacity, cudaStream_t s);
+
 // state layout conversion
 cudaError_t launch_public_to_slab(const float* pos, const float* quat, const float* vel,
                                   const float* omega, const float* qpos, const float* qvel,

@@ -1,0 +1,165 @@
+"""GPU parity of the collision front-end (comfree_load_geometry /
+comfree_collide) with the fp64 oracle
+(oracle/collision.py): contact sets bit-exact (counts, world ids, body and
+link ids, order), records within fp32 tolerance; then the closed-loop hand
+(collide -> articulated upstream -> step on the GPU, every step) against the
+same loop in the oracle."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import articulation as ar
+from oracle import collision as co
+from harness import scenes
+from harness.types import Config, Geometry, Inputs, State
+from _gpu import assert_close, compare_step
+
+pytestmark = pytest.mark.gpu
+
+CFG = Config()
+ART = scenes.hand_articulation()
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2603_12185_b200 as cf
+    cf._lib.load()
+
+
+def _tie_worlds(geo, st, art):
+    """Worlds with a candidate within 2e-5 of the emission threshold (the fp32
+    and fp64 decisions may differ there): excluded from the set comparison."""
+    loose = Geometry(geo.kind, geo.body, geo.link, geo.size, geo.local, geo.pairs, margin=1e9, mu=geo.mu,
+                     condim=geo.condim)
+    allc = co.collide(loose, st, art)
+    return set(allc.world[np.abs(allc.c0[:, 3] - geo.margin) < 2e-5].tolist())
+
+
+def _compare(dc, link, ref, skip=()):
+    """Contact sets equal (ids exact, same order), records within fp32 tolerance,
+    on every world not in `skip`."""
+    w = dc.world.cpu().numpy()
+    gm = ~np.isin(w, list(skip))
+    rm = ~np.isin(ref.world, list(skip))
+    assert gm.sum() == rm.sum()
+    c3 = dc.c3.cpu().numpy()[gm]
+    np.testing.assert_array_equal(w[gm], ref.world[rm])
+    np.testing.assert_array_equal(c3[:, 0], ref.body_a[rm])
+    np.testing.assert_array_equal(c3[:, 1], ref.body_b[rm])
+    np.testing.assert_array_equal(c3[:, 3], ref.condim[rm])
+    np.testing.assert_array_equal(link.cpu().numpy()[gm], ref.meta["link"][rm])
+    assert_close(dc.c0.cpu().numpy()[gm, :3], ref.c0[rm, :3], rtol=0, atol=2e-6, what="contact point")
+    assert_close(dc.c0.cpu().numpy()[gm, 3], ref.c0[rm, 3], rtol=0, atol=1e-6, what="phi")
+    assert_close(dc.c1.cpu().numpy()[gm], ref.c1[rm], rtol=0, atol=2e-5, what="normal, mu_t")
+    assert_close(dc.c2.cpu().numpy()[gm], ref.c2[rm], rtol=0, atol=2e-5, what="t1, mu_tor")
+
+
+def test_hand_contacts_match_oracle():
+    import paper_2603_12185_b200 as cf
+    scene, st, _, _ = scenes.c3_hand(n_worlds=128)
+    geo = scenes.hand_geometry(margin=0.01)
+    st64 = st.astype(np.float64)
+    skip = _tie_worlds(geo, st64, ART)
+    assert len(skip) < 8
+    ctx = cf.Context(CFG)
+    ctx.load_scene(scene, st.n_worlds, st)
+    ctx.load_articulation(ART)
+    ctx.load_geometry(geo)
+    dc, link = ctx.collide(capacity=128 * 40)
+    ref = co.collide(geo, st64, ART)
+    assert ref.n > 128                     # the test sees contacts of every kind
+    _compare(dc, link, ref, skip)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_random_spheres_boxes_plane(seed):
+    """Free spheres and boxes above a plane, random poses; all supported pair kinds."""
+    import paper_2603_12185_b200 as cf
+    rng = np.random.default_rng(seed)
+    W, B = 16, 6
+    kind = [2] + [0, 1, 0, 1, 0, 1]
+    body = [-1] + list(range(B))
+    size = [(0, 0, 1.0)] + [(0.03, 0, 0), (0.04, 0.03, 0.02)] * 3
+    geo = Geometry(np.array(kind, np.int32), np.array(body, np.int32), np.zeros(B + 1, np.int32),
+                   np.array(size), np.zeros((B + 1, 3)),
+                   np.array([(0, g) for g in range(1, B + 1)] + [(1, 3), (1, 2), (4, 5), (2, 3), (5, 6)], np.int32),
+                   margin=0.02, mu=(0.7, 0.01, 0.001), condim=4)
+    pos = rng.uniform([-0.04, -0.04, 0.0], [0.04, 0.04, 0.06], (W, B, 3))
+    quat = rng.normal(size=(W, B, 4))
+    quat /= np.linalg.norm(quat, axis=2, keepdims=True)
+    st = State(pos, quat, np.zeros((W, B, 3)), np.zeros((W, B, 3)), np.zeros((W, 0)), np.zeros((W, 0)))
+    st32 = st.astype(np.float32)
+    st64 = st32.astype(np.float64)
+    skip = _tie_worlds(geo, st64, None)
+    from harness.types import Scene
+    scene = Scene(np.full(B, 2.0, np.float32), np.full((B, 3), 500.0, np.float32))
+    ctx = cf.Context(CFG)
+    ctx.load_scene(scene, W, st32)
+    ctx.load_geometry(geo)
+    dc, link = ctx.collide(capacity=W * 60)
+    _compare(dc, link, co.collide(geo, st64, None), skip)
+
+
+def test_capacity_and_validation():
+    import paper_2603_12185_b200 as cf
+    scene, st, _, _ = scenes.c3_hand(n_worlds=8)
+    ctx = cf.Context(CFG)
+    ctx.load_scene(scene, 8, st)
+    with pytest.raises(cf.ComfreeError) as ei:            # chain geoms before the articulation
+        ctx.load_geometry(scenes.hand_geometry())
+    assert ei.value.status == 6
+    ctx.load_articulation(ART)
+    bad = scenes.hand_geometry()
+    bad.pairs = np.array([(1, 1)], np.int32)              # box-box: not a supported pair
+    with pytest.raises(cf.ComfreeError) as ei:
+        ctx.load_geometry(bad)
+    assert ei.value.status == 2
+    ctx.load_geometry(scenes.hand_geometry(margin=10.0))  # every candidate emits: 36 per world
+    with pytest.raises(cf.ComfreeError) as ei:
+        ctx.collide(capacity=10)
+    assert ei.value.status == 3
+
+
+def test_closed_loop_hand():
+    """collide -> articulated upstream -> step, every step, 25 steps, on the GPU
+    and in the oracle; contact sets equal each step, states within 1e-3."""
+    import paper_2603_12185_b200 as cf
+    import torch
+    scene, st, _, inp = scenes.c3_hand(n_worlds=16)
+    geo = scenes.hand_geometry(margin=0.002)
+    ctx = cf.Context(CFG)
+    ctx.load_scene(scene, st.n_worlds, st)
+    ctx.load_articulation(ART)
+    ctx.load_geometry(geo)
+    W, T, Q = st.n_worlds, 4, 16
+    tL = torch.zeros((W, T, 10), device="cuda")
+    tt = torch.zeros((W, Q), device="cuda")
+    te = torch.from_numpy(np.ascontiguousarray(inp.tree_tau, np.float32)).cuda()
+    so = st.astype(np.float64)
+    for k in range(25):
+        dc, link = ctx.collide(capacity=W * 40)
+        ctx.articulation_update(tL, tt, dc, link, tau_ext=te)
+        ctx.step(dc, Inputs(None, tL, tt), dt=CFG.dt)
+        # oracle: same loop from its own state (fp32 records, like the product's)
+        cref = co.collide(geo, so, ART)
+        assert dc.n == cref.n, f"step {k}: {dc.n} vs {cref.n} contacts"
+        L, tau = ar.upstream(ART, so.qpos, so.qvel, CFG.gravity, inp.tree_tau.astype(np.float64))
+        J = np.zeros((cref.n, 2, 6, 4))
+        for i in range(cref.n):
+            for side, bid in enumerate((int(cref.body_a[i]), int(cref.body_b[i]))):
+                if bid < -1:
+                    t = -2 - bid
+                    J[i, side] = ar.point_rows(ART, t, so.qpos[int(cref.world[i]), 4 * t:4 * t + 4],
+                                               int(cref.meta["link"][i, side]), cref.c0[i, :3])
+        cref.jrow = J
+        so = oracle.step(CFG, scene, so, cref, Inputs(None, L, tau))["state"]
+    out = ctx.get_state()
+    for key in ("qvel", "qpos", "vel", "omega", "pos"):
+        ref = getattr(so, key)
+        err = np.abs(out[key] - ref)
+        assert np.all(err <= 1e-3 * np.abs(ref) + 1e-5), (key, float(err.max()))
