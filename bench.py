@@ -62,9 +62,16 @@ def parse():
     ap.add_argument("--upstream", action="store_true",
                     help="hand / mixed: run the articulated upstream (FK, M(q), Cholesky, c(q,v), chain J rows) "
                          "on the GPU every step before the contact resolution (SURVEY 8(f) rank 2)")
+    ap.add_argument("--collide", action="store_true",
+                    help="hand: closed loop - the GPU collision front-end (SURVEY 8(f) rank 1) builds the contacts "
+                         "every step, then the upstream and the step (implies --upstream; direct launches: "
+                         "comfree_collide reads its contact count back)")
     ap.add_argument("--workload", default="pile", choices=["pile", "hand", "mixed"],
                     help="pile: config 4 (the BASELINE metric); hand: config 3; mixed: config 5")
     a = ap.parse_args()
+    if a.collide:
+        a.upstream = True
+        a.no_graph = True
     if a.worlds is None:
         a.worlds = {"hand": 4096, "mixed": 65536}.get(a.workload, 1024)
     return a
@@ -180,6 +187,8 @@ def workload(args, rank, world_size):
         name += " + exact-diagonal impedance (Eq. 11)"
     if args.upstream:
         name += " + articulated upstream on the GPU every step"
+    if args.collide:
+        name += " + GPU collision front-end every step (closed loop)"
     return parts, name, n
 
 
@@ -321,6 +330,8 @@ def run_ours(args, rank, world_size, local):
             p.ctx.load_articulation(_sc.hand_articulation())
             p.up = (torch.from_numpy(np.ascontiguousarray(p.c.meta["link"], np.int32)).to(dev),
                     p.tin.tree_tau.clone())          # applied joint torques; tree_tau receives tau - c
+            if args.collide:
+                p.ctx.load_geometry(_sc.hand_geometry(margin=0.005))
     alg_up = sum(p.W * p.scene.n_trees * (2 * 4 * p.scene.tree_ndof + 4 * 10 + 4 * p.scene.tree_ndof)
                  + int(np.count_nonzero(p.c.body_a < -1) + np.count_nonzero(p.c.body_b < -1)) * (16 + 4 + 96)
                  for p in parts if p.up is not None)
@@ -342,6 +353,9 @@ def run_ours(args, rank, world_size, local):
                 p.stream.wait_stream(s0)
             ps = s0 if i == 0 else p.stream
             if p.up is not None:
+                if args.collide:                     # contacts from the current state (closed loop)
+                    p.dc, lk = p.ctx.collide(capacity=p.W * 40, stream=ps)
+                    p.up = (lk, p.up[1])
                 p.ctx.articulation_update(p.tin.tree_L, p.tin.tree_tau, p.dc, p.up[0], tau_ext=p.up[1], stream=ps)
             p.ctx.step(p.dc, p.tin, dt=cfg.dt, stream=ps)
         for p in parts[1:]:

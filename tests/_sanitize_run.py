@@ -29,4 +29,20 @@ scene, st, c, inp = scenes.random_instance(13, n_worlds=3, n_bodies=4, contacts_
 c = scenes.shuffle_contacts(c, 2)
 c.kd = np.tile(np.array([0.3, 0.002], np.float32), (c.n, 1))
 gpu_step(cfg, scene, st, c, inp)                                                 # per-contact impedance, sort + gather
+gpu_step(cfg.with_(impedance="exact_diagonal"), scene, st, c, inp)            # exact-diagonal impedance (Eq. (11))
+# articulated upstream + collision front-end + step (the closed-loop hand)
+import torch  # noqa: E402
+from harness.types import Inputs  # noqa: E402
+scene, st, c, inp = scenes.c3_hand(n_worlds=3)
+ctx = cf.Context(cfg)
+ctx.load_scene(scene, 3, st)
+ctx.load_articulation(scenes.hand_articulation())
+ctx.load_geometry(scenes.hand_geometry(margin=0.01))
+tL = torch.zeros((3, 4, 10), device="cuda")
+tt = torch.zeros((3, 16), device="cuda")
+for _ in range(2):
+    dc, link = ctx.collide(capacity=3 * 40)
+    ctx.articulation_update(tL, tt, dc, link)
+    ctx.step(dc, Inputs(None, tL, tt), dt=cfg.dt)
+ctx.get_state()
 print("sanitize run ok")
