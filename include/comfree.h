@@ -341,6 +341,50 @@ comfree_status comfree_collide(comfree_ctx* ctx, int64_t first_world, int64_t n_
                                int32_t* world, float* c0, float* c1, float* c2, int32_t* c3, int32_t* link,
                                int64_t* n_contacts, void* stream);
 
+/* ---- MPPI on the batched step -------------------------
+ * PAPER.md §V, Eq. (14)-(15), P:490-512 (reading R27).  The rollout
+ * worlds of a context are P problems x N samples, world w belonging to problem
+ * w / N; plans and samples are DEVICE arrays in DoF-minor layout: plan
+ * [P][H][Q], U [P][N][H][Q] (Q = the scene's chain DoFs).  A control step is
+ * mppi_sample, then for t = 0..H-1 {mppi_cost (running), mppi_control,
+ * collide / articulation_update / step}, mppi_cost (terminal), mppi_update. */
+typedef struct {
+  int32_t object_body;       /* the manipulated free body */
+  const float* target_pos;   /* [P][3] DEVICE */
+  const float* target_quat;  /* [P][4] DEVICE (w, x, y, z) */
+  const float* q_ref;        /* [Q] DEVICE home pose */
+  float w[6];                /* Eq. (15): quat, |dx|, |dy|, |dz|, fingertip-object, joint */
+  float omega_fallen, z_fallen;  /* Omega, fallen when p_z < z_fallen */
+  float phi1, phi2;          /* terminal V */
+} comfree_mppi_task;
+
+/* U = clip(plan + eps, lo, hi), eps_k = sigma sqrt(-2 ln(1 - u1)) cos(2 pi u2)
+ * with u1, u2 the top 24 bits of SplitMix64(seed + 2k), SplitMix64(seed + 2k + 1)
+ * over 2^24 and k = iteration * (P N H Q) + the element index (counter-based:
+ * reproducible, independent of launch shape).  sigma > 0, lo <= hi. */
+comfree_status comfree_mppi_sample(comfree_ctx* ctx, int32_t n_problems, int32_t n_samples, int32_t horizon,
+                                   const float* plan, float sigma, float lo, float hi, uint64_t seed,
+                                   uint64_t iteration, float* U, void* stream);
+
+/* Incremental position control for worlds [first_world, +n_worlds): command
+ * [n_worlds][Q] += U[w][t], then tau[n_worlds][Q] = kp (command - q) - kd qdot
+ * from the current state (pass tau as tau_ext to comfree_articulation_update). */
+comfree_status comfree_mppi_control(comfree_ctx* ctx, int64_t first_world, int64_t n_worlds, const float* U,
+                                    int32_t t, int32_t horizon, float kp, float kd, float* command, float* tau,
+                                    void* stream);
+
+/* J[n_worlds] += Eq. (15)'s running cost c(x) (terminal = 0) or terminal V(x)
+ * (terminal = 1) of the current state of each world (fingertips = chain tips
+ * from the loaded articulation; needs comfree_load_articulation). */
+comfree_status comfree_mppi_cost(comfree_ctx* ctx, int64_t first_world, int64_t n_worlds, int32_t n_samples,
+                                 const comfree_mppi_task* task, int32_t terminal, float* J, void* stream);
+
+/* Per problem: w_i = exp(-(J_i - min J)/lambda) / sum (weights [P][N] or
+ * NULL), plan[P][H][Q] = clip(sum_i w_i U_i, lo, hi).  lambda > 0; N <= 12288. */
+comfree_status comfree_mppi_update(comfree_ctx* ctx, int32_t n_problems, int32_t n_samples, int32_t horizon,
+                                   const float* J, const float* U, float lambda, float lo, float hi, float* plan,
+                                   float* weights, void* stream);
+
 /* Aggregate statistics of the last step (requires COMFREE_FLAG_STATS for
  * contacts / facets / penetration / energy; the non-finite check is always
  * on unless COMFREE_FLAG_NO_FINITE_CHECK).  Synchronises. */

@@ -54,6 +54,12 @@ class comfree_geometry(ct.Structure):
                 ("margin", ct.c_float), ("mu", ct.c_float * 3), ("condim", ct.c_int32)]
 
 
+class comfree_mppi_task(ct.Structure):
+    _fields_ = [("object_body", ct.c_int32), ("target_pos", ct.c_void_p), ("target_quat", ct.c_void_p),
+                ("q_ref", ct.c_void_p), ("w", ct.c_float * 6), ("omega_fallen", ct.c_float), ("z_fallen", ct.c_float),
+                ("phi1", ct.c_float), ("phi2", ct.c_float)]
+
+
 class comfree_worlds(ct.Structure):
     _fields_ = [("first_world", ct.c_int64), ("n_worlds", ct.c_int64), ("f_ext", ct.c_void_p),
                 ("tree_L", ct.c_void_p), ("tree_tau", ct.c_void_p), ("location", ct.c_int32)]
@@ -94,6 +100,14 @@ SIGNATURES = {
     "comfree_get_stats": (ct.c_int, [P, ct.POINTER(comfree_stats), P]),
     "comfree_load_articulation": (ct.c_int, [P, ct.POINTER(comfree_articulation)]),
     "comfree_load_geometry": (ct.c_int, [P, ct.POINTER(comfree_geometry)]),
+    "comfree_mppi_sample": (ct.c_int, [P, ct.c_int32, ct.c_int32, ct.c_int32, P, ct.c_float, ct.c_float, ct.c_float,
+                                       ct.c_uint64, ct.c_uint64, P, P]),
+    "comfree_mppi_control": (ct.c_int, [P, ct.c_int64, ct.c_int64, P, ct.c_int32, ct.c_int32, ct.c_float, ct.c_float,
+                                        P, P, P]),
+    "comfree_mppi_cost": (ct.c_int, [P, ct.c_int64, ct.c_int64, ct.c_int32, ct.POINTER(comfree_mppi_task), ct.c_int32,
+                                     P, P]),
+    "comfree_mppi_update": (ct.c_int, [P, ct.c_int32, ct.c_int32, ct.c_int32, P, P, ct.c_float, ct.c_float, ct.c_float,
+                                       P, P, P]),
     "comfree_collide": (ct.c_int, [P, ct.c_int64, ct.c_int64, ct.c_int64, P, P, P, P, P, P, ct.POINTER(ct.c_int64), P]),
     "comfree_articulation_update": (ct.c_int, [P, ct.c_int64, ct.c_int64, P, P, P, ct.c_int64, P, P, P, P, P, P]),
     "comfree_get_world_stats": (ct.c_int, [P, ct.c_int64, ct.c_int64, P, ct.c_int32, P]),

@@ -810,6 +810,74 @@ comfree_status comfree_collide(comfree_ctx* ctx, int64_t first, int64_t nw, int6
   return COMFREE_OK;
 }
 
+comfree_status comfree_mppi_sample(comfree_ctx* ctx, int32_t P, int32_t N, int32_t H, const float* plan, float sigma,
+                                   float lo, float hi, uint64_t seed, uint64_t iteration, float* U, void* stream) {
+  if (!ctx) return COMFREE_ERR_INVALID_ARGUMENT;
+  if (!ctx->loaded) return fail(ctx, COMFREE_ERR_STATE, "mppi_sample before load_scene");
+  if (P < 0 || N < 1 || H < 1 || (P > 0 && (!plan || !U))) return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "mppi_sample: sizes / arrays");
+  if (!(sigma > 0.f) || !(lo <= hi)) return fail(ctx, COMFREE_ERR_VALIDATION, "mppi_sample: sigma > 0 and lo <= hi");
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  CUDA_TRY(ctx, cf::mppi_sample(plan, P, N, H, ctx->sc.Q, sigma, lo, hi, seed, iteration, U, static_cast<cudaStream_t>(stream)));
+  ctx->launches += P > 0;
+  return COMFREE_OK;
+}
+
+comfree_status comfree_mppi_control(comfree_ctx* ctx, int64_t first, int64_t nw, const float* U, int32_t t, int32_t H,
+                                    float kp, float kd, float* command, float* tau, void* stream) {
+  if (!ctx) return COMFREE_ERR_INVALID_ARGUMENT;
+  if (!ctx->loaded) return fail(ctx, COMFREE_ERR_STATE, "mppi_control before load_scene");
+  if (first < 0 || nw < 0 || first + nw > ctx->W || t < 0 || t >= H || (nw > 0 && (!U || !command || !tau)))
+    return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "mppi_control: range / arrays");
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  CUDA_TRY(ctx, cf::mppi_control(ctx->sc, ctx->slab + (size_t)first * ctx->sc.slab, nw, U, t, H, kp, kd, command, tau,
+                                 static_cast<cudaStream_t>(stream)));
+  ctx->launches += nw > 0;
+  return COMFREE_OK;
+}
+
+comfree_status comfree_mppi_cost(comfree_ctx* ctx, int64_t first, int64_t nw, int32_t n_samples,
+                                 const comfree_mppi_task* task, int32_t terminal, float* J, void* stream) {
+  if (!ctx || !task) return COMFREE_ERR_INVALID_ARGUMENT;
+  if (!ctx->art_loaded) return fail(ctx, COMFREE_ERR_STATE, "mppi_cost before load_articulation");
+  if (first < 0 || nw < 0 || first + nw > ctx->W || n_samples < 1 || (nw > 0 && !J))
+    return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "mppi_cost: range / arrays");
+  if (task->object_body < 0 || task->object_body >= ctx->sc.B || !task->target_pos || !task->target_quat || !task->q_ref)
+    return fail(ctx, COMFREE_ERR_VALIDATION, "mppi_cost: object body / targets");
+  cf::MppiCostParams C{};
+  C.sc = ctx->sc;
+  C.slab = ctx->slab + (size_t)first * ctx->sc.slab;
+  C.model = static_cast<const float*>(ctx->art.p);
+  C.n_worlds = nw;
+  C.n_samples = n_samples;
+  C.obj = task->object_body;
+  C.target_pos = task->target_pos;
+  C.target_quat = task->target_quat;
+  C.q_ref = task->q_ref;
+  for (int k = 0; k < 6; ++k) C.w[k] = task->w[k];
+  C.omega_fallen = task->omega_fallen;
+  C.z_fallen = task->z_fallen;
+  C.phi1 = task->phi1;
+  C.phi2 = task->phi2;
+  C.terminal = terminal != 0;
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  CUDA_TRY(ctx, cf::mppi_cost(C, J, static_cast<cudaStream_t>(stream)));
+  ctx->launches += nw > 0;
+  return COMFREE_OK;
+}
+
+comfree_status comfree_mppi_update(comfree_ctx* ctx, int32_t P, int32_t N, int32_t H, const float* J, const float* U,
+                                   float lambda, float lo, float hi, float* plan, float* weights, void* stream) {
+  if (!ctx) return COMFREE_ERR_INVALID_ARGUMENT;
+  if (!ctx->loaded) return fail(ctx, COMFREE_ERR_STATE, "mppi_update before load_scene");
+  if (P < 0 || N < 1 || H < 1 || (P > 0 && (!J || !U || !plan))) return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "mppi_update: sizes / arrays");
+  if (!(lambda > 0.f) || !(lo <= hi)) return fail(ctx, COMFREE_ERR_VALIDATION, "mppi_update: lambda > 0 and lo <= hi");
+  if ((size_t)N * sizeof(float) > 48 * 1024) return fail(ctx, COMFREE_ERR_CAPACITY, "mppi_update: more than 12288 samples per problem");
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  CUDA_TRY(ctx, cf::mppi_update(J, U, P, N, H, ctx->sc.Q, lambda, lo, hi, plan, weights, static_cast<cudaStream_t>(stream)));
+  ctx->launches += P > 0;
+  return COMFREE_OK;
+}
+
 comfree_status comfree_set_state(comfree_ctx* ctx, int64_t first, int64_t nw, const comfree_state* in, void* stream) {
   if (!ctx || !in) return COMFREE_ERR_INVALID_ARGUMENT;
   if (!ctx->loaded) return fail(ctx, COMFREE_ERR_STATE, "set_state before load_scene");

@@ -127,6 +127,29 @@ cudaError_t collide_count_scan(const CollideParams& P, int32_t* counts, int32_t*
                                size_t* temp_bytes, cudaStream_t s);
 cudaError_t collide_emit(const CollideParams& P, const int32_t* offs, int64_t capacity, cudaStream_t s);
 
+// MPPI (mppi.cu)
+struct MppiCostParams {
+  SceneDev sc;
+  const float* slab;          // world 0 of the range
+  const float* model;         // articulation model (fingertips)
+  int64_t n_worlds;
+  int n_samples;              // world w belongs to problem w / n_samples
+  int obj;                    // object body index
+  const float* target_pos;    // [P][3]
+  const float* target_quat;   // [P][4]
+  const float* q_ref;         // [Q]
+  float w[6];
+  float omega_fallen, z_fallen, phi1, phi2;
+  int terminal;
+};
+cudaError_t mppi_sample(const float* plan, int P, int N, int H, int Q, float sigma, float lo, float hi, uint64_t seed,
+                        uint64_t iteration, float* U, cudaStream_t s);
+cudaError_t mppi_control(const SceneDev& sc, const float* slab, int64_t W, const float* U, int t, int H, float kp,
+                         float kd, float* command, float* tau, cudaStream_t s);
+cudaError_t mppi_cost(const MppiCostParams& C, float* J, cudaStream_t s);
+cudaError_t mppi_update(const float* J, const float* U, int P, int N, int H, int Q, float lambda, float lo, float hi,
+                        float* plan, float* weights, cudaStream_t s);
+
 // state layout conversion
 cudaError_t launch_public_to_slab(const float* pos, const float* quat, const float* vel,
                                   const float* omega, const float* qpos, const float* qvel,
