@@ -45,4 +45,11 @@ for _ in range(2):
     ctx.articulation_update(tL, tt, dc, link)
     ctx.step(dc, Inputs(None, tL, tt), dt=cfg.dt)
 ctx.get_state()
+# MPPI kernels (sample, control, cost, update) on a tiny rollout batch
+from paper_2603_12185_b200.mppi import MPPI, MppiConfig  # noqa: E402
+task = dict(object_body=0, target_pos=np.tile([0.02, 0.0, 0.05], (2, 1)), target_quat=np.tile([1.0, 0, 0, 0], (2, 1)),
+            q_ref=np.zeros(16), w=[1.0, 1.0, 1.0, 1.0, 1.0, 0.1], omega_fallen=10.0, z_fallen=0.03, phi1=1.0, phi2=1.0)
+m = MPPI(Config(dt=0.004), scene, scenes.hand_articulation(), scenes.hand_geometry(margin=0.003),
+         MppiConfig(n_problems=2, n_samples=4, horizon=2, task=task))
+m.control_step(st.world_slice(0, 2), np.zeros((2, 16)))
 print("sanitize run ok")
