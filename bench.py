@@ -64,14 +64,12 @@ def parse():
                          "on the GPU every step before the contact resolution (SURVEY 8(f) rank 2)")
     ap.add_argument("--collide", action="store_true",
                     help="hand: closed loop - the GPU collision front-end (SURVEY 8(f) rank 1) builds the contacts "
-                         "every step, then the upstream and the step (implies --upstream; direct launches: "
-                         "comfree_collide reads its contact count back)")
+                         "every step (count kept on the device), then the upstream and the step (implies --upstream)")
     ap.add_argument("--workload", default="pile", choices=["pile", "hand", "mixed"],
                     help="pile: config 4 (the BASELINE metric); hand: config 3; mixed: config 5")
     a = ap.parse_args()
     if a.collide:
         a.upstream = True
-        a.no_graph = True
     if a.worlds is None:
         a.worlds = {"hand": 4096, "mixed": 65536}.get(a.workload, 1024)
     return a
@@ -354,7 +352,7 @@ def run_ours(args, rank, world_size, local):
             ps = s0 if i == 0 else p.stream
             if p.up is not None:
                 if args.collide:                     # contacts from the current state (closed loop)
-                    p.dc, lk = p.ctx.collide(capacity=p.W * 40, stream=ps)
+                    p.dc, lk = p.ctx.collide(capacity=p.W * 40, stream=ps, device_count=True)
                     p.up = (lk, p.up[1])
                 p.ctx.articulation_update(p.tin.tree_L, p.tin.tree_tau, p.dc, p.up[0], tau_ext=p.up[1], stream=ps)
             p.ctx.step(p.dc, p.tin, dt=cfg.dt, stream=ps)

@@ -180,6 +180,11 @@ typedef struct {
   int64_t impulses_capacity; /* elements available at impulses (checked) */
   uint32_t flags;
   int32_t location;
+  /* optional DEVICE count of the contacts in use (<= n_contacts, which is then
+   * the length / stride of every stream), e.g. from comfree_collide in its
+   * asynchronous mode: no host round trip, graph-capturable.  Needs sorted
+   * DEVICE contacts with world[], no off[], impulses or foff. */
+  const int64_t* n_device;
 } comfree_contacts;
 
 /* Aggregate statistics of the last step. */
@@ -294,8 +299,9 @@ comfree_status comfree_load_articulation(comfree_ctx* ctx, const comfree_articul
  * COMFREE_ERR_VALIDATION. */
 comfree_status comfree_articulation_update(comfree_ctx* ctx, int64_t first_world, int64_t n_worlds,
                                            const float* tau_ext, float* tree_L, float* tree_tau,
-                                           int64_t n_contacts, const int32_t* world, const float* c0,
-                                           const int32_t* c3, const int32_t* link, float* jrow, void* stream);
+                                           int64_t n_contacts, const int64_t* n_device, const int32_t* world,
+                                           const float* c0, const int32_t* c3, const int32_t* link, float* jrow,
+                                           void* stream);
 
 /* ---- Collision front-end -------------------------------
  * Primitive narrowphase over a candidate pair list shared by every world,
@@ -331,15 +337,19 @@ typedef struct {
 comfree_status comfree_load_geometry(comfree_ctx* ctx, const comfree_geometry* geo);
 
 /* Contacts of worlds [first_world, first_world + n_worlds) at the current
- * state into DEVICE arrays of `capacity` records: world[n] (absolute ids,
- * sorted), c0/c1/c2 [n][4], c3 [n][4] (the comfree_contacts streams) and
+ * state into DEVICE arrays of `capacity` records: world[n] (ids relative to
+ * first_world, as comfree_step takes them; sorted), c0/c1/c2 [n][4], c3 [n][4] (the comfree_contacts streams) and
  * link [n][2] (link index of chain sides, for comfree_articulation_update);
  * world-major, candidate-pair order within a world (deterministic).
- * Synchronises `stream` once to read the count into *n_contacts;
- * COMFREE_ERR_CAPACITY (with *n_contacts set) when it exceeds capacity. */
+ * With n_device == NULL: synchronises `stream` once to read the count into
+ * *n_contacts (HOST); COMFREE_ERR_CAPACITY (with *n_contacts set) when it
+ * exceeds capacity.  With n_device (DEVICE int64): asynchronous, the count
+ * (clamped to capacity) goes to *n_device for comfree_contacts.n_device and
+ * comfree_articulation_update; an overflow is reported as
+ * COMFREE_ERR_CAPACITY by the next synchronising call. */
 comfree_status comfree_collide(comfree_ctx* ctx, int64_t first_world, int64_t n_worlds, int64_t capacity,
                                int32_t* world, float* c0, float* c1, float* c2, int32_t* c3, int32_t* link,
-                               int64_t* n_contacts, void* stream);
+                               int64_t* n_contacts, int64_t* n_device, void* stream);
 
 /* ---- MPPI on the batched step -------------------------
  * PAPER.md §V, Eq. (14)-(15), P:490-512 (reading R27).  The rollout

@@ -161,6 +161,7 @@ class DeviceContacts:
     jrow: object
     sorted: bool
     kd: object = None                      # (C, 2) per-contact (k_user, d_user) or None
+    n_dev: object = None                   # device int64 count of contacts in use (n = capacity), or None
 
     @staticmethod
     def from_host(contacts, device=None) -> "DeviceContacts":
@@ -258,26 +259,40 @@ class Context:
         self._col = None
         return self
 
-    def collide(self, capacity: int, first_world: int = 0, n_worlds: Optional[int] = None, stream=None):
+    def collide(self, capacity: int, first_world: int = 0, n_worlds: Optional[int] = None, stream=None,
+                device_count: bool = False):
         """comfree_collide into device buffers of ``capacity`` records (kept by
         the context and reused).  Returns (DeviceContacts, link (n,2) int32);
         the contacts carry a zero J-row buffer when the scene has chains (for
-        articulation_update)."""
+        articulation_update).  device_count=True: asynchronous mode, the count
+        stays on the device (contacts.n = capacity, contacts.n_dev = the count;
+        no host round trip, CUDA-graph capturable)."""
         torch = _torch()
         nw = self.n_worlds - first_world if n_worlds is None else int(n_worlds)
         dev = torch.device("cuda", self.device)
-        if self._col is None or self._col["cap"] < capacity:
+        if self._col is None or self._col["cap"] != capacity:
             cap = max(int(capacity), 1)
-            self._col = dict(cap=cap, world=torch.empty(cap, dtype=torch.int32, device=dev),
-                             c0=torch.empty((cap, 4), device=dev), c1=torch.empty((cap, 4), device=dev),
-                             c2=torch.empty((cap, 4), device=dev),
-                             c3=torch.empty((cap, 4), dtype=torch.int32, device=dev),
-                             link=torch.empty((cap, 2), dtype=torch.int32, device=dev))
+            self._col = dict(cap=cap, world=torch.zeros(cap, dtype=torch.int32, device=dev),
+                             c0=torch.zeros((cap, 4), device=dev), c1=torch.zeros((cap, 4), device=dev),
+                             c2=torch.zeros((cap, 4), device=dev),
+                             c3=torch.zeros((cap, 4), dtype=torch.int32, device=dev),
+                             link=torch.zeros((cap, 2), dtype=torch.int32, device=dev),
+                             n_dev=torch.zeros(1, dtype=torch.int64, device=dev),
+                             jrow=torch.zeros((12, cap, 4), device=dev))
         b = self._col
+        if device_count:
+            st = self._lib.comfree_collide(self.h, int(first_world), nw, int(capacity), _ptr(b["world"]),
+                                           _ptr(b["c0"]), _ptr(b["c1"]), _ptr(b["c2"]), _ptr(b["c3"]),
+                                           _ptr(b["link"]), None, _ptr(b["n_dev"]), _stream_handle(stream))
+            self._check(st, "comfree_collide")
+            jrow = b["jrow"] if (self.scene is not None and self.scene.n_trees > 0) else None
+            dc = DeviceContacts(int(capacity), b["world"], b["c0"], b["c1"], b["c2"], b["c3"], jrow, True,
+                                n_dev=b["n_dev"])
+            return dc, b["link"]
         n = ct.c_int64(0)
         st = self._lib.comfree_collide(self.h, int(first_world), nw, int(capacity), _ptr(b["world"]), _ptr(b["c0"]),
                                        _ptr(b["c1"]), _ptr(b["c2"]), _ptr(b["c3"]), _ptr(b["link"]), ct.byref(n),
-                                       _stream_handle(stream))
+                                       None, _stream_handle(stream))
         self._check(st, "comfree_collide")
         k = int(n.value)
         jrow = None
@@ -300,7 +315,7 @@ class Context:
         s = _stream_handle(stream)
         st = self._lib.comfree_articulation_update(
             self.h, int(first_world), nw, _ptr(tau_ext), _ptr(tree_L), _ptr(tree_tau), n,
-            _ptr(contacts.world) if n else None, _ptr(contacts.c0) if n else None,
+            _ptr(getattr(contacts, "n_dev", None)) if n else None, _ptr(contacts.world) if n else None, _ptr(contacts.c0) if n else None,
             _ptr(contacts.c3) if n else None, _ptr(link) if n else None, _ptr(contacts.jrow) if n else None, s)
         self._check(st, "comfree_articulation_update")
 
@@ -321,7 +336,8 @@ class Context:
                                   _ptr(off), _ptr(contacts.c0), _ptr(contacts.c1), _ptr(contacts.c2),
                                   _ptr(contacts.c3), _ptr(contacts.jrow), _ptr(getattr(contacts, "kd", None)),
                                   _ptr(impulses), _ptr(foff),
-                                  int(cap), CONTACTS_SORTED if srt else 0, loc)
+                                  int(cap), CONTACTS_SORTED if srt else 0, loc,
+                                  _ptr(getattr(contacts, "n_dev", None)))
         wloc = MEM_DEVICE
         fe = tl = tt = None
         if inputs is not None:

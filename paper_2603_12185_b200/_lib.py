@@ -69,7 +69,8 @@ class comfree_contacts(ct.Structure):
     _fields_ = [("n_contacts", ct.c_int64), ("world", ct.c_void_p), ("off", ct.c_void_p),
                 ("c0", ct.c_void_p), ("c1", ct.c_void_p), ("c2", ct.c_void_p), ("c3", ct.c_void_p),
                 ("jrow", ct.c_void_p), ("kd", ct.c_void_p), ("impulses", ct.c_void_p), ("foff", ct.c_void_p),
-                ("impulses_capacity", ct.c_int64), ("flags", ct.c_uint32), ("location", ct.c_int32)]
+                ("impulses_capacity", ct.c_int64), ("flags", ct.c_uint32), ("location", ct.c_int32),
+                ("n_device", ct.c_void_p)]
 
 
 class comfree_stats(ct.Structure):
@@ -108,8 +109,8 @@ SIGNATURES = {
                                      P, P]),
     "comfree_mppi_update": (ct.c_int, [P, ct.c_int32, ct.c_int32, ct.c_int32, P, P, ct.c_float, ct.c_float, ct.c_float,
                                        P, P, P]),
-    "comfree_collide": (ct.c_int, [P, ct.c_int64, ct.c_int64, ct.c_int64, P, P, P, P, P, P, ct.POINTER(ct.c_int64), P]),
-    "comfree_articulation_update": (ct.c_int, [P, ct.c_int64, ct.c_int64, P, P, P, ct.c_int64, P, P, P, P, P, P]),
+    "comfree_collide": (ct.c_int, [P, ct.c_int64, ct.c_int64, ct.c_int64, P, P, P, P, P, P, P, P, P]),
+    "comfree_articulation_update": (ct.c_int, [P, ct.c_int64, ct.c_int64, P, P, P, ct.c_int64, P, P, P, P, P, P, P]),
     "comfree_get_world_stats": (ct.c_int, [P, ct.c_int64, ct.c_int64, P, ct.c_int32, P]),
     "comfree_segment_info": (ct.c_int, [P, P, P, P]),
     "comfree_set_timing": (ct.c_int, [P, ct.c_int]),

@@ -119,14 +119,14 @@ __global__ void k_chain_dynamics(const float* __restrict__ model, int T, int nd,
 // link[2c + s] in [0, nd)) at the contact point, in the [12][n][4] layout;
 // rows of free / static sides are left untouched (the step ignores them).
 __global__ void k_contact_rows(const float* __restrict__ model, int T, int nd, const float* __restrict__ slab,
-                               int slab_stride, int qoff, int64_t first_world, int64_t n_worlds, int64_t n,
+                               int slab_stride, int qoff, int64_t n_worlds, int64_t n, const int64_t* __restrict__ n_dev,
                                const int32_t* __restrict__ world, const float4* __restrict__ c0,
                                const int4* __restrict__ c3, const int32_t* __restrict__ link,
                                float4* __restrict__ jrow, int* __restrict__ err) {
   const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= n) return;
+  if (c >= n || (n_dev && c >= *n_dev)) return;
   const int4 ids = c3[c];
-  const int64_t w = (int64_t)world[c] - first_world;
+  const int64_t w = world[c];  // relative to the range's first world, like comfree_step
   const float4 pc = c0[c];
   const V3 p = v3(pc.x, pc.y, pc.z);
 #pragma unroll
@@ -175,12 +175,12 @@ cudaError_t launch_chain_dynamics(const float* model, const SceneDev& sc, const 
   return cudaGetLastError();
 }
 
-cudaError_t launch_contact_rows(const float* model, const SceneDev& sc, const float* slab, int64_t first_world,
-                                int64_t n_worlds, int64_t n, const int32_t* world, const float4* c0, const int4* c3,
-                                const int32_t* link, float4* jrow, int* err, cudaStream_t s) {
+cudaError_t launch_contact_rows(const float* model, const SceneDev& sc, const float* slab, int64_t n_worlds,
+                                int64_t n, const int64_t* n_dev, const int32_t* world, const float4* c0,
+                                const int4* c3, const int32_t* link, float4* jrow, int* err, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   k_contact_rows<<<blocks(n, 128), 128, 0, s>>>(model, sc.T, sc.nd, slab, sc.slab, N_BODY_PLANES * sc.Bp,
-                                                first_world, n_worlds, n, world, c0, c3, link, jrow, err);
+                                                n_worlds, n, n_dev, world, c0, c3, link, jrow, err);
   return cudaGetLastError();
 }
 

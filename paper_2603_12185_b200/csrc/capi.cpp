@@ -133,6 +133,8 @@ comfree_status check_latched(comfree_ctx* ctx, cudaStream_t s) {
   const unsigned long long none = ~0ull;
   CUDA_TRY(ctx, cudaMemcpy(ctx->d_err, &zero, sizeof zero, cudaMemcpyHostToDevice));
   CUDA_TRY(ctx, cudaMemcpy(ctx->d_first_bad, &none, sizeof none, cudaMemcpyHostToDevice));
+  if (e & cf::ERR_CONTACT_CAP)
+    return fail(ctx, COMFREE_ERR_CAPACITY, "collide: more contacts than the output capacity (flags 0x%x)", e);
   if (e & (cf::ERR_UNSORTED | cf::ERR_WORLD_RANGE | cf::ERR_BODY_RANGE | cf::ERR_CONDIM | cf::ERR_IMPULSE_CAP |
            cf::ERR_IMPEDANCE | cf::ERR_WORLD_CONTACTS | cf::ERR_ARTICULATION))
     return fail(ctx, COMFREE_ERR_VALIDATION, "device validation failed (flags 0x%x):%s%s%s%s%s%s%s%s", e,
@@ -400,6 +402,10 @@ comfree_status comfree_step(comfree_ctx* ctx, const comfree_worlds* wd, const co
   if (sc.T > 0 && nw > 0 && (!wd->tree_L || !wd->tree_tau)) return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "step: chains need tree_L and tree_tau");
   if (c->location != COMFREE_MEM_DEVICE && c->location != COMFREE_MEM_HOST) return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "step: bad contacts location");
   if (c->impulses && c->impulses_capacity < 0) return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "step: impulses_capacity");
+  if (c->n_device && (!(c->flags & COMFREE_CONTACTS_SORTED) || !c->world || c->off || c->impulses || c->foff ||
+                      c->location != COMFREE_MEM_DEVICE))
+    return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT,
+                "step: n_device needs sorted DEVICE contacts with world[] and no off[] / impulses / foff");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   CUDA_TRY(ctx, cudaSetDevice(ctx->device));
   const int loc = c->location;
@@ -442,7 +448,7 @@ comfree_status comfree_step(comfree_ctx* ctx, const comfree_worlds* wd, const co
   if (!off) {
     CUDA_TRY(ctx, ensure(ctx->off, (size_t)(nw + 1) * sizeof(int64_t)));
     int64_t* doff = static_cast<int64_t*>(ctx->off.p);
-    if ((c->flags & COMFREE_CONTACTS_SORTED) && n > 0) {
+    if ((c->flags & COMFREE_CONTACTS_SORTED) && (n > 0 || c->n_device)) {
       // fused S0: the step kernel locates each world's range and verifies the ids
       fused_world = world;
     } else if (c->flags & COMFREE_CONTACTS_SORTED) {
@@ -546,6 +552,7 @@ comfree_status comfree_step(comfree_ctx* ctx, const comfree_worlds* wd, const co
   P.off_out = fused_world ? const_cast<int64_t*>(off) : nullptr;
   P.c0 = k0; P.c1 = k1; P.c2 = k2; P.c3 = k3; P.jrow = kj; P.kd = kk;
   P.n_contacts = n;
+  P.n_dev = c->n_device;
   P.perm = perm;
   P.foff = foff;
   P.impulses = imp;
@@ -669,9 +676,9 @@ comfree_status comfree_load_articulation(comfree_ctx* ctx, const comfree_articul
 }
 
 comfree_status comfree_articulation_update(comfree_ctx* ctx, int64_t first, int64_t nw, const float* tau_ext,
-                                           float* tree_L, float* tree_tau, int64_t n, const int32_t* world,
-                                           const float* c0, const int32_t* c3, const int32_t* link, float* jrow,
-                                           void* stream) {
+                                           float* tree_L, float* tree_tau, int64_t n, const int64_t* n_device,
+                                           const int32_t* world, const float* c0, const int32_t* c3,
+                                           const int32_t* link, float* jrow, void* stream) {
   if (!ctx) return COMFREE_ERR_INVALID_ARGUMENT;
   if (!ctx->art_loaded) return fail(ctx, COMFREE_ERR_STATE, "articulation_update before load_articulation");
   if (first < 0 || nw < 0 || first + nw > ctx->W) return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "articulation_update: world range");
@@ -685,7 +692,7 @@ comfree_status comfree_articulation_update(comfree_ctx* ctx, int64_t first, int6
   const float* slab = ctx->slab + (size_t)first * sc.slab;
   const float* model = static_cast<const float*>(ctx->art.p);
   CUDA_TRY(ctx, cf::launch_chain_dynamics(model, sc, slab, nw, tau_ext, ctx->cfg.gravity, tree_L, tree_tau, ctx->d_err, s));
-  CUDA_TRY(ctx, cf::launch_contact_rows(model, sc, slab, first, nw, n, world, reinterpret_cast<const float4*>(c0),
+  CUDA_TRY(ctx, cf::launch_contact_rows(model, sc, slab, nw, n, n_device, world, reinterpret_cast<const float4*>(c0),
                                         reinterpret_cast<const int4*>(c3), link, reinterpret_cast<float4*>(jrow),
                                         ctx->d_err, s));
   ctx->launches += (nw > 0) + (n > 0);
@@ -756,9 +763,9 @@ comfree_status comfree_load_geometry(comfree_ctx* ctx, const comfree_geometry* g
 
 comfree_status comfree_collide(comfree_ctx* ctx, int64_t first, int64_t nw, int64_t capacity, int32_t* world,
                                float* c0, float* c1, float* c2, int32_t* c3, int32_t* link, int64_t* n_out,
-                               void* stream) {
-  if (!ctx || !n_out) return COMFREE_ERR_INVALID_ARGUMENT;
-  *n_out = 0;
+                               int64_t* n_device, void* stream) {
+  if (!ctx || (!n_out && !n_device)) return COMFREE_ERR_INVALID_ARGUMENT;
+  if (n_out) *n_out = 0;
   if (!ctx->geo_loaded) return fail(ctx, COMFREE_ERR_STATE, "collide before load_geometry");
   if (first < 0 || nw < 0 || first + nw > ctx->W) return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "collide: world range");
   if (capacity < 0 || (capacity > 0 && (!world || !c0 || !c1 || !c2 || !c3 || !link)))
@@ -799,11 +806,17 @@ comfree_status comfree_collide(comfree_ctx* ctx, int64_t first, int64_t nw, int6
   tb = ctx->col_tmp.cap;
   int32_t* offs = static_cast<int32_t*>(ctx->col_offs.p);
   CUDA_TRY(ctx, cf::collide_count_scan(P, static_cast<int32_t*>(ctx->col_counts.p), offs, ctx->col_tmp.p, &tb, s));
+  ctx->launches += 2;
+  if (n_device) {  // asynchronous: count on the device, overflow latched as COMFREE_ERR_CAPACITY
+    CUDA_TRY(ctx, cf::collide_store_count(offs + (m - 1), capacity, n_device, ctx->d_err, s));
+    CUDA_TRY(ctx, cf::collide_emit(P, offs, capacity, s));
+    ctx->launches += 2;
+    return COMFREE_OK;
+  }
   int32_t total = 0;
   CUDA_TRY(ctx, cudaMemcpyAsync(&total, offs + (m - 1), sizeof total, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(ctx, cudaStreamSynchronize(s));
   *n_out = total;
-  ctx->launches += 2;
   if (total > capacity) return fail(ctx, COMFREE_ERR_CAPACITY, "collide: %d contacts, capacity %lld", total, (long long)capacity);
   CUDA_TRY(ctx, cf::collide_emit(P, offs, capacity, s));
   ctx->launches += 1;

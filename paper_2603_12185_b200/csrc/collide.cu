@@ -175,7 +175,7 @@ __device__ int pair_contacts(const CollideParams& P, int pi, int64_t w, int64_t 
       P.c1[c] = make_float4(nrm[k].x, nrm[k].y, nrm[k].z, P.mu_t);
       P.c2[c] = make_float4(t1.x, t1.y, t1.z, P.mu_tor);
       P.c3[c] = make_int4(g1.y, g2.y, __float_as_int(P.mu_rol), P.condim);
-      P.world[c] = (int32_t)(P.first_world + w);
+      P.world[c] = (int32_t)w;  // relative to the range's first world, like comfree_step
       P.link[c] = make_int2(la, lb);
     }
   }
@@ -213,6 +213,18 @@ cudaError_t collide_count_scan(const CollideParams& P, int32_t* counts, int32_t*
   if (n > 0) k_collide_count<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(P, counts);
   cudaMemsetAsync(counts + n, 0, sizeof(int32_t), s);
   return cub::DeviceScan::ExclusiveSum(temp, *temp_bytes, counts, offs, (int)(n + 1), s);
+}
+
+__global__ void k_store_count(const int32_t* __restrict__ total, int64_t capacity, int64_t* __restrict__ n_dev,
+                              int* __restrict__ err) {
+  const int64_t t = *total;
+  if (t > capacity) atomicOr(err, ERR_CONTACT_CAP);
+  *n_dev = t < capacity ? t : capacity;
+}
+
+cudaError_t collide_store_count(const int32_t* total, int64_t capacity, int64_t* n_dev, int* err, cudaStream_t s) {
+  k_store_count<<<1, 1, 0, s>>>(total, capacity, n_dev, err);
+  return cudaGetLastError();
 }
 
 cudaError_t collide_emit(const CollideParams& P, const int32_t* offs, int64_t capacity, cudaStream_t s) {

@@ -18,7 +18,8 @@ enum : int {
   ERR_IMPULSE_CAP = 32, // impulses buffer too small
   ERR_IMPEDANCE = 64,   // per-contact (k_user, d_user) negative or non-finite
   ERR_WORLD_CONTACTS = 128, // more contacts in one world than the S6 fixed-point bound (65536)
-  ERR_ARTICULATION = 256    // articulated upstream: M(q) not positive definite, or a bad chain/link id
+  ERR_ARTICULATION = 256,   // articulated upstream: M(q) not positive definite, or a bad chain/link id
+  ERR_CONTACT_CAP = 512     // collision front-end (device count): more contacts than the capacity
 };
 
 // State slab: per world, 13 planes of Bp floats (px py pz qw qx qy qz vx vy vz
@@ -60,7 +61,8 @@ struct StepParams {
   const int4* c3;
   const float4* jrow;           // [12][n_contacts] or null
   const float2* kd;             // [n_contacts] per-contact (k_user, d_user) or null
-  int64_t n_contacts;
+  int64_t n_contacts;           // stream length (capacity when n_dev is given)
+  const int64_t* n_dev;         // device-side count of contacts in use, or null
   const int32_t* perm;          // sorted position -> input index, or null (identity)
   const int64_t* foff;          // [n_contacts + 1] facet offsets (input order) or null
   float* impulses;              // or null
@@ -99,9 +101,9 @@ cudaError_t launch_iota(int32_t* out, int64_t n, cudaStream_t s);
 cudaError_t launch_chain_dynamics(const float* model, const SceneDev& sc, const float* slab, int64_t n_worlds,
                                   const float* tau_ext, const float g[3], float* L_out, float* tau_out, int* err,
                                   cudaStream_t s);
-cudaError_t launch_contact_rows(const float* model, const SceneDev& sc, const float* slab, int64_t first_world,
-                                int64_t n_worlds, int64_t n, const int32_t* world, const float4* c0, const int4* c3,
-                                const int32_t* link, float4* jrow, int* err, cudaStream_t s);
+cudaError_t launch_contact_rows(const float* model, const SceneDev& sc, const float* slab, int64_t n_worlds,
+                                int64_t n, const int64_t* n_dev, const int32_t* world, const float4* c0,
+                                const int4* c3, const int32_t* link, float4* jrow, int* err, cudaStream_t s);
 
 // collision front-end (collide.cu)
 struct CollideParams {
@@ -126,6 +128,7 @@ struct CollideParams {
 cudaError_t collide_count_scan(const CollideParams& P, int32_t* counts, int32_t* offs, void* temp,
                                size_t* temp_bytes, cudaStream_t s);
 cudaError_t collide_emit(const CollideParams& P, const int32_t* offs, int64_t capacity, cudaStream_t s);
+cudaError_t collide_store_count(const int32_t* total, int64_t capacity, int64_t* n_dev, int* err, cudaStream_t s);
 
 // MPPI (mppi.cu)
 struct MppiCostParams {

@@ -517,7 +517,9 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
   // S0 (sorted input, fused): the first warp of the group issues its range probe
   // now and resolves it after its share of S1 (the probe's latency overlaps S1).
   int probe = 0;
-  if (P.world_sorted && gt < 32) probe = probe_issue(P.world_sorted, P.n_contacts, P.n_worlds, w, w + 1, lane);
+  // contacts in use: the device-side count when given (the streams' capacity is P.n_contacts)
+  const int64_t ncon = P.n_dev ? min(*P.n_dev, P.n_contacts) : P.n_contacts;
+  if (P.world_sorted && gt < 32) probe = probe_issue(P.world_sorted, ncon, P.n_worlds, w, w + 1, lane);
   const float k = P.k, kappa_g = P.kappa;
   int n_active = 0;
   float max_pen = 0.f;
@@ -600,7 +602,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
   // S0: the first warp resolves the contact range of this world.
   if (P.world_sorted && gt < 32) {
     int64_t b0, b1;
-    lower_bound2(P.world_sorted, P.n_contacts, P.n_worlds, w, w + 1, lane, probe, b0, b1);
+    lower_bound2(P.world_sorted, ncon, P.n_worlds, w, w + 1, lane, probe, b0, b1);
     TL_MARK(4);
     if (lane == 0) {
       rng[0] = b0;
@@ -608,7 +610,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
       P.off_out[w] = b0;
       if (w == P.n_worlds - 1) P.off_out[w + 1] = b1;
       // coverage: ids below 0 precede world 0, ids >= n_worlds follow the last world
-      if ((w == 0 && b0 != 0) || (w == P.n_worlds - 1 && b1 != P.n_contacts)) atomicOr(P.err, ERR_WORLD_RANGE);
+      if ((w == 0 && b0 != 0) || (w == P.n_worlds - 1 && b1 != ncon)) atomicOr(P.err, ERR_WORLD_RANGE);
       if (b1 < b0) {  // only possible when the ids are not sorted
         atomicOr(P.err, ERR_UNSORTED);
         rng[1] = b0;

@@ -3,7 +3,9 @@ P:490-512; reading R27) — thin orchestration of C-ABI calls: every
 arithmetic step (sampling, control, collision, articulated upstream, contact
 resolution, costs, the weighted update) runs in libcomfree.so kernels.
 
-One control step for P problems x N samples x horizon H:
+One control step for P problems x N samples x horizon H (the H-step rollout
+is captured once in a CUDA graph and replayed; the collision keeps its
+contact count on the device, so nothing in it waits on the host):
   broadcast the live states to the P*N rollout worlds (comfree_set_state),
   U = clip(plan + eps)                                  comfree_mppi_sample
   for t < H:  J += c(x_t)                               comfree_mppi_cost
@@ -44,7 +46,7 @@ class MppiConfig:
 class MPPI:
     """Rollout context of P*N worlds plus the MPPI buffers (device)."""
 
-    def __init__(self, cfg, scene, articulation, geometry, mc: MppiConfig, device: int = 0):
+    def __init__(self, cfg, scene, articulation, geometry, mc: MppiConfig, device: int = 0, use_graph: bool = True):
         import torch
         self.torch = torch
         self.mc = mc
@@ -76,13 +78,15 @@ class MPPI:
                                              float(t["phi1"]), float(t["phi2"]))
         self.iteration = 0
         self._lib = _lib.load()
+        self.use_graph = use_graph
+        self.graph = None
 
     def _chk(self, st, what):
         self.ctx._check(st, what)
 
-    def rollout_costs(self, live_state, command, stream=None):
-        """Broadcast, sample, roll out H steps; returns J (P*N) on the device."""
-        from harness.types import Inputs, State
+    def _prepare(self, live_state, command, stream=None):
+        """Broadcast the live states / commands to the rollout worlds, zero J, sample U."""
+        from harness.types import State
         torch = self.torch
         mc, P, N, H = self.mc, self.mc.n_problems, self.mc.n_samples, self.mc.horizon
         rep = State(*(np.repeat(np.asarray(getattr(live_state, k), np.float32), N, axis=0)
@@ -90,20 +94,53 @@ class MPPI:
         self.ctx.set_state(rep, stream=stream)
         self.command.copy_(torch.as_tensor(np.repeat(np.asarray(command, np.float32), N, axis=0),
                                            device=self.command.device))
-        s = _stream_handle(stream)
         self.J.zero_()
         self._chk(self._lib.comfree_mppi_sample(self.ctx.h, P, N, H, _ptr(self.plan), mc.sigma, mc.u_min, mc.u_max,
-                                                mc.seed, self.iteration, _ptr(self.U), s), "comfree_mppi_sample")
+                                                mc.seed, self.iteration, _ptr(self.U), _stream_handle(stream)),
+                  "comfree_mppi_sample")
+
+    def _rollout(self, stream=None):
+        """H steps of (cost, control, collide, upstream, step), the terminal
+        cost: launches only (device-side contact counts), CUDA-graph capturable."""
+        from harness.types import Inputs
+        mc, N, H = self.mc, self.mc.n_samples, self.mc.horizon
+        s = _stream_handle(stream)
         for t in range(H):
             self._chk(self._lib.comfree_mppi_cost(self.ctx.h, 0, self.W, N, ct.byref(self.task_c), 0, _ptr(self.J), s),
                       "comfree_mppi_cost")
             self._chk(self._lib.comfree_mppi_control(self.ctx.h, 0, self.W, _ptr(self.U), t, H, mc.kp, mc.kd,
                                                      _ptr(self.command), _ptr(self.tau), s), "comfree_mppi_control")
-            dc, link = self.ctx.collide(capacity=self.W * mc.contacts_per_world, stream=stream)
+            dc, link = self.ctx.collide(capacity=self.W * mc.contacts_per_world, stream=stream, device_count=True)
             self.ctx.articulation_update(self.tL, self.tt, dc, link, tau_ext=self.tau, stream=stream)
             self.ctx.step(dc, Inputs(None, self.tL, self.tt), dt=self.dt, stream=stream)
         self._chk(self._lib.comfree_mppi_cost(self.ctx.h, 0, self.W, N, ct.byref(self.task_c), 1, _ptr(self.J), s),
                   "comfree_mppi_cost")
+
+    def rollout_costs(self, live_state, command, stream=None):
+        """Broadcast, sample, roll out H steps; returns J (P*N) on the device.
+        With use_graph the H-step rollout is one CUDA-graph replay (captured
+        on the first call, after an eager warm-up that sizes every buffer)."""
+        torch = self.torch
+        self._prepare(live_state, command, stream)
+        if not self.use_graph:
+            self._rollout(stream)
+            return self.J
+        if self.graph is None:
+            state0 = self.ctx.get_state()                     # warm-up run sizes the buffers, then restore
+            cmd0, J0 = self.command.clone(), self.J.clone()
+            self._rollout(stream)
+            torch.cuda.synchronize()
+            from harness.types import State
+            self.ctx.set_state(State(*(state0[k] for k in ("pos", "quat", "vel", "omega", "qpos", "qvel"))))
+            self.command.copy_(cmd0)
+            self.J.copy_(J0)
+            side = torch.cuda.Stream(device=self.J.device)
+            side.wait_stream(torch.cuda.current_stream())
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph, stream=side):
+                self._rollout(side)
+            torch.cuda.current_stream().wait_stream(side)
+        self.graph.replay()
         return self.J
 
     def update(self, stream=None):

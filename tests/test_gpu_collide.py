@@ -163,3 +163,38 @@ def test_closed_loop_hand():
         ref = getattr(so, key)
         err = np.abs(out[key] - ref)
         assert np.all(err <= 1e-3 * np.abs(ref) + 1e-5), (key, float(err.max()))
+
+
+def test_device_count_mode_matches_host_count_mode():
+    """comfree_collide with the count kept on the device (capacity-length
+    streams, comfree_contacts.n_device) gives bitwise the same closed-loop
+    trajectory as the host-count mode, and overflow is reported as
+    COMFREE_ERR_CAPACITY at the next synchronising call."""
+    import paper_2603_12185_b200 as cf
+    import torch
+    scene, st, _, inp = scenes.c3_hand(n_worlds=32)
+    geo = scenes.hand_geometry(margin=0.002)
+    outs = []
+    for dev_count in (False, True):
+        ctx = cf.Context(CFG)
+        ctx.load_scene(scene, st.n_worlds, st)
+        ctx.load_articulation(ART)
+        ctx.load_geometry(geo)
+        tL = torch.zeros((32, 4, 10), device="cuda")
+        tt = torch.zeros((32, 16), device="cuda")
+        te = torch.from_numpy(np.ascontiguousarray(inp.tree_tau, np.float32)).cuda()
+        for _ in range(10):
+            dc, link = ctx.collide(capacity=32 * 40, device_count=dev_count)
+            ctx.articulation_update(tL, tt, dc, link, tau_ext=te)
+            ctx.step(dc, Inputs(None, tL, tt), dt=CFG.dt)
+        outs.append(ctx.get_state())
+    for k in ("pos", "quat", "vel", "omega", "qpos", "qvel"):
+        np.testing.assert_array_equal(outs[0][k], outs[1][k])
+    ctx = cf.Context(CFG)
+    ctx.load_scene(scene, st.n_worlds, st)
+    ctx.load_articulation(ART)
+    ctx.load_geometry(scenes.hand_geometry(margin=10.0))   # 36 candidates per world emit
+    ctx.collide(capacity=100, device_count=True)
+    with pytest.raises(cf.ComfreeError) as ei:
+        ctx.get_state()
+    assert ei.value.status == 3
