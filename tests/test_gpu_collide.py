@@ -198,3 +198,44 @@ def test_device_count_mode_matches_host_count_mode():
     with pytest.raises(cf.ComfreeError) as ei:
         ctx.get_state()
     assert ei.value.status == 3
+
+
+def test_closed_loop_full_size_sampled_worlds():
+    """Config-3 size (4096 hand worlds), the bench's closed-loop launch
+    (device-side count): after 3 steps, sampled worlds against the oracle loop
+    run on those worlds alone."""
+    import paper_2603_12185_b200 as cf
+    import torch
+    scene, st, _, inp = scenes.c3_hand(n_worlds=4096)
+    geo = scenes.hand_geometry(margin=0.005)
+    ctx = cf.Context(CFG)
+    ctx.load_scene(scene, 4096, st)
+    ctx.load_articulation(ART)
+    ctx.load_geometry(geo)
+    tL = torch.zeros((4096, 4, 10), device="cuda")
+    tt = torch.zeros((4096, 16), device="cuda")
+    te = torch.from_numpy(np.ascontiguousarray(inp.tree_tau, np.float32)).cuda()
+    for _ in range(3):
+        dc, link = ctx.collide(capacity=4096 * 40, device_count=True)
+        ctx.articulation_update(tL, tt, dc, link, tau_ext=te)
+        ctx.step(dc, Inputs(None, tL, tt), dt=CFG.dt)
+    out = ctx.get_state()
+    for w in (0, 1234, 4095):
+        so = st.world_slice(w, w + 1).astype(np.float64)
+        tau_w = inp.tree_tau[w:w + 1].astype(np.float64)
+        for _ in range(3):
+            cref = co.collide(geo, so, ART)
+            J = np.zeros((cref.n, 2, 6, 4))
+            for i in range(cref.n):
+                for side, bid in enumerate((int(cref.body_a[i]), int(cref.body_b[i]))):
+                    if bid < -1:
+                        t = -2 - bid
+                        J[i, side] = ar.point_rows(ART, t, so.qpos[0, 4 * t:4 * t + 4],
+                                                   int(cref.meta["link"][i, side]), cref.c0[i, :3])
+            cref.jrow = J
+            L, tau = ar.upstream(ART, so.qpos, so.qvel, CFG.gravity, tau_w)
+            so = oracle.step(CFG, scene, so, cref, Inputs(None, L, tau))["state"]
+        for key in ("qvel", "qpos", "vel", "omega", "pos"):
+            ref = getattr(so, key)
+            err = np.abs(out[key][w:w + 1] - ref)
+            assert np.all(err <= 1e-4 * np.abs(ref) + 1e-6), (w, key, float(err.max()))

@@ -57,3 +57,23 @@ def test_exact_differs_from_heuristic_on_gpu():
     a = gpu_step(EX, scene, st, c, inp)["impulses"]
     b = gpu_step(EX.with_(impedance="heuristic"), scene, st, c, inp)["impulses"]
     assert np.max(np.abs(a - b)) > 1e-3 * np.max(np.abs(b))
+
+
+def test_exact_c4_full_size_sampled_worlds():
+    """The exact-diagonal variant at BASELINE config-4 size (1024 worlds x 500
+    bodies x 2000 contacts, the bench's --impedance exact_diagonal launch);
+    sampled worlds against the oracle one by one."""
+    import paper_2603_12185_b200 as cf
+    from harness.types import State
+    scene, st, c = scenes.c4_pile(n_worlds=1024, contacts_per_world=2000)
+    ctx = cf.Context(EX)
+    ctx.load_scene(scene, 1024, st)
+    ctx.step(cf.DeviceContacts.from_host(c), None, dt=EX.dt)
+    out = ctx.get_state()
+    for w in (0, 333, 1023):
+        sel = np.nonzero(c.world == w)[0]
+        cw = c.take(sel)
+        cw.world = np.zeros(len(sel), np.int32)
+        o = oracle.step(EX, scene, st.world_slice(w, w + 1), cw, None)
+        gst = State(*(out[k][w:w + 1] for k in ("pos", "quat", "vel", "omega", "qpos", "qvel")))
+        compare_step(dict(state=gst), o)
