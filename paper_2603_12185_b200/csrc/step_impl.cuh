@@ -48,6 +48,9 @@ namespace cf {
 #ifndef CF_L2AHEAD
 #define CF_L2AHEAD 0  // measured slightly slower (59.7 vs 59.4 us, C4)
 #endif
+#ifndef CF_EARLY_RANGE
+#define CF_EARLY_RANGE 1
+#endif
 static constexpr int kS1Unroll = CF_S1_UNROLL;  // S1 bodies per thread in flight (unstaged S1)
 static constexpr int kWarps = 8;
 static constexpr int kThreads = kWarps * 32;
@@ -519,7 +522,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
   int probe = 0;
   // contacts in use: the device-side count when given (the streams' capacity is P.n_contacts)
   const int64_t ncon = P.n_dev ? min(*P.n_dev, P.n_contacts) : P.n_contacts;
-  if (P.world_sorted && gt < 32) probe = probe_issue(P.world_sorted, ncon, P.n_worlds, w, w + 1, lane);
+  if (P.world_sorted && (CF_EARLY_RANGE || gt < 32)) probe = probe_issue(P.world_sorted, ncon, P.n_worlds, w, w + 1, lane);
   const float k = P.k, kappa_g = P.kappa;
   int n_active = 0;
   float max_pen = 0.f;
@@ -599,10 +602,18 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
     s1_body(i, nullptr, omz, im, ib, ibi);
   }
   TL_MARK(5);
-  // S0: the first warp resolves the contact range of this world.
+  // S0: the contact range of this world (CF_EARLY_RANGE: every warp resolves it
+  // itself and issues its first contact loads before the group barrier;
+  // otherwise the first warp resolves it and shares it through shared memory)
+  int64_t e_b0 = 0, e_b1 = 0;
+  if (CF_EARLY_RANGE && P.world_sorted) {
+    lower_bound2(P.world_sorted, ncon, P.n_worlds, w, w + 1, lane, probe, e_b0, e_b1);
+    if (e_b1 < e_b0) e_b1 = e_b0;  // unsorted ids (reported below)
+  }
   if (P.world_sorted && gt < 32) {
     int64_t b0, b1;
-    lower_bound2(P.world_sorted, ncon, P.n_worlds, w, w + 1, lane, probe, b0, b1);
+    if (CF_EARLY_RANGE) { b0 = e_b0; b1 = e_b1; }
+    else lower_bound2(P.world_sorted, ncon, P.n_worlds, w, w + 1, lane, probe, b0, b1);
     TL_MARK(4);
     if (lane == 0) {
       rng[0] = b0;
@@ -615,6 +626,18 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
         atomicOr(P.err, ERR_UNSORTED);
         rng[1] = b0;
       }
+    }
+  }
+  int64_t cbeg = 0;
+  int nloc = 0;
+  int WID = (int)w;  // world id of the prefetched contact (fused S0 check)
+  if (CF_EARLY_RANGE) {  // first contact of this lane in flight across the barrier
+    cbeg = P.world_sorted ? e_b0 : P.off[w];
+    nloc = (int)((P.world_sorted ? e_b1 : P.off[w + 1]) - cbeg);
+    if (base + lane < nloc) {
+      const int64_t g = cbeg + base + lane;
+      C0 = ld_stream(P.c0 + g); C1 = ld_stream(P.c1 + g); C2 = ld_stream(P.c2 + g); C3 = ld_stream(P.c3 + g);
+      if (P.world_sorted) WID = ld_id(P.world_sorted + g);
     }
   }
   {  // zero the accumulators (12 Bp words = 3 Bp uint4)
@@ -653,8 +676,10 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
   TL_MARK(1);
 
   // Contact range of this world.
-  const int64_t cbeg = P.world_sorted ? rng[0] : P.off[w];
-  const int nloc = (int)((P.world_sorted ? rng[1] : P.off[w + 1]) - cbeg);
+  if (!CF_EARLY_RANGE) {
+    cbeg = P.world_sorted ? rng[0] : P.off[w];
+    nloc = (int)((P.world_sorted ? rng[1] : P.off[w + 1]) - cbeg);
+  }
   const float4* C0p = P.c0 + cbeg;
   const float4* C1p = P.c1 + cbeg;
   const float4* C2p = P.c2 + cbeg;
@@ -666,8 +691,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
   // ---------------- S2-S6: contacts ----------------
   // Warp-uniform loop: lane l of warp j handles local contact base + l; base
   // advances by the group's thread count; the next contact is prefetched.
-  int WID = (int)w;  // world id of the prefetched contact (fused S0 check)
-  if (base + lane < nloc) {
+  if (!CF_EARLY_RANGE && base + lane < nloc) {
     const int j = base + lane;
     C0 = ld_stream(C0p + j); C1 = ld_stream(C1p + j); C2 = ld_stream(C2p + j); C3 = ld_stream(C3p + j);
     if (Wp) WID = ld_id(Wp + j);
