@@ -107,3 +107,54 @@ def test_chain_spheres_follow_forward_kinematics():
         assert c.body_a[k] == -2 - t and c.meta["link"][k, 0] == 3
         kp = 16 + 3 * t + 2                               # pair (palm, tip sphere of chain t)
         assert c.c0[kp, 3] == pytest.approx(tip[2] - 0.008, abs=1e-14)
+
+
+def _q_axis_angle(axis, ang):
+    axis = np.asarray(axis, float) / np.linalg.norm(axis)
+    return (np.cos(ang / 2), *(np.sin(ang / 2) * axis))
+
+
+def test_capsule_pairs_closed_forms():
+    R, hl = 0.015, 0.02
+    # tilted capsule above the plane: ends at z0 -+ hl cos(th)
+    th = 0.6
+    geo = _geo([2, 3], [-1, 0], [(0, 0, 1), (R, hl, 0)], [(0, 0, 0)] * 2, [(0, 1)], margin=0.05)
+    c = co.collide(geo, _state([(0.1, 0.0, 0.03)], [_q_axis_angle((1, 0, 0), th)]))
+    assert c.n == 2
+    np.testing.assert_allclose(c.c0[:, 3], [0.03 - hl * np.cos(th) - R, 0.03 + hl * np.cos(th) - R], atol=1e-15)
+    # sphere beside the capsule's side: distance = lateral offset - R - Rs
+    geo = _geo([0, 3], [0, 1], [(0.01, 0, 0), (R, hl, 0)], [(0, 0, 0)] * 2, [(0, 1)], margin=0.05)
+    c = co.collide(geo, _state([(0.03, 0.0, 0.005), (0, 0, 0)], [(1, 0, 0, 0)] * 2))
+    assert c.n == 1 and c.c0[0, 3] == pytest.approx(0.03 - 0.01 - R, abs=1e-15)
+    np.testing.assert_allclose(c.c1[0, :3], (-1, 0, 0), atol=1e-15)      # from the sphere to the capsule
+    # perpendicular crossing capsules: distance between the axes minus the radii
+    geo = _geo([3, 3], [0, 1], [(R, hl, 0), (R, hl, 0)], [(0, 0, 0)] * 2, [(0, 1)], margin=0.05)
+    c = co.collide(geo, _state([(0, 0, 0), (0.004, 0.0, 0.027)], [(1, 0, 0, 0), _q_axis_angle((1, 0, 0), np.pi / 2)]))
+    assert c.n == 1 and c.c0[0, 3] == pytest.approx(np.hypot(0.004, 0.027 - hl) - 2 * R, abs=1e-14)
+    # parallel side by side: the s = 0 end of the first segment, distance = offset - 2R
+    c = co.collide(geo, _state([(0, 0, 0), (0.028, 0.0, 0.005)], [(1, 0, 0, 0)] * 2))
+    assert c.n == 1 and c.c0[0, 3] == pytest.approx(0.028 - 2 * R, abs=1e-15)
+    # capsule standing on a box: both end spheres tested against the box
+    geo = _geo([3, 1], [0, 1], [(R, hl, 0), (0.05, 0.05, 0.01)], [(0, 0, 0)] * 2, [(0, 1)], margin=0.005)
+    c = co.collide(geo, _state([(0.0, 0.0, 0.01 + hl + R - 0.0007), (0, 0, 0)], [(1, 0, 0, 0)] * 2))
+    assert c.n == 1 and c.c0[0, 3] == pytest.approx(-0.0007, abs=1e-14)
+    np.testing.assert_allclose(c.c1[0, :3], (0, 0, -1), atol=1e-15)      # from the capsule (g1) to the box
+
+
+def test_box_on_box_vertex_face():
+    """A small box resting on a big one: its 4 bottom corners on the big box's
+    top face, none of the big box's corners within the small box's faces."""
+    hb, hs = (0.1, 0.1, 0.02), (0.02, 0.03, 0.01)
+    geo = _geo([1, 1], [0, 1], [hb, hs], [(0, 0, 0)] * 2, [(0, 1)], margin=0.002)
+    yaw = _q_axis_angle((0, 0, 1), 0.3)
+    z = 0.02 + 0.01 - 0.0004
+    c = co.collide(geo, _state([(0, 0, 0), (0.01, -0.02, z)], [(1, 0, 0, 0), yaw]))
+    assert c.n == 4
+    np.testing.assert_allclose(c.c0[:, 3], -0.0004, atol=1e-15)
+    np.testing.assert_allclose(c.c1[:, :3], np.tile((0, 0, 1.0), (4, 1)), atol=1e-15)   # from g1 (big) to g2
+    # the same pair listed the other way round: normals flip, points and gaps stay
+    geo2 = _geo([1, 1], [1, 0], [hs, hb], [(0, 0, 0)] * 2, [(0, 1)], margin=0.002)
+    c2 = co.collide(geo2, _state([(0, 0, 0), (0.01, -0.02, z)], [(1, 0, 0, 0), yaw]))
+    assert c2.n == 4
+    np.testing.assert_allclose(c2.c1[:, :3], np.tile((0, 0, -1.0), (4, 1)), atol=1e-15)
+    np.testing.assert_allclose(sorted(c2.c0[:, 3]), sorted(c.c0[:, 3]), atol=1e-15)
