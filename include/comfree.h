@@ -308,11 +308,14 @@ comfree_status comfree_articulation_update(comfree_ctx* ctx, int64_t first_world
  * emitting the step's contact records (the paper takes them from MJWarp's
  * collision; records as PAPER.md P:244-246).  Geom k: kind[k] 0 sphere
  * (size[k][0] = radius), 1 box (size = half extents along the frame's axes),
- * 2 plane (static; size = unit normal, local[k][0] = offset, n . x = offset);
+ * 2 plane (static; size = unit normal, local[k][0] = offset, n . x = offset),
+ * 3 capsule (size = (radius, half length), segment along the frame's z);
  * attached to body[k] (>= 0 free body, -1 world, -(2+t) chain t at link[k],
  * which needs comfree_load_articulation) at local[k] in that frame.  Pair p =
- * (pairs[2p], pairs[2p+1]) = (g1, g2) in {sphere-sphere, plane-sphere,
- * plane-box, sphere-box, box-sphere}; the contact normal points from g1 to g2
+ * (pairs[2p], pairs[2p+1]) = (g1, g2): plane first with a sphere, box or
+ * capsule, or any two of sphere / box / capsule (box-box by vertex-face,
+ * capsule-box by the capsule's end spheres: DESIGN.md R25; at most 16
+ * contacts per pair); the contact normal points from g1 to g2
  * (body_a = body of g1), phi is the signed surface distance, the point the
  * midpoint of the two surface points, t1 the branch-free basis of Duff et al.
  * (2017); a pair emits when phi < margin (plane-box: every corner below).

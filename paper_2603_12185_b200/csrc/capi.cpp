@@ -714,7 +714,7 @@ comfree_status comfree_load_geometry(comfree_ctx* ctx, const comfree_geometry* g
   bool chains = false;
   for (int k = 0; k < G; ++k) {
     const int kind = g->kind[k], body = g->body[k], link = g->link[k];
-    if (kind < 0 || kind > 2 || body >= sc.B || body < -1 - sc.T) return fail(ctx, COMFREE_ERR_VALIDATION, "load_geometry: geom %d kind/body", k);
+    if (kind < 0 || kind > 3 || body >= sc.B || body < -1 - sc.T) return fail(ctx, COMFREE_ERR_VALIDATION, "load_geometry: geom %d kind/body", k);
     if (body < -1 && (link < 0 || link >= sc.nd)) return fail(ctx, COMFREE_ERR_VALIDATION, "load_geometry: geom %d link", k);
     if (kind == 2 && body != -1) return fail(ctx, COMFREE_ERR_VALIDATION, "load_geometry: planes must be static");
     chains |= body < -1;
@@ -723,7 +723,7 @@ comfree_status comfree_load_geometry(comfree_ctx* ctx, const comfree_geometry* g
     if (kind == 2) {
       const float nrm = std::sqrt(sz[0] * sz[0] + sz[1] * sz[1] + sz[2] * sz[2]);
       if (!(std::fabs(nrm - 1.f) < 1e-3f)) return fail(ctx, COMFREE_ERR_VALIDATION, "load_geometry: plane normal not unit");
-    } else if (!(sz[0] > 0.f && (kind == 0 || (sz[1] > 0.f && sz[2] > 0.f)))) {
+    } else if (!(sz[0] > 0.f && (kind == 0 || (kind == 3 && sz[1] > 0.f) || (sz[1] > 0.f && sz[2] > 0.f)))) {
       return fail(ctx, COMFREE_ERR_VALIDATION, "load_geometry: geom %d size", k);
     }
     gi[k] = make_int4(kind, body, link, 0);
@@ -735,7 +735,8 @@ comfree_status comfree_load_geometry(comfree_ctx* ctx, const comfree_geometry* g
     const int a = g->pairs[2 * k], b = g->pairs[2 * k + 1];
     if (a < 0 || a >= G || b < 0 || b >= G) return fail(ctx, COMFREE_ERR_VALIDATION, "load_geometry: pair %d index", k);
     const int ka = g->kind[a], kb = g->kind[b];
-    const bool ok = (ka == 0 && kb == 0) || (ka == 2 && (kb == 0 || kb == 1)) || (ka == 0 && kb == 1) || (ka == 1 && kb == 0);
+    // supported: plane-{sphere, box, capsule} and every pair of {sphere, box, capsule}
+    const bool ok = kb != 2 && ka >= 0 && kb >= 0;
     if (!ok) return fail(ctx, COMFREE_ERR_VALIDATION, "load_geometry: pair %d kinds %d-%d not supported", k, ka, kb);
     if (g->body[a] == g->body[b] && g->body[a] >= 0)
       return fail(ctx, COMFREE_ERR_VALIDATION, "load_geometry: pair %d on one body", k);
@@ -770,7 +771,7 @@ comfree_status comfree_collide(comfree_ctx* ctx, int64_t first, int64_t nw, int6
   if (first < 0 || nw < 0 || first + nw > ctx->W) return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "collide: world range");
   if (capacity < 0 || (capacity > 0 && (!world || !c0 || !c1 || !c2 || !c3 || !link)))
     return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "collide: output arrays");
-  if (nw * (int64_t)ctx->n_pairs * 8 >= INT32_MAX) return fail(ctx, COMFREE_ERR_CAPACITY, "collide: too many candidate pairs");
+  if (nw * (int64_t)ctx->n_pairs * 16 >= INT32_MAX) return fail(ctx, COMFREE_ERR_CAPACITY, "collide: too many candidate pairs");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   CUDA_TRY(ctx, cudaSetDevice(ctx->device));
   cf::CollideParams P{};

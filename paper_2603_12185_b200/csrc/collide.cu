@@ -24,7 +24,8 @@ namespace {
 
 using namespace chain;
 
-enum { G_SPHERE = 0, G_BOX = 1, G_PLANE = 2 };
+enum { G_SPHERE = 0, G_BOX = 1, G_PLANE = 2, G_CAPSULE = 3 };
+constexpr int kMaxPairContacts = 16;  // box-box vertex-face: 8 corners each way
 
 struct Frame {
   float R[9];
@@ -84,102 +85,214 @@ __device__ __forceinline__ V3 tangent(V3 n) {
   return v3(1.f + s * n.x * n.x * a, s * b, -s * n.x);
 }
 
+struct Out {
+  V3 p[kMaxPairContacts], n[kMaxPairContacts];
+  float phi[kMaxPairContacts];
+  int k;
+  __device__ void add(V3 pp, float ph, V3 nn) {
+    if (k < kMaxPairContacts) { p[k] = pp; phi[k] = ph; n[k] = nn; ++k; }
+  }
+};
+
+// Capsule segment ends (end -1 first): x -+ half_len * the frame's z axis.
+__device__ __forceinline__ void capsule_ends(const CollideParams& P, int g, int64_t w, V3& a, V3& b) {
+  const Frame F = geom_frame(P, g, w);
+  const float hl = P.size[g].y;
+  const V3 z = v3(F.R[2], F.R[5], F.R[8]);
+  a = sub(F.x, mul(hl, z));
+  b = add(F.x, mul(hl, z));
+}
+
+__device__ __forceinline__ V3 closest_on_segment(V3 a, V3 b, V3 c) {
+  const V3 d = sub(b, a);
+  const float t = fminf(fmaxf(dot(sub(c, a), d) / dot(d, d), 0.f), 1.f);
+  return add(a, mul(t, d));
+}
+
+// Closest points of segments p1-q1 and p2-q2 (Ericson 5.1.9; parallel -> s = 0).
+__device__ __forceinline__ void closest_segments(V3 p1, V3 q1, V3 p2, V3 q2, V3& c1, V3& c2) {
+  const V3 d1 = sub(q1, p1), d2 = sub(q2, p2), r = sub(p1, p2);
+  const float a = dot(d1, d1), e = dot(d2, d2), f = dot(d2, r), c = dot(d1, r), b = dot(d1, d2);
+  const float denom = a * e - b * b;
+  float s = denom > 1e-12f * a * e ? fminf(fmaxf((b * f - c * e) / denom, 0.f), 1.f) : 0.f;
+  float t = (b * s + f) / e;
+  if (t < 0.f) { t = 0.f; s = fminf(fmaxf(-c / a, 0.f), 1.f); }
+  else if (t > 1.f) { t = 1.f; s = fminf(fmaxf((b - c) / a, 0.f), 1.f); }
+  c1 = add(p1, mul(s, d1));
+  c2 = add(p2, mul(t, d2));
+}
+
+__device__ __forceinline__ void two_spheres(V3 c1, float R1, V3 c2, float R2, float margin, Out& o) {
+  const V3 d = sub(c2, c1);
+  const float dist = sqrtf(dot(d, d));
+  const V3 nn = mul(1.f / dist, d);
+  const float phi = dist - R1 - R2;
+  if (phi < margin) o.add(add(c1, mul(R1 + 0.5f * phi, nn)), phi, nn);
+}
+
+// Sphere (centre c, radius R) against a box frame: phi, box-outward normal, box surface point.
+__device__ __forceinline__ float sphere_box(V3 c, float R, const Frame& Fb, float4 h4, V3& nbox, V3& qs) {
+  const float h[3] = {h4.x, h4.y, h4.z};
+  const V3 cl3 = rtmul(Fb.R, sub(c, Fb.x));
+  const float cl[3] = {cl3.x, cl3.y, cl3.z};
+  float ql[3], nl[3] = {0.f, 0.f, 0.f}, dist;
+  const bool inside = fabsf(cl[0]) <= h[0] && fabsf(cl[1]) <= h[1] && fabsf(cl[2]) <= h[2];
+  if (inside) {
+    int i = 0;
+    float best = h[0] - fabsf(cl[0]);
+#pragma unroll
+    for (int k = 1; k < 3; ++k) {
+      const float dk = h[k] - fabsf(cl[k]);
+      if (dk < best) { best = dk; i = k; }
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) ql[k] = cl[k];
+    nl[i] = cl[i] >= 0.f ? 1.f : -1.f;
+    ql[i] = nl[i] * h[i];
+    dist = -best;
+  } else {
+    float d2 = 0.f, dd[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      ql[k] = fminf(fmaxf(cl[k], -h[k]), h[k]);
+      dd[k] = cl[k] - ql[k];
+      d2 += dd[k] * dd[k];
+    }
+    dist = sqrtf(d2);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) nl[k] = dd[k] / dist;
+  }
+  nbox = rmul(Fb.R, v3(nl[0], nl[1], nl[2]));
+  qs = add(Fb.x, rmul(Fb.R, v3(ql[0], ql[1], ql[2])));
+  return dist - R;
+}
+
+// Corners of box B against the faces of box A (vertex-face).
+__device__ __forceinline__ void box_corners_on(const Frame& A, float4 hA, const Frame& Bf, float4 hB, float margin,
+                                               bool flip, Out& o) {
+  const float ha[3] = {hA.x, hA.y, hA.z};
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const V3 sl = v3((k & 1) ? hB.x : -hB.x, (k & 2) ? hB.y : -hB.y, (k & 4) ? hB.z : -hB.z);
+    const V3 corner = add(Bf.x, rmul(Bf.R, sl));
+    const V3 c3 = rtmul(A.R, sub(corner, A.x));
+    const float cl[3] = {c3.x, c3.y, c3.z};
+    float ex[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) ex[j] = fabsf(cl[j]) - ha[j];
+    int i = 0;
+    if (ex[1] > ex[i]) i = 1;
+    if (ex[2] > ex[i]) i = 2;
+    const float sd = ex[i];
+    bool ok = sd < margin;
+#pragma unroll
+    for (int j = 0; j < 3; ++j) ok &= (j == i) || ex[j] <= 0.f;
+    if (ok) {
+      float nl[3] = {0.f, 0.f, 0.f};
+      nl[i] = cl[i] >= 0.f ? 1.f : -1.f;
+      const V3 nn = rmul(A.R, v3(nl[0], nl[1], nl[2]));
+      o.add(sub(corner, mul(0.5f * sd, nn)), sd, flip ? mul(-1.f, nn) : nn);
+    }
+  }
+}
+
 // Contacts of pair pi in world w: returns the count; with out != null writes them
 // from index `base` on.
 __device__ int pair_contacts(const CollideParams& P, int pi, int64_t w, int64_t base, bool emit) {
   const int2 pr = P.pairs[pi];
   const int4 g1 = P.geom[pr.x], g2 = P.geom[pr.y];
   const float margin = P.margin;
-  V3 pts[8], nrm[8];
-  float phis[8];
-  int n = 0;
-  if (g1.x == G_PLANE) {
+  Out o;
+  o.k = 0;
+  const int k1 = g1.x, k2 = g2.x;
+  if (k1 == G_PLANE) {
     const float4 s1 = P.size[pr.x];
     const V3 pn = v3(s1.x, s1.y, s1.z);
     const float off = P.local[pr.x].x;
-    const Frame F2 = geom_frame(P, pr.y, w);
-    if (g2.x == G_SPHERE) {
+    if (k2 == G_CAPSULE) {
+      V3 e[2];
+      capsule_ends(P, pr.y, w, e[0], e[1]);
       const float R = P.size[pr.y].x;
-      const float phi = dot(pn, F2.x) - off - R;
-      if (phi < margin) { pts[n] = sub(F2.x, mul(R + 0.5f * phi, pn)); nrm[n] = pn; phis[n] = phi; ++n; }
-    } else if (g2.x == G_BOX) {
-      const float4 h = P.size[pr.y];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const V3 sl = v3((k & 1) ? h.x : -h.x, (k & 2) ? h.y : -h.y, (k & 4) ? h.z : -h.z);
-        const V3 corner = add(F2.x, rmul(F2.R, sl));
-        const float phi = dot(pn, corner) - off;
-        if (phi < margin) { pts[n] = sub(corner, mul(0.5f * phi, pn)); nrm[n] = pn; phis[n] = phi; ++n; }
+      for (int q = 0; q < 2; ++q) {
+        const float phi = dot(pn, e[q]) - off - R;
+        if (phi < margin) o.add(sub(e[q], mul(R + 0.5f * phi, pn)), phi, pn);
       }
-    }
-  } else if (g1.x == G_SPHERE && g2.x == G_SPHERE) {
-    const Frame F1 = geom_frame(P, pr.x, w), F2 = geom_frame(P, pr.y, w);
-    const float R1 = P.size[pr.x].x, R2 = P.size[pr.y].x;
-    const V3 d = sub(F2.x, F1.x);
-    const float dist = sqrtf(dot(d, d));
-    const V3 nn = mul(1.f / dist, d);
-    const float phi = dist - R1 - R2;
-    if (phi < margin) { pts[n] = add(F1.x, mul(R1 + 0.5f * phi, nn)); nrm[n] = nn; phis[n] = phi; ++n; }
-  } else {  // sphere-box or box-sphere
-    const bool sphere_first = g1.x == G_SPHERE;
-    const int gs = sphere_first ? pr.x : pr.y, gb = sphere_first ? pr.y : pr.x;
-    const Frame Fs = geom_frame(P, gs, w), Fb = geom_frame(P, gb, w);
-    const float R = P.size[gs].x;
-    const float4 h4 = P.size[gb];
-    const float h[3] = {h4.x, h4.y, h4.z};
-    const V3 cl3 = rtmul(Fb.R, sub(Fs.x, Fb.x));
-    const float cl[3] = {cl3.x, cl3.y, cl3.z};
-    float ql[3], nl[3] = {0.f, 0.f, 0.f}, dist;
-    const bool inside = fabsf(cl[0]) <= h[0] && fabsf(cl[1]) <= h[1] && fabsf(cl[2]) <= h[2];
-    if (inside) {
-      int i = 0;
-      float best = h[0] - fabsf(cl[0]);
-#pragma unroll
-      for (int k = 1; k < 3; ++k) {
-        const float dk = h[k] - fabsf(cl[k]);
-        if (dk < best) { best = dk; i = k; }
-      }
-#pragma unroll
-      for (int k = 0; k < 3; ++k) ql[k] = cl[k];
-      nl[i] = cl[i] >= 0.f ? 1.f : -1.f;
-      ql[i] = nl[i] * h[i];
-      dist = -best;
     } else {
-      float d2 = 0.f, dd[3];
+      const Frame F2 = geom_frame(P, pr.y, w);
+      if (k2 == G_SPHERE) {
+        const float R = P.size[pr.y].x;
+        const float phi = dot(pn, F2.x) - off - R;
+        if (phi < margin) o.add(sub(F2.x, mul(R + 0.5f * phi, pn)), phi, pn);
+      } else {  // box: every corner within the margin
+        const float4 h = P.size[pr.y];
 #pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        ql[k] = fminf(fmaxf(cl[k], -h[k]), h[k]);
-        dd[k] = cl[k] - ql[k];
-        d2 += dd[k] * dd[k];
+        for (int k = 0; k < 8; ++k) {
+          const V3 sl = v3((k & 1) ? h.x : -h.x, (k & 2) ? h.y : -h.y, (k & 4) ? h.z : -h.z);
+          const V3 corner = add(F2.x, rmul(F2.R, sl));
+          const float phi = dot(pn, corner) - off;
+          if (phi < margin) o.add(sub(corner, mul(0.5f * phi, pn)), phi, pn);
+        }
       }
-      dist = sqrtf(d2);
-#pragma unroll
-      for (int k = 0; k < 3; ++k) nl[k] = dd[k] / dist;
     }
-    const float phi = dist - R;
-    if (phi < margin) {
-      const V3 nbox = rmul(Fb.R, v3(nl[0], nl[1], nl[2]));
-      const V3 qs = add(Fb.x, rmul(Fb.R, v3(ql[0], ql[1], ql[2])));
-      pts[n] = mul(0.5f, add(qs, sub(Fs.x, mul(R, nbox))));
-      nrm[n] = sphere_first ? mul(-1.f, nbox) : nbox;
-      phis[n] = phi;
-      ++n;
+  } else if ((k1 == G_SPHERE || k1 == G_CAPSULE) && (k2 == G_SPHERE || k2 == G_CAPSULE)) {
+    const float R1 = P.size[pr.x].x, R2 = P.size[pr.y].x;
+    V3 c1, c2;
+    if (k1 == G_SPHERE && k2 == G_SPHERE) {
+      c1 = geom_frame(P, pr.x, w).x;
+      c2 = geom_frame(P, pr.y, w).x;
+    } else if (k1 == G_CAPSULE && k2 == G_CAPSULE) {
+      V3 a1, b1, a2, b2;
+      capsule_ends(P, pr.x, w, a1, b1);
+      capsule_ends(P, pr.y, w, a2, b2);
+      closest_segments(a1, b1, a2, b2, c1, c2);
+    } else if (k1 == G_CAPSULE) {
+      V3 a1, b1;
+      capsule_ends(P, pr.x, w, a1, b1);
+      c2 = geom_frame(P, pr.y, w).x;
+      c1 = closest_on_segment(a1, b1, c2);
+    } else {
+      V3 a2, b2;
+      c1 = geom_frame(P, pr.x, w).x;
+      capsule_ends(P, pr.y, w, a2, b2);
+      c2 = closest_on_segment(a2, b2, c1);
+    }
+    two_spheres(c1, R1, c2, R2, margin, o);
+  } else if (k1 == G_BOX && k2 == G_BOX) {
+    const Frame A = geom_frame(P, pr.x, w), Bf = geom_frame(P, pr.y, w);
+    const float4 hA = P.size[pr.x], hB = P.size[pr.y];
+    box_corners_on(A, hA, Bf, hB, margin, false, o);
+    box_corners_on(Bf, hB, A, hA, margin, true, o);
+  } else {  // sphere or capsule against a box
+    const bool round_first = k1 != G_BOX;
+    const int gr = round_first ? pr.x : pr.y, gb = round_first ? pr.y : pr.x;
+    const Frame Fb = geom_frame(P, gb, w);
+    const float R = P.size[gr].x;
+    const float4 h4 = P.size[gb];
+    V3 e[2];
+    int ne = 1;
+    if (P.geom[gr].x == G_CAPSULE) { capsule_ends(P, gr, w, e[0], e[1]); ne = 2; }
+    else e[0] = geom_frame(P, gr, w).x;
+    for (int q = 0; q < ne; ++q) {
+      V3 nbox, qs;
+      const float phi = sphere_box(e[q], R, Fb, h4, nbox, qs);
+      if (phi < margin) o.add(mul(0.5f, add(qs, sub(e[q], mul(R, nbox)))), phi, round_first ? mul(-1.f, nbox) : nbox);
     }
   }
   if (emit) {
     const int la = g1.y < -1 ? g1.z : 0, lb = g2.y < -1 ? g2.z : 0;
-    for (int k = 0; k < n; ++k) {
+    for (int k = 0; k < o.k; ++k) {
       const int64_t c = base + k;
-      const V3 t1 = tangent(nrm[k]);
-      P.c0[c] = make_float4(pts[k].x, pts[k].y, pts[k].z, phis[k]);
-      P.c1[c] = make_float4(nrm[k].x, nrm[k].y, nrm[k].z, P.mu_t);
+      const V3 t1 = tangent(o.n[k]);
+      P.c0[c] = make_float4(o.p[k].x, o.p[k].y, o.p[k].z, o.phi[k]);
+      P.c1[c] = make_float4(o.n[k].x, o.n[k].y, o.n[k].z, P.mu_t);
       P.c2[c] = make_float4(t1.x, t1.y, t1.z, P.mu_tor);
       P.c3[c] = make_int4(g1.y, g2.y, __float_as_int(P.mu_rol), P.condim);
       P.world[c] = (int32_t)w;  // relative to the range's first world, like comfree_step
       P.link[c] = make_int2(la, lb);
     }
   }
-  return n;
+  return o.k;
 }
 
 __global__ void k_collide_count(const __grid_constant__ CollideParams P, int32_t* __restrict__ counts) {
@@ -195,7 +308,7 @@ __global__ void k_collide_emit(const __grid_constant__ CollideParams P, const in
   if (id >= P.n_worlds * P.n_pairs) return;
   const int64_t w = id / P.n_pairs;
   const int64_t base = offs[id];
-  if (base + 8 > capacity) {  // a pair emits at most 8; only the tail can overflow
+  if (base + kMaxPairContacts > capacity) {  // only the tail can overflow
     const int n = pair_contacts(P, (int)(id - w * P.n_pairs), w, 0, false);
     if (base + n > capacity) return;
   }

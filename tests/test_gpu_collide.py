@@ -115,7 +115,7 @@ def test_capacity_and_validation():
     assert ei.value.status == 6
     ctx.load_articulation(ART)
     bad = scenes.hand_geometry()
-    bad.pairs = np.array([(1, 1)], np.int32)              # box-box: not a supported pair
+    bad.pairs = np.array([(1, 0)], np.int32)              # box-plane with the plane second: not supported
     with pytest.raises(cf.ComfreeError) as ei:
         ctx.load_geometry(bad)
     assert ei.value.status == 2
@@ -239,3 +239,36 @@ def test_closed_loop_full_size_sampled_worlds():
             ref = getattr(so, key)
             err = np.abs(out[key][w:w + 1] - ref)
             assert np.all(err <= 1e-4 * np.abs(ref) + 1e-6), (w, key, float(err.max()))
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_random_capsules_boxes_spheres(seed):
+    """Every supported pair kind including capsules and box-box, random poses."""
+    import paper_2603_12185_b200 as cf
+    from harness.types import Scene
+    rng = np.random.default_rng(100 + seed)
+    W, B = 24, 6
+    kind = [2, 0, 1, 3, 1, 3, 0]
+    body = [-1] + list(range(B))
+    size = [(0, 0, 1.0), (0.02, 0, 0), (0.03, 0.025, 0.02), (0.015, 0.02, 0), (0.025, 0.02, 0.03),
+            (0.012, 0.03, 0), (0.018, 0, 0)]
+    pairs = [(0, g) for g in range(1, B + 1)] + [(1, 2), (2, 3), (3, 4), (4, 2), (3, 5), (5, 6), (6, 3),
+                                                 (1, 3), (5, 4), (2, 6)]
+    geo = Geometry(np.array(kind, np.int32), np.array(body, np.int32), np.zeros(B + 1, np.int32),
+                   np.array(size), np.zeros((B + 1, 3)), np.array(pairs, np.int32), margin=0.01,
+                   mu=(0.8, 0.01, 0.001), condim=3)
+    pos = rng.uniform([-0.03, -0.03, 0.0], [0.03, 0.03, 0.05], (W, B, 3))
+    quat = rng.normal(size=(W, B, 4))
+    quat /= np.linalg.norm(quat, axis=2, keepdims=True)
+    st = State(pos, quat, np.zeros((W, B, 3)), np.zeros((W, B, 3)), np.zeros((W, 0)), np.zeros((W, 0)))
+    st32 = st.astype(np.float32)
+    st64 = st32.astype(np.float64)
+    skip = _tie_worlds(geo, st64, None)
+    scene = Scene(np.full(B, 2.0, np.float32), np.full((B, 3), 500.0, np.float32))
+    ctx = cf.Context(CFG)
+    ctx.load_scene(scene, W, st32)
+    ctx.load_geometry(geo)
+    dc, link = ctx.collide(capacity=W * 200)
+    ref = co.collide(geo, st64, None)
+    assert ref.n > W
+    _compare(dc, link, ref, skip)
