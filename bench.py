@@ -63,8 +63,9 @@ def parse():
                     help="hand / mixed: run the articulated upstream (FK, M(q), Cholesky, c(q,v), chain J rows) "
                          "on the GPU every step before the contact resolution (SURVEY 8(f) rank 2)")
     ap.add_argument("--collide", action="store_true",
-                    help="hand: closed loop - the GPU collision front-end (SURVEY 8(f) rank 1) builds the contacts "
-                         "every step (count kept on the device), then the upstream and the step (implies --upstream)")
+                    help="closed loop: the GPU collision front-end (SURVEY 8(f) rank 1) builds the contacts every "
+                         "step (count kept on the device); hand: then the upstream and the step (implies --upstream); "
+                         "pile: lattice-neighbour candidate pairs, then the step (the full-step metric, P:389-390)")
     ap.add_argument("--workload", default="pile", choices=["pile", "hand", "mixed"],
                     help="pile: config 4 (the BASELINE metric); hand: config 3; mixed: config 5")
     a = ap.parse_args()
@@ -187,6 +188,8 @@ def workload(args, rank, world_size):
         name += " + articulated upstream on the GPU every step"
     if args.collide:
         name += " + GPU collision front-end every step (closed loop)"
+        if args.workload == "pile":
+            name += "; contacts from geometry, not the generator's 2000"
     return parts, name, n
 
 
@@ -323,6 +326,13 @@ def run_ours(args, rank, world_size, local):
         # part 0 on the caller's stream, the others on their own streams (fork / join)
         p.stream = stream if i == 0 else torch.cuda.Stream(device=dev)
         p.up = None
+        p.col = None
+        if args.collide and p.scene.n_trees == 0:    # pile: contacts from the GPU front-end every step
+            from harness import scenes as _sc
+            B = p.scene.n_bodies
+            lat = {500: (10, 10, 5), 100: (5, 5, 4)}[B]
+            p.ctx.load_geometry(_sc.pile_geometry(lat))
+            p.col = p.W * 4 * args.contacts         # output capacity
         if args.upstream and p.scene.n_trees > 0:     # articulated upstream every step
             from harness import scenes as _sc
             p.ctx.load_articulation(_sc.hand_articulation())
@@ -350,6 +360,8 @@ def run_ours(args, rank, world_size, local):
             if i != 0:
                 p.stream.wait_stream(s0)
             ps = s0 if i == 0 else p.stream
+            if p.col is not None:
+                p.dc, _ = p.ctx.collide(capacity=p.col, stream=ps, device_count=True)
             if p.up is not None:
                 if args.collide:                     # contacts from the current state (closed loop)
                     p.dc, lk = p.ctx.collide(capacity=p.W * 40, stream=ps, device_count=True)
@@ -362,6 +374,11 @@ def run_ours(args, rank, world_size, local):
     for _ in range(max(args.warmup, 3)):
         one_step(stream)
     torch.cuda.synchronize()
+    for p in parts:                                   # collision-built contacts: the step's real count
+        if p.col is not None:
+            nc = int(p.dc.n_dev.item())
+            p.alg_bytes = nc * BYTES_PER_CONTACT + p.W * p.scene.n_bodies * BYTES_PER_BODY
+            p.c_count = nc
     # direct launches with the library's own event timing around each fused kernel
     for p in parts:
         p.ctx.get_timing()
@@ -419,7 +436,7 @@ def run_ours(args, rank, world_size, local):
     ms_per_step = total_ms / args.steps
     world_steps = n_local * world_size * args.steps
     value = world_steps / (total_ms * 1e-3)
-    n_contacts = sum(p.c.n for p in parts)
+    n_contacts = sum(getattr(p, "c_count", p.c.n) for p in parts)
     contacts_per_s = value * (n_contacts / n_local)
 
     # roofline of the dominant kernel (part 0: the pile / pile-lite k_step).  With
@@ -427,13 +444,14 @@ def run_ours(args, rank, world_size, local):
     # replay bracket exactly that kernel; with several parts the kernel's own
     # events (library timing, direct launches, parts running concurrently) are used.
     dom = parts[0]
-    k_ms = (total_ms / args.steps) if (graph is not None and len(parts) == 1 and dom.up is None) else dom.k_ms_direct
+    k_ms = (total_ms / args.steps) if (graph is not None and len(parts) == 1 and dom.up is None
+                                       and dom.col is None) else dom.k_ms_direct
     peak, peak_kind = peaks()
     achieved = dom.alg_bytes / (k_ms * 1e-3) / 1e9
     tr = ncu_traffic()
     traffic = None
     if tr and tr.get("workload") == args.workload and tr.get("worlds") == dom.W and \
-            tr.get("contacts_per_world") == dom.c.n // dom.W:
+            tr.get("contacts_per_world") == dom.c.n // dom.W and dom.col is None:
         traffic = tr.get("dram_bytes_per_launch")
 
     # after the timed region: final states all-gathered (NCCL) for verification

@@ -278,6 +278,33 @@ def _pile_template(nx, ny, nz):
     return kinds, np.asarray(rows, np.int64)
 
 
+def pile_geometry(lattice=(10, 10, 5), margin=0.001, mu=(1.0, 0.005, 0.0001), condim=3):
+    """Collision geometry of the config-4 pile for the GPU front-end: the floor
+    plane z = 0, one geom per body (sphere R 2.5 cm / box half 2.5 cm / capsule
+    R 1.5 cm, half-length 2 cm, as PILE_SHAPES), candidate pairs = the floor with
+    the bottom layer and every lattice-neighbour pair (the generator's pairs)."""
+    from .types import Geometry
+    nx, ny, nz = lattice
+    B = nx * ny * nz
+    kinds, _ = _pile_template(nx, ny, nz)
+    kmap = {"sphere": 0, "box": 1, "capsule": 3}
+    kind, body, size = [2], [-1], [(0.0, 0.0, 1.0)]
+    for i in range(B):
+        g = PILE_SHAPES[kinds[i]]
+        kind.append(kmap[g.kind])
+        body.append(i)
+        sz = tuple(g.size) + (0.0,) * (3 - len(g.size))
+        size.append(sz)
+    idx = np.arange(B).reshape(nz, ny, nx)
+    pairs = [(0, 1 + int(i)) for i in idx[0].ravel()]
+    for (da, db) in ((idx[:, :, :-1], idx[:, :, 1:]), (idx[:, :-1, :], idx[:, 1:, :]), (idx[:-1, :, :], idx[1:, :, :])):
+        pairs += [(1 + int(a), 1 + int(b)) for a, b in zip(da.ravel(), db.ravel())]
+    G = B + 1
+    return Geometry(np.array(kind, np.int32), np.array(body, np.int32), np.zeros(G, np.int32),
+                    np.array(size, np.float64), np.zeros((G, 3)), np.array(pairs, np.int32),
+                    margin=margin, mu=mu, condim=condim)
+
+
 def c4_pile(n_worlds=1024, contacts_per_world=2000, lattice=(10, 10, 5), seed=0,
             world_offset=0, condim=3, mu=(1.0, 0.005, 0.0001)):
     """Config 4: per world a jittered nx*ny*nz lattice (5 cm pitch) of
