@@ -49,7 +49,7 @@ namespace cf {
 #define CF_L2AHEAD 0  // measured slightly slower (59.7 vs 59.4 us, C4)
 #endif
 #ifndef CF_EARLY_RANGE
-#define CF_EARLY_RANGE 1
+#define CF_EARLY_RANGE 0  // measured: C4 neutral, C3 hand -2%, C5 mixed +2% (profiles/r01_ab_session2.txt)
 #endif
 static constexpr int kS1Unroll = CF_S1_UNROLL;  // S1 bodies per thread in flight (unstaged S1)
 static constexpr int kWarps = 8;

@@ -7,6 +7,10 @@ timeout 600 python bench.py > gpurun_out/${TAG}_bench_pile.json 2> gpurun_out/${
 timeout 600 python bench.py --flush-mode write --cpu-seconds 1 > gpurun_out/${TAG}_bench_pile_writeflush.json 2> /dev/null
 timeout 600 python bench.py --workload hand --cpu-seconds 5 > gpurun_out/${TAG}_bench_hand.json 2> gpurun_out/${TAG}_bench_hand.err
 timeout 600 python bench.py --workload hand --upstream --cpu-seconds 2 > gpurun_out/${TAG}_bench_hand_upstream.json 2> /dev/null
+timeout 600 python bench.py --workload hand --collide --cpu-seconds 1 > gpurun_out/${TAG}_bench_hand_closed_loop.json 2> /dev/null
+timeout 600 python bench.py --collide --cpu-seconds 1 > gpurun_out/${TAG}_bench_pile_closed_loop.json 2> /dev/null
+timeout 600 python tools/mppi_bench.py > gpurun_out/${TAG}_mppi_p16.json 2> /dev/null
+timeout 600 python tools/mppi_bench.py --problems 1 > gpurun_out/${TAG}_mppi_p1.json 2> /dev/null
 timeout 900 python bench.py --workload mixed --cpu-seconds 5 --steps 100 > gpurun_out/${TAG}_bench_mixed.json 2> gpurun_out/${TAG}_bench_mixed.err
 timeout 600 python bench.py --kd --cpu-seconds 0.5 > gpurun_out/${TAG}_bench_pile_kd.json 2> /dev/null
 timeout 600 python bench.py --impedance exact_diagonal --cpu-seconds 0.5 > gpurun_out/${TAG}_bench_pile_exact_diag.json 2> /dev/null
