@@ -48,6 +48,9 @@ namespace cf {
 #ifndef CF_L2AHEAD
 #define CF_L2AHEAD 0  // measured slightly slower (59.7 vs 59.4 us, C4)
 #endif
+#ifndef CF_NEG_HEADS
+#define CF_NEG_HEADS 1
+#endif
 #ifndef CF_EARLY_RANGE
 #define CF_EARLY_RANGE 0  // measured: C4 neutral, C3 hand -2%, C5 mixed +2% (profiles/r01_ab_session2.txt)
 #endif
@@ -231,7 +234,13 @@ __device__ __forceinline__ void channel2(float A, float kmu, float w1, float w2,
 __device__ __forceinline__ bool seg_sum6(int key, float v[6], int lane) {
   const unsigned full = 0xffffffffu;
   const int prev = __shfl_up_sync(full, key, 1);
+#if CF_NEG_HEADS
+  // lanes without a body to add to (static / chain side, key < 0) are runs of
+  // their own: a warp of floor contacts needs no sums at all
+  const bool head = lane == 0 || prev != key || key < 0;
+#else
   const bool head = lane == 0 || prev != key;
+#endif
   const unsigned heads = __ballot_sync(full, head);
   if (__popc(heads) >= CF_DIRECT_RUNS) return true;  // warp-uniform: direct adds
   const int next = __shfl_down_sync(full, key, 1);
