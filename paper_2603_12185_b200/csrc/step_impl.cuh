@@ -48,6 +48,9 @@ namespace cf {
 #ifndef CF_L2AHEAD
 #define CF_L2AHEAD 0  // measured slightly slower (59.7 vs 59.4 us, C4)
 #endif
+#ifndef CF_EARLY_C3
+#define CF_EARLY_C3 1
+#endif
 #ifndef CF_NEG_HEADS
 #define CF_NEG_HEADS 1
 #endif
@@ -720,8 +723,11 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
       // kernel parameters each time (no per-stream 64-bit pointers held live)
       int64_t g = cbeg + jn;
       asm volatile("" : "+l"(g));
-      C0 = ld_stream(P.c0 + g); C1 = ld_stream(P.c1 + g); C2 = ld_stream(P.c2 + g); C3 = ld_stream(P.c3 + g);
-      if (P.world_sorted) WID = ld_id(P.world_sorted + g);
+      C0 = ld_stream(P.c0 + g); C1 = ld_stream(P.c1 + g); C2 = ld_stream(P.c2 + g);
+      if (!(CF_EARLY_C3 && kLatePrefetch)) {
+        C3 = ld_stream(P.c3 + g);
+        if (P.world_sorted) WID = ld_id(P.world_sorted + g);
+      }
 #if CF_L2AHEAD
       // one iteration further: pull the contact after next into L2 (no registers), so
       // the register prefetch above waits on L2 rather than HBM latency
@@ -800,6 +806,12 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
         vrel.x += sg * vp[0]; vrel.y += sg * vp[1]; vrel.z += sg * vp[2];
         wrel.x += sg * wp[0]; wrel.y += sg * wp[1]; wrel.z += sg * wp[2];
       }
+    }
+    if (CF_EARLY_C3 && kLatePrefetch) {  // the next contact's ids first: the loop head waits on them
+      int64_t g = cbeg + min(j + kGT, nloc - 1);
+      asm volatile("" : "+l"(g));
+      C3 = ld_stream(P.c3 + g);
+      if (P.world_sorted) WID = ld_id(P.world_sorted + g);
     }
     // S3-S5, computed for every lane (invalid lanes are masked by select at the end)
     float3 f, tau = make_float3(0.f, 0.f, 0.f);
