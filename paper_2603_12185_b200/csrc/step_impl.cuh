@@ -48,6 +48,9 @@ namespace cf {
 #ifndef CF_L2AHEAD
 #define CF_L2AHEAD 0  // measured slightly slower (59.7 vs 59.4 us, C4)
 #endif
+#ifndef CF_EARLY_C0
+#define CF_EARLY_C0 0
+#endif
 #ifndef CF_EARLY_C3
 #define CF_EARLY_C3 1
 #endif
@@ -723,7 +726,8 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
       // kernel parameters each time (no per-stream 64-bit pointers held live)
       int64_t g = cbeg + jn;
       asm volatile("" : "+l"(g));
-      C0 = ld_stream(P.c0 + g); C1 = ld_stream(P.c1 + g); C2 = ld_stream(P.c2 + g);
+      if (!(CF_EARLY_C0 && kLatePrefetch)) C0 = ld_stream(P.c0 + g);
+      C1 = ld_stream(P.c1 + g); C2 = ld_stream(P.c2 + g);
       if (!(CF_EARLY_C3 && kLatePrefetch)) {
         C3 = ld_stream(P.c3 + g);
         if (P.world_sorted) WID = ld_id(P.world_sorted + g);
@@ -811,6 +815,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
       int64_t g = cbeg + min(j + kGT, nloc - 1);
       asm volatile("" : "+l"(g));
       C3 = ld_stream(P.c3 + g);
+      if (CF_EARLY_C0) C0 = ld_stream(P.c0 + g);
       if (P.world_sorted) WID = ld_id(P.world_sorted + g);
     }
     // S3-S5, computed for every lane (invalid lanes are masked by select at the end)
