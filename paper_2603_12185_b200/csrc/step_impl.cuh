@@ -728,7 +728,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
       asm volatile("" : "+l"(g));
       if (!(CF_EARLY_C0 && kLatePrefetch)) C0 = ld_stream(P.c0 + g);
       C1 = ld_stream(P.c1 + g); C2 = ld_stream(P.c2 + g);
-      if (!(CF_EARLY_C3 && kLatePrefetch)) {
+      if (!(CF_EARLY_C3 && kLatePrefetch && FAST)) {
         C3 = ld_stream(P.c3 + g);
         if (P.world_sorted) WID = ld_id(P.world_sorted + g);
       }
@@ -811,7 +811,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
         wrel.x += sg * wp[0]; wrel.y += sg * wp[1]; wrel.z += sg * wp[2];
       }
     }
-    if (CF_EARLY_C3 && kLatePrefetch) {  // the next contact's ids first: the loop head waits on them
+    if (CF_EARLY_C3 && kLatePrefetch && FAST) {  // the next contact's ids first: the loop head waits on them
       int64_t g = cbeg + min(j + kGT, nloc - 1);
       asm volatile("" : "+l"(g));
       C3 = ld_stream(P.c3 + g);
