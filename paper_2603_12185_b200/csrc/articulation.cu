@@ -24,12 +24,11 @@ namespace {
 using namespace chain;
 
 // One thread per (world, chain): M, its Cholesky factor, tau - c.
-__global__ void k_chain_dynamics(const float* __restrict__ model, int T, int nd, const float* __restrict__ slab,
-                                 int slab_stride, int qoff, int Qp, int64_t n_worlds, const float* __restrict__ tau_ext,
-                                 float gx, float gy, float gz, float* __restrict__ L_out, float* __restrict__ tau_out,
-                                 int* __restrict__ err) {
-  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (id >= n_worlds * T) return;
+__device__ __forceinline__ void chain_dynamics(int64_t id, const float* __restrict__ model, int T, int nd,
+                                               const float* __restrict__ slab, int slab_stride, int qoff, int Qp,
+                                               const float* __restrict__ tau_ext, float gx, float gy, float gz,
+                                               float* __restrict__ L_out, float* __restrict__ tau_out,
+                                               int* __restrict__ err) {
   const int64_t w = id / T;
   const int t = (int)(id - w * T);
   const float* m = model + (size_t)t * (3 + 7 * nd);
@@ -118,13 +117,13 @@ __global__ void k_chain_dynamics(const float* __restrict__ model, int T, int nd,
 // One thread per contact: J rows of its chain sides (side s is chain -(2+t),
 // link[2c + s] in [0, nd)) at the contact point, in the [12][n][4] layout;
 // rows of free / static sides are left untouched (the step ignores them).
-__global__ void k_contact_rows(const float* __restrict__ model, int T, int nd, const float* __restrict__ slab,
-                               int slab_stride, int qoff, int64_t n_worlds, int64_t n, const int64_t* __restrict__ n_dev,
-                               const int32_t* __restrict__ world, const float4* __restrict__ c0,
-                               const int4* __restrict__ c3, const int32_t* __restrict__ link,
-                               float4* __restrict__ jrow, int* __restrict__ err) {
-  const int64_t c = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= n || (n_dev && c >= *n_dev)) return;
+__device__ __forceinline__ void contact_rows(int64_t c, const float* __restrict__ model, int T, int nd,
+                                             const float* __restrict__ slab, int slab_stride, int qoff,
+                                             int64_t n_worlds, int64_t n, const int64_t* __restrict__ n_dev,
+                                             const int32_t* __restrict__ world, const float4* __restrict__ c0,
+                                             const int4* __restrict__ c3, const int32_t* __restrict__ link,
+                                             float4* __restrict__ jrow, int* __restrict__ err) {
+  if (n_dev && c >= *n_dev) return;
   const int4 ids = c3[c];
   const int64_t w = world[c];  // relative to the range's first world, like comfree_step
   const float4 pc = c0[c];
@@ -161,26 +160,36 @@ __global__ void k_contact_rows(const float* __restrict__ model, int T, int nd, c
   }
 }
 
+// One launch: threads [0, W T) build the chains' factors and bias, threads
+// [W T, W T + n) the contacts' chain rows (independent: both read q only).
+__global__ void k_upstream(const float* __restrict__ model, int T, int nd, const float* __restrict__ slab,
+                           int slab_stride, int qoff, int Qp, int64_t n_worlds, const float* __restrict__ tau_ext,
+                           float gx, float gy, float gz, float* __restrict__ L_out, float* __restrict__ tau_out,
+                           int64_t n, const int64_t* __restrict__ n_dev, const int32_t* __restrict__ world,
+                           const float4* __restrict__ c0, const int4* __restrict__ c3, const int32_t* __restrict__ link,
+                           float4* __restrict__ jrow, int* __restrict__ err) {
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t nt = n_worlds * T;
+  if (id < nt) {
+    chain_dynamics(id, model, T, nd, slab, slab_stride, qoff, Qp, tau_ext, gx, gy, gz, L_out, tau_out, err);
+  } else if (id - nt < n) {
+    contact_rows(id - nt, model, T, nd, slab, slab_stride, qoff, n_worlds, n, n_dev, world, c0, c3, link, jrow, err);
+  }
+}
+
 int blocks(int64_t n, int bs) { return (int)((n + bs - 1) / bs); }
 
 }  // namespace
 
-cudaError_t launch_chain_dynamics(const float* model, const SceneDev& sc, const float* slab, int64_t n_worlds,
-                                  const float* tau_ext, const float g[3], float* L_out, float* tau_out, int* err,
-                                  cudaStream_t s) {
-  const int64_t n = n_worlds * sc.T;
-  if (n == 0) return cudaSuccess;
-  k_chain_dynamics<<<blocks(n, 128), 128, 0, s>>>(model, sc.T, sc.nd, slab, sc.slab, N_BODY_PLANES * sc.Bp, sc.Qp,
-                                                  n_worlds, tau_ext, g[0], g[1], g[2], L_out, tau_out, err);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_contact_rows(const float* model, const SceneDev& sc, const float* slab, int64_t n_worlds,
-                                int64_t n, const int64_t* n_dev, const int32_t* world, const float4* c0,
-                                const int4* c3, const int32_t* link, float4* jrow, int* err, cudaStream_t s) {
-  if (n == 0) return cudaSuccess;
-  k_contact_rows<<<blocks(n, 128), 128, 0, s>>>(model, sc.T, sc.nd, slab, sc.slab, N_BODY_PLANES * sc.Bp,
-                                                n_worlds, n, n_dev, world, c0, c3, link, jrow, err);
+cudaError_t launch_upstream(const float* model, const SceneDev& sc, const float* slab, int64_t n_worlds,
+                            const float* tau_ext, const float g[3], float* L_out, float* tau_out, int64_t n,
+                            const int64_t* n_dev, const int32_t* world, const float4* c0, const int4* c3,
+                            const int32_t* link, float4* jrow, int* err, cudaStream_t s) {
+  const int64_t total = n_worlds * sc.T + n;
+  if (total == 0) return cudaSuccess;
+  k_upstream<<<blocks(total, 128), 128, 0, s>>>(model, sc.T, sc.nd, slab, sc.slab, N_BODY_PLANES * sc.Bp, sc.Qp,
+                                                n_worlds, tau_ext, g[0], g[1], g[2], L_out, tau_out, n, n_dev, world,
+                                                c0, c3, link, jrow, err);
   return cudaGetLastError();
 }
 

@@ -691,11 +691,10 @@ comfree_status comfree_articulation_update(comfree_ctx* ctx, int64_t first, int6
   const cf::SceneDev& sc = ctx->sc;
   const float* slab = ctx->slab + (size_t)first * sc.slab;
   const float* model = static_cast<const float*>(ctx->art.p);
-  CUDA_TRY(ctx, cf::launch_chain_dynamics(model, sc, slab, nw, tau_ext, ctx->cfg.gravity, tree_L, tree_tau, ctx->d_err, s));
-  CUDA_TRY(ctx, cf::launch_contact_rows(model, sc, slab, nw, n, n_device, world, reinterpret_cast<const float4*>(c0),
-                                        reinterpret_cast<const int4*>(c3), link, reinterpret_cast<float4*>(jrow),
-                                        ctx->d_err, s));
-  ctx->launches += (nw > 0) + (n > 0);
+  CUDA_TRY(ctx, cf::launch_upstream(model, sc, slab, nw, tau_ext, ctx->cfg.gravity, tree_L, tree_tau, n, n_device,
+                                    world, reinterpret_cast<const float4*>(c0), reinterpret_cast<const int4*>(c3), link,
+                                    reinterpret_cast<float4*>(jrow), ctx->d_err, s));
+  ctx->launches += (nw > 0 || n > 0);
   return COMFREE_OK;
 }
 
@@ -809,9 +808,8 @@ comfree_status comfree_collide(comfree_ctx* ctx, int64_t first, int64_t nw, int6
   CUDA_TRY(ctx, cf::collide_count_scan(P, static_cast<int32_t*>(ctx->col_counts.p), offs, ctx->col_tmp.p, &tb, s));
   ctx->launches += 2;
   if (n_device) {  // asynchronous: count on the device, overflow latched as COMFREE_ERR_CAPACITY
-    CUDA_TRY(ctx, cf::collide_store_count(offs + (m - 1), capacity, n_device, ctx->d_err, s));
-    CUDA_TRY(ctx, cf::collide_emit(P, offs, capacity, s));
-    ctx->launches += 2;
+    CUDA_TRY(ctx, cf::collide_emit(P, offs, capacity, n_device, ctx->d_err, s));
+    ctx->launches += 1;
     return COMFREE_OK;
   }
   int32_t total = 0;
@@ -819,7 +817,7 @@ comfree_status comfree_collide(comfree_ctx* ctx, int64_t first, int64_t nw, int6
   CUDA_TRY(ctx, cudaStreamSynchronize(s));
   *n_out = total;
   if (total > capacity) return fail(ctx, COMFREE_ERR_CAPACITY, "collide: %d contacts, capacity %lld", total, (long long)capacity);
-  CUDA_TRY(ctx, cf::collide_emit(P, offs, capacity, s));
+  CUDA_TRY(ctx, cf::collide_emit(P, offs, capacity, nullptr, nullptr, s));
   ctx->launches += 1;
   return COMFREE_OK;
 }

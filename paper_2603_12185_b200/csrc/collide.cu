@@ -297,14 +297,20 @@ __device__ int pair_contacts(const CollideParams& P, int pi, int64_t w, int64_t 
 
 __global__ void k_collide_count(const __grid_constant__ CollideParams P, int32_t* __restrict__ counts) {
   const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id == P.n_worlds * P.n_pairs) counts[id] = 0;  // the scan's closing element (total = its prefix)
   if (id >= P.n_worlds * P.n_pairs) return;
   const int64_t w = id / P.n_pairs;
   counts[id] = pair_contacts(P, (int)(id - w * P.n_pairs), w, 0, false);
 }
 
 __global__ void k_collide_emit(const __grid_constant__ CollideParams P, const int32_t* __restrict__ offs,
-                               int64_t capacity) {
+                               int64_t capacity, int64_t* __restrict__ n_dev, int* __restrict__ err) {
   const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (n_dev && id == 0) {  // asynchronous mode: the count (clamped) for the step, overflow latched
+    const int64_t t = offs[P.n_worlds * P.n_pairs];
+    if (t > capacity) atomicOr(err, ERR_CONTACT_CAP);
+    *n_dev = t < capacity ? t : capacity;
+  }
   if (id >= P.n_worlds * P.n_pairs) return;
   const int64_t w = id / P.n_pairs;
   const int64_t base = offs[id];
@@ -323,27 +329,15 @@ cudaError_t collide_count_scan(const CollideParams& P, int32_t* counts, int32_t*
                                size_t* temp_bytes, cudaStream_t s) {
   const int64_t n = P.n_worlds * P.n_pairs;
   if (!temp) return cub::DeviceScan::ExclusiveSum(nullptr, *temp_bytes, counts, offs, (int)(n + 1), s);
-  if (n > 0) k_collide_count<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(P, counts);
-  cudaMemsetAsync(counts + n, 0, sizeof(int32_t), s);
+  k_collide_count<<<(unsigned)((n + 1 + 127) / 128), 128, 0, s>>>(P, counts);
   return cub::DeviceScan::ExclusiveSum(temp, *temp_bytes, counts, offs, (int)(n + 1), s);
 }
 
-__global__ void k_store_count(const int32_t* __restrict__ total, int64_t capacity, int64_t* __restrict__ n_dev,
-                              int* __restrict__ err) {
-  const int64_t t = *total;
-  if (t > capacity) atomicOr(err, ERR_CONTACT_CAP);
-  *n_dev = t < capacity ? t : capacity;
-}
-
-cudaError_t collide_store_count(const int32_t* total, int64_t capacity, int64_t* n_dev, int* err, cudaStream_t s) {
-  k_store_count<<<1, 1, 0, s>>>(total, capacity, n_dev, err);
-  return cudaGetLastError();
-}
-
-cudaError_t collide_emit(const CollideParams& P, const int32_t* offs, int64_t capacity, cudaStream_t s) {
+cudaError_t collide_emit(const CollideParams& P, const int32_t* offs, int64_t capacity, int64_t* n_dev, int* err,
+                         cudaStream_t s) {
   const int64_t n = P.n_worlds * P.n_pairs;
-  if (n == 0) return cudaSuccess;
-  k_collide_emit<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(P, offs, capacity);
+  if (n == 0 && !n_dev) return cudaSuccess;
+  k_collide_emit<<<(unsigned)((n + 127) / 128 > 0 ? (n + 127) / 128 : 1), 128, 0, s>>>(P, offs, capacity, n_dev, err);
   return cudaGetLastError();
 }
 

@@ -98,12 +98,10 @@ cudaError_t launch_iota(int32_t* out, int64_t n, cudaStream_t s);
 
 // articulated upstream (articulation.cu); model: per chain base[3] + per joint
 // (axis[3], length, mass, inertia, armature), slab: world 0 of the range
-cudaError_t launch_chain_dynamics(const float* model, const SceneDev& sc, const float* slab, int64_t n_worlds,
-                                  const float* tau_ext, const float g[3], float* L_out, float* tau_out, int* err,
-                                  cudaStream_t s);
-cudaError_t launch_contact_rows(const float* model, const SceneDev& sc, const float* slab, int64_t n_worlds,
-                                int64_t n, const int64_t* n_dev, const int32_t* world, const float4* c0,
-                                const int4* c3, const int32_t* link, float4* jrow, int* err, cudaStream_t s);
+cudaError_t launch_upstream(const float* model, const SceneDev& sc, const float* slab, int64_t n_worlds,
+                            const float* tau_ext, const float g[3], float* L_out, float* tau_out, int64_t n,
+                            const int64_t* n_dev, const int32_t* world, const float4* c0, const int4* c3,
+                            const int32_t* link, float4* jrow, int* err, cudaStream_t s);
 
 // collision front-end (collide.cu)
 struct CollideParams {
@@ -127,8 +125,9 @@ struct CollideParams {
 };
 cudaError_t collide_count_scan(const CollideParams& P, int32_t* counts, int32_t* offs, void* temp,
                                size_t* temp_bytes, cudaStream_t s);
-cudaError_t collide_emit(const CollideParams& P, const int32_t* offs, int64_t capacity, cudaStream_t s);
-cudaError_t collide_store_count(const int32_t* total, int64_t capacity, int64_t* n_dev, int* err, cudaStream_t s);
+// n_dev != null: also stores the (clamped) total for the asynchronous mode
+cudaError_t collide_emit(const CollideParams& P, const int32_t* offs, int64_t capacity, int64_t* n_dev, int* err,
+                         cudaStream_t s);
 
 // MPPI (mppi.cu)
 struct MppiCostParams {
