@@ -392,6 +392,13 @@ comfree_status comfree_mppi_control(comfree_ctx* ctx, int64_t first_world, int64
 comfree_status comfree_mppi_cost(comfree_ctx* ctx, int64_t first_world, int64_t n_worlds, int32_t n_samples,
                                  const comfree_mppi_task* task, int32_t terminal, float* J, void* stream);
 
+/* comfree_mppi_cost (running, terminal = 0) and comfree_mppi_control of the
+ * same rollout step t in one launch (both read the current state only). */
+comfree_status comfree_mppi_cost_control(comfree_ctx* ctx, int64_t first_world, int64_t n_worlds,
+                                         int32_t n_samples, const comfree_mppi_task* task, float* J,
+                                         const float* U, int32_t t, int32_t horizon, float kp, float kd,
+                                         float* command, float* tau, void* stream);
+
 /* Per problem: w_i = exp(-(J_i - min J)/lambda) / sum (weights [P][N] or
  * NULL), plan[P][H][Q] = clip(sum_i w_i U_i, lo, hi).  lambda > 0; N <= 12288. */
 comfree_status comfree_mppi_update(comfree_ctx* ctx, int32_t n_problems, int32_t n_samples, int32_t horizon,

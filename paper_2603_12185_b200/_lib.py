@@ -107,6 +107,8 @@ SIGNATURES = {
                                         P, P, P]),
     "comfree_mppi_cost": (ct.c_int, [P, ct.c_int64, ct.c_int64, ct.c_int32, ct.POINTER(comfree_mppi_task), ct.c_int32,
                                      P, P]),
+    "comfree_mppi_cost_control": (ct.c_int, [P, ct.c_int64, ct.c_int64, ct.c_int32, ct.POINTER(comfree_mppi_task), P,
+                                             P, ct.c_int32, ct.c_int32, ct.c_float, ct.c_float, P, P, P]),
     "comfree_mppi_update": (ct.c_int, [P, ct.c_int32, ct.c_int32, ct.c_int32, P, P, ct.c_float, ct.c_float, ct.c_float,
                                        P, P, P]),
     "comfree_collide": (ct.c_int, [P, ct.c_int64, ct.c_int64, ct.c_int64, P, P, P, P, P, P, P, P, P]),

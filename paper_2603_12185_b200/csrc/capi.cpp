@@ -847,15 +847,33 @@ comfree_status comfree_mppi_control(comfree_ctx* ctx, int64_t first, int64_t nw,
   return COMFREE_OK;
 }
 
-comfree_status comfree_mppi_cost(comfree_ctx* ctx, int64_t first, int64_t nw, int32_t n_samples,
-                                 const comfree_mppi_task* task, int32_t terminal, float* J, void* stream) {
+static comfree_status mppi_cost_params(comfree_ctx* ctx, int64_t first, int64_t nw, int32_t n_samples,
+                                       const comfree_mppi_task* task, int32_t terminal, const float* J,
+                                       cf::MppiCostParams& C);
+
+comfree_status comfree_mppi_cost_control(comfree_ctx* ctx, int64_t first, int64_t nw, int32_t n_samples,
+                                         const comfree_mppi_task* task, float* J, const float* U, int32_t t,
+                                         int32_t H, float kp, float kd, float* command, float* tau, void* stream) {
   if (!ctx || !task) return COMFREE_ERR_INVALID_ARGUMENT;
+  if (t < 0 || t >= H || (nw > 0 && (!U || !command || !tau)))
+    return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "mppi_cost_control: step / arrays");
+  cf::MppiCostParams C{};
+  comfree_status st = mppi_cost_params(ctx, first, nw, n_samples, task, 0, J, C);
+  if (st != COMFREE_OK) return st;
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  CUDA_TRY(ctx, cf::mppi_cost_control(C, J, U, t, H, kp, kd, command, tau, static_cast<cudaStream_t>(stream)));
+  ctx->launches += nw > 0;
+  return COMFREE_OK;
+}
+
+static comfree_status mppi_cost_params(comfree_ctx* ctx, int64_t first, int64_t nw, int32_t n_samples,
+                                       const comfree_mppi_task* task, int32_t terminal, const float* J,
+                                       cf::MppiCostParams& C) {
   if (!ctx->art_loaded) return fail(ctx, COMFREE_ERR_STATE, "mppi_cost before load_articulation");
   if (first < 0 || nw < 0 || first + nw > ctx->W || n_samples < 1 || (nw > 0 && !J))
     return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "mppi_cost: range / arrays");
   if (task->object_body < 0 || task->object_body >= ctx->sc.B || !task->target_pos || !task->target_quat || !task->q_ref)
     return fail(ctx, COMFREE_ERR_VALIDATION, "mppi_cost: object body / targets");
-  cf::MppiCostParams C{};
   C.sc = ctx->sc;
   C.slab = ctx->slab + (size_t)first * ctx->sc.slab;
   C.model = static_cast<const float*>(ctx->art.p);
@@ -871,6 +889,15 @@ comfree_status comfree_mppi_cost(comfree_ctx* ctx, int64_t first, int64_t nw, in
   C.phi1 = task->phi1;
   C.phi2 = task->phi2;
   C.terminal = terminal != 0;
+  return COMFREE_OK;
+}
+
+comfree_status comfree_mppi_cost(comfree_ctx* ctx, int64_t first, int64_t nw, int32_t n_samples,
+                                 const comfree_mppi_task* task, int32_t terminal, float* J, void* stream) {
+  if (!ctx || !task) return COMFREE_ERR_INVALID_ARGUMENT;
+  cf::MppiCostParams C{};
+  comfree_status st = mppi_cost_params(ctx, first, nw, n_samples, task, terminal, J, C);
+  if (st != COMFREE_OK) return st;
   CUDA_TRY(ctx, cudaSetDevice(ctx->device));
   CUDA_TRY(ctx, cf::mppi_cost(C, J, static_cast<cudaStream_t>(stream)));
   ctx->launches += nw > 0;

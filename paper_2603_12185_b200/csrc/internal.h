@@ -149,6 +149,8 @@ cudaError_t mppi_sample(const float* plan, int P, int N, int H, int Q, float sig
 cudaError_t mppi_control(const SceneDev& sc, const float* slab, int64_t W, const float* U, int t, int H, float kp,
                          float kd, float* command, float* tau, cudaStream_t s);
 cudaError_t mppi_cost(const MppiCostParams& C, float* J, cudaStream_t s);
+cudaError_t mppi_cost_control(const MppiCostParams& C, float* J, const float* U, int t, int H, float kp, float kd,
+                              float* command, float* tau, cudaStream_t s);
 cudaError_t mppi_update(const float* J, const float* U, int P, int N, int H, int Q, float lambda, float lo, float hi,
                         float* plan, float* weights, cudaStream_t s);
 

@@ -9,6 +9,8 @@
 //   k_mppi_cost     Eq. (15) running cost c(x_t) or terminal V(x_H) of every
 //                   world, accumulated into J[w], thread per world (fingertips
 //                   from the chain forward kinematics)
+//   k_mppi_cost_control  the running cost and the control of one rollout step in
+//                   one launch (both read x_t only)
 //   k_mppi_update   one CTA per problem: min over the N costs, weights
 //                   exp(-(J - min)/lambda) normalised, plan = clip(sum w U)
 #include <cuda_runtime.h>
@@ -46,11 +48,9 @@ __global__ void k_mppi_sample(const float* __restrict__ plan, int P, int N, int 
   U[e] = fminf(fmaxf(plan[p * hq + th] + eps, lo), hi);
 }
 
-__global__ void k_mppi_control(const float* __restrict__ slab, int slab_stride, int qoff, int Qp, int Q, int64_t W,
-                               const float* __restrict__ U, int t, int H, float kp, float kd,
-                               float* __restrict__ command, float* __restrict__ tau) {
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= W * Q) return;
+__device__ __forceinline__ void mppi_control_elem(int64_t e, const float* __restrict__ slab, int slab_stride, int qoff,
+                                                  int Qp, int Q, const float* __restrict__ U, int t, int H, float kp,
+                                                  float kd, float* __restrict__ command, float* __restrict__ tau) {
   const int64_t w = e / Q;
   const int j = (int)(e - w * Q);
   const float* sq = slab + (size_t)w * slab_stride + qoff;
@@ -59,9 +59,15 @@ __global__ void k_mppi_control(const float* __restrict__ slab, int slab_stride, 
   tau[e] = kp * (cmd - sq[j]) - kd * sq[Qp + j];
 }
 
-__global__ void k_mppi_cost(const __grid_constant__ MppiCostParams C, float* __restrict__ J) {
-  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (w >= C.n_worlds) return;
+__global__ void k_mppi_control(const float* __restrict__ slab, int slab_stride, int qoff, int Qp, int Q, int64_t W,
+                               const float* __restrict__ U, int t, int H, float kp, float kd,
+                               float* __restrict__ command, float* __restrict__ tau) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= W * Q) return;
+  mppi_control_elem(e, slab, slab_stride, qoff, Qp, Q, U, t, H, kp, kd, command, tau);
+}
+
+__device__ __forceinline__ void mppi_cost_world(int64_t w, const MppiCostParams& C, float* __restrict__ J) {
   const int p = (int)(w / C.n_samples);
   const float* sp = C.slab + (size_t)w * C.sc.slab + C.obj;
   const size_t pb = (size_t)C.sc.Bp;
@@ -100,6 +106,27 @@ __global__ void k_mppi_cost(const __grid_constant__ MppiCostParams C, float* __r
     c += C.w[4] * ctip + C.w[5] * cj + (po.z < C.z_fallen ? C.omega_fallen : 0.f);
   }
   J[w] += c;
+}
+
+__global__ void k_mppi_cost(const __grid_constant__ MppiCostParams C, float* __restrict__ J) {
+  const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (w >= C.n_worlds) return;
+  mppi_cost_world(w, C, J);
+}
+
+// Running cost and control of one rollout step in one launch (both read x_t only):
+// threads [0, W) the costs, threads [W, W + W Q) the commands and torques.
+__global__ void k_mppi_cost_control(const __grid_constant__ MppiCostParams C, float* __restrict__ J,
+                                    const float* __restrict__ U, int t, int H, float kp, float kd,
+                                    float* __restrict__ command, float* __restrict__ tau) {
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t W = C.n_worlds, Q = C.sc.Q;
+  if (id < W) {
+    mppi_cost_world(id, C, J);
+  } else if (id - W < W * Q) {
+    mppi_control_elem(id - W, C.slab, C.sc.slab, N_BODY_PLANES * C.sc.Bp, C.sc.Qp, (int)Q, U, t, H, kp, kd, command,
+                      tau);
+  }
 }
 
 // One CTA per problem (blockDim = 256): weights over the N samples, then the
@@ -177,6 +204,14 @@ cudaError_t mppi_control(const SceneDev& sc, const float* slab, int64_t W, const
 cudaError_t mppi_cost(const MppiCostParams& C, float* J, cudaStream_t s) {
   if (C.n_worlds == 0) return cudaSuccess;
   k_mppi_cost<<<nblk(C.n_worlds), 256, 0, s>>>(C, J);
+  return cudaGetLastError();
+}
+
+cudaError_t mppi_cost_control(const MppiCostParams& C, float* J, const float* U, int t, int H, float kp, float kd,
+                              float* command, float* tau, cudaStream_t s) {
+  const int64_t n = C.n_worlds * (1 + C.sc.Q);
+  if (n == 0) return cudaSuccess;
+  k_mppi_cost_control<<<nblk(n), 256, 0, s>>>(C, J, U, t, H, kp, kd, command, tau);
   return cudaGetLastError();
 }
 

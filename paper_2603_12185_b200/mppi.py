@@ -8,8 +8,7 @@ is captured once in a CUDA graph and replayed; the collision keeps its
 contact count on the device, so nothing in it waits on the host):
   broadcast the live states to the P*N rollout worlds (comfree_set_state),
   U = clip(plan + eps)                                  comfree_mppi_sample
-  for t < H:  J += c(x_t)                               comfree_mppi_cost
-              command += u_t, tau = PD                  comfree_mppi_control
+  for t < H:  J += c(x_t); command += u_t, tau = PD   comfree_mppi_cost_control (one launch)
               contacts, J rows, L, tau - c              comfree_collide / comfree_articulation_update
               x_{t+1}                                   comfree_step
   J += V(x_H); plan = clip(sum_i w_i U_i)              comfree_mppi_cost / comfree_mppi_update
@@ -106,10 +105,10 @@ class MPPI:
         mc, N, H = self.mc, self.mc.n_samples, self.mc.horizon
         s = _stream_handle(stream)
         for t in range(H):
-            self._chk(self._lib.comfree_mppi_cost(self.ctx.h, 0, self.W, N, ct.byref(self.task_c), 0, _ptr(self.J), s),
-                      "comfree_mppi_cost")
-            self._chk(self._lib.comfree_mppi_control(self.ctx.h, 0, self.W, _ptr(self.U), t, H, mc.kp, mc.kd,
-                                                     _ptr(self.command), _ptr(self.tau), s), "comfree_mppi_control")
+            self._chk(self._lib.comfree_mppi_cost_control(self.ctx.h, 0, self.W, N, ct.byref(self.task_c),
+                                                          _ptr(self.J), _ptr(self.U), t, H, mc.kp, mc.kd,
+                                                          _ptr(self.command), _ptr(self.tau), s),
+                      "comfree_mppi_cost_control")
             dc, link = self.ctx.collide(capacity=self.W * mc.contacts_per_world, stream=stream, device_count=True)
             self.ctx.articulation_update(self.tL, self.tt, dc, link, tau_ext=self.tau, stream=stream)
             self.ctx.step(dc, Inputs(None, self.tL, self.tt), dt=self.dt, stream=stream)
