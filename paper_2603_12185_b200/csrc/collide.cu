@@ -85,12 +85,18 @@ __device__ __forceinline__ V3 tangent(V3 n) {
   return v3(1.f + s * n.x * n.x * a, s * b, -s * n.x);
 }
 
+// Contact sink of one pair: EMIT = false only counts (no staging arrays: the
+// count pass has no stack frame); EMIT = true stages the records for the writes.
+template <bool EMIT>
 struct Out {
-  V3 p[kMaxPairContacts], n[kMaxPairContacts];
-  float phi[kMaxPairContacts];
+  V3 p[EMIT ? kMaxPairContacts : 1], n[EMIT ? kMaxPairContacts : 1];
+  float phi[EMIT ? kMaxPairContacts : 1];
   int k;
   __device__ void add(V3 pp, float ph, V3 nn) {
-    if (k < kMaxPairContacts) { p[k] = pp; phi[k] = ph; n[k] = nn; ++k; }
+    if (k < kMaxPairContacts) {
+      if (EMIT) { p[k] = pp; phi[k] = ph; n[k] = nn; }
+      ++k;
+    }
   }
 };
 
@@ -122,7 +128,8 @@ __device__ __forceinline__ void closest_segments(V3 p1, V3 q1, V3 p2, V3 q2, V3&
   c2 = add(p2, mul(t, d2));
 }
 
-__device__ __forceinline__ void two_spheres(V3 c1, float R1, V3 c2, float R2, float margin, Out& o) {
+template <class O>
+__device__ __forceinline__ void two_spheres(V3 c1, float R1, V3 c2, float R2, float margin, O& o) {
   const V3 d = sub(c2, c1);
   const float dist = sqrtf(dot(d, d));
   const V3 nn = mul(1.f / dist, d);
@@ -168,8 +175,9 @@ __device__ __forceinline__ float sphere_box(V3 c, float R, const Frame& Fb, floa
 }
 
 // Corners of box B against the faces of box A (vertex-face).
+template <class O>
 __device__ __forceinline__ void box_corners_on(const Frame& A, float4 hA, const Frame& Bf, float4 hB, float margin,
-                                               bool flip, Out& o) {
+                                               bool flip, O& o) {
   const float ha[3] = {hA.x, hA.y, hA.z};
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
@@ -198,11 +206,13 @@ __device__ __forceinline__ void box_corners_on(const Frame& A, float4 hA, const 
 
 // Contacts of pair pi in world w: returns the count; with out != null writes them
 // from index `base` on.
-__device__ int pair_contacts(const CollideParams& P, int pi, int64_t w, int64_t base, bool emit) {
+template <bool EMIT>
+__device__ int pair_contacts(const CollideParams& P, int pi, int64_t w, int64_t base) {
+  constexpr bool emit = EMIT;
   const int2 pr = P.pairs[pi];
   const int4 g1 = P.geom[pr.x], g2 = P.geom[pr.y];
   const float margin = P.margin;
-  Out o;
+  Out<EMIT> o;
   o.k = 0;
   const int k1 = g1.x, k2 = g2.x;
   if (k1 == G_PLANE) {
@@ -281,6 +291,7 @@ __device__ int pair_contacts(const CollideParams& P, int pi, int64_t w, int64_t 
   }
   if (emit) {
     const int la = g1.y < -1 ? g1.z : 0, lb = g2.y < -1 ? g2.z : 0;
+#pragma unroll 1
     for (int k = 0; k < o.k; ++k) {
       const int64_t c = base + k;
       const V3 t1 = tangent(o.n[k]);
@@ -300,7 +311,7 @@ __global__ void k_collide_count(const __grid_constant__ CollideParams P, int32_t
   if (id == P.n_worlds * P.n_pairs) counts[id] = 0;  // the scan's closing element (total = its prefix)
   if (id >= P.n_worlds * P.n_pairs) return;
   const int64_t w = id / P.n_pairs;
-  counts[id] = pair_contacts(P, (int)(id - w * P.n_pairs), w, 0, false);
+  counts[id] = pair_contacts<false>(P, (int)(id - w * P.n_pairs), w, 0);
 }
 
 __global__ void k_collide_emit(const __grid_constant__ CollideParams P, const int32_t* __restrict__ offs,
@@ -315,10 +326,10 @@ __global__ void k_collide_emit(const __grid_constant__ CollideParams P, const in
   const int64_t w = id / P.n_pairs;
   const int64_t base = offs[id];
   if (base + kMaxPairContacts > capacity) {  // only the tail can overflow
-    const int n = pair_contacts(P, (int)(id - w * P.n_pairs), w, 0, false);
+    const int n = pair_contacts<false>(P, (int)(id - w * P.n_pairs), w, 0);
     if (base + n > capacity) return;
   }
-  pair_contacts(P, (int)(id - w * P.n_pairs), w, base, true);
+  pair_contacts<true>(P, (int)(id - w * P.n_pairs), w, base);
 }
 
 }  // namespace
