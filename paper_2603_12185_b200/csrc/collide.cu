@@ -325,6 +325,7 @@ __global__ void k_collide_emit(const __grid_constant__ CollideParams P, const in
   if (id >= P.n_worlds * P.n_pairs) return;
   const int64_t w = id / P.n_pairs;
   const int64_t base = offs[id];
+  if (offs[id + 1] == base) return;  // the count pass found no contact for this pair
   if (base + kMaxPairContacts > capacity) {  // only the tail can overflow
     const int n = pair_contacts<false>(P, (int)(id - w * P.n_pairs), w, 0);
     if (base + n > capacity) return;
