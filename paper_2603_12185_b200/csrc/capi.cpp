@@ -66,7 +66,7 @@ struct comfree_ctx {
   DevBuf art;
   bool art_loaded = false;
   // collision front-end: device geometry (comfree_load_geometry) and scan scratch
-  DevBuf geo, col_counts, col_offs, col_tmp;
+  DevBuf geo, col_counts, col_offs, col_tmp, col_frames;
   int32_t n_geoms = 0, n_pairs = 0;
   float col_margin = 0.f, col_mu[3] = {0.f, 0.f, 0.f};
   int32_t col_condim = 3;
@@ -798,6 +798,11 @@ comfree_status comfree_collide(comfree_ctx* ctx, int64_t first, int64_t nw, int6
   P.world = world;
   P.link = reinterpret_cast<int2*>(link);
   const size_t m = (size_t)nw * ctx->n_pairs + 1;
+  P.n_geoms = ctx->n_geoms;
+  CUDA_TRY(ctx, ensure(ctx->col_frames, std::max<size_t>(1, (size_t)nw * ctx->n_geoms) * 3 * sizeof(float4)));
+  P.frames = static_cast<float4*>(ctx->col_frames.p);
+  CUDA_TRY(ctx, cf::collide_frames(P, s));
+  ctx->launches += 1;
   CUDA_TRY(ctx, ensure(ctx->col_counts, m * sizeof(int32_t)));
   CUDA_TRY(ctx, ensure(ctx->col_offs, m * sizeof(int32_t)));
   size_t tb = 0;
@@ -1019,7 +1024,7 @@ void comfree_destroy(comfree_ctx* ctx) {
                     &ctx->sj, &ctx->skd, &ctx->nf, &ctx->foff, &ctx->cub_tmp, &ctx->in_world, &ctx->in_off, &ctx->in_c0,
                     &ctx->in_c1, &ctx->in_c2, &ctx->in_c3, &ctx->in_jrow, &ctx->in_kd, &ctx->in_fext, &ctx->in_L,
                     &ctx->in_tau, &ctx->imp, &ctx->st_tmp, &ctx->art, &ctx->geo, &ctx->col_counts,
-                    &ctx->col_offs, &ctx->col_tmp};
+                    &ctx->col_offs, &ctx->col_tmp, &ctx->col_frames};
   for (DevBuf* b : bufs) release(*b);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->slab) cudaFree(ctx->slab);

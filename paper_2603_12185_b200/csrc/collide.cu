@@ -78,6 +78,19 @@ __device__ Frame geom_frame(const CollideParams& P, int g, int64_t w) {
   return F;
 }
 
+// Geom frame from the frame pass (one evaluation per (world, geom) instead of
+// one per candidate pair and pass).
+__device__ __forceinline__ Frame load_frame(const CollideParams& P, int g, int64_t w) {
+  const float4* f = P.frames + ((size_t)w * P.n_geoms + g) * 3;
+  const float4 a = f[0], b = f[1], c = f[2];
+  Frame F;
+  F.R[0] = a.x; F.R[1] = a.y; F.R[2] = a.z;
+  F.R[3] = b.x; F.R[4] = b.y; F.R[5] = b.z;
+  F.R[6] = c.x; F.R[7] = c.y; F.R[8] = c.z;
+  F.x = v3(a.w, b.w, c.w);
+  return F;
+}
+
 __device__ __forceinline__ V3 tangent(V3 n) {
   const float s = copysignf(1.f, n.z);
   const float a = -1.f / (s + n.z);
@@ -122,7 +135,7 @@ __device__ __forceinline__ void Out<EMIT>::add(V3 pp, float ph, V3 nn) {
 
 // Capsule segment ends (end -1 first): x -+ half_len * the frame's z axis.
 __device__ __forceinline__ void capsule_ends(const CollideParams& P, int g, int64_t w, V3& a, V3& b) {
-  const Frame F = geom_frame(P, g, w);
+  const Frame F = load_frame(P, g, w);
   const float hl = P.size[g].y;
   const V3 z = v3(F.R[2], F.R[5], F.R[8]);
   a = sub(F.x, mul(hl, z));
@@ -256,7 +269,7 @@ __device__ int pair_contacts(const CollideParams& P, int pi, int64_t w, int64_t 
         if (phi < margin) o.add(sub(e[q], mul(R + 0.5f * phi, pn)), phi, pn);
       }
     } else {
-      const Frame F2 = geom_frame(P, pr.y, w);
+      const Frame F2 = load_frame(P, pr.y, w);
       if (k2 == G_SPHERE) {
         const float R = P.size[pr.y].x;
         const float phi = dot(pn, F2.x) - off - R;
@@ -276,8 +289,8 @@ __device__ int pair_contacts(const CollideParams& P, int pi, int64_t w, int64_t 
     const float R1 = P.size[pr.x].x, R2 = P.size[pr.y].x;
     V3 c1, c2;
     if (k1 == G_SPHERE && k2 == G_SPHERE) {
-      c1 = geom_frame(P, pr.x, w).x;
-      c2 = geom_frame(P, pr.y, w).x;
+      c1 = load_frame(P, pr.x, w).x;
+      c2 = load_frame(P, pr.y, w).x;
     } else if (k1 == G_CAPSULE && k2 == G_CAPSULE) {
       V3 a1, b1, a2, b2;
       capsule_ends(P, pr.x, w, a1, b1);
@@ -286,30 +299,30 @@ __device__ int pair_contacts(const CollideParams& P, int pi, int64_t w, int64_t 
     } else if (k1 == G_CAPSULE) {
       V3 a1, b1;
       capsule_ends(P, pr.x, w, a1, b1);
-      c2 = geom_frame(P, pr.y, w).x;
+      c2 = load_frame(P, pr.y, w).x;
       c1 = closest_on_segment(a1, b1, c2);
     } else {
       V3 a2, b2;
-      c1 = geom_frame(P, pr.x, w).x;
+      c1 = load_frame(P, pr.x, w).x;
       capsule_ends(P, pr.y, w, a2, b2);
       c2 = closest_on_segment(a2, b2, c1);
     }
     two_spheres(c1, R1, c2, R2, margin, o);
   } else if (k1 == G_BOX && k2 == G_BOX) {
-    const Frame A = geom_frame(P, pr.x, w), Bf = geom_frame(P, pr.y, w);
+    const Frame A = load_frame(P, pr.x, w), Bf = load_frame(P, pr.y, w);
     const float4 hA = P.size[pr.x], hB = P.size[pr.y];
     box_corners_on(A, hA, Bf, hB, margin, false, o);
     box_corners_on(Bf, hB, A, hA, margin, true, o);
   } else {  // sphere or capsule against a box
     const bool round_first = k1 != G_BOX;
     const int gr = round_first ? pr.x : pr.y, gb = round_first ? pr.y : pr.x;
-    const Frame Fb = geom_frame(P, gb, w);
+    const Frame Fb = load_frame(P, gb, w);
     const float R = P.size[gr].x;
     const float4 h4 = P.size[gb];
     V3 e[2];
     int ne = 1;
     if (P.geom[gr].x == G_CAPSULE) { capsule_ends(P, gr, w, e[0], e[1]); ne = 2; }
-    else e[0] = geom_frame(P, gr, w).x;
+    else e[0] = load_frame(P, gr, w).x;
     for (int q = 0; q < ne; ++q) {
       V3 nbox, qs;
       const float phi = sphere_box(e[q], R, Fb, h4, nbox, qs);
@@ -331,6 +344,18 @@ __device__ int pair_contacts(const CollideParams& P, int pi, int64_t w, int64_t 
     }
   }
   return o.k;
+}
+
+__global__ void k_geom_frames(const __grid_constant__ CollideParams P) {
+  const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (id >= P.n_worlds * P.n_geoms) return;
+  const int64_t w = id / P.n_geoms;
+  const int g = (int)(id - w * P.n_geoms);
+  const Frame F = geom_frame(P, g, w);
+  float4* f = P.frames + (size_t)id * 3;
+  f[0] = make_float4(F.R[0], F.R[1], F.R[2], F.x.x);
+  f[1] = make_float4(F.R[3], F.R[4], F.R[5], F.x.y);
+  f[2] = make_float4(F.R[6], F.R[7], F.R[8], F.x.z);
 }
 
 __global__ void k_collide_count(const __grid_constant__ CollideParams P, int32_t* __restrict__ counts) {
@@ -364,6 +389,13 @@ __global__ void k_collide_emit(const __grid_constant__ CollideParams P, const in
 
 // counts: [n_worlds * n_pairs + 1] int32 scratch, offs: same size; temp: CUB
 // scratch (temp == nullptr queries *temp_bytes).  Writes the total to *total_dev.
+cudaError_t collide_frames(const CollideParams& P, cudaStream_t s) {
+  const int64_t n = P.n_worlds * P.n_geoms;
+  if (n == 0) return cudaSuccess;
+  k_geom_frames<<<(unsigned)((n + 127) / 128), 128, 0, s>>>(P);
+  return cudaGetLastError();
+}
+
 cudaError_t collide_count_scan(const CollideParams& P, int32_t* counts, int32_t* offs, void* temp,
                                size_t* temp_bytes, cudaStream_t s) {
   const int64_t n = P.n_worlds * P.n_pairs;

@@ -122,7 +122,10 @@ struct CollideParams {
   int4* c3;
   int32_t* world;
   int2* link;
+  float4* frames;             // [n_worlds][n_geoms][3] geom world frames (rows of R | x), filled by the frame pass
+  int n_geoms;
 };
+cudaError_t collide_frames(const CollideParams& P, cudaStream_t s);
 cudaError_t collide_count_scan(const CollideParams& P, int32_t* counts, int32_t* offs, void* temp,
                                size_t* temp_bytes, cudaStream_t s);
 // n_dev != null: also stores the (clamped) total for the asynchronous mode
