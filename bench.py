@@ -5,8 +5,10 @@ Workload (BASELINE.json metric, config 4 "dense pile"): per GPU 1024 worlds x
 500 free bodies (spheres / boxes / capsules) x 2000 contacts, condim 3, 4-facet
 cone, dt = 0.002, synthetic seeded inputs (harness/scenes.py c4_pile).  One
 step = S0 (world offsets from the sorted world ids) + the fused S1-S7 kernel,
-inputs resident in HBM; the per-step footprint (184 MB) exceeds the 126 MB L2
-and L2 is additionally flushed between timed steps.
+inputs resident in HBM and pre-segmented (the caller passes off[W+1], so S0 is
+skipped); the per-step footprint (184.3 MB = 1024 x (2000 x 64 B
++ 500 x 104 B)) exceeds the 126 MB L2 and L2 is additionally
+flushed between timed steps.
 
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
     torchrun --nproc-per-node N bench.py --gpus N   (weak scaling: 1024 worlds per GPU)
@@ -32,7 +34,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "world-steps/s (dense pile, 1024 worlds x 2000 contacts per GPU)"
-BYTES_PER_CONTACT = 68      # c0..c3 float4 streams (64 B) + the world id read by fused S0
+BYTES_PER_CONTACT = 64      # c0..c3 float4 streams; pre-segmented: no world-id stream
 BYTES_PER_BODY = 104        # 52 B state read + 52 B written
 
 
@@ -57,8 +59,11 @@ def parse():
                     help="pile contact dimensionality (3: the BASELINE config; 6: the 6D variant, n_t = n_rol = 4)")
     ap.add_argument("--kd", action="store_true",
                     help="per-contact (k_user, d_user) impedance arrays (learned-impedance variant, P:206-208)")
-    ap.add_argument("--impedance", default="heuristic", choices=["heuristic", "exact_diagonal"],
-                    help="exact_diagonal: Eq. (11) per facet (reading R24) instead of the trace heuristic")
+    ap.add_argument("--impedance", default="heuristic", choices=["heuristic", "exact_diagonal", "facet_diagonal"],
+                    help="exact_diagonal: Eq. (11) per facet (reading R24); facet_diagonal: Eq. (12) with the "
+                         "facet diagonal (reading R28); default: the trace heuristic of Eq. (12)")
+    ap.add_argument("--world-ids", action="store_true",
+                    help="pass sorted world ids instead of off[W+1] (S0 fused into the step; +4 B per contact)")
     ap.add_argument("--upstream", action="store_true",
                     help="hand / mixed: run the articulated upstream (FK, M(q), Cholesky, c(q,v), chain J rows) "
                          "on the GPU every step before the contact resolution (SURVEY 8(f) rank 2)")
@@ -184,6 +189,8 @@ def workload(args, rank, world_size):
         name += " + per-contact impedance"
     if args.impedance == "exact_diagonal":
         name += " + exact-diagonal impedance (Eq. 11)"
+    elif args.impedance == "facet_diagonal":
+        name += " + facet-diagonal impedance (Eq. 12 with the facet diagonal)"
     if args.upstream:
         name += " + articulated upstream on the GPU every step"
     if args.collide:
@@ -229,28 +236,51 @@ def _sample(part, max_worlds):
     return W, st, c, inp
 
 
-def cpu_oracle_rate(parts, cfg, seconds: float, max_worlds: int):
-    """The fp64 oracle as it stands, OpenMP across worlds on all host cores,
-    repeated steps over a bounded sample of each part's worlds."""
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def _oracle_rate(parts, cfg, seconds, max_worlds, threads):
     import oracle
-    cores = os.cpu_count() or 1
     samples = [(p, _sample(p, max_worlds)) for p in parts]
     for p, (W, st, c, inp) in samples:
-        oracle.step(cfg, p.scene, st, c, inp, n_threads=cores)   # warm
+        oracle.step(cfg, p.scene, st, c, inp, n_threads=threads)   # warm
     n = 0
     t0 = time.perf_counter()
     while True:
         for p, (W, st, c, inp) in samples:
-            oracle.step(cfg, p.scene, st, c, inp, n_threads=cores)
+            oracle.step(cfg, p.scene, st, c, inp, n_threads=threads)
         n += 1
         if time.perf_counter() - t0 >= seconds:
             break
     dt = time.perf_counter() - t0
     Ws = sum(x[1][0] for x in samples)
     nc = sum(x[1][2].n for x in samples)
-    return dict(value=n * Ws / dt, unit="world-steps/s", cores=cores, kind="oracle",
+    return n * Ws / dt, n, Ws, nc, dt
+
+
+def cpu_oracle_rate(parts, cfg, seconds: float, max_worlds: int):
+    """The fp64 oracle as it stands, timed twice on the host: OpenMP across
+    worlds on all host cores (`value`, `cores`), and on one core, each over
+    repeated steps of a bounded sample of each part's worlds."""
+    cores = os.cpu_count() or 1
+    v, n, Ws, nc, dt = _oracle_rate(parts, cfg, seconds, max_worlds, cores)
+    v1, n1, Ws1, nc1, dt1 = _oracle_rate(parts, cfg, 0.5 * seconds, max(1, max_worlds // 8), 1)
+    return dict(value=v, unit="world-steps/s", cores=cores, kind="oracle", cpu_model=cpu_model(),
+                all_cores={"value": v, "threads": cores,
+                           "sample": f"{n} oracle steps x {Ws} worlds ({nc} contacts), {dt:.1f} s"},
+                single_core={"value": v1, "threads": 1,
+                             "sample": f"{n1} oracle steps x {Ws1} worlds ({nc1} contacts), {dt1:.1f} s"},
                 sample=f"{n} oracle steps x {Ws} worlds of the same workload ({nc} contacts), fp64, "
-                       f"{dt:.1f} s, OpenMP over worlds")
+                       f"{dt:.1f} s, OpenMP over worlds on all {cores} host threads; single core: "
+                       f"{v1:.4g} world-steps/s over {n1} x {Ws1} worlds")
 
 
 # ---------------------------------------------------------------- main arms
@@ -303,11 +333,18 @@ def run_ours(args, rank, world_size, local):
     from paper_2603_12185_b200.dist import all_gather_worlds, reduce_max, uniform_ranges
     from harness.types import Config
 
-    local = local % max(torch.cuda.device_count(), 1)
+    n_dev = max(torch.cuda.device_count(), 1)
+    shared = world_size > n_dev            # several ranks on one GPU: plumbing only, no throughput claim
+    if shared and args.dist_backend == "nccl":
+        raise SystemExit(f"bench.py: {world_size} ranks but {n_dev} visible GPU(s); one rank per GPU is required "
+                         f"(--dist-backend gloo runs the multi-rank plumbing without a throughput value)")
+    local = local % n_dev
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world_size > 1:
         if args.dist_backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")          # communicator init in the log
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
         else:                              # plumbing check with several ranks on one GPU
             dist.init_process_group(args.dist_backend)
@@ -319,6 +356,9 @@ def run_ours(args, rank, world_size, local):
         p.ctx.load_scene(p.scene, p.W, p.st)
         p.dc = cf.DeviceContacts.from_host(p.c, dev)
         assert p.dc.sorted
+        # pre-segmented input (the benchmark default): off[W+1]
+        p.off = None if args.world_ids else torch.from_numpy(
+            np.searchsorted(p.c.world, np.arange(p.W + 1)).astype(np.int64)).to(dev)
         p.tin = None
         if p.inp is not None:
             p.tin = type(p.inp)(*(None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(dev)
@@ -367,7 +407,7 @@ def run_ours(args, rank, world_size, local):
                     p.dc, lk = p.ctx.collide(capacity=p.W * 40, stream=ps, device_count=True)
                     p.up = (lk, p.up[1])
                 p.ctx.articulation_update(p.tin.tree_L, p.tin.tree_tau, p.dc, p.up[0], tau_ext=p.up[1], stream=ps)
-            p.ctx.step(p.dc, p.tin, dt=cfg.dt, stream=ps)
+            p.ctx.step(p.dc, p.tin, dt=cfg.dt, stream=ps, off=None if (p.col is not None or args.collide) else p.off)
         for p in parts[1:]:
             s0.wait_stream(p.stream)
 
@@ -499,7 +539,7 @@ def run_ours(args, rank, world_size, local):
     e2e_value = n_local * world_size * e2e_steps / (e2e_ms * 1e-3)
 
     cpu = None
-    if rank == 0 and world_size == 1:
+    if rank == 0:                      # rank 0 only (the other ranks wait at the barrier)
         cpu = cpu_oracle_rate(parts, cfg, args.cpu_seconds, max_worlds=(parts[0].W if args.workload != "mixed" else 256))
     if world_size > 1:
         dist.barrier()
@@ -527,9 +567,11 @@ def run_ours(args, rank, world_size, local):
                        "parallelism": f"world-sharded x{world_size}"},
             "contacts_per_s": contacts_per_s,
             "gpu_launches": int(launches),
-            "kernel_ms": {**{f"fused_step[{p.name}]_direct_launch": p.k_ms_direct for p in parts},
-                          "step_graph": total_ms / args.steps,
+            "kernel_ms": {**{f"k_step[{p.name}]_events_direct_launch": p.k_ms_direct for p in parts},
+                          "step_graph_replay_events": total_ms / args.steps,
                           "segment_s0_separate": sum(p.kt["segment_ms"] / max(p.kt["step_launches"], 1) for p in parts)},
+            "segmentation": ("world ids (S0 fused into the step)" if args.world_ids or args.collide
+                             else "pre-segmented off[W+1] from the caller (S0 skipped, SURVEY 8(a))"),
             "cuda_graph": graph is not None,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_kind,
@@ -543,6 +585,9 @@ def run_ours(args, rank, world_size, local):
                        "full-step numbers, not this path alone",
             "final_state_finite": finite,
         }
+        if shared:                     # ranks share a GPU: the multi-rank plumbing ran, no throughput claim
+            line.update(value=None, contacts_per_s=None, plumbing_only=True,
+                        note=f"{world_size} ranks on {n_dev} GPU(s) ({args.dist_backend}): plumbing check only")
         print(json.dumps(line), flush=True)
     for p in parts:
         p.ctx.close()

@@ -38,7 +38,8 @@ class Config:
     n_rol: int = 4
     gravity: tuple = (0.0, 0.0, -9.81)
     dt: float = 0.002            # P:376 "we use dt=0.002s in all benchmarks"
-    impedance: str = "heuristic" # "heuristic": M(phi) of Eq. (12); "exact_diagonal": Eq. (11) (reading R24)
+    impedance: str = "heuristic" # "heuristic": M(phi) of Eq. (12); "exact_diagonal": Eq. (11) literally
+                                 # (reading R24); "facet_diagonal": Eq. (12) with the facet diagonal (R28)
 
     def with_(self, **kw) -> "Config":
         return replace(self, **kw)

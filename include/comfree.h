@@ -75,11 +75,18 @@ enum {
   COMFREE_FLAG_DETERMINISTIC = 1u << 1, /* accepted, no effect: every step is bitwise deterministic
                                            (fixed-point accumulation, see comfree_step) */
   COMFREE_FLAG_NO_FINITE_CHECK = 1u << 2,
-  /* Eq. (11) instead of the trace heuristic of Eq. (12): every
-   * facet f uses its own diagonal entry, M_f = r/(1-r) / (J~_f M^-1 J~_f^T),
-   * K_f = k M_f/dt, D_f = d M_f/dt (reading R24).  Costs one
-   * quadratic form per facet and side (general kernel variant). */
-  COMFREE_FLAG_EXACT_DIAGONAL = 1u << 3
+  /* Eq. (11) instead of the heuristic of Eq. (12): every facet f
+   * takes K_f dt + D_f = 1 / (dt A_f) with its own diagonal entry
+   * A_f = J~_f M^-1 J~_f^T, split K_f dt : D_f = k dt : d (DESIGN.md reading
+   * R24), i.e. Lambda_f = (-k phi - kappa s_f)_+ / (kappa A_f), kappa = k dt + d
+   * (per-contact (k, d) pairs must then have kappa > 0, else
+   * COMFREE_ERR_VALIDATION).  Costs one quadratic form per facet and side
+   * (general kernel variant). */
+  COMFREE_FLAG_EXACT_DIAGONAL = 1u << 3,
+  /* Eq. (12) with the facet's own diagonal entry in place of the trace
+   * heuristic (reading R28, not Eq. (11)): M_f = r/(1-r) / A_f,
+   * K_f = k M_f/dt, D_f = d M_f/dt.  Exclusive with EXACT_DIAGONAL. */
+  COMFREE_FLAG_FACET_DIAGONAL = 1u << 4
 };
 
 /* comfree_contacts.flags */
@@ -240,9 +247,11 @@ comfree_status comfree_load_scene(comfree_ctx* ctx, const comfree_scene* scene, 
  * generalized impulse in 64-bit fixed point (scale 2^(exponent(m^-1)+33)
  * linear, 2^(exponent(max diag I_w^-1)+33) angular, i.e. a velocity
  * resolution near 1e-10) with integer atomics, so the result is bitwise
- * identical run to run for the same input (contact order included).  A
- * velocity change beyond ~2^28 in one step exceeds the range and is reported
- * as COMFREE_ERR_NONFINITE. */
+ * identical run to run for the same input (contact order included).  Every
+ * add is bounded by 2^62 / (2 n_c + 2) for a world of n_c contacts (about
+ * 2^17 m/s of velocity change per contact at 2000 contacts), so no sum can
+ * wrap; an add beyond the bound, or a non-finite impulse (from a non-finite
+ * contact record), is reported as COMFREE_ERR_NONFINITE for its world. */
 comfree_status comfree_step(comfree_ctx* ctx, const comfree_worlds* worlds,
                             const comfree_contacts* c, float dt, void* stream);
 
@@ -418,6 +427,12 @@ comfree_status comfree_get_world_stats(comfree_ctx* ctx, int64_t first_world, in
  * off[n_worlds + 1] int64, perm[n_contacts] int32 (stable world order; the
  * identity when the input was already grouped).  Synchronises. */
 comfree_status comfree_segment_info(comfree_ctx* ctx, int64_t* off, int32_t* perm, void* stream);
+
+/* Synchronise `stream` and surface the device errors latched by earlier
+ * asynchronous calls (collision overflow, device validation, non-finite
+ * state), then clear them: COMFREE_OK when none.  A cheap check (one 4-byte
+ * read) for loops that never call comfree_get_* (e.g. MPPI control steps). */
+comfree_status comfree_check(comfree_ctx* ctx, void* stream);
 
 /* Instrumentation: while enabled, every comfree_step records CUDA events on
  * its own stream around the S0 kernels and around the fused step kernel. */

@@ -91,7 +91,7 @@ def _cfg(cfg: Config) -> _Cfg:
     for i in range(3):
         c.gravity[i] = cfg.gravity[i]
     c.dt = cfg.dt
-    c.exact_diagonal = 1 if getattr(cfg, "impedance", "heuristic") == "exact_diagonal" else 0
+    c.exact_diagonal = {"heuristic": 0, "exact_diagonal": 1, "facet_diagonal": 2}[getattr(cfg, "impedance", "heuristic")]
     return c
 
 

@@ -153,8 +153,16 @@ def dense_world_step(cfg: Config, scene: Scene, state: State, contacts: Contacts
                               float(contacts.mu_rol[c]), int(contacts.condim[c]), Jc):
             s = row @ v_s
             Kf, Df = K, D
-            if getattr(cfg, "impedance", "heuristic") == "exact_diagonal":
-                # Eq. (11): the diagonal entry J~_f M^-1 J~_f^T of this facet
+            imp = getattr(cfg, "impedance", "heuristic")
+            if imp == "exact_diagonal":
+                # Eq. (11): K_f dt + D_f = (1/dt) (J~_f M^-1 J~_f^T)^-1 in
+                # diagonal form, split K_f dt : D_f = k dt : d (reading R24)
+                A = float(row @ np.linalg.solve(M, row))
+                total = 1.0 / (dt * A)
+                Kf = total * (ku * dt / (ku * dt + du)) / dt
+                Df = total * (du / (ku * dt + du))
+            elif imp == "facet_diagonal":
+                # Eq. (12) with this facet's diagonal entry in place of the trace (reading R28)
                 A = float(row @ np.linalg.solve(M, row))
                 Mf = r / (1 - r) / A
                 Kf, Df = ku * Mf / dt, du * Mf / dt

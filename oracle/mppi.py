@@ -14,7 +14,9 @@ S:393-457).  Plain fp64 numpy; shares no code with the CUDA path.
              + Omega [p_z < z_fallen];  V(x) = phi1 |p_obj - p_t|^2 + phi2 (1 - (q_t . q_obj)^2)
              J_i = sum_{t=0}^{H-1} c(x_t) + V(x_H)   (Eq. (14))
   update     w_i = exp(-(J_i - min J)/lambda) / sum, U_bar <- clip(sum_i w_i U_i, lo, hi)
-             (min subtraction, normalised weights)
+             (min subtraction, normalised weights); a non-finite J_i
+             (diverged rollout) counts as +inf, weight 0, and a problem with no
+             finite J keeps its plan (reading R29; the paper is silent)
 """
 from __future__ import annotations
 
@@ -73,10 +75,16 @@ def cost(task, p_obj, q_obj, tips, q_robot, problem, terminal: bool):
     return c
 
 
-def update(J, U, lam, lo, hi):
+def update(J, U, lam, lo, hi, plan_prev=None):
     """J (P, N), U (P, N, H, Q) -> new plan (P, H, Q), weights (P, N)."""
-    Jm = J - J.min(axis=1, keepdims=True)
-    w = np.exp(-Jm / lam)
-    w = w / w.sum(axis=1, keepdims=True)
-    plan = np.einsum("pn,pnhq->phq", w, U)
-    return np.clip(plan, lo, hi), w
+    P, N, H, Q = U.shape
+    plan = np.zeros((P, H, Q)) if plan_prev is None else np.array(plan_prev, np.float64)
+    w = np.zeros((P, N))
+    for p in range(P):
+        Jp = np.where(np.isfinite(J[p]), J[p], np.inf)     # reading R29
+        if not np.isfinite(Jp).any():
+            continue                                        # keep the previous plan, weights 0
+        e = np.where(np.isfinite(Jp), np.exp(-(Jp - Jp.min()) / lam), 0.0)
+        w[p] = e / e.sum()
+        plan[p] = np.clip(np.einsum("n,nhq->hq", w[p], U[p]), lo, hi)
+    return plan, w

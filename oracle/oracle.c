@@ -383,12 +383,21 @@ static int step_world(const orc_config* cfg, const orc_scene* sc, int64_t w,
       }
       double s = dot3(gl, vc) + dot3(ga, wc);                 /* s = J~ v_s */
       double Kf = K, Df = D;
-      if (cfg->exact_diagonal) {  /* Eq. (11): this facet's own J~_f M^-1 J~_f^T (reading R24) */
+      if (cfg->exact_diagonal) {  /* this facet's own diagonal entry A_f = J~_f M^-1 J~_f^T */
         double A = side_quad(a, p, pos_w, sc->inv_mass, bw, L_w, nd, Ja, gl, ga)
                  + side_quad(b, p, pos_w, sc->inv_mass, bw, L_w, nd, Jb, gl, ga);
-        double Mf = r / (1.0 - r) / A;
-        Kf = kc * Mf / dt;
-        Df = dc * Mf / dt;
+        if (cfg->exact_diagonal == 1) {
+          /* Eq. (11), literally: K_f dt + D_f = 1 / (dt A_f), split in
+           * the user's ratio K_f dt : D_f = k dt : d (reading R24)            */
+          double kap = kc * dt + dc;
+          Kf = (kc / kap) / (dt * A);
+          Df = (dc / kap) / (dt * A);
+        } else {
+          /* Eq. (12) with the facet diagonal in place of the trace (reading R28) */
+          double Mf = r / (1.0 - r) / A;
+          Kf = kc * Mf / dt;
+          Df = dc * Mf / dt;
+        }
       }
       double lam = orc_facet_lambda(Kf, Df, s, phi, dt);      /* Eq. (9) */
       double Lam = lam * dt;                                  /* impulse, Eq. (10) */
@@ -489,6 +498,9 @@ int orc_step(const orc_config* cfg, const orc_scene* sc, int64_t n_worlds,
   for (int64_t c = 0; c < n; ++c) {
     /* per-contact impedance: finite and non-negative, like the global pair */
     if (kd && !(kd[2 * c] >= 0.0 && kd[2 * c + 1] >= 0.0 && kd[2 * c] < HUGE_VAL && kd[2 * c + 1] < HUGE_VAL))
+      return ORC_EINVAL;
+    /* Eq. (11)'s split k dt : d needs k dt + d > 0 */
+    if (cfg->exact_diagonal == 1 && !((kd ? kd[2 * c] : cfg->k_user) * cfg->dt + (kd ? kd[2 * c + 1] : cfg->d_user) > 0.0))
       return ORC_EINVAL;
     int32_t ids[2] = {body_a[c], body_b[c]};
     for (int s = 0; s < 2; ++s) {

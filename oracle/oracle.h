@@ -30,9 +30,11 @@ typedef struct {
   double gravity[3];
   double dt;
   int32_t exact_diagonal;   /* 0: M(phi) of Eq. (12) (trace heuristic);
-                               1: Eq. (11) diagonal, reading R24 in DESIGN.md:
-                               per facet M_f = r/(1-r) / (J~_f M^-1 J~_f^T),
-                               K_f = k M_f/dt, D_f = d M_f/dt               */
+                               1: Eq. (11) literally (reading R24): per facet
+                               K_f dt + D_f = 1/(dt A_f), A_f = J~_f M^-1 J~_f^T,
+                               split K_f dt : D_f = k dt : d;
+                               2: Eq. (12) with the facet diagonal (reading R28):
+                               M_f = r/(1-r) / A_f, K_f = k M_f/dt, D_f = d M_f/dt */
 } orc_config;
 
 typedef struct {

@@ -60,8 +60,10 @@ def make_config(cfg=None, flags: int = 0, **kw) -> _lib.comfree_config:
     impedance = src.pop("impedance", getattr(cfg, "impedance", "heuristic"))
     if impedance == "exact_diagonal":      # Eq. (11) per facet (reading R24)
         flags |= _lib.FLAG_EXACT_DIAGONAL
+    elif impedance == "facet_diagonal":    # Eq. (12) with the facet diagonal (reading R28)
+        flags |= _lib.FLAG_FACET_DIAGONAL
     elif impedance != "heuristic":
-        raise ValueError(f"impedance must be 'heuristic' or 'exact_diagonal', not {impedance!r}")
+        raise ValueError(f"impedance must be 'heuristic', 'exact_diagonal' or 'facet_diagonal', not {impedance!r}")
     for k, v in src.items():
         if k == "gravity":
             for i in range(3):
@@ -403,6 +405,11 @@ class Context:
         self._check(self._lib.comfree_segment_info(self.h, off.ctypes.data, perm.ctypes.data,
                                                    _stream_handle(stream)), "comfree_segment_info")
         return off, perm[:n_contacts]
+
+    def check(self, stream=None):
+        """Synchronise and raise the device errors latched by earlier
+        asynchronous calls (comfree_check)."""
+        self._check(self._lib.comfree_check(self.h, _stream_handle(stream)), "comfree_check")
 
     def set_timing(self, enable: bool = True):
         self._check(self._lib.comfree_set_timing(self.h, int(bool(enable))), "comfree_set_timing")

@@ -139,14 +139,15 @@ comfree_status check_latched(comfree_ctx* ctx, cudaStream_t s) {
            cf::ERR_IMPEDANCE | cf::ERR_WORLD_CONTACTS | cf::ERR_ARTICULATION))
     return fail(ctx, COMFREE_ERR_VALIDATION, "device validation failed (flags 0x%x):%s%s%s%s%s%s%s%s", e,
                 (e & cf::ERR_UNSORTED) ? " contacts not sorted by world;" : "",
-                (e & cf::ERR_WORLD_RANGE) ? " world id out of range;" : "",
+                (e & cf::ERR_WORLD_RANGE) ? " world id out of range or off[] inconsistent;" : "",
                 (e & cf::ERR_BODY_RANGE) ? " body id out of range or chain side without J rows;" : "",
                 (e & cf::ERR_CONDIM) ? " condim not in {1,3,4,6};" : "",
                 (e & cf::ERR_IMPULSE_CAP) ? " impulses buffer too small;" : "",
                 (e & cf::ERR_IMPEDANCE) ? " per-contact impedance negative or non-finite;" : "",
                 (e & cf::ERR_WORLD_CONTACTS) ? " more than 65536 contacts in one world;" : "",
                 (e & cf::ERR_ARTICULATION) ? " articulation: M(q) not positive definite or bad chain/link id;" : "");
-  return fail(ctx, COMFREE_ERR_NONFINITE, "non-finite state in world %lld", (long long)bad);
+  return fail(ctx, COMFREE_ERR_NONFINITE, "non-finite state (or impulse beyond the fixed-point range) in world %lld",
+              (long long)bad);
 }
 
 // Copy a caller buffer to device staging when it lives on the host.
@@ -232,6 +233,8 @@ comfree_status comfree_validate_config(const comfree_config* c) {
   ok = ok && c->n_t >= 4 && c->n_t <= 32 && c->n_t % 2 == 0;
   ok = ok && c->n_rol >= 2 && c->n_rol <= 32 && c->n_rol % 2 == 0;
   ok = ok && finite(c->gravity[0]) && finite(c->gravity[1]) && finite(c->gravity[2]);
+  // one impedance model at a time
+  ok = ok && !((c->flags & COMFREE_FLAG_EXACT_DIAGONAL) && (c->flags & COMFREE_FLAG_FACET_DIAGONAL));
   return ok ? COMFREE_OK : COMFREE_ERR_VALIDATION;
 }
 
@@ -562,7 +565,7 @@ comfree_status comfree_step(comfree_ctx* ctx, const comfree_worlds* wd, const co
   P.first_bad = ctx->d_first_bad;
   P.world_base = first;
   P.check_finite = !(cf_.flags & COMFREE_FLAG_NO_FINITE_CHECK);
-  P.exact_diag = (cf_.flags & COMFREE_FLAG_EXACT_DIAGONAL) != 0;
+  P.exact_diag = (cf_.flags & COMFREE_FLAG_EXACT_DIAGONAL) ? 1 : ((cf_.flags & COMFREE_FLAG_FACET_DIAGONAL) ? 2 : 0);
 #ifdef CF_TIMELINE
   P.timeline = cf_debug_timeline_buf();
 #endif
@@ -990,6 +993,11 @@ comfree_status comfree_set_timing(comfree_ctx* ctx, int enable) {
   if (!ctx) return COMFREE_ERR_INVALID_ARGUMENT;
   ctx->timing = enable != 0;
   return COMFREE_OK;
+}
+
+comfree_status comfree_check(comfree_ctx* ctx, void* stream) {
+  if (!ctx) return COMFREE_ERR_INVALID_ARGUMENT;
+  return check_latched(ctx, static_cast<cudaStream_t>(stream));
 }
 
 comfree_status comfree_get_timing(comfree_ctx* ctx, double out[3]) {

@@ -369,10 +369,22 @@ __global__ void k_collide_count(const __grid_constant__ CollideParams P, int32_t
 __global__ void k_collide_emit(const __grid_constant__ CollideParams P, const int32_t* __restrict__ offs,
                                int64_t capacity, int64_t* __restrict__ n_dev, int* __restrict__ err) {
   const int64_t id = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (n_dev && id == 0) {  // asynchronous mode: the count (clamped) for the step, overflow latched
-    const int64_t t = offs[P.n_worlds * P.n_pairs];
-    if (t > capacity) atomicOr(err, ERR_CONTACT_CAP);
-    *n_dev = t < capacity ? t : capacity;
+  if (n_dev && id == 0) {  // asynchronous mode: the count for the step, overflow latched
+    const int64_t np = P.n_worlds * P.n_pairs;
+    const int64_t t = offs[np];
+    if (t > capacity) {
+      atomicOr(err, ERR_CONTACT_CAP);
+      // only whole pairs are emitted: the count is the offset of the first pair
+      // that does not fit, i.e. the largest offs[k] <= capacity (offs is monotone)
+      int64_t lo = 0, hi = np;  // offs[lo] <= capacity < offs[hi]
+      while (hi - lo > 1) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (offs[mid] <= capacity) lo = mid; else hi = mid;
+      }
+      *n_dev = offs[lo];
+    } else {
+      *n_dev = t;
+    }
   }
   if (id >= P.n_worlds * P.n_pairs) return;
   const int64_t w = id / P.n_pairs;

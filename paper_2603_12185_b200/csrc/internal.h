@@ -72,7 +72,8 @@ struct StepParams {
   unsigned long long* first_bad;// min world id with a non-finite state
   int64_t world_base;           // absolute id of world 0 of the range (error reporting)
   int check_finite;
-  int exact_diag;               // Eq. (11) per-facet impedance (COMFREE_FLAG_EXACT_DIAGONAL), general variants only
+  int exact_diag;               // per-facet impedance, general variants only: 1 Eq. (11) (COMFREE_FLAG_EXACT_DIAGONAL),
+                                // 2 Eq. (12) with the facet diagonal (COMFREE_FLAG_FACET_DIAGONAL)
   unsigned* timeline;           // CF_TIMELINE builds only: per CTA (smid, t0, t1, t2, t3) globaltimer ns
 };
 

@@ -130,7 +130,11 @@ __global__ void k_mppi_cost_control(const __grid_constant__ MppiCostParams C, fl
 }
 
 // One CTA per problem (blockDim = 256): weights over the N samples, then the
-// weighted plan, clipped.
+// weighted plan, clipped.  A sample whose cost is not finite (a diverged
+// rollout) counts as J = +inf, i.e. weight 0; when no sample of a problem has
+// a finite cost the problem keeps its previous plan (weights 0).
+__device__ __forceinline__ float finite_cost(float j) { return isfinite(j) ? j : INFINITY; }
+
 __global__ void k_mppi_update(const float* __restrict__ J, const float* __restrict__ U, int N, int H, int Q,
                               float lambda, float lo, float hi, float* __restrict__ plan, float* __restrict__ weights) {
   extern __shared__ float sw[];  // N weights
@@ -138,7 +142,7 @@ __global__ void k_mppi_update(const float* __restrict__ J, const float* __restri
   const int p = blockIdx.x;
   const float* Jp = J + (size_t)p * N;
   float m = INFINITY;
-  for (int i = threadIdx.x; i < N; i += blockDim.x) m = fminf(m, Jp[i]);
+  for (int i = threadIdx.x; i < N; i += blockDim.x) m = fminf(m, finite_cost(Jp[i]));
   for (int o = 16; o > 0; o >>= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
   __syncthreads();
@@ -150,9 +154,15 @@ __global__ void k_mppi_update(const float* __restrict__ J, const float* __restri
   __syncthreads();
   const float jmin = red[0];
   __syncthreads();
+  if (!isfinite(jmin)) {  // every rollout of this problem diverged: keep the plan
+    for (int i = threadIdx.x; i < N; i += blockDim.x)
+      if (weights) weights[(size_t)p * N + i] = 0.f;
+    return;
+  }
   float s = 0.f;
   for (int i = threadIdx.x; i < N; i += blockDim.x) {
-    const float wi = expf(-(Jp[i] - jmin) / lambda);
+    const float ji = finite_cost(Jp[i]);
+    const float wi = isfinite(ji) ? expf(-(ji - jmin) / lambda) : 0.f;
     sw[i] = wi;
     s += wi;
   }

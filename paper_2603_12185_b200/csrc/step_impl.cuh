@@ -272,12 +272,13 @@ __device__ __forceinline__ bool seg_sum6(int key, float v[6], int lane) {
 // deterministic.  The scale 2^e is per body and per component group:
 // e = exponent(m^-1) + 33 for the linear part, exponent(max diag I_w^-1) + 33
 // for the angular part, i.e. a velocity resolution of about 2^-33 (1.2e-10).
-// Split form (default): the lo plane receives the low 16 bits of x (unsigned)
-// and the hi plane x >> 16, so neither atomic needs the other's result (no
-// carry, no returned value); the sum is hi * 2^16 + lo exactly while a world
-// has at most 65536 contacts (lo < 2^32) and |x| < 2^47 per add (checked,
-// ~16000 m/s of velocity change per contact).  CF_FX_SPLIT=0: lo/hi words of
-// one 64-bit integer with an explicit carry (the previous form).
+// Carry form (default, CF_FX_SPLIT=0): lo/hi words of one 64-bit integer, the
+// hi add takes the carry out of the lo add.  Split form (CF_FX_SPLIT=1, a
+// variant): the lo plane receives the low 16 bits of x (unsigned) and the hi
+// plane x >> 16, so neither atomic needs the other's result (no carry, no
+// returned value); the sum is hi * 2^16 + lo exactly while a world has at most
+// 65536 contacts (lo < 2^32) and |x| < 2^47 per add.  Both forms check every
+// add against fx_threshold (below), so a sum can never wrap.
 #ifndef CF_FX_SPLIT
 #define CF_FX_SPLIT 0  // split: measured neutral on C4 (61.6 us both), kept as a variant
 #endif
@@ -313,9 +314,25 @@ __device__ __forceinline__ void fx_add(unsigned* lo, int* hi, float v, float sca
   atomicAdd(hi, h);
 #endif
 }
-// per-add range of the split form: |v| * scale < 2^47 (max over a group of values)
-__device__ __forceinline__ bool fx_over(float vmax_abs, float scale) {
-  return CF_FX_SPLIT && !(vmax_abs * scale < 1.40737488e14f);  // 2^47; NaN counts as over
+// Per-add range.  Every add is |x| = |v| * scale < thr, thr = 2^62 / (2 n_c + 2)
+// for a world of n_c contacts (a body receives at most 2 n_c adds per
+// component), so no sum can wrap and the 64-bit total stays below 2^62; the
+// split form also needs |x| < 2^47.  The lanes keep a NaN-propagating running
+// maximum of |v| * scale (max.NaN: a NaN impulse, which the float-to-int
+// conversion would turn into 0, poisons it) and compare it once after the loop.
+__device__ __forceinline__ float max_nan(float a, float b) {
+  float r;
+  asm("max.NaN.f32 %0, %1, %2;" : "=f"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float fx_mag(const float v[6], float sl, float sa) {
+  const float ml = max_nan(max_nan(fabsf(v[0]), fabsf(v[1])), fabsf(v[2]));
+  const float ma = max_nan(max_nan(fabsf(v[3]), fabsf(v[4])), fabsf(v[5]));
+  return max_nan(ml * sl, ma * sa);
+}
+__device__ __forceinline__ float fx_threshold(int64_t n_contacts) {
+  const float t = 4.61168602e18f / (float)(2 * n_contacts + 2);  // 2^62 / (2 n_c + 2)
+  return CF_FX_SPLIT ? fminf(t, 1.40737488e14f) : t;               // split: also 2^47
 }
 __device__ __forceinline__ float fx_get(unsigned lo, int hi, float inv_scale) {
 #if CF_FX_SPLIT
@@ -469,7 +486,7 @@ __device__ __forceinline__ float side_quad_tree(const float4* jr, int64_t stride
 
 template <bool RUNS, bool OWN>
 __device__ __forceinline__ void scatter_side(unsigned* accl, const float4* rec, int Bp, int key, float v[6], int lane,
-                                             float im_own, float dm_own, bool& ovf) {
+                                             float im_own, float dm_own, float& mag) {
   const bool tail = (!RUNS || seg_sum6(key, v, lane)) && key >= 0;
   if (tail) {
     // scales: OWN = from the run's last lane's own side-a record (registers of
@@ -482,8 +499,7 @@ __device__ __forceinline__ void scatter_side(unsigned* accl, const float4* rec, 
       dmax = fmaxf(fmaxf(r[4 * (Bp + key) + 3], r[4 * (2 * Bp + key) + 3]), r[4 * (3 * Bp + key)]);
     }
     const float sl = fx_scale(im), sa = fx_scale(dmax);
-    ovf |= fx_over(fmaxf(fmaxf(fabsf(v[0]), fabsf(v[1])), fabsf(v[2])), sl) |
-           fx_over(fmaxf(fmaxf(fabsf(v[3]), fabsf(v[4])), fabsf(v[5])), sa);
+    mag = max_nan(mag, fx_mag(v, sl, sa));
 #pragma unroll
     for (int q = 0; q < 6; ++q) fx_add(ACC_LO(q, key), ACC_HI(q, key), v[q], q < 3 ? sl : sa);
   }
@@ -492,11 +508,10 @@ __device__ __forceinline__ void scatter_side(unsigned* accl, const float4* rec, 
 // S6 for a side whose body record is still in registers (direct adds, no runs):
 // the scales come from the lane's own m^-1 and max diag I_w^-1.
 __device__ __forceinline__ void scatter_own(unsigned* accl, int Bp, int key, const float v[6], float im,
-                                            float dmax, bool& ovf) {
+                                            float dmax, float& mag) {
   if (key >= 0) {
     const float sl = fx_scale(im), sa = fx_scale(dmax);
-    ovf |= fx_over(fmaxf(fmaxf(fabsf(v[0]), fabsf(v[1])), fabsf(v[2])), sl) |
-           fx_over(fmaxf(fmaxf(fabsf(v[3]), fabsf(v[4])), fabsf(v[5])), sa);
+    mag = max_nan(mag, fx_mag(v, sl, sa));
 #pragma unroll
     for (int q = 0; q < 6; ++q) fx_add(ACC_LO(q, key), ACC_HI(q, key), v[q], q < 3 ? sl : sa);
   }
@@ -695,12 +710,20 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
     cbeg = P.world_sorted ? rng[0] : P.off[w];
     nloc = (int)((P.world_sorted ? rng[1] : P.off[w + 1]) - cbeg);
   }
+  if (!P.world_sorted) {  // caller's off[]: monotone, inside [0, n], off[0] = 0, off[W] = n
+    const int64_t cend = cbeg + nloc;
+    if (cbeg < 0 || nloc < 0 || cend > ncon || (w == 0 && cbeg != 0) || (w == P.n_worlds - 1 && cend != ncon)) {
+      if (gt == 0) atomicOr(P.err, ERR_WORLD_RANGE);
+      cbeg = 0;
+      nloc = 0;
+    }
+  }
   const float4* C0p = P.c0 + cbeg;
   const float4* C1p = P.c1 + cbeg;
   const float4* C2p = P.c2 + cbeg;
   const int4* C3p = P.c3 + cbeg;
   if (nloc > kMaxWorldContacts && gt == 0) atomicOr(P.err, ERR_WORLD_CONTACTS);  // S6 lo-plane bound
-  bool fx_ovf = false;  // S6 per-add fixed-point range exceeded (reported as non-finite)
+  float fx_mag_max = 0.f;  // S6: running max of |value| * scale over this lane's adds (NaN-propagating)
   const int32_t* Wp = P.world_sorted ? P.world_sorted + cbeg : nullptr;
 
   // ---------------- S2-S6: contacts ----------------
@@ -836,10 +859,12 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
       float kc = k, kappa = kappa_g;
       if (P.kd) {  // warp-uniform
         const float2 kd = P.kd[cbeg + min(j, max(nloc - 1, 0))];
-        if (valid && !(kd.x >= 0.f && kd.y >= 0.f && kd.x < INFINITY && kd.y < INFINITY))
-          atomicOr(P.err, ERR_IMPEDANCE);
         kc = kd.x;
         kappa = kd.x * P.dt + kd.y;
+        // Eq. (11)'s split k dt : d (exact_diag == 1) needs kappa > 0
+        if (valid && !(kd.x >= 0.f && kd.y >= 0.f && kd.x < INFINITY && kd.y < INFINITY &&
+                       (FAST || P.exact_diag != 1 || kappa > 0.f)))
+          atomicOr(P.err, ERR_IMPEDANCE);
       }
       const float A = -kc * phi - kappa * un;
       float N = 0.f, F1 = 0.f, F2 = 0.f;
@@ -864,10 +889,15 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
         if (IMP && out) out[0] = Mc * N;
       }
       if (stats) n_active += valid ? act_t : 0;
-      if (!FAST && P.exact_diag) {  // warp-uniform: Eq. (11) per facet (reading R24)
+      if (!FAST && P.exact_diag) {  // warp-uniform: a facet's own diagonal entry A_f per facet
         // every facet f: row g_f = (gl, ga), s_f = g_f . (v_rel, w_rel),
-        // M_f = r/(1-r) / (J~_f M^-1 J~_f^T), Lambda_f = M_f (-k phi - kappa s_f)_+;
+        // A_f = J~_f M^-1 J~_f^T and Lambda_f = M_f (-k phi - kappa s_f)_+ with
+        //   exact_diag 1, Eq. (11) literally (K_f dt + D_f = 1/(dt A_f), split
+        //                 k dt : d, reading R24): M_f = 1 / (kappa A_f);
+        //   exact_diag 2, Eq. (12) with the facet diagonal (reading R28):
+        //                 M_f = r/(1-r) / A_f;
         // the contact wrench is (sum Lambda_f gl, sum Lambda_f ga)
+        const bool eq11 = P.exact_diag == 1;
         const float rho = r * rcp_approx(1.f - r);
         const float mu_tor = c2.w, mu_rol = __int_as_float(c3.z);
         const int nf = cd == 1 ? 1 : P.n_t + (cd >= 4 ? 2 : 0) + (cd == 6 ? P.n_rol : 0);
@@ -902,7 +932,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
               }
             }
           }
-          const float Lf = rho * rcp_approx(Af) * fmaxf(-kc * phi - kappa * sf, 0.f);
+          const float Lf = (eq11 ? rcp_approx(kappa * Af) : rho * rcp_approx(Af)) * fmaxf(-kc * phi - kappa * sf, 0.f);
           fs = make_float3(fs.x + Lf * gl.x, fs.y + Lf * gl.y, fs.z + Lf * gl.z);
           ts = make_float3(ts.x + Lf * ga.x, ts.y + Lf * ga.y, ts.z + Lf * ga.z);
           act += Lf > 0.f;
@@ -949,9 +979,9 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
     {
       const float3 ma = cross3(ra, f), mb = cross3(rb, f);
       float va[6] = {-f.x, -f.y, -f.z, -(ma.x + tau.x), -(ma.y + tau.y), -(ma.z + tau.z)};
-      scatter_side<true, !TREES>(accl, rec, Bp, ida >= 0 ? ida : -1, va, lane, ima, dma, fx_ovf);
+      scatter_side<true, !TREES>(accl, rec, Bp, ida >= 0 ? ida : -1, va, lane, ima, dma, fx_mag_max);
       float vb[6] = {f.x, f.y, f.z, mb.x + tau.x, mb.y + tau.y, mb.z + tau.z};
-      scatter_own(accl, Bp, idb >= 0 ? idb : -1, vb, imb, dmb, fx_ovf);
+      scatter_own(accl, Bp, idb >= 0 ? idb : -1, vb, imb, dmb, fx_mag_max);
     }
     if (TREES) {
 #pragma unroll
@@ -974,7 +1004,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
           }
           const float sv[4] = {s4.x, s4.y, s4.z, s4.w};
           const float scl = fx_pow2(__float_as_int(tL[16 * t + 14]));
-          fx_ovf |= fx_over(fmaxf(fmaxf(fabsf(s4.x), fabsf(s4.y)), fmaxf(fabsf(s4.z), fabsf(s4.w))), scl);
+          fx_mag_max = max_nan(fx_mag_max, max_nan(max_nan(fabsf(s4.x), fabsf(s4.y)), max_nan(fabsf(s4.z), fabsf(s4.w))) * scl);
 #pragma unroll
           for (int jj = 0; jj < 4; ++jj)
             if (jj < nd) fx_add(tacl + 4 * t + jj, tach + 4 * t + jj, sg * sv[jj], scl);
@@ -987,7 +1017,8 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
 
   // ---------------- S7: velocity correction + integration (Kernel IV) ----------------
   float ke = 0.f;
-  bool nonfinite = P.check_finite && fx_ovf;
+  // S6 range: every add of this lane below the world's per-add bound (NaN fails)
+  bool nonfinite = P.check_finite && !(fx_mag_max < fx_threshold(nloc));
   for (int i = gt; i < B; i += kGT) {
     const float4 r0 = rec[i], r1 = rec[Bp + i], r2 = rec[2 * Bp + i], r3 = rec[3 * Bp + i];
     float* sp = slab + i;

@@ -152,6 +152,7 @@ class MPPI:
         """One MPPI control step: returns u_0 (P, Q) as numpy; shifts the plan."""
         self.rollout_costs(live_state, command, stream)
         self.update(stream)
+        self.ctx.check(stream)          # collision overflow / non-finite rollouts surface here
         u0 = self.plan[:, 0].cpu().numpy()
         self.plan[:, :-1] = self.plan[:, 1:].clone()
         self.plan[:, -1] = 0.0

@@ -82,3 +82,27 @@ def compare_step(g, o, pos_tol=1e-6, quat_tol=2e-6):
     if "impulses" in g and "impulses" in o:
         np.testing.assert_array_equal(g["foff"], o["foff"])
         assert_close(g["impulses"], o["impulses"], what="Lambda")
+
+
+# Trajectories: per element, |d| <= 1e-3 |ref| + atol (north star: 1e-3
+# relative over 100-step trajectories).  The absolute floors (DESIGN.md,
+# "Trajectory tolerance") are 100 x the per-step floor of 1e-6 for velocities
+# (m/s, rad/s): 1e-4; its time integral over a 0.2 s trajectory for positions:
+# 2e-5 m (chain joint angles: 2e-5 rad); and for the unit quaternion the same
+# 2e-5 rad of rotation (|dq| <= |d theta| / 2).
+TRAJ_RTOL = 1e-3
+TRAJ_ATOL = dict(pos=2e-5, quat=2e-5, vel=1e-4, omega=1e-4, qpos=2e-5, qvel=1e-4)
+
+
+def traj_assert(sg, so, what="", keys=None):
+    """sg / so: State-like objects or dicts of arrays."""
+    get = (lambda o, k: o[k]) if isinstance(sg, dict) else getattr
+    geto = (lambda o, k: o[k]) if isinstance(so, dict) else getattr
+    for k, atol in TRAJ_ATOL.items():
+        if keys is not None and k not in keys:
+            continue
+        a, b = np.asarray(get(sg, k), np.float64), np.asarray(geto(so, k), np.float64)
+        if k == "quat":                               # q and -q are the same rotation
+            sgn = np.sign(np.sum(a * b, axis=-1, keepdims=True))
+            a = a * np.where(sgn == 0, 1.0, sgn)
+        assert_close(a, b, rtol=TRAJ_RTOL, atol=atol, what=f"{what} {k}")

@@ -67,6 +67,35 @@ def test_sample_control_update_match_oracle():
     assert_close(m.plan.cpu().numpy(), plan, rtol=1e-4, atol=1e-7, what="plan")
 
 
+def _oracle_J(m, scene, st, command, U, task, p, i, H):
+    """The oracle rolling out sample i of problem p (the GPU-drawn U) through
+    collision, upstream and step for H steps; returns J (Eq. (14))."""
+    s = State(*(np.asarray(getattr(st, k)[p:p + 1], np.float64)
+                for k in ("pos", "quat", "vel", "omega", "qpos", "qvel")))
+    cmd = command[p].astype(np.float64).copy()
+    Jr = 0.0
+
+    def c_of(s, terminal):
+        tips = [ar.fk(ART, t, s.qpos[0, 4 * t:4 * t + 4])[3] for t in range(4)]
+        return om.cost(task, s.pos[0, 0], s.quat[0, 0], tips, s.qpos[0], p, terminal)
+    for t in range(H):
+        Jr += c_of(s, False)
+        cmd = cmd + U[p, i, t]
+        tau_ext = om.pd_torque(cmd, s.qpos[0], s.qvel[0], m.mc.kp, m.mc.kd)[None]
+        c = co.collide(GEO, s, ART)
+        Jrow = np.zeros((c.n, 2, 6, 4))
+        for k in range(c.n):
+            for side, bid in enumerate((int(c.body_a[k]), int(c.body_b[k]))):
+                if bid < -1:
+                    tt = -2 - bid
+                    Jrow[k, side] = ar.point_rows(ART, tt, s.qpos[0, 4 * tt:4 * tt + 4],
+                                                  int(c.meta["link"][k, side]), c.c0[k, :3])
+        c.jrow = Jrow
+        L, tau = ar.upstream(ART, s.qpos, s.qvel, CFG.gravity, tau_ext)
+        s = oracle.step(CFG, scene, s, c, Inputs(None, L, tau))["state"]
+    return Jr + c_of(s, True)
+
+
 def test_rollout_costs_match_oracle():
     """P=2 problems x N=4 samples x H=3 steps: J of every sample vs the oracle
     rolling out the same (GPU-drawn) samples through collision, upstream, step."""
@@ -78,31 +107,55 @@ def test_rollout_costs_match_oracle():
     task = _task(P)
     for p in range(P):
         for i in range(N):
-            s = State(*(np.asarray(getattr(st, k)[p:p + 1], np.float64)
-                        for k in ("pos", "quat", "vel", "omega", "qpos", "qvel")))
-            cmd = command[p].astype(np.float64).copy()
-            Jr = 0.0
-
-            def c_of(s, terminal):
-                tips = [ar.fk(ART, t, s.qpos[0, 4 * t:4 * t + 4])[3] for t in range(4)]
-                return om.cost(task, s.pos[0, 0], s.quat[0, 0], tips, s.qpos[0], p, terminal)
-            for t in range(H):
-                Jr += c_of(s, False)
-                cmd = cmd + U[p, i, t]
-                tau_ext = om.pd_torque(cmd, s.qpos[0], s.qvel[0], m.mc.kp, m.mc.kd)[None]
-                c = co.collide(GEO, s, ART)
-                Jrow = np.zeros((c.n, 2, 6, 4))
-                for k in range(c.n):
-                    for side, bid in enumerate((int(c.body_a[k]), int(c.body_b[k]))):
-                        if bid < -1:
-                            tt = -2 - bid
-                            Jrow[k, side] = ar.point_rows(ART, tt, s.qpos[0, 4 * tt:4 * tt + 4],
-                                                          int(c.meta["link"][k, side]), c.c0[k, :3])
-                c.jrow = Jrow
-                L, tau = ar.upstream(ART, s.qpos, s.qvel, CFG.gravity, tau_ext)
-                s = oracle.step(CFG, scene, s, c, Inputs(None, L, tau))["state"]
-            Jr += c_of(s, True)
+            Jr = _oracle_J(m, scene, st, command, U, task, p, i, H)
             assert J[p * N + i] == pytest.approx(Jr, rel=2e-4, abs=1e-6), (p, i)
+
+
+def test_rollout_costs_bench_shape_sampled():
+    """The benchmarked shape (P = 16 problems x N = 256 samples x H = 48, the
+    rollout as one CUDA-graph replay, as tools/mppi_bench.py times it):
+    sampled rollouts' J against the oracle's 48-step rollouts of the same
+    samples, and the weighted update of the whole batch against the oracle's.
+    Tolerance: J sums 49 costs of states that went through 48 fp32 steps
+    (per-step parity 1e-5 relative), so 1e-3 relative."""
+    P, N, H = 16, 256, 48
+    m, scene, st = _mppi(P, N, H)
+    command = np.tile([0.0, 0.5, 0.5, 0.5], (P, 4))
+    J = m.rollout_costs(st, command).cpu().numpy()
+    U = m.U.cpu().numpy().astype(np.float64)
+    task = _task(P)
+    for p, i in ((0, 0), (3, 77), (9, 128), (15, 255)):
+        Jr = _oracle_J(m, scene, st, command, U, task, p, i, H)
+        assert J[p * N + i] == pytest.approx(Jr, rel=1e-3, abs=1e-5), (p, i, J[p * N + i], Jr)
+    plan0 = m.plan.cpu().numpy().astype(np.float64)
+    m.update()
+    plan, w = om.update(J.reshape(P, N).astype(np.float64), U, m.mc.lam, -0.1, 0.1, plan_prev=plan0)
+    assert_close(m.weights.cpu().numpy(), w, rtol=1e-4, atol=1e-7, what="weights")
+    assert_close(m.plan.cpu().numpy(), plan, rtol=1e-4, atol=1e-7, what="plan")
+
+
+def test_update_non_finite_costs():
+    """Reading R29 on the GPU: NaN / inf costs get weight 0; a problem whose
+    costs are all non-finite keeps its plan."""
+    import torch
+    m, scene, st = _mppi(3, 16, 5)
+    rng = np.random.default_rng(2)
+    m.plan.copy_(torch.as_tensor(rng.uniform(-0.08, 0.08, tuple(m.plan.shape)), dtype=torch.float32))
+    m.rollout_costs(st, np.zeros((3, 16)))
+    U = m.U.cpu().numpy().astype(np.float64)
+    plan0 = m.plan.cpu().numpy().astype(np.float64)
+    J = rng.uniform(0, 0.05, (3, 16)).astype(np.float32)
+    J[0, 5] = np.nan
+    J[1, 0] = np.inf
+    J[2, :] = np.nan
+    m.J.copy_(torch.as_tensor(J.reshape(-1)))
+    m.update()
+    plan, w = om.update(J.astype(np.float64), U, m.mc.lam, -0.1, 0.1, plan_prev=plan0)
+    gw = m.weights.cpu().numpy()
+    assert np.all(np.isfinite(gw)) and gw[0, 5] == 0.0 and gw[1, 0] == 0.0 and np.all(gw[2] == 0.0)
+    assert_close(gw, w, rtol=1e-4, atol=1e-7, what="weights")
+    assert_close(m.plan.cpu().numpy(), plan, rtol=1e-4, atol=1e-7, what="plan")
+    np.testing.assert_array_equal(m.plan.cpu().numpy()[2], plan0[2].astype(np.float32))
 
 
 def test_control_step_shifts_plan_and_is_reproducible():

@@ -13,7 +13,7 @@ import pytest
 import oracle
 from harness import scenes
 from harness.types import Config, Contacts, Inputs, State
-from _gpu import assert_close, compare_step, gpu_step
+from _gpu import assert_close, compare_step, gpu_step, traj_assert
 from _helpers import run_trajectory
 
 pytestmark = pytest.mark.gpu
@@ -326,7 +326,7 @@ def test_stats_match_oracle():
 
 
 # ---------------------------------------------------------------- trajectories (100 steps)
-def _traj_compare(cfg, scene, st, geo, steps=100, rtol=1e-3):
+def _traj_compare(cfg, scene, st, geo, steps=100):
     import paper_2603_12185_b200 as cf
     ctx = cf.Context(cfg)
     ctx.load_scene(scene, st.n_worlds, st)
@@ -340,10 +340,7 @@ def _traj_compare(cfg, scene, st, geo, steps=100, rtol=1e-3):
         return o["state"], None
     sg, _ = run_trajectory(gstep, geo, st, steps)
     so, _ = run_trajectory(ostep, geo, st.astype(np.float64), steps)
-    for k in ("pos", "vel"):
-        a, b = getattr(sg, k), getattr(so, k)
-        scale = np.max(np.abs(b)) + 1e-3
-        assert np.max(np.abs(a - b)) <= rtol * scale, (k, np.max(np.abs(a - b)), scale)
+    traj_assert(sg, so, f"{steps}-step trajectory")
 
 
 def test_trajectory_c1_sphere_and_sliding_box():
@@ -527,3 +524,57 @@ def test_fused_segmentation_uneven_worlds():
     off_o, _, _ = oracle.segment(c, len(cpw), CFG)
     np.testing.assert_array_equal(off_g, off_o)
     compare_step(g, oracle.step(CFG, scene, st, c, inp))
+
+
+# ---------------------------------------------------------------- S6 range, off[] validation
+def test_fixed_point_two_overflowing_adds_and_nan_normal():
+    """Every S6 add is bounded so a sum cannot wrap: two contacts pushing one
+    body far beyond the range (whose saturated adds would cancel if
+    unchecked) are reported for their world, and so is a NaN normal (whose
+    impulse the float-to-int conversion would turn into 0)."""
+    import paper_2603_12185_b200 as cf
+    scene, st, c = scenes.c4_pile(n_worlds=4, contacts_per_world=50)
+    idx = np.nonzero((c.world == 1) & (c.body_b >= 0))[0]
+    b = int(c.body_b[idx[0]])
+    two = idx[c.body_b[idx] == b][:1].tolist()
+    k2 = int(np.nonzero((c.world == 1) & (c.body_a >= 0) & (c.body_a != b))[0][0])
+    c.body_a[k2] = b                                   # a second contact on body b, as side a
+    st.vel[1, b] = -1e13 * c.c1[two[0], :3]
+    ctx = cf.Context(CFG)
+    ctx.load_scene(scene, 4, st)
+    ctx.step(cf.DeviceContacts.from_host(c), None)
+    with pytest.raises(cf.ComfreeError) as ei:
+        ctx.get_state()
+    assert ei.value.status == 4 and "world 1" in str(ei.value)
+    scene, st, c = scenes.c4_pile(n_worlds=4, contacts_per_world=50)
+    i = int(np.nonzero(c.world == 2)[0][3])
+    c.c1[i, :3] = np.nan
+    ctx = cf.Context(CFG)
+    ctx.load_scene(scene, 4, st)
+    ctx.step(cf.DeviceContacts.from_host(c), None)
+    with pytest.raises(cf.ComfreeError) as ei:
+        ctx.get_state()
+    assert ei.value.status == 4 and "world 2" in str(ei.value)
+
+
+def test_presegmented_off_matches_and_is_validated():
+    """The benchmark's input form: off[W+1] from the caller (S0 skipped) gives
+    the same bits as sorted world ids; an inconsistent off[] is a validation
+    error."""
+    import torch
+    import paper_2603_12185_b200 as cf
+    scene, st, c = scenes.c4_pile(n_worlds=7, contacts_per_world=400)
+    off = np.searchsorted(c.world, np.arange(8)).astype(np.int64)
+    a = gpu_step(CFG, scene, st, c, None, impulses=False)
+    ctx = cf.Context(CFG)
+    ctx.load_scene(scene, 7, st)
+    ctx.step(cf.DeviceContacts.from_host(c), None, off=torch.from_numpy(off).cuda())
+    out = ctx.get_state()
+    for k in ("pos", "quat", "vel", "omega"):
+        np.testing.assert_array_equal(out[k], getattr(a["state"], k))
+    bad = off.copy()
+    bad[-1] -= 1
+    ctx.step(cf.DeviceContacts.from_host(c), None, off=torch.from_numpy(bad).cuda())
+    with pytest.raises(cf.ComfreeError) as ei:
+        ctx.get_state()
+    assert ei.value.status == 2 and "off[]" in str(ei.value)

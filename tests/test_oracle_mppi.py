@@ -55,3 +55,23 @@ def test_cost_terms():
     assert c == pytest.approx(4 * 0.03 + 5 * 4 * 0.02 ** 2 + 100.0, rel=1e-12)
     v = mppi.cost(task, np.array([0.0, 0.03, 0.05]), np.array([half, 0, half, 0]), None, None, 0, True)
     assert v == pytest.approx(7.0 * 0.03 ** 2 + 8.0 * 0.5, rel=1e-12)
+
+
+def test_update_non_finite_costs_reading_r29():
+    """A diverged rollout (J = NaN or inf) gets weight 0 and the others are the
+    update without it; a problem with no finite cost keeps its plan (R29)."""
+    rng = np.random.default_rng(3)
+    U = rng.uniform(-0.1, 0.1, (3, 6, 2, 4))
+    J = rng.uniform(0.0, 0.01, (3, 6))
+    prev = rng.uniform(-0.05, 0.05, (3, 2, 4))
+    Jb = J.copy()
+    Jb[0, 2] = np.nan
+    Jb[1, 4] = np.inf
+    Jb[2, :] = np.nan
+    plan, w = mppi.update(Jb, U, 2e-3, -0.1, 0.1, plan_prev=prev)
+    assert w[0, 2] == 0.0 and w[1, 4] == 0.0 and np.all(w[2] == 0.0)
+    keep0 = [0, 1, 3, 4, 5]
+    p0, w0 = mppi.update(J[:1, keep0], U[:1, keep0], 2e-3, -0.1, 0.1)
+    np.testing.assert_allclose(w[0, keep0], w0[0], rtol=1e-15)
+    np.testing.assert_allclose(plan[0], p0[0], rtol=1e-15)
+    np.testing.assert_array_equal(plan[2], prev[2])
