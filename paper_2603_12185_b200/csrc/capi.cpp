@@ -56,6 +56,7 @@ struct comfree_ctx {
   float* inv_inertia = nullptr;
   comfree_world_stats* wstats = nullptr;
   int* d_err = nullptr;
+  int* d_queue = nullptr;  // persistent step kernel's world queue: [ticket, CTAs done] (self-resetting)
   unsigned long long* d_first_bad = nullptr;
   // S0 scratch
   DevBuf off, keys, perm, iota, s0, s1, s2, s3, sj, skd, nf, foff, cub_tmp;
@@ -283,12 +284,14 @@ comfree_status comfree_create(const comfree_config* cfg, int device, comfree_ctx
   directions(cfg->n_t, ctx->dir_t);
   directions(cfg->n_rol, ctx->dir_r);
   if (cudaSetDevice(device) != cudaSuccess || cudaMalloc(&ctx->d_err, sizeof(int)) != cudaSuccess ||
-      cudaMalloc(&ctx->d_first_bad, sizeof(unsigned long long)) != cudaSuccess) {
+      cudaMalloc(&ctx->d_first_bad, sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMalloc(&ctx->d_queue, 2 * sizeof(int)) != cudaSuccess) {
     delete ctx;
     return COMFREE_ERR_CUDA;
   }
   const unsigned long long none = ~0ull;
   cudaMemset(ctx->d_err, 0, sizeof(int));
+  cudaMemset(ctx->d_queue, 0, 2 * sizeof(int));
   cudaMemcpy(ctx->d_first_bad, &none, sizeof none, cudaMemcpyHostToDevice);
   *out = ctx;
   return COMFREE_OK;
@@ -563,6 +566,7 @@ comfree_status comfree_step(comfree_ctx* ctx, const comfree_worlds* wd, const co
   P.wstats = (cf_.flags & COMFREE_FLAG_STATS) ? ctx->wstats + first : nullptr;
   P.err = ctx->d_err;
   P.first_bad = ctx->d_first_bad;
+  P.queue = ctx->d_queue;
   P.world_base = first;
   P.check_finite = !(cf_.flags & COMFREE_FLAG_NO_FINITE_CHECK);
   P.exact_diag = (cf_.flags & COMFREE_FLAG_EXACT_DIAGONAL) ? 1 : ((cf_.flags & COMFREE_FLAG_FACET_DIAGONAL) ? 2 : 0);
@@ -583,7 +587,18 @@ comfree_status comfree_step(comfree_ctx* ctx, const comfree_worlds* wd, const co
     cudaEvent_t e = next_event(ctx, &st_e0);
     if (e) cudaEventRecord(e, s);
   }
-  CUDA_TRY(ctx, cf::launch_step(P, wpw, s));
+  // Opt-in (COMFREE_PERSIST=1, big free-body worlds): the persistent kernel
+  // (CTAs stepping their worlds in turn, the next world TMA-staged or
+  // L2-prefetched).  Measured slower than one CTA per world on C4 in every
+  // mode (profiles/r02_ab_kernel.txt), so not the default.
+  bool persist = false;
+  if (const char* e = getenv("COMFREE_PERSIST"))
+    persist = atoi(e) != 0 && sc.T == 0 && wpw == 8 && cf::step_persist_smem_bytes(sc) <= 227 * 1024;
+  if (persist) {
+    CUDA_TRY(ctx, cf::launch_step_persist(P, s));
+  } else {
+    CUDA_TRY(ctx, cf::launch_step(P, wpw, s));
+  }
   if (st_e0 >= 0) {
     cudaEvent_t e = next_event(ctx, &st_e1);
     if (e) {
@@ -1041,6 +1056,7 @@ void comfree_destroy(comfree_ctx* ctx) {
   if (ctx->wstats) cudaFree(ctx->wstats);
   if (ctx->d_err) cudaFree(ctx->d_err);
   if (ctx->d_first_bad) cudaFree(ctx->d_first_bad);
+  if (ctx->d_queue) cudaFree(ctx->d_queue);
   delete ctx;
 }
 

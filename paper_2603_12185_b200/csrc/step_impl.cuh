@@ -31,6 +31,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <climits>
+#include <cstdlib>
 
 #include "internal.h"
 
@@ -80,9 +81,14 @@ __host__ __device__ inline GroupLayout group_layout(const SceneDev& sc) {
   L.tL = o;   o += 16 * sc.T;    // float L[T][16]: 10 packed, 4 reciprocal diagonals, scale, -
   L.tacl = o; o += 4 * sc.T;     // uint32 chain impulse lo[T][4]
   L.tach = o; o += 4 * sc.T;     // int32  chain impulse hi[T][4]
-  L.red = o;  o += 16;           // reductions / contact range
+  L.red = o;  o += 48;           // reductions: counters [0, 8), contact range [12, 16), per-warp KE [16, 48)
   L.total = (o + 3) & ~3;
   return L;
+}
+
+// persistent kernel: one group layout (+ two slab staging buffers + 2 mbarriers)
+__host__ __device__ inline size_t persist_smem_bytes(const SceneDev& sc, bool stage) {
+  return (size_t)(group_layout(sc).total + (stage ? 2 * N_BODY_PLANES * sc.Bp : 0)) * sizeof(float) + 16;
 }
 
 template <int WPW, int CW = kWarps>
@@ -199,7 +205,8 @@ __device__ __forceinline__ void facet_pair(float A, float a, float& Lp, float& L
 }
 
 // Facets of one 2-D channel (tangential or rolling), d_j and d_{j+n/2} = -d_j:
-// N += sum L, F += sum L d.  NT = 4 is the exact axis set.
+// N += sum L, F += sum L d.  NT = 4 is the exact axis set and is only used for
+// the first channel (tangential): it assigns N, F instead of adding to zero.
 template <int NT, bool IMP>
 __device__ __forceinline__ void channel2(float A, float kmu, float w1, float w2, const float2* dir, int n,
                                          float& N, float& F1, float& F2, int& act, float* out, float Mc) {
@@ -207,9 +214,9 @@ __device__ __forceinline__ void channel2(float A, float kmu, float w1, float w2,
     float L0, L2, d0, L1, L3, d1;
     facet_pair(A, kmu * w1, L0, L2, d0);
     facet_pair(A, kmu * w2, L1, L3, d1);
-    N += (L0 + L2) + (L1 + L3);
-    F1 += d0;
-    F2 += d1;
+    N = (L0 + L2) + (L1 + L3);
+    F1 = d0;
+    F2 = d1;
     act += (L0 > 0.f) + (L1 > 0.f) + (L2 > 0.f) + (L3 > 0.f);
     if (IMP && out) { out[0] = Mc * L0; out[1] = Mc * L1; out[2] = Mc * L2; out[3] = Mc * L3; }
   } else {
@@ -280,7 +287,7 @@ __device__ __forceinline__ bool seg_sum6(int key, float v[6], int lane) {
 // 65536 contacts (lo < 2^32) and |x| < 2^47 per add.  Both forms check every
 // add against fx_threshold (below), so a sum can never wrap.
 #ifndef CF_FX_SPLIT
-#define CF_FX_SPLIT 0  // split: measured neutral on C4 (61.6 us both), kept as a variant
+#define CF_FX_SPLIT 0  // split: -0.6 us on C4 but its range is 2^15 times smaller (variant only)
 #endif
 static constexpr int kMaxWorldContacts = CF_FX_SPLIT ? 65536 : 0x7fffffff;
 __device__ __forceinline__ int fx_exp(float inv) {
@@ -301,7 +308,11 @@ __device__ __forceinline__ float rcp_approx(float x) {
   return r;
 }
 __device__ __forceinline__ void fx_add(unsigned* lo, int* hi, float v, float scale) {
+#if CF_XU_TEST  // timing probe only (wrong beyond 2^31): is the 64-bit conversion on the XU pipe the limiter?
+  const long long x = (long long)__float2int_rn(v * scale);
+#else
   const long long x = __float2ll_rn(v * scale);
+#endif
 #if CF_FX_SPLIT
   atomicAdd(lo, (unsigned)x & 0xffffu);
   atomicAdd(hi, (int)(x >> 16));
@@ -331,8 +342,9 @@ __device__ __forceinline__ float fx_mag(const float v[6], float sl, float sa) {
   return max_nan(ml * sl, ma * sa);
 }
 __device__ __forceinline__ float fx_threshold(int64_t n_contacts) {
-  const float t = 4.61168602e18f / (float)(2 * n_contacts + 2);  // 2^62 / (2 n_c + 2)
-  return CF_FX_SPLIT ? fminf(t, 1.40737488e14f) : t;               // split: also 2^47
+  // carry form: the 64-bit sum stays below 2^62; split form: the hi plane's sum
+  // of x >> 16 stays below 2^31, i.e. sum |x| < 2^47
+  return (CF_FX_SPLIT ? 1.40737488e14f : 4.61168602e18f) / (float)(2 * n_contacts + 2);
 }
 __device__ __forceinline__ float fx_get(unsigned lo, int hi, float inv_scale) {
 #if CF_FX_SPLIT
@@ -517,19 +529,61 @@ __device__ __forceinline__ void scatter_own(unsigned* accl, int Bp, int key, con
   }
 }
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+// L2 prefetch of a world the step will reach later (its slab planes 0-12 and
+// its first contacts), issued by one thread through the bulk-copy engine.
+#ifndef CF_PF_CONTACTS
+#define CF_PF_CONTACTS 512
+#endif
+__device__ __forceinline__ void prefetch_world_l2(const StepParams& P, int64_t w) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(P.slab + (size_t)w * P.sc.slab),
+               "r"((uint32_t)(N_BODY_PLANES * P.sc.Bp * sizeof(float))) : "memory");
+  if (CF_PF_CONTACTS > 0 && P.off) {
+    const int64_t c0 = P.off[w], c1 = P.off[w + 1];
+    const int64_t n = c1 - c0 < CF_PF_CONTACTS ? c1 - c0 : CF_PF_CONTACTS;
+    if (n > 0) {
+      const uint32_t nb = (uint32_t)(n * 16);
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(P.c0 + c0), "r"(nb) : "memory");
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(P.c1 + c0), "r"(nb) : "memory");
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(P.c2 + c0), "r"(nb) : "memory");
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(P.c3 + c0), "r"(nb) : "memory");
+    }
+  }
+}
+
+// One world's step (S0-S8) by the world group `group` (WPW warps) of the CTA.
+// stg: the world's slab planes 0-12 already staged in shared memory (the
+// persistent kernel's TMA bulk copy), else null (S1 and S7 read the slab in HBM).
 template <int CW, int WPW, bool FAST, bool TREES, bool IMP>
-__global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 2 : (CW == 32 ? 1 : 16))) k_step(const __grid_constant__ StepParams P) {
-  extern __shared__ float4 smem4[];
-  float* smem = reinterpret_cast<float*>(smem4);
+__device__ __forceinline__ void world_step(const StepParams& P, float* smem, const int64_t w, const int group,
+                                           const float* stg) {
   const SceneDev& sc = P.sc;
   const GroupLayout GL = group_layout(sc);
-  constexpr int kGroups = CW / WPW;
   constexpr int kGT = WPW * 32;
-  const int group = threadIdx.x / kGT;
   const int gt = threadIdx.x % kGT;
   const int lane = threadIdx.x & 31;
-  const int64_t w = (int64_t)blockIdx.x * kGroups + group;
-  if (w >= P.n_worlds) return;  // whole group leaves together
 
   TL_MARK(0);
   float* G = smem + (size_t)group * GL.total;
@@ -619,7 +673,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
   };
   auto s1_params = [&](int i, float& omz, float& im, float3& ib, float3& ibi) {
     const size_t pb = (size_t)Bp;
-    omz = slab[12 * pb + i];
+    omz = (stg ? stg : slab)[12 * pb + i];
     im = sc.inv_mass[i];
     ib = make_float3(sc.inv_inertia[i], sc.inv_inertia[pb + i], sc.inv_inertia[2 * pb + i]);
     ibi = make_float3(sc.inertia[i], sc.inertia[pb + i], sc.inertia[2 * pb + i]);
@@ -629,7 +683,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
     float omz, im;
     float3 ib, ibi;
     s1_params(i, omz, im, ib, ibi);
-    s1_body(i, nullptr, omz, im, ib, ibi);
+    s1_body(i, stg, omz, im, ib, ibi);
   }
   TL_MARK(5);
   // S0: the contact range of this world (CF_EARLY_RANGE: every warp resolves it
@@ -704,6 +758,10 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
   if (gt < 8) red[gt] = 0.f;
   group_sync<WPW, CW>(group);
   TL_MARK(1);
+  // The world the CTA slot that frees next will start (P.pf_ahead worlds on:
+  // the resident world slots of the grid) into L2 while this world runs, so
+  // that world's prologue does not wait on HBM.
+  if (P.pf_ahead > 0 && gt == 0 && !stg && w + P.pf_ahead < P.n_worlds) prefetch_world_l2(P, w + P.pf_ahead);
 
   // Contact range of this world.
   if (!CF_EARLY_RANGE) {
@@ -734,12 +792,33 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
     C0 = ld_stream(C0p + j); C1 = ld_stream(C1p + j); C2 = ld_stream(C2p + j); C3 = ld_stream(C3p + j);
     if (Wp) WID = ld_id(Wp + j);
   }
+#ifndef CF_ROLL_PF
+#define CF_ROLL_PF 0
+#endif
   for (; base < nloc; base += kGT) {
     const int j = base + lane;
+#if CF_ROLL_PF
+    // rolling bulk L2 prefetch: the group's contact block CF_ROLL_PF iterations
+    // ahead, one bulk request per stream from the group's first lane
+    if (gt == 0) {
+      const int64_t pb = (int64_t)base + (int64_t)CF_ROLL_PF * kGT;
+      if (pb < nloc) {
+        const int64_t cnt = (nloc - pb) < kGT ? (nloc - pb) : kGT;
+        const uint32_t nb = (uint32_t)(cnt * 16);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(P.c0 + cbeg + pb), "r"(nb) : "memory");
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(P.c1 + cbeg + pb), "r"(nb) : "memory");
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(P.c2 + cbeg + pb), "r"(nb) : "memory");
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(P.c3 + cbeg + pb), "r"(nb) : "memory");
+      }
+    }
+#endif
     // Next-contact prefetch: free-body variants load it once this contact's
     // fields are dead (after S5), so the loads reuse the same registers (no
     // copies); chain variants load it here, at the top of the iteration.
-    constexpr bool kLatePrefetch = !TREES;
+#ifndef CF_EARLY_PF
+#define CF_EARLY_PF 0
+#endif
+    constexpr bool kLatePrefetch = !TREES && !CF_EARLY_PF;
     const float4 c0 = C0, c1 = C1, c2 = C2;
     const int4 c3 = C3;
     const int wid = WID;
@@ -786,54 +865,56 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
     }
     if (!valid) { ida = -1; idb = -1; }
     const float3 p = make_float3(c0.x, c0.y, c0.z);
-    // S2: relative twist of b w.r.t. a, and the traces of S3
-    float3 vrel = make_float3(0.f, 0.f, 0.f), wrel = make_float3(0.f, 0.f, 0.f);
-    float tr = 0.f;
-    float3 ra = make_float3(0.f, 0.f, 0.f), rb = make_float3(0.f, 0.f, 0.f);
-    float ima = 0.f, dma = 0.f, imb = 0.f, dmb = 0.f;  // m^-1 and max diag I_w^-1 per side (S6 scales)
+    // S2: relative twist of b w.r.t. a, and the traces of S3.  Each side's
+    // point velocity, angular velocity and trace are formed on their own and
+    // combined once (no accumulation into zero-initialised sums).
+    float3 vs2[2], ws2[2], rs2[2];
+    float trs2[2], ims2[2], dms2[2];
 #pragma unroll
     for (int side = 0; side < 2; ++side) {
       const int id = side ? idb : ida;
-      const float sg = side ? 1.f : -1.f;
-      {  // free body (branch-free: a static or chain side reads the all-zero record B,
-         // whose velocity, inverse mass and inverse inertia contribute exactly 0)
-        const int ix = id >= 0 ? id : B;
-        const float4 r0 = rec[ix], r1 = rec[Bp + ix], r2 = rec[2 * Bp + ix], r3 = rec[3 * Bp + ix];
-        const float3 r = make_float3(p.x - r2.x, p.y - r2.y, p.z - r2.z);
-        const float3 wxr = cross3(make_float3(r1.x, r1.y, r1.z), r);
-        vrel.x += sg * (r0.x + wxr.x);
-        vrel.y += sg * (r0.y + wxr.y);
-        vrel.z += sg * (r0.z + wxr.z);
-        wrel.x += sg * r1.x;
-        wrel.y += sg * r1.y;
-        wrel.z += sg * r1.z;
-        // tr(J M^-1 J^T) of the linear point Jacobian: 3 im + tr(I)|r|^2 - r^T I r
-        const float Ixx = r1.w, Iyy = r2.w, Izz = r3.x, Ixy = r3.y, Ixz = r3.z, Iyz = r3.w;
-        const float3 Ir = make_float3(Ixx * r.x + Ixy * r.y + Ixz * r.z, Ixy * r.x + Iyy * r.y + Iyz * r.z,
-                                      Ixz * r.x + Iyz * r.y + Izz * r.z);
-        const float trs = 3.f * r0.w + (Ixx + Iyy + Izz) * dot3(r, r) - dot3(r, Ir);
-        tr += trs;
-        const float dm = fmaxf(fmaxf(Ixx, Iyy), Izz);
-        if (side) { rb = r; imb = r0.w; dmb = dm; } else { ra = r; ima = r0.w; dma = dm; }
-      }
+      // free body (branch-free: a static or chain side reads the all-zero record B,
+      // whose velocity, inverse mass and inverse inertia contribute exactly 0)
+      const int ix = id >= 0 ? id : B;
+      const float4 r0 = rec[ix], r1 = rec[Bp + ix], r2 = rec[2 * Bp + ix], r3 = rec[3 * Bp + ix];
+      const float3 r = make_float3(p.x - r2.x, p.y - r2.y, p.z - r2.z);
+      const float3 wxr = cross3(make_float3(r1.x, r1.y, r1.z), r);
+      vs2[side] = make_float3(r0.x + wxr.x, r0.y + wxr.y, r0.z + wxr.z);
+      ws2[side] = make_float3(r1.x, r1.y, r1.z);
+      // tr(J M^-1 J^T) of the linear point Jacobian: 3 im + tr(I)|r|^2 - r^T I r
+      const float Ixx = r1.w, Iyy = r2.w, Izz = r3.x, Ixy = r3.y, Ixz = r3.z, Iyz = r3.w;
+      const float3 Ir = make_float3(Ixx * r.x + Ixy * r.y + Ixz * r.z, Ixy * r.x + Iyy * r.y + Iyz * r.z,
+                                    Ixz * r.x + Iyz * r.y + Izz * r.z);
+      trs2[side] = fmaf(3.f, r0.w, fmaf(Ixx + Iyy + Izz, dot3(r, r), -dot3(r, Ir)));
+      rs2[side] = r;
+      ims2[side] = r0.w;
+      dms2[side] = fmaxf(fmaxf(Ixx, Iyy), Izz);
       if (TREES && id < -1) {
         const int t = -2 - id;
         const float4 qd = tq[t];
         const float* Ls = tL + 16 * t;
         const float4* jr = P.jrow + (size_t)(side * 6) * P.n_contacts + cbeg + j;
         float vp[3], wp[3];
+        float trc = 0.f;
 #pragma unroll
         for (int kk = 0; kk < 3; ++kk) {
           const float4 jl = ld_stream(jr + (size_t)kk * P.n_contacts);
           const float4 ja = ld_stream(jr + (size_t)(kk + 3) * P.n_contacts);
           vp[kk] = dot4(jl, qd);
           wp[kk] = dot4(ja, qd);
-          tr += chol_quad(Ls, nd, jl);
+          trc += chol_quad(Ls, nd, jl);
         }
-        vrel.x += sg * vp[0]; vrel.y += sg * vp[1]; vrel.z += sg * vp[2];
-        wrel.x += sg * wp[0]; wrel.y += sg * wp[1]; wrel.z += sg * wp[2];
+        // the all-zero record contributed exactly 0 above
+        vs2[side] = make_float3(vp[0], vp[1], vp[2]);
+        ws2[side] = make_float3(wp[0], wp[1], wp[2]);
+        trs2[side] = trc;
       }
     }
+    const float3 vrel = make_float3(vs2[1].x - vs2[0].x, vs2[1].y - vs2[0].y, vs2[1].z - vs2[0].z);
+    const float3 wrel = make_float3(ws2[1].x - ws2[0].x, ws2[1].y - ws2[0].y, ws2[1].z - ws2[0].z);
+    const float tr = trs2[0] + trs2[1];
+    const float3 ra = rs2[0], rb = rs2[1];
+    const float ima = ims2[0], dma = dms2[0], imb = ims2[1], dmb = dms2[1];  // S6 scales
     if (CF_EARLY_C3 && kLatePrefetch && FAST) {  // the next contact's ids first: the loop head waits on them
       int64_t g = cbeg + min(j + kGT, nloc - 1);
       asm volatile("" : "+l"(g));
@@ -981,7 +1062,12 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
       float va[6] = {-f.x, -f.y, -f.z, -(ma.x + tau.x), -(ma.y + tau.y), -(ma.z + tau.z)};
       scatter_side<true, !TREES>(accl, rec, Bp, ida >= 0 ? ida : -1, va, lane, ima, dma, fx_mag_max);
       float vb[6] = {f.x, f.y, f.z, mb.x + tau.x, mb.y + tau.y, mb.z + tau.z};
+#if CF_PROBE_B  // timing probe only (wrong results): side b adds to 32 distinct, bank-disjoint bodies
+      for (int q = 0; q < 6; ++q) vb[q] *= 0.f;
+      scatter_own(accl, Bp, idb >= 0 ? lane % B : -1, vb, imb, dmb, fx_mag_max);
+#else
       scatter_own(accl, Bp, idb >= 0 ? idb : -1, vb, imb, dmb, fx_mag_max);
+#endif
     }
     if (TREES) {
 #pragma unroll
@@ -1023,7 +1109,8 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
     const float4 r0 = rec[i], r1 = rec[Bp + i], r2 = rec[2 * Bp + i], r3 = rec[3 * Bp + i];
     float* sp = slab + i;
     const size_t pb = (size_t)Bp;
-    const float4 q = make_float4(sp[3 * pb], sp[4 * pb], sp[5 * pb], sp[6 * pb]);
+    const float* sq = stg ? stg + i : sp;  // step-start orientation
+    const float4 q = make_float4(sq[3 * pb], sq[4 * pb], sq[5 * pb], sq[6 * pb]);
     const float im = r0.w;
     const float Ixx = r1.w, Iyy = r2.w, Izz = r3.x, Ixy = r3.y, Ixz = r3.z, Iyz = r3.w;
     const float isl = fx_inv(fx_scale(im)), isa = fx_inv(fx_scale(fmaxf(fmaxf(Ixx, Iyy), Izz)));
@@ -1135,7 +1222,7 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
     if (lane == 0) {  // integer counters are order-free; energy is summed in warp order below
       atomicAdd(reinterpret_cast<int*>(&red[0]), n_active);
       atomicMax(reinterpret_cast<int*>(&red[1]), __float_as_int(fmaxf(max_pen, 0.f)));
-      red[8 + (gt >> 5)] = ke;
+      red[16 + (gt >> 5)] = ke;
     }
     group_sync<WPW, CW>(group);
     if (gt == 0) {
@@ -1144,11 +1231,132 @@ __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 
       ws.active_facets = *reinterpret_cast<int*>(&red[0]);
       ws.max_penetration = __int_as_float(*reinterpret_cast<int*>(&red[1]));
       float kes = 0.f;
-      for (int q8 = 0; q8 < WPW; ++q8) kes += red[8 + q8];
+      for (int q8 = 0; q8 < WPW; ++q8) kes += red[16 + q8];
       ws.kinetic_energy = kes;
       P.wstats[w] = ws;
     }
   }
+}
+
+template <int CW, int WPW, bool FAST, bool TREES, bool IMP>
+__global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 2 : (CW == 32 ? 1 : 16))) k_step(const __grid_constant__ StepParams P) {
+  extern __shared__ float4 smem4[];
+  constexpr int kGroups = CW / WPW;
+  const int group = threadIdx.x / (WPW * 32);
+  const int64_t w = (int64_t)blockIdx.x * kGroups + group;
+  if (w >= P.n_worlds) return;  // whole group leaves together
+  world_step<CW, WPW, FAST, TREES, IMP>(P, reinterpret_cast<float*>(smem4), w, group, nullptr);
+}
+
+// ---- persistent variant: CTAs that step their worlds in turn ----
+// CTA b (one world group of WPW warps) steps worlds b, b + G, b + 2G, ... (G =
+// the grid, sized to the CTAs the SMs hold at once).  While it runs world k,
+// one elected thread prepares world k + G:
+//   STAGE: the Tensor Memory Accelerator's bulk copy engine (cp.async.bulk,
+//          completion counted on an mbarrier) brings the next world's slab
+//          planes 0-12 (x, q, v, omega: 52 B per body, one contiguous range)
+//          into the second of two shared-memory staging buffers, so S1 of the
+//          next world starts from shared memory;
+//   else:  the next world's slab is prefetched into L2
+//          (cp.async.bulk.prefetch.L2);
+// and in both cases the first contacts of the next world are prefetched into
+// L2.  The next world's prologue then no longer waits on HBM latency, which in
+// the one-world-per-CTA kernel stalls every SM at the start and again when the
+// second wave of CTAs starts together.
+#ifndef CF_PERSIST_PF_CONTACTS
+#define CF_PERSIST_PF_CONTACTS 512  // contacts of the next world prefetched into L2 (per stream)
+#endif
+template <bool STAGE>
+__device__ __forceinline__ void prepare_world(const StepParams& P, float* buf, uint64_t* bar, int64_t w) {
+  const uint32_t bytes = (uint32_t)(N_BODY_PLANES * P.sc.Bp * sizeof(float));
+  const float* src = P.slab + (size_t)w * P.sc.slab;
+  if (STAGE) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads of buf precede the async write
+    mbar_expect_tx(bar, bytes);
+    bulk_g2s(buf, src, bytes, bar);
+  } else {
+    bulk_prefetch_l2(src, bytes);
+  }
+  if (CF_PERSIST_PF_CONTACTS > 0 && P.off) {  // the first contacts of the next world into L2
+    const int64_t c0 = P.off[w], c1 = P.off[w + 1];
+    const int64_t n = c1 - c0 < CF_PERSIST_PF_CONTACTS ? c1 - c0 : CF_PERSIST_PF_CONTACTS;
+    if (n > 0) {
+      const uint32_t nb = (uint32_t)(n * 16);
+      bulk_prefetch_l2(P.c0 + c0, nb);
+      bulk_prefetch_l2(P.c1 + c0, nb);
+      bulk_prefetch_l2(P.c2 + c0, nb);
+      bulk_prefetch_l2(P.c3 + c0, nb);
+    }
+  }
+}
+
+// Worlds are handed out by a global ticket counter (P.queue[0]), one world
+// ahead: a CTA that finishes early takes the next unclaimed world, so the SMs
+// stay balanced whichever CTAs they hold.  The last CTA to finish resets the
+// counters for the next launch (stream order makes the reset visible to it).
+template <int WPW, bool STAGE, bool FAST, bool IMP>
+__global__ void __launch_bounds__(WPW * 32, 32 / WPW) k_step_persist(const __grid_constant__ StepParams P) {
+  extern __shared__ float4 smem4[];
+  __shared__ int64_t s_next;
+  float* smem = reinterpret_cast<float*>(smem4);
+  const GroupLayout GL = group_layout(P.sc);
+  const int stage_f = STAGE ? N_BODY_PLANES * P.sc.Bp : 0;
+  float* buf0 = smem + GL.total;
+  float* buf1 = buf0 + stage_f;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(buf1 + stage_f);
+  int64_t w = 0, nxt = 0;
+  if (threadIdx.x == 0) {
+    w = atomicAdd(&P.queue[0], 1);
+    nxt = atomicAdd(&P.queue[0], 1);
+    if (STAGE) {
+      mbar_init(&bar[0], 1);
+      mbar_init(&bar[1], 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      if (w < P.n_worlds) prepare_world<true>(P, buf0, &bar[0], w);
+    }
+    s_next = w;
+  }
+  __syncthreads();
+  w = s_next;
+  for (int k = 0; w < P.n_worlds; ++k) {
+    const int b = k & 1;
+    // the next world: staged into the other buffer (free: its last reader, the
+    // previous world's S7, finished before the barrier that ended that world)
+    // or prefetched into L2
+    if (threadIdx.x == 0 && nxt < P.n_worlds) prepare_world<STAGE>(P, b ? buf0 : buf1, &bar[b ^ 1], nxt);
+    if (STAGE) mbar_wait(&bar[b], (uint32_t)((k >> 1) & 1));
+    world_step<WPW, WPW, FAST, false, IMP>(P, smem, w, 0, STAGE ? (b ? buf1 : buf0) : nullptr);
+    if (threadIdx.x == 0) {
+      s_next = nxt;
+      nxt = nxt < P.n_worlds ? atomicAdd(&P.queue[0], 1) : nxt;
+    }
+    __syncthreads();  // S7 done with rec / acc / the staging buffer before the next world
+    w = s_next;
+    __syncthreads();  // s_next read before it is rewritten
+  }
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(&P.queue[1], 1) == (int)gridDim.x - 1) {  // last CTA: reset for the next launch
+      P.queue[0] = 0;
+      P.queue[1] = 0;
+    }
+  }
+}
+
+template <int WPW, bool STAGE, bool FAST, bool IMP>
+cudaError_t launch_persist_variant(const StepParams& p, cudaStream_t s, int n_sm) {
+  const size_t smem = persist_smem_bytes(p.sc, STAGE);
+  cudaError_t e = cudaFuncSetAttribute(k_step_persist<WPW, STAGE, FAST, IMP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_persist<WPW, STAGE, FAST, IMP>, WPW * 32, smem);
+  if (e != cudaSuccess) return e;
+  const int64_t slots = (int64_t)n_sm * (per_sm > 0 ? per_sm : 1);
+  const unsigned grid = (unsigned)(p.n_worlds < slots ? p.n_worlds : slots);
+  if (grid == 0) return cudaSuccess;
+  k_step_persist<WPW, STAGE, FAST, IMP><<<grid, WPW * 32, smem, s>>>(p);
+  return cudaGetLastError();
 }
 
 template <int CW, int WPW, bool FAST, bool TREES, bool IMP>
@@ -1160,7 +1368,17 @@ cudaError_t launch_variant(const StepParams& p, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(k_step<CW, WPW, FAST, TREES, IMP>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_step<CW, WPW, FAST, TREES, IMP><<<grid, CW * 32, smem, s>>>(p);
+  StepParams q = p;
+  q.pf_ahead = 0;
+  const char* pf = getenv("COMFREE_PF");  // opt-in (measured +1.6 us on C4): next-world L2 prefetch
+  if (pf && atoi(pf) != 0) {
+    int dev = 0, n_sm = 0, per_sm = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step<CW, WPW, FAST, TREES, IMP>, CW * 32, smem) == cudaSuccess &&
+        (int64_t)grid > (int64_t)n_sm * per_sm)
+      q.pf_ahead = (int64_t)n_sm * per_sm * groups;  // worlds resident at once
+  }
+  k_step<CW, WPW, FAST, TREES, IMP><<<grid, CW * 32, smem, s>>>(q);
   return cudaGetLastError();
 }
 

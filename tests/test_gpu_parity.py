@@ -571,3 +571,20 @@ def test_presegmented_off_matches_and_is_validated():
     with pytest.raises(cf.ComfreeError) as ei:
         ctx.get_state()
     assert ei.value.status == 2 and "off[]" in str(ei.value)
+
+
+@pytest.mark.parametrize("mode", [1, 2, 3])
+def test_persistent_kernel_variants_bit_identical(mode, monkeypatch):
+    """The opt-in persistent step kernel (COMFREE_PERSIST=1; mode 1: 8 warps,
+    next world prefetched into L2; 2 / 3: 16 / 32 warps, next world's slab
+    staged into shared memory by TMA bulk copies on an mbarrier) gives the
+    same bits as the default kernel (per-world arithmetic is independent of
+    the CTA that runs it), across more worlds than the grid holds at once."""
+    scene, st, c = scenes.c4_pile(n_worlds=700, contacts_per_world=600)
+    ref = gpu_step(CFG, scene, st, c, None, impulses=False)
+    monkeypatch.setenv("COMFREE_PERSIST", "1")
+    monkeypatch.setenv("COMFREE_PERSIST_MODE", str(mode))
+    for _ in range(2):                              # the world queue resets itself between launches
+        g = gpu_step(CFG, scene, st, c, None, impulses=False)
+        for k in ("pos", "quat", "vel", "omega"):
+            np.testing.assert_array_equal(getattr(g["state"], k), getattr(ref["state"], k))
