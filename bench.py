@@ -38,7 +38,7 @@ BYTES_PER_CONTACT = 64      # c0..c3 float4 streams; pre-segment
 BYTES_PER_BODY = 104        # 52 B state read + 52 B written
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--impedance", default="heuristic", choices=["heuristic", "exact_diagonal", "facet_diagonal"],
                     help="exact_diagonal: Eq. (11) per facet (reading R24); facet_diagonal: Eq. (12) with the "
                          "facet diagonal (reading R28); default: the trace heuristic of Eq. (12)")
+    ap.add_argument("--nt", type=int, default=4, help="tangential facets per contact (even, >= 4)")
+    ap.add_argument("--nrol", type=int, default=4, help="rolling facets per contact at condim 6 (even)")
     ap.add_argument("--world-ids", action="store_true",
                     help="pass sorted world ids instead of off[W+1] (S0 fused into the step; +4 B per contact)")
     ap.add_argument("--upstream", action="store_true",
@@ -73,7 +75,7 @@ def parse():
                          "pile: lattice-neighbour candidate pairs, then the step (the full-step metric, P:389-390)")
     ap.add_argument("--workload", default="pile", choices=["pile", "hand", "mixed"],
                     help="pile: config 4 (the BASELINE metric); hand: config 3; mixed: config 5")
-    a = ap.parse_args()
+    a = ap.parse_args(argv)
     if a.collide:
         a.upstream = True
     if a.worlds is None:
@@ -84,6 +86,11 @@ def parse():
 METRICS = {"pile": METRIC,
            "hand": "world-steps/s (LEAP-like hand + cube, 4096 worlds per GPU)",
            "mixed": "world-steps/s (mixed hand + pile-lite, 65536 worlds in total)"}
+
+
+def facets(args) -> int:
+    """Facets per contact of the pile's condim (reading R11): 1, n_t, n_t + 2, n_t + 2 + n_rol."""
+    return {1: 1, 3: args.nt, 4: args.nt + 2, 6: args.nt + 2 + args.nrol}[args.condim]
 
 
 def dist_env():
@@ -200,27 +207,123 @@ def workload(args, rank, world_size):
     return parts, name, n
 
 
-def _workload(args, rank, world_size):
+# World generators by global world id (harness/scenes.py seeds world g from
+# (260312185, ..., g), so a world's bytes do not depend on the rank holding it).
+# kind: "pile" (C4), "hand" (C3), and C5's "pile-lite" / "hand5" (seed 5).
+UNIQUE = {"pile": 1 << 30, "hand": 1 << 30, "pile-lite": 4096, "hand5": 1024}
+
+
+def gen_worlds(args, kind, first, count):
+    """(scene, state, contacts, inputs) of global worlds [first, first + count)
+    of one kind; at most UNIQUE[kind] distinct worlds are generated and tiled
+    (local world k is a copy of global world first + k mod U)."""
     from harness import scenes
-    if args.workload == "hand":
+    U = max(1, min(count, UNIQUE[kind]))
+    if kind in ("hand", "hand5"):
+        scene, st, c, inp = scenes.c3_hand(n_worlds=U, seed=5 if kind == "hand5" else 0, world_offset=first)
+    elif kind == "pile-lite":
+        scene, st, c = scenes.c4_pile(n_worlds=U, contacts_per_world=400, lattice=(5, 5, 4), seed=5,
+                                      world_offset=first)
+        inp = None
+    else:
+        scene, st, c = scenes.c4_pile(n_worlds=U, contacts_per_world=args.contacts, world_offset=first,
+                                      condim=args.condim)
+        inp = None
+    if count != U:
+        st, c, inp = scenes.tile_worlds(st, c, inp, count)
+    return scene, st, c, inp
+
+
+def gen_copy_source(kind, first, local):
+    """Global id of the generated world that local world `local` of a part
+    starting at `first` copies (tiling, gen_worlds)."""
+    return first + local % max(1, UNIQUE[kind])
+
+
+def shard_plan(args, world_size):
+    """Per rank, per part kind: (first global id, count).  Weak scaling (pile,
+    hand): args.worlds per rank, rank r holding ids [r W, (r + 1) W).  C5
+    (strong scaling): one global sequence of args.worlds worlds alternating
+    pile-lite (even positions) and hand (odd), split into contiguous ranges
+    balanced by per-world bytes 64 C_w + 104 B_w (+ chain rows for hands,
+    SURVEY §8(e)) with dist.shard_ranges."""
+    from paper_2603_12185_b200.dist import shard_ranges
+    if args.workload != "mixed":
+        kind = "hand" if args.workload == "hand" else "pile"
         W = args.worlds
-        scene, st, c, inp = scenes.c3_hand(n_worlds=W, world_offset=rank * W)
-        return [Part("hand", scene, st, c, inp, _hand_bytes(scene, c, W))], \
-            "c3 LEAP-like hand + cube (4x4-DoF chains + free cube)", W
+        return [{kind: (r * W, W)} for r in range(world_size)]
+    n = args.worlds
+    cost_pile = 400 * BYTES_PER_CONTACT + 100 * BYTES_PER_BODY
+    cost_hand = 20 * BYTES_PER_CONTACT + 16 * 96 + BYTES_PER_BODY + 16 * 16 + 4 * 40 + 16 * 4
+    costs = np.where(np.arange(n) % 2 == 0, cost_pile, cost_hand).astype(np.float64)
+    plan = []
+    for lo, hi in shard_ranges(costs, world_size):
+        pf, pl = (lo + 1) // 2, (hi + 1) // 2          # even positions -> pile-lite ids
+        hf, hl = lo // 2, hi // 2                      # odd positions -> hand ids
+        plan.append({"pile-lite": (pf, pl - pf), "hand5": (hf, hl - hf)})
+    return plan
+
+
+def _workload(args, rank, world_size):
+    plan = shard_plan(args, world_size)[rank]
+    parts = []
+    for kind, (first, count) in plan.items():
+        scene, st, c, inp = gen_worlds(args, kind, first, count)
+        if kind in ("hand", "hand5"):
+            ab = _hand_bytes(scene, c, count)
+        else:
+            ab = c.n * BYTES_PER_CONTACT + count * scene.n_bodies * BYTES_PER_BODY
+        p = Part({"hand5": "hand"}.get(kind, kind), scene, st, c, inp, ab)
+        p.kind, p.first = kind, first
+        parts.append(p)
+    n = sum(p.W for p in parts)
+    if args.workload == "hand":
+        return parts, "c3 LEAP-like hand + cube (4x4-DoF chains + free cube)", n
     if args.workload == "mixed":
-        n = args.worlds // world_size                # strong scaling: the total is fixed
-        d = scenes.c5_mixed(n_worlds=n, world_offset=rank * n)
-        sh, sth, ch, ih = d["hand"]
-        sp, stp, cp = d["pile"]
-        parts = [Part("pile-lite", sp, stp, cp, None,
-                      cp.n * BYTES_PER_CONTACT + stp.n_worlds * sp.n_bodies * BYTES_PER_BODY),
-                 Part("hand", sh, sth, ch, ih, _hand_bytes(sh, ch, sth.n_worlds))]
-        return parts, "c5 mixed: half c3 hand, half pile-lite (100 bodies, 400 contacts)", n
-    W = args.worlds
-    scene, st, c = scenes.c4_pile(n_worlds=W, contacts_per_world=args.contacts, world_offset=rank * W,
-                                  condim=args.condim)
-    return [Part("pile", scene, st, c, None, W * (args.contacts * BYTES_PER_CONTACT + scene.n_bodies * BYTES_PER_BODY))], \
-        "c4 dense pile" + ("" if args.condim == 3 else f" (condim {args.condim})"), W
+        return parts, "c5 mixed: half c3 hand, half pile-lite (100 bodies, 400 contacts), cost-weighted shards", n
+    return parts, "c4 dense pile" + ("" if args.condim == 3 else f" (condim {args.condim})") + \
+        ("" if (args.nt, args.nrol) == (4, 4) else f" (n_t {args.nt}, n_rol {args.nrol}: {facets(args)} facets)"), n
+
+
+# ---------------------------------------------------------------- multi-rank verification
+def verify_shards(args, parts, finals, rank, world_size, n_steps, stepper, device=None, samples_per_rank=2):
+    """After the timed region: all-gather every part's final states (NCCL, or
+    gloo on CPU) into global world order, and on rank 0 re-run sampled worlds
+    -- the first and last world of every rank's range -- alone (one world per
+    call, `stepper(part, scene, st, c, inp, n_steps) -> dict of final arrays`)
+    and compare bit for bit: per-world arithmetic does not depend on the
+    sharding, and the step is deterministic (fixed-point S6).  Returns
+    (gathered MB, report dict on rank 0 / None)."""
+    import torch
+    from paper_2603_12185_b200.dist import all_gather_worlds
+    plan = shard_plan(args, world_size)
+    keys = ("pos", "quat", "vel", "omega", "qpos", "qvel")
+    mb = 0.0
+    report = {"checked_worlds": 0, "bitwise_equal": True, "n_steps": int(n_steps), "mismatch": []}
+    for p in parts:
+        ranges = []
+        for r in range(world_size):
+            f, cnt = plan[r][p.kind]
+            ranges.append((f - plan[0][p.kind][0], f - plan[0][p.kind][0] + cnt))
+        loc = {k: torch.from_numpy(np.ascontiguousarray(finals[p.name][k])).to(device or "cpu") for k in keys}
+        full = all_gather_worlds(loc, ranges)
+        mb += sum(v.numel() * v.element_size() for v in full.values()) / 1e6
+        if rank != 0:
+            continue
+        full = {k: v.cpu().numpy() for k, v in full.items()}
+        for r in range(world_size):
+            f, cnt = plan[r][p.kind]
+            for local in (sorted({0, cnt - 1})[:samples_per_rank] if cnt and stepper is not None else []):
+                src = gen_copy_source(p.kind, f, local)
+                scene, st, c, inp = gen_worlds(args, p.kind, src, 1)
+                one = stepper(p, scene, st, c, inp, n_steps)
+                g = (f - plan[0][p.kind][0]) + local
+                same = all(np.array_equal(np.asarray(one[k]).reshape(full[k][g].shape), full[k][g]) for k in keys)
+                report["checked_worlds"] += 1
+                if not same:
+                    report["bitwise_equal"] = False
+                    report["mismatch"].append({"part": p.name, "rank": r, "local": int(local)})
+    return mb, (report if rank == 0 else None)
 
 
 # ---------------------------------------------------------------- oracle (CPU) timing
@@ -291,7 +394,7 @@ def run_reference(args, rank, world_size):
     if rank != 0:
         return
     import oracle
-    cfg = Config(impedance=args.impedance)
+    cfg = Config(impedance=args.impedance, n_t=args.nt, n_rol=args.nrol)
     parts, wname, n_local = workload(args, 0, world_size)
     cores = os.cpu_count() or 1
     Wcap = 64 if args.workload == "pile" else 256
@@ -317,7 +420,7 @@ def run_reference(args, rank, world_size):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": wname, "worlds_per_gpu": n_local,
                        "contacts_per_world": sum(p.c.n for p in parts) // max(n_local, 1),
-                       "facets_per_contact": 4, "dt": cfg.dt, "sample_worlds_per_step": Ws},
+                       "facets_per_contact": facets(args), "dt": cfg.dt, "sample_worlds_per_step": Ws},
             "cpu_baseline": {"value": v, "unit": "world-steps/s", "cores": cores, "kind": "oracle",
                              "sample": f"{args.steps} steps x {Ws} of {n_local} worlds, fp64 oracle, OpenMP over worlds"},
             "e2e": {"value": v, "unit": "world-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -348,7 +451,7 @@ def run_ours(args, rank, world_size, local):
             dist.init_process_group("nccl", device_id=dev)
         else:                              # plumbing check with several ranks on one GPU
             dist.init_process_group(args.dist_backend)
-    cfg = Config(impedance=args.impedance)
+    cfg = Config(impedance=args.impedance, n_t=args.nt, n_rol=args.nrol)
     parts, wname, n_local = workload(args, rank, world_size)
     stream = torch.cuda.current_stream()
     for i, p in enumerate(parts):
@@ -394,8 +497,11 @@ def run_ours(args, rank, world_size, local):
         if args.flush_mode == "write+read":
             torch.sum(flush, dim=0, keepdim=True, out=flush_sink)
 
-    def one_step(s0):
+    applied = [0]          # steps applied to the states (graph capture records, does not run)
+
+    def one_step(s0, capturing=False):
         """One step of every part: part 0 on s0, the rest forked from s0 and joined back."""
+        applied[0] += 0 if capturing else 1
         for i, p in enumerate(parts):
             if i != 0:
                 p.stream.wait_stream(s0)
@@ -438,7 +544,7 @@ def run_ours(args, rank, world_size, local):
         side.wait_stream(stream)
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph, stream=side):
-            one_step(side)
+            one_step(side, capturing=True)
         stream.wait_stream(side)
         torch.cuda.synchronize()
     launches0 = sum(p.ctx.kernel_launches for p in parts)
@@ -454,6 +560,7 @@ def run_ours(args, rank, world_size, local):
             evs[i][0].record(stream)
             if graph is not None:
                 graph.replay()
+                applied[0] += 1
             else:
                 one_step(stream)
             evs[i][1].record(stream)
@@ -474,7 +581,8 @@ def run_ours(args, rank, world_size, local):
         launches = args.steps * (sum(p.ctx.kernel_launches for p in parts) - n0)
     total_ms = reduce_max(total_ms, dev)   # the job is as slow as its slowest rank
     ms_per_step = total_ms / args.steps
-    world_steps = n_local * world_size * args.steps
+    total_worlds = sum(c for pl in shard_plan(args, world_size) for _, c in pl.values())
+    world_steps = total_worlds * args.steps
     value = world_steps / (total_ms * 1e-3)
     n_contacts = sum(getattr(p, "c_count", p.c.n) for p in parts)
     contacts_per_s = value * (n_contacts / n_local)
@@ -494,19 +602,31 @@ def run_ours(args, rank, world_size, local):
             tr.get("contacts_per_world") == dom.c.n // dom.W and dom.col is None:
         traffic = tr.get("dram_bytes_per_launch")
 
-    # after the timed region: final states all-gathered (NCCL) for verification
+    # after the timed region: final states all-gathered (NCCL) and, on rank 0,
+    # sampled worlds re-run alone on this GPU and compared bit for bit
     finite = True
-    gathered_mb = None
+    gathered_mb = verification = None
     for p in parts:
         p.final = p.ctx.get_state()
         finite &= bool(np.isfinite(p.final["vel"]).all() and np.isfinite(p.final["pos"]).all())
     if world_size > 1:
-        gathered_mb = 0.0
-        for p in parts:
-            ranges = uniform_ranges(p.W * world_size, world_size)
-            loc = {k: torch.from_numpy(p.final[k]).to(dev) for k in ("pos", "quat", "vel", "omega")}
-            full = all_gather_worlds(loc, ranges)
-            gathered_mb += sum(v.numel() * v.element_size() for v in full.values()) / 1e6
+        plain = not (args.upstream or args.collide or args.kd)   # inputs constant over the steps
+
+        def gpu_stepper(p, scene, st, c, inp, n):
+            ctx = cf.Context(cfg, device=local)
+            ctx.load_scene(scene, 1, st)
+            dc = cf.DeviceContacts.from_host(c, dev)
+            off = torch.tensor([0, c.n], dtype=torch.int64, device=dev)
+            tin = None if inp is None else type(inp)(*(None if a is None else torch.from_numpy(
+                np.ascontiguousarray(a)).to(dev) for a in (inp.f_ext, inp.tree_L, inp.tree_tau)))
+            for _ in range(n):
+                ctx.step(dc, tin, dt=cfg.dt, off=None if args.world_ids else off)
+            out = ctx.get_state()
+            ctx.close()
+            return out
+        gathered_mb, verification = verify_shards(args, parts, {p.name: p.final for p in parts}, rank, world_size,
+                                                  applied[0], gpu_stepper if plain else None, device=dev,
+                                                  samples_per_rank=2 if plain else 0)
         finite = bool(reduce_max(0.0 if finite else 1.0, dev) == 0.0)
 
     # e2e: the same metric through the C ABI with HOST buffers (pinned), H2D of the
@@ -536,7 +656,7 @@ def run_ours(args, rank, world_size, local):
     e1.record(stream)
     torch.cuda.synchronize()
     e2e_ms = reduce_max(e0.elapsed_time(e1), dev)
-    e2e_value = n_local * world_size * e2e_steps / (e2e_ms * 1e-3)
+    e2e_value = total_worlds * e2e_steps / (e2e_ms * 1e-3)
 
     cpu = None
     if rank == 0:                      # rank 0 only (the other ranks wait at the barrier)
@@ -556,7 +676,7 @@ def run_ours(args, rank, world_size, local):
                        "parts": {p.name: {"worlds": p.W, "contacts_per_world": p.c.n // p.W,
                                           "bodies_per_world": p.scene.n_bodies, "chains_per_world": p.scene.n_trees}
                                  for p in parts},
-                       "facets_per_contact": {1: 1, 3: 4, 4: 6, 6: 10}[args.condim], "condim": args.condim,
+                       "facets_per_contact": facets(args), "condim": args.condim, "n_t": args.nt, "n_rol": args.nrol,
                        "dt": cfg.dt,
                        "l2": (("flushed between timed steps (256 MB write, then read back: cold clean L2)"
                                if args.flush_mode == "write+read" else "flushed between timed steps (256 MB write)")
@@ -581,6 +701,7 @@ def run_ours(args, rank, world_size, local):
                     "d2h_bytes_per_step": d2h, "steps": e2e_steps},
             "cpu_baseline": cpu,
             "allgather_final_state_mb": gathered_mb,
+            "sharded_verification": verification,
             "context": "paper: 2-3x MJWarp throughput in dense contact on one RTX 4090 (PAPER.md P:11, P:274); "
                        "full-step numbers, not this path alone",
             "final_state_finite": finite,
