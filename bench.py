@@ -51,7 +51,7 @@ def parse(argv=None):
                     help="L2 flush between timed steps: write 256 MB (leaves L2 full of dirty lines whose "
                          "write-back the next step pays), or write then read it back (cold, clean L2)")
     ap.add_argument("--no-graph", action="store_true", help="direct launches instead of CUDA-graph replay")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo only to exercise the multi-rank path on a single GPU")
@@ -630,33 +630,63 @@ def run_ours(args, rank, world_size, local):
         finite = bool(reduce_max(0.0 if finite else 1.0, dev) == 0.0)
 
     # e2e: the same metric through the C ABI with HOST buffers (pinned), H2D of the
-    # step's contacts and D2H of the resulting state inside the timed region
+    # step's contacts (and inputs) and D2H of the resulting state inside the
+    # timed region, every step.  Pipelined (COMFREE_MEM_HOST_ASYNC, the value
+    # reported): step k + 1's upload runs on the context's copy-in stream while
+    # step k's kernel and download run; serial (COMFREE_MEM_HOST, context): each
+    # call copies, steps and synchronises in turn.
+    from harness.types import Inputs
     e2e_steps = max(1, args.e2e_steps)
     h2d = d2h = 0
+
+    def pinned(a):
+        return None if a is None else torch.from_numpy(np.ascontiguousarray(a, np.float32)).pin_memory().numpy()
     for p in parts:
-        p.hc = cf.HostContacts.from_arrays(p.c, pin=True)
-        p.ctx.step(p.hc, p.inp, dt=cfg.dt)           # warm the staging buffers
+        p.hc = cf.HostContacts.from_arrays(p.c, pin=True, n_worlds=None if args.world_ids else p.W)
+        p.hca = cf.HostContacts.from_arrays(p.c, pin=True, asynchronous=True, n_worlds=None if args.world_ids else p.W)
+        p.inp_h = None if p.inp is None else Inputs(*(pinned(a) for a in (p.inp.f_ext, p.inp.tree_L, p.inp.tree_tau)))
+        p.ctx.step(p.hc, p.inp_h, dt=cfg.dt)          # warm the staging buffers
+        p.ctx.step(p.hca, p.inp_h, dt=cfg.dt)
+        p.ctx.step(p.hca, p.inp_h, dt=cfg.dt)
         p.out_host = {k: torch.empty(v.shape, dtype=torch.float32).pin_memory().numpy() for k, v in p.final.items()}
+        p.ctx.get_state_async(p.out_host)
+        p.ctx.get_state_async(p.out_host)
+        p.ctx.wait_async()
+        p.ctx.check()
         p.st_h = _lib.comfree_state(*[p.out_host[k].ctypes.data if p.out_host[k].size else None
                                       for k in ("pos", "quat", "vel", "omega", "qpos", "qvel")], _lib.MEM_HOST)
-        h2d += p.hc.h2d_bytes() + (0 if p.inp is None else sum(a.nbytes for a in (p.inp.f_ext, p.inp.tree_L, p.inp.tree_tau)
-                                                                if a is not None))
+        h2d += p.hc.h2d_bytes() + (0 if p.inp_h is None else sum(a.nbytes for a in (p.inp_h.f_ext, p.inp_h.tree_L,
+                                                                                    p.inp_h.tree_tau) if a is not None))
         d2h += sum(v.nbytes for v in p.out_host.values())
-    if world_size > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(e2e_steps):
+
+    def e2e_run(asynchronous):
+        if world_size > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(e2e_steps):
+            for p in parts:
+                if asynchronous:
+                    p.ctx.step(p.hca, p.inp_h, dt=cfg.dt, stream=stream)
+                    p.ctx.get_state_async(p.out_host, stream=stream)
+                else:
+                    p.ctx.step(p.hc, p.inp_h, dt=cfg.dt, stream=stream)
+                    rc = p.ctx._lib.comfree_get_state(p.ctx.h, 0, p.W, ct.byref(p.st_h), stream.cuda_stream)
+                    p.ctx._check(rc, "comfree_get_state")
+        if asynchronous:
+            for p in parts:
+                p.ctx.wait_async(stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
         for p in parts:
-            p.ctx.step(p.hc, p.inp, dt=cfg.dt, stream=stream)
-            rc = p.ctx._lib.comfree_get_state(p.ctx.h, 0, p.W, ct.byref(p.st_h), stream.cuda_stream)
-            p.ctx._check(rc, "comfree_get_state")
-    e1.record(stream)
-    torch.cuda.synchronize()
-    e2e_ms = reduce_max(e0.elapsed_time(e1), dev)
+            p.ctx.check(stream)                       # latched errors of the asynchronous calls
+        return reduce_max(e0.elapsed_time(e1), dev)
+    e2e_serial_ms = e2e_run(False)
+    e2e_ms = e2e_run(True)
     e2e_value = total_worlds * e2e_steps / (e2e_ms * 1e-3)
+    e2e_serial_value = total_worlds * e2e_steps / (e2e_serial_ms * 1e-3)
 
     cpu = None
     if rank == 0:                      # rank 0 only (the other ranks wait at the barrier)
@@ -698,7 +728,12 @@ def run_ours(args, rank, world_size, local):
                          "kernel": f"k_step (S1-S7 fused) [{dom.name}]", "algorithmic_bytes_per_launch": dom.alg_bytes},
             "clocks": clock.summary(),
             "e2e": {"value": e2e_value, "unit": "world-steps/s", "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "steps": e2e_steps},
+                    "d2h_bytes_per_step": d2h, "steps": e2e_steps,
+                    "mode": "pinned host buffers through comfree_step / comfree_get_state (COMFREE_MEM_HOST_ASYNC): "
+                            "step k+1's upload overlaps step k's kernel and download",
+                    "ms_per_step": e2e_ms / e2e_steps,
+                    "pcie_gbs": (h2d + d2h) / (e2e_ms / e2e_steps * 1e-3) / 1e9,
+                    "serial_value": e2e_serial_value, "serial_ms_per_step": e2e_serial_ms / e2e_steps},
             "cpu_baseline": cpu,
             "allgather_final_state_mb": gathered_mb,
             "sharded_verification": verification,

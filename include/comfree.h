@@ -67,7 +67,18 @@ typedef enum {
 } comfree_status;
 
 /* memory location of caller buffers */
-enum { COMFREE_MEM_DEVICE = 0, COMFREE_MEM_HOST = 1 };
+/* COMFREE_MEM_HOST_ASYNC: page-locked (pinned) HOST buffers, copied without
+ * synchronising.  comfree_step stages contacts and world inputs into one of
+ * two device slots over the context's copy-in stream (which first waits for
+ * the caller's stream to reach the call) and makes the caller's stream wait
+ * for the copies; comfree_get_state converts the state on the caller's stream
+ * and copies it out over the context's copy-out stream, without making the
+ * caller's stream wait.  So step k + 1's upload overlaps step k's kernel and
+ * download.  The caller keeps a step's input buffers unchanged, and reads the
+ * output buffers only after comfree_wait_async(ctx, stream) plus a
+ * synchronisation of `stream` (or comfree_check).  Errors surface at the next
+ * comfree_check / synchronising call.  Not with impulses, foff or n_device. */
+enum { COMFREE_MEM_DEVICE = 0, COMFREE_MEM_HOST = 1, COMFREE_MEM_HOST_ASYNC = 2 };
 
 /* comfree_config.flags */
 enum {
@@ -433,6 +444,11 @@ comfree_status comfree_segment_info(comfree_ctx* ctx, int64_t* off, int32_t* per
  * state), then clear them: COMFREE_OK when none.  A cheap check (one 4-byte
  * read) for loops that never call comfree_get_* (e.g. MPPI control steps). */
 comfree_status comfree_check(comfree_ctx* ctx, void* stream);
+
+/* Make `stream` wait (on the device, no host sync) for every copy the
+ * COMFREE_MEM_HOST_ASYNC path has enqueued so far, so that an event recorded
+ * on `stream` afterwards, or a synchronisation of `stream`, covers them. */
+comfree_status comfree_wait_async(comfree_ctx* ctx, void* stream);
 
 /* Instrumentation: while enabled, every comfree_step records CUDA events on
  * its own stream around the S0 kernels and around the fused step kernel. */

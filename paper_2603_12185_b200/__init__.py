@@ -21,7 +21,7 @@ import numpy as np
 
 from . import _lib
 from ._lib import (CONTACTS_SORTED, FLAG_DETERMINISTIC, FLAG_NO_FINITE_CHECK, FLAG_STATS,
-                   MEM_DEVICE, MEM_HOST)
+                   MEM_DEVICE, MEM_HOST, MEM_HOST_ASYNC)
 
 __all__ = ["Context", "DeviceContacts", "HostContacts", "ComfreeError", "make_config",
            "pack_c3", "pack_jrow", "FLAG_STATS", "FLAG_DETERMINISTIC", "FLAG_NO_FINITE_CHECK",
@@ -122,9 +122,14 @@ class HostContacts:
     jrow: object
     sorted: bool
     kd: object = None
+    asynchronous: bool = False             # COMFREE_MEM_HOST_ASYNC: pinned, copies overlap (comfree.h)
+    off: object = None                     # pinned int64 off[W+1] (pre-segmented; world ids not copied)
 
     @staticmethod
-    def from_arrays(contacts, pin: bool = True) -> "HostContacts":
+    def from_arrays(contacts, pin: bool = True, asynchronous: bool = False, n_worlds=None) -> "HostContacts":
+        """asynchronous (needs pin): the step's copies run on the context's own
+        streams and overlap the previous step; with n_worlds, off[W+1] is
+        passed instead of the world ids (the contacts must be sorted by world)."""
         torch = _torch()
 
         def host(a, dt):
@@ -133,19 +138,27 @@ class HostContacts:
                 t = torch.from_numpy(a).pin_memory()
                 return t
             return a
+        if asynchronous and not pin:
+            raise ValueError("asynchronous host contacts must be pinned")
         w = np.ascontiguousarray(contacts.world, np.int32)
         srt = bool(np.all(np.diff(w) >= 0)) if len(w) else True
-        return HostContacts(contacts.n, host(w, np.int32), host(contacts.c0, np.float32),
+        off = None
+        if n_worlds is not None:
+            if not srt:
+                raise ValueError("off[] needs contacts sorted by world")
+            off = host(np.searchsorted(w, np.arange(n_worlds + 1)).astype(np.int64), np.int64)
+        return HostContacts(contacts.n, None if off is not None else host(w, np.int32), host(contacts.c0, np.float32),
                             host(contacts.c1, np.float32), host(contacts.c2, np.float32),
                             host(pack_c3(contacts.body_a, contacts.body_b, contacts.mu_rol,
                                          contacts.condim), np.int32),
                             None if contacts.jrow is None else host(pack_jrow(contacts.jrow), np.float32),
                             srt,
-                            None if getattr(contacts, "kd", None) is None else host(contacts.kd, np.float32))
+                            None if getattr(contacts, "kd", None) is None else host(contacts.kd, np.float32),
+                            asynchronous, off)
 
     def h2d_bytes(self) -> int:
         tot = 0
-        for a in (self.world, self.c0, self.c1, self.c2, self.c3, self.jrow, self.kd):
+        for a in (self.world, self.off, self.c0, self.c1, self.c2, self.c3, self.jrow, self.kd):
             if a is not None:
                 tot += a.nbytes if isinstance(a, np.ndarray) else a.numel() * a.element_size()
         return tot
@@ -329,7 +342,10 @@ class Context:
         ``foff``: optional output buffers of the same location."""
         nw = self.n_worlds - first_world if n_worlds is None else int(n_worlds)
         host = isinstance(contacts, HostContacts)
-        loc = MEM_HOST if host else MEM_DEVICE
+        asyn = host and contacts.asynchronous
+        loc = MEM_HOST_ASYNC if asyn else (MEM_HOST if host else MEM_DEVICE)
+        if host and off is None and contacts.off is not None:
+            off = contacts.off
         srt = contacts.sorted if sorted_hint is None else sorted_hint
         cap = 0
         if impulses is not None:
@@ -345,7 +361,7 @@ class Context:
         if inputs is not None:
             arrs = [getattr(inputs, k, None) for k in ("f_ext", "tree_L", "tree_tau")]
             if any(isinstance(a, np.ndarray) for a in arrs):
-                wloc = MEM_HOST
+                wloc = MEM_HOST_ASYNC if asyn else MEM_HOST
                 arrs = [None if a is None else np.ascontiguousarray(a, np.float32) for a in arrs]
             fe, tl, tt = arrs
         w = _lib.comfree_worlds(int(first_world), nw, _ptr(fe), _ptr(tl), _ptr(tt), wloc)
@@ -366,6 +382,20 @@ class Context:
         self._check(self._lib.comfree_get_state(self.h, int(first_world), nw, ct.byref(st),
                                                 _stream_handle(stream)), "comfree_get_state")
         return out
+
+    def get_state_async(self, out: dict, first_world: int = 0, n_worlds: Optional[int] = None, stream=None):
+        """comfree_get_state into caller-owned PINNED host arrays without
+        synchronising (COMFREE_MEM_HOST_ASYNC): valid after wait_async(stream)
+        and a synchronisation of `stream`."""
+        nw = self.n_worlds - first_world if n_worlds is None else int(n_worlds)
+        st = _lib.comfree_state(*[out[k].ctypes.data if out.get(k) is not None and out[k].size else None
+                                  for k in ("pos", "quat", "vel", "omega", "qpos", "qvel")], MEM_HOST_ASYNC)
+        self._check(self._lib.comfree_get_state(self.h, int(first_world), nw, ct.byref(st),
+                                                _stream_handle(stream)), "comfree_get_state")
+
+    def wait_async(self, stream=None):
+        """comfree_wait_async: `stream` waits for the asynchronous host copies."""
+        self._check(self._lib.comfree_wait_async(self.h, _stream_handle(stream)), "comfree_wait_async")
 
     def get_state_device(self, out: dict, first_world: int = 0, n_worlds: Optional[int] = None, stream=None):
         """comfree_get_state into caller-owned device tensors (async)."""

@@ -19,7 +19,7 @@ if os.environ.get("COMFREE_LIB"):
 COMFREE_OK = 0
 STATUS_NAMES = {0: "OK", 1: "ERR_INVALID_ARGUMENT", 2: "ERR_VALIDATION", 3: "ERR_CAPACITY",
                 4: "ERR_NONFINITE", 5: "ERR_CUDA", 6: "ERR_STATE"}
-MEM_DEVICE, MEM_HOST = 0, 1
+MEM_DEVICE, MEM_HOST, MEM_HOST_ASYNC = 0, 1, 2
 FLAG_STATS, FLAG_DETERMINISTIC, FLAG_NO_FINITE_CHECK, FLAG_EXACT_DIAGONAL, FLAG_FACET_DIAGONAL = 1, 2, 4, 8, 16
 CONTACTS_SORTED = 1
 
@@ -118,6 +118,7 @@ SIGNATURES = {
     "comfree_set_timing": (ct.c_int, [P, ct.c_int]),
     "comfree_get_timing": (ct.c_int, [P, ct.POINTER(ct.c_double)]),
     "comfree_check": (ct.c_int, [P, P]),
+    "comfree_wait_async": (ct.c_int, [P, P]),
     "comfree_kernel_launches": (ct.c_int64, [P]),
     "comfree_destroy": (None, [P]),
     "comfree_last_error": (ct.c_char_p, [P]),

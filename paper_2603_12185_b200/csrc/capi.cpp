@@ -63,6 +63,15 @@ struct comfree_ctx {
   // host-input staging
   DevBuf in_world, in_off, in_c0, in_c1, in_c2, in_c3, in_jrow, in_kd, in_fext, in_L, in_tau, imp;
   DevBuf st_tmp;
+  // COMFREE_MEM_HOST_ASYNC: two staging slots, a copy-in and a copy-out stream
+  struct AsyncSlot {
+    DevBuf world, off, c0, c1, c2, c3, jrow, kd, fext, L, tau, out;
+  } aslot[2];
+  int a_in = 0, a_out = 0;               // next slot of comfree_step / comfree_get_state
+  cudaStream_t s_h2d = nullptr, s_h2d2 = nullptr, s_d2h = nullptr;  // two copy-in streams (two copy engines)
+  cudaEvent_t ev_h2d2[2] = {nullptr, nullptr};
+  cudaEvent_t ev_entry = nullptr, ev_h2d[2] = {nullptr, nullptr}, ev_conv[2] = {nullptr, nullptr},
+              ev_d2h[2] = {nullptr, nullptr};
   // articulated upstream: device copy of the chain model (comfree_load_articulation)
   DevBuf art;
   bool art_loaded = false;
@@ -123,6 +132,22 @@ void directions(int n, float2* out) {
   }
 }
 
+// Lazily created streams / events of the asynchronous host path.
+cudaError_t async_init(comfree_ctx* ctx) {
+  if (ctx->s_h2d) return cudaSuccess;
+  cudaError_t e = cudaStreamCreateWithFlags(&ctx->s_h2d, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->s_h2d2, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->s_d2h, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_entry, cudaEventDisableTiming);
+  for (int k = 0; k < 2 && e == cudaSuccess; ++k) {
+    e = cudaEventCreateWithFlags(&ctx->ev_h2d[k], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_h2d2[k], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_conv[k], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->ev_d2h[k], cudaEventDisableTiming);
+  }
+  return e;
+}
+
 comfree_status check_latched(comfree_ctx* ctx, cudaStream_t s) {
   CUDA_TRY(ctx, cudaStreamSynchronize(s));
   int e = 0;
@@ -160,6 +185,7 @@ comfree_status stage(comfree_ctx* ctx, DevBuf& buf, const T* src, size_t count, 
     return COMFREE_OK;
   }
   CUDA_TRY(ctx, ensure(buf, count * sizeof(T)));
+  // HOST_ASYNC: s is the context's copy-in stream, buf the step's staging slot
   CUDA_TRY(ctx, cudaMemcpyAsync(buf.p, src, count * sizeof(T), cudaMemcpyHostToDevice, s));
   *out = static_cast<const T*>(buf.p);
   return COMFREE_OK;
@@ -406,7 +432,13 @@ comfree_status comfree_step(comfree_ctx* ctx, const comfree_worlds* wd, const co
   if (n > 0 && !c->off && !c->world) return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "step: world[] or off[] required");
   const cf::SceneDev& sc = ctx->sc;
   if (sc.T > 0 && nw > 0 && (!wd->tree_L || !wd->tree_tau)) return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "step: chains need tree_L and tree_tau");
-  if (c->location != COMFREE_MEM_DEVICE && c->location != COMFREE_MEM_HOST) return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "step: bad contacts location");
+  if (c->location != COMFREE_MEM_DEVICE && c->location != COMFREE_MEM_HOST && c->location != COMFREE_MEM_HOST_ASYNC)
+    return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "step: bad contacts location");
+  if ((c->location == COMFREE_MEM_HOST_ASYNC) != (wd->location == COMFREE_MEM_HOST_ASYNC) &&
+      !(c->location == COMFREE_MEM_HOST_ASYNC && !wd->f_ext && !wd->tree_L && !wd->tree_tau))
+    return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "step: HOST_ASYNC contacts and world inputs go together");
+  if (c->location == COMFREE_MEM_HOST_ASYNC && (c->impulses || c->foff || c->n_device))
+    return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "step: HOST_ASYNC takes no impulses / foff / n_device");
   if (c->impulses && c->impulses_capacity < 0) return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "step: impulses_capacity");
   if (c->n_device && (!(c->flags & COMFREE_CONTACTS_SORTED) || !c->world || c->off || c->impulses || c->foff ||
                       c->location != COMFREE_MEM_DEVICE))
@@ -414,8 +446,26 @@ comfree_status comfree_step(comfree_ctx* ctx, const comfree_worlds* wd, const co
                 "step: n_device needs sorted DEVICE contacts with world[] and no off[] / impulses / foff");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   CUDA_TRY(ctx, cudaSetDevice(ctx->device));
-  const int loc = c->location;
-  const bool host_io = (loc == COMFREE_MEM_HOST) || (wd->location == COMFREE_MEM_HOST);
+  const bool async_io = c->location == COMFREE_MEM_HOST_ASYNC;
+  const int loc = async_io ? COMFREE_MEM_HOST : c->location;
+  const bool host_io = !async_io && ((loc == COMFREE_MEM_HOST) || (wd->location == COMFREE_MEM_HOST));
+  // HOST_ASYNC: the inputs go to staging slot a_in over the copy-in stream,
+  // which first waits for the caller's stream to reach this call (so slot
+  // a_in's previous user, two steps back, has finished with it); the caller's
+  // stream then waits for the copies, and the call returns without a sync.
+  cudaStream_t s_stage = s;
+  comfree_ctx::AsyncSlot* as = nullptr;
+  int aslot = 0;
+  if (async_io) {
+    CUDA_TRY(ctx, async_init(ctx));
+    aslot = ctx->a_in;
+    ctx->a_in ^= 1;
+    as = &ctx->aslot[aslot];
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_entry, s));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->s_h2d, ctx->ev_entry, 0));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->s_h2d2, ctx->ev_entry, 0));
+    s_stage = ctx->s_h2d;
+  }
 
   // ---- stage inputs ----
   const int32_t* world = nullptr;
@@ -423,20 +473,39 @@ comfree_status comfree_step(comfree_ctx* ctx, const comfree_worlds* wd, const co
   const float *c0 = nullptr, *c1 = nullptr, *c2 = nullptr, *jrow = nullptr;
   const int32_t* c3 = nullptr;
   comfree_status st;
-  if ((st = stage(ctx, ctx->in_world, c->off ? nullptr : c->world, (size_t)n, loc, s, &world)) != COMFREE_OK) return st;
-  if ((st = stage(ctx, ctx->in_off, c->off, (size_t)nw + 1, loc, s, &off_in)) != COMFREE_OK) return st;
-  if ((st = stage(ctx, ctx->in_c0, c->c0, (size_t)n * 4, loc, s, &c0)) != COMFREE_OK) return st;
-  if ((st = stage(ctx, ctx->in_c1, c->c1, (size_t)n * 4, loc, s, &c1)) != COMFREE_OK) return st;
-  if ((st = stage(ctx, ctx->in_c2, c->c2, (size_t)n * 4, loc, s, &c2)) != COMFREE_OK) return st;
-  if ((st = stage(ctx, ctx->in_c3, c->c3, (size_t)n * 4, loc, s, &c3)) != COMFREE_OK) return st;
-  if ((st = stage(ctx, ctx->in_jrow, c->jrow, (size_t)n * 48, loc, s, &jrow)) != COMFREE_OK) return st;
+  DevBuf& b_world = as ? as->world : ctx->in_world;
+  DevBuf& b_off = as ? as->off : ctx->in_off;
+  DevBuf& b_c0 = as ? as->c0 : ctx->in_c0;
+  DevBuf& b_c1 = as ? as->c1 : ctx->in_c1;
+  DevBuf& b_c2 = as ? as->c2 : ctx->in_c2;
+  DevBuf& b_c3 = as ? as->c3 : ctx->in_c3;
+  DevBuf& b_jrow = as ? as->jrow : ctx->in_jrow;
+  DevBuf& b_kd = as ? as->kd : ctx->in_kd;
+  DevBuf& b_fext = as ? as->fext : ctx->in_fext;
+  DevBuf& b_L = as ? as->L : ctx->in_L;
+  DevBuf& b_tau = as ? as->tau : ctx->in_tau;
+  if ((st = stage(ctx, b_world, c->off ? nullptr : c->world, (size_t)n, loc, s_stage, &world)) != COMFREE_OK) return st;
+  if ((st = stage(ctx, b_off, c->off, (size_t)nw + 1, loc, s_stage, &off_in)) != COMFREE_OK) return st;
+  if ((st = stage(ctx, b_c0, c->c0, (size_t)n * 4, loc, s_stage, &c0)) != COMFREE_OK) return st;
+  if ((st = stage(ctx, b_c1, c->c1, (size_t)n * 4, loc, s_stage, &c1)) != COMFREE_OK) return st;
+  // streams c2, c3 over the second copy-in stream (a second copy engine)
+  cudaStream_t s_stage2 = async_io ? ctx->s_h2d2 : s;
+  if ((st = stage(ctx, b_c2, c->c2, (size_t)n * 4, loc, s_stage2, &c2)) != COMFREE_OK) return st;
+  if ((st = stage(ctx, b_c3, c->c3, (size_t)n * 4, loc, s_stage2, &c3)) != COMFREE_OK) return st;
+  if ((st = stage(ctx, b_jrow, c->jrow, (size_t)n * 48, loc, s_stage, &jrow)) != COMFREE_OK) return st;
   const float* kdp = nullptr;
-  if ((st = stage(ctx, ctx->in_kd, c->kd, (size_t)n * 2, loc, s, &kdp)) != COMFREE_OK) return st;
+  if ((st = stage(ctx, b_kd, c->kd, (size_t)n * 2, loc, s_stage, &kdp)) != COMFREE_OK) return st;
   const float *fext = nullptr, *tL = nullptr, *ttau = nullptr;
-  const int wloc = wd->location;
-  if ((st = stage(ctx, ctx->in_fext, wd->f_ext, (size_t)nw * sc.B * 6, wloc, s, &fext)) != COMFREE_OK) return st;
-  if ((st = stage(ctx, ctx->in_L, sc.T ? wd->tree_L : nullptr, (size_t)nw * sc.T * 10, wloc, s, &tL)) != COMFREE_OK) return st;
-  if ((st = stage(ctx, ctx->in_tau, sc.T ? wd->tree_tau : nullptr, (size_t)nw * sc.Q, wloc, s, &ttau)) != COMFREE_OK) return st;
+  const int wloc = async_io ? COMFREE_MEM_HOST : wd->location;
+  if ((st = stage(ctx, b_fext, wd->f_ext, (size_t)nw * sc.B * 6, wloc, s_stage, &fext)) != COMFREE_OK) return st;
+  if ((st = stage(ctx, b_L, sc.T ? wd->tree_L : nullptr, (size_t)nw * sc.T * 10, wloc, s_stage, &tL)) != COMFREE_OK) return st;
+  if ((st = stage(ctx, b_tau, sc.T ? wd->tree_tau : nullptr, (size_t)nw * sc.Q, wloc, s_stage, &ttau)) != COMFREE_OK) return st;
+  if (async_io) {
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_h2d[aslot], ctx->s_h2d));
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_h2d2[aslot], ctx->s_h2d2));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_h2d[aslot], 0));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_h2d2[aslot], 0));
+  }
 
   // ---- S0: segmentation ----
   const int64_t* off = off_in;
@@ -628,6 +697,32 @@ static comfree_status get_state_impl(comfree_ctx* ctx, int64_t first, int64_t nw
                                      cudaStream_t s) {
   const cf::SceneDev& sc = ctx->sc;
   const float* src = ctx->slab + (size_t)first * sc.slab;
+  if (out->location == COMFREE_MEM_HOST_ASYNC) {
+    // public layout into staging slot a_out on the caller's stream (after that
+    // slot's previous copy-out), then copied out on the copy-out stream; the
+    // caller's stream does not wait for the copy (comfree_wait_async)
+    CUDA_TRY(ctx, async_init(ctx));
+    const int k = ctx->a_out;
+    ctx->a_out ^= 1;
+    const size_t nb = (size_t)nw * sc.B, nq = (size_t)nw * sc.Q;
+    CUDA_TRY(ctx, ensure(ctx->aslot[k].out, std::max<size_t>(1, nb * 13 + nq * 2) * sizeof(float)));
+    float* d = static_cast<float*>(ctx->aslot[k].out.p);
+    float* dp[6] = {d, d + 3 * nb, d + 7 * nb, d + 10 * nb, d + 13 * nb, d + 13 * nb + nq};
+    float* hp[6] = {out->pos, out->quat, out->vel, out->omega, out->qpos, out->qvel};
+    const size_t cnt[6] = {3 * nb, 4 * nb, 3 * nb, 3 * nb, nq, nq};
+    CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_d2h[k], 0));
+    CUDA_TRY(ctx, cf::launch_slab_to_public(src, nw, sc, hp[0] ? dp[0] : nullptr, hp[1] ? dp[1] : nullptr,
+                                            hp[2] ? dp[2] : nullptr, hp[3] ? dp[3] : nullptr,
+                                            hp[4] ? dp[4] : nullptr, hp[5] ? dp[5] : nullptr, s));
+    ctx->launches += 1;
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_conv[k], s));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_conv[k], 0));
+    for (int q = 0; q < 6; ++q)
+      if (hp[q] && cnt[q])
+        CUDA_TRY(ctx, cudaMemcpyAsync(hp[q], dp[q], cnt[q] * sizeof(float), cudaMemcpyDeviceToHost, ctx->s_d2h));
+    CUDA_TRY(ctx, cudaEventRecord(ctx->ev_d2h[k], ctx->s_d2h));
+    return COMFREE_OK;
+  }
   if (out->location == COMFREE_MEM_DEVICE) {
     CUDA_TRY(ctx, cf::launch_slab_to_public(src, nw, sc, out->pos, out->quat, out->vel, out->omega, out->qpos, out->qvel, s));
     ctx->launches += 1;
@@ -657,7 +752,21 @@ comfree_status comfree_get_state(comfree_ctx* ctx, int64_t first, int64_t nw, co
   CUDA_TRY(ctx, cudaSetDevice(ctx->device));
   comfree_status st = get_state_impl(ctx, first, nw, out, s);
   if (st != COMFREE_OK) return st;
+  if (out->location == COMFREE_MEM_HOST_ASYNC) return COMFREE_OK;  // errors surface at comfree_check
   return check_latched(ctx, s);
+}
+
+comfree_status comfree_wait_async(comfree_ctx* ctx, void* stream) {
+  if (!ctx) return COMFREE_ERR_INVALID_ARGUMENT;
+  if (!ctx->s_h2d) return COMFREE_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  for (int k = 0; k < 2; ++k) {
+    CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_h2d[k], 0));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_h2d2[k], 0));
+    CUDA_TRY(ctx, cudaStreamWaitEvent(s, ctx->ev_d2h[k], 0));
+  }
+  return COMFREE_OK;
 }
 
 comfree_status comfree_load_articulation(comfree_ctx* ctx, const comfree_articulation* a) {
@@ -1057,6 +1166,16 @@ void comfree_destroy(comfree_ctx* ctx) {
   if (ctx->d_err) cudaFree(ctx->d_err);
   if (ctx->d_first_bad) cudaFree(ctx->d_first_bad);
   if (ctx->d_queue) cudaFree(ctx->d_queue);
+  for (auto& sl : ctx->aslot)
+    for (DevBuf* b : {&sl.world, &sl.off, &sl.c0, &sl.c1, &sl.c2, &sl.c3, &sl.jrow, &sl.kd, &sl.fext, &sl.L, &sl.tau, &sl.out})
+      if (b->p) cudaFree(b->p);
+  if (ctx->s_h2d) cudaStreamDestroy(ctx->s_h2d);
+  if (ctx->s_d2h) cudaStreamDestroy(ctx->s_d2h);
+  if (ctx->s_h2d2) cudaStreamDestroy(ctx->s_h2d2);
+  for (cudaEvent_t e : {ctx->ev_entry, ctx->ev_h2d[0], ctx->ev_h2d[1], ctx->ev_h2d2[0], ctx->ev_h2d2[1],
+                        ctx->ev_conv[0], ctx->ev_conv[1],
+                        ctx->ev_d2h[0], ctx->ev_d2h[1]})
+    if (e) cudaEventDestroy(e);
   delete ctx;
 }
 

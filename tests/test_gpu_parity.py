@@ -588,3 +588,36 @@ def test_persistent_kernel_variants_bit_identical(mode, monkeypatch):
         g = gpu_step(CFG, scene, st, c, None, impulses=False)
         for k in ("pos", "quat", "vel", "omega"):
             np.testing.assert_array_equal(getattr(g["state"], k), getattr(ref["state"], k))
+
+
+def test_async_host_pipeline_matches_device_path():
+    """COMFREE_MEM_HOST_ASYNC (pinned host buffers, the e2e pipeline): three
+    steps, each state copied out asynchronously into its own pinned buffers,
+    equal the device path's per-step states bit for bit; the copies of step
+    k + 1 overlap step k (two staging slots, include/comfree.h)."""
+    import torch
+    import paper_2603_12185_b200 as cf
+    scene, st, c = scenes.c4_pile(n_worlds=9, contacts_per_world=700)
+    ref = cf.Context(CFG)
+    ref.load_scene(scene, 9, st)
+    dc = cf.DeviceContacts.from_host(c)
+    want = []
+    for _ in range(3):
+        ref.step(dc, None)
+        want.append(ref.get_state())
+    ctx = cf.Context(CFG)
+    ctx.load_scene(scene, 9, st)
+    hca = cf.HostContacts.from_arrays(c, pin=True, asynchronous=True, n_worlds=9)
+    outs = []
+    s = torch.cuda.Stream()
+    for _ in range(3):
+        ctx.step(hca, None, stream=s)
+        o = {k: torch.empty(v.shape, dtype=torch.float32).pin_memory().numpy() for k, v in want[0].items()}
+        ctx.get_state_async(o, stream=s)
+        outs.append(o)
+    ctx.wait_async(s)
+    s.synchronize()
+    ctx.check(s)
+    for o, w in zip(outs, want):
+        for k in ("pos", "quat", "vel", "omega"):
+            np.testing.assert_array_equal(o[k], w[k])
