@@ -33,8 +33,26 @@ t1 = (1 + s n_x^2 a, s b, -s n_x).
                  signed face distance s = max_i (|c_i| - h_i) in g1's frame is below
                  the margin and lies within the other two face extents emits on
                  that face of g1 (n = sign(c_i) e_i, phi = s, p = corner - phi n/2),
-                 then the corners of g1 against g2 (normal negated); edge-edge
-                 contacts are not generated
+                 then the corners of g1 against g2 (normal negated); then edge-edge
+                 (reading R33): the separating-axis test over the 15 axes (face
+                 normals of g1, of g2, then the 9 edge cross products e1_i x e2_j,
+                 i-major, skipped when |e1_i x e2_j| <= 1e-6) gives the overlap
+                 o(L) = r1(L) + r2(L) - |L . (x2 - x1)|, r_b(L) = sum_k h_bk |L . R_b e_k|;
+                 when the first axis of minimum overlap is an edge axis and
+                 -o < margin, one contact: n = L oriented from g1 to g2, phi = -o,
+                 p = the midpoint of the closest points (Ericson 5.1.9) of g1's edge
+                 along e1_i through its support point in direction n and g2's edge
+                 along e2_j through its support point in direction -n
+
+Broadphase (reading R32, geometry without a candidate list): the candidates of
+a world are every geom pair (g1 < g2, planes first in the geom list) whose geoms
+are not on the same body / chain and not both static, and whose world AABBs,
+grown by margin/2 on every side, overlap on all three axes (closed intervals);
+a plane g1 is a candidate with g2 when g2's grown AABB reaches below
+offset + margin/2 along the plane normal.  AABBs: sphere c +- R; box
+x +- |R| h (element-wise |R|); capsule: the two end points +- R.  Candidate
+order: (g1, g2) lexicographic.  Any pair with a contact (phi < margin) is a
+candidate (the grown AABBs of two geoms within the margin overlap).
 """
 from __future__ import annotations
 
@@ -149,9 +167,91 @@ def _box_corners_on(RA, xA, hA, RB, xB, hB, margin, flip):
     return out
 
 
-def pair_contacts(geo, pi, state, w, art):
-    """Contacts of candidate pair pi in world w: list of (p, phi, n, body_a, body_b, link_a, link_b)."""
-    g1, g2 = int(geo.pairs[pi, 0]), int(geo.pairs[pi, 1])
+def _box_edge_edge(RA, xA, hA, RB, xB, hB, margin):
+    """Reading R33: one edge-edge contact of boxes A (g1) and B (g2) when the
+    separating-axis test's first minimum-overlap axis is an edge cross product."""
+    d = xB - xA
+    axes = [RA[:, i] for i in range(3)] + [RB[:, j] for j in range(3)]
+    kinds = [None] * 6
+    for i in range(3):
+        for j in range(3):
+            L = np.cross(RA[:, i], RB[:, j])
+            nl = float(np.linalg.norm(L))
+            if nl <= 1e-6:
+                continue
+            axes.append(L / nl)
+            kinds.append((i, j))
+    best, bo = None, None
+    for k, L in enumerate(axes):
+        rA = sum(hA[m] * abs(float(L @ RA[:, m])) for m in range(3))
+        rB = sum(hB[m] * abs(float(L @ RB[:, m])) for m in range(3))
+        o = rA + rB - abs(float(L @ d))
+        if bo is None or o < bo:
+            best, bo = k, o
+    if kinds[best] is None or not (-bo < margin):
+        return []
+    i, j = kinds[best]
+    n = axes[best] if float(axes[best] @ d) >= 0.0 else -axes[best]
+    # support points: A towards +n, B towards -n; the edges through them
+    pa = xA + sum((1.0 if float(n @ RA[:, m]) >= 0.0 else -1.0) * hA[m] * RA[:, m] for m in range(3) if m != i)
+    pb = xB - sum((1.0 if float(n @ RB[:, m]) >= 0.0 else -1.0) * hB[m] * RB[:, m] for m in range(3) if m != j)
+    c1, c2 = _closest_segments(pa - hA[i] * RA[:, i], pa + hA[i] * RA[:, i], pb - hB[j] * RB[:, j],
+                               pb + hB[j] * RB[:, j])
+    return [(0.5 * (c1 + c2), -bo, n)]
+
+
+def aabb(geo, g, state, w, art):
+    """World AABB (lo, hi) of geom g, grown by margin/2 (reading R32); planes: None."""
+    k = int(geo.kind[g])
+    if k == PLANE:
+        return None
+    R, x = geom_frame(geo, g, state, w, art)
+    if k == SPHERE:
+        e = np.full(3, float(geo.size[g, 0]))
+        lo, hi = x - e, x + e
+    elif k == BOX:
+        e = np.abs(R) @ np.asarray(geo.size[g], float)
+        lo, hi = x - e, x + e
+    else:
+        a, b = _segment(geo, g, state, w, art)
+        r = float(geo.size[g, 0])
+        lo, hi = np.minimum(a, b) - r, np.maximum(a, b) + r
+    m = 0.5 * geo.margin
+    return lo - m, hi + m
+
+
+def _same_owner(geo, g1, g2):
+    b1, b2 = int(geo.body[g1]), int(geo.body[g2])
+    return b1 == b2                    # same free body, both static (-1), or the same chain
+
+
+def broadphase(geo, state, w, art=None):
+    """Candidate pairs of world w by the definition of reading R32 (every pair
+    tested, no acceleration structure): list of (g1, g2), lexicographic."""
+    G = len(geo.kind)
+    kind = np.asarray(geo.kind)
+    boxes = [aabb(geo, g, state, w, art) for g in range(G)]
+    lo = np.array([b[0] if b is not None else np.zeros(3) for b in boxes])
+    hi = np.array([b[1] if b is not None else np.zeros(3) for b in boxes])
+    plane = kind == PLANE
+    body = np.asarray(geo.body)
+    # every pair (g1 < g2): grown AABBs overlap on all three axes
+    ov = np.all((lo[:, None, :] <= hi[None, :, :]) & (lo[None, :, :] <= hi[:, None, :]), axis=2)
+    # plane g1: g2's grown AABB reaches below offset + margin/2 along the normal
+    for g1 in np.nonzero(plane)[0]:
+        n = np.asarray(geo.size[g1], float)
+        c, e = 0.5 * (lo + hi), 0.5 * (hi - lo)
+        ov[g1] = (c @ n - e @ np.abs(n) - float(geo.local[g1, 0])) < 0.5 * geo.margin
+    ok = ov & (body[:, None] != body[None, :]) & ~plane[None, :]
+    ok &= np.triu(np.ones((G, G), bool), 1)
+    ok[~plane[:, None] & plane[None, :]] = False
+    return [(int(a), int(b)) for a, b in zip(*np.nonzero(ok))]
+
+
+def pair_contacts(geo, pi, state, w, art, g12=None):
+    """Contacts of candidate pair pi (or the geom pair g12) in world w: list of
+    (p, phi, n, body_a, body_b, link_a, link_b)."""
+    g1, g2 = g12 if g12 is not None else (int(geo.pairs[pi, 0]), int(geo.pairs[pi, 1]))
     k1, k2 = int(geo.kind[g1]), int(geo.kind[g2])
     ba, bb = int(geo.body[g1]), int(geo.body[g2])
     la = int(geo.link[g1]) if ba < -1 else 0
@@ -200,6 +300,7 @@ def pair_contacts(geo, pi, state, w, art):
         hA, hB = np.asarray(geo.size[g1], float), np.asarray(geo.size[g2], float)
         out += _box_corners_on(RA, xA, hA, RB, xB, hB, m, False)
         out += _box_corners_on(RB, xB, hB, RA, xA, hA, m, True)
+        out += _box_edge_edge(RA, xA, hA, RB, xB, hB, m)
     elif k1 == PLANE:
         n = np.asarray(geo.size[g1], float)
         off = float(geo.local[g1, 0])
@@ -247,9 +348,11 @@ def collide(geo, state, art=None):
     harness.types.Contacts (fp64 records) with meta['link'] (C,2)."""
     from harness.types import Contacts
     rows = []
+    bp = geo.pairs is None or len(geo.pairs) == 0       # broadphase mode (reading R32)
     for w in range(state.n_worlds):
-        for pi in range(geo.pairs.shape[0]):
-            for rec in pair_contacts(geo, pi, state, w, art):
+        cands = broadphase(geo, state, w, art) if bp else [(int(a), int(b)) for a, b in geo.pairs]
+        for g12 in cands:
+            for rec in pair_contacts(geo, None, state, w, art, g12=g12):
                 rows.append((w,) + rec)
     n = len(rows)
     c0, c1, c2 = np.zeros((n, 4)), np.zeros((n, 4)), np.zeros((n, 4))

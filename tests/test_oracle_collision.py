@@ -158,3 +158,154 @@ def test_box_on_box_vertex_face():
     assert c2.n == 4
     np.testing.assert_allclose(c2.c1[:, :3], np.tile((0, 0, -1.0), (4, 1)), atol=1e-15)
     np.testing.assert_allclose(sorted(c2.c0[:, 3]), sorted(c.c0[:, 3]), atol=1e-15)
+
+
+# ---------------------------------------------------------------- broadphase (reading R32)
+def _random_geometry(seed, n=12, with_plane=True, margin=0.01):
+    from harness.types import Geometry
+    rng = np.random.default_rng(seed)
+    kind, body, size, local = [], [], [], []
+    if with_plane:
+        kind.append(co.PLANE); body.append(-1); size.append((0.0, 0.0, 1.0)); local.append((0.0, 0, 0))
+    for i in range(n):
+        k = int(rng.integers(0, 3))
+        kk = [co.SPHERE, co.BOX, co.CAPSULE][k]
+        kind.append(kk)
+        body.append(i)
+        size.append((rng.uniform(0.01, 0.03), 0, 0) if kk == co.SPHERE else
+                    tuple(rng.uniform(0.008, 0.03, 3)) if kk == co.BOX else (rng.uniform(0.008, 0.02), rng.uniform(0.005, 0.03), 0))
+        local.append((0.0, 0.0, 0.0))
+    G = len(kind)
+    return Geometry(np.array(kind, np.int32), np.array(body, np.int32), np.zeros(G, np.int32), np.array(size, float),
+                    np.array(local, float), None, margin=margin, mu=(0.7, 0.01, 0.001), condim=3)
+
+
+def _random_poses(seed, W, B, spread=0.08):
+    from harness.types import State
+    rng = np.random.default_rng(seed + 100)
+    pos = rng.uniform([-spread, -spread, 0.0], [spread, spread, spread], (W, B, 3))
+    quat = rng.normal(size=(W, B, 4))
+    quat /= np.linalg.norm(quat, axis=2, keepdims=True)
+    z = np.zeros((W, B, 3))
+    return State(pos, quat, z, z.copy(), np.zeros((W, 0)), np.zeros((W, 0)))
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_broadphase_loses_no_contact(seed):
+    """Conservativeness (R32): the contacts of the broadphase candidates equal
+    those of every valid pair tested explicitly (same records, same order)."""
+    from harness.types import Geometry
+    geo = _random_geometry(seed)
+    st = _random_poses(seed, 3, 12)
+    G = len(geo.kind)
+    allp = [(a, b) for a in range(G) for b in range(a + 1, G)
+            if geo.body[a] != geo.body[b] and geo.kind[b] != co.PLANE]
+    full = Geometry(geo.kind, geo.body, geo.link, geo.size, geo.local, np.array(allp, np.int32),
+                    margin=geo.margin, mu=geo.mu, condim=geo.condim)
+    a, b = co.collide(geo, st, None), co.collide(full, st, None)
+    assert b.n > 10                                   # the scenes have contacts of several kinds
+    np.testing.assert_array_equal(a.world, b.world)
+    np.testing.assert_array_equal(a.body_a, b.body_a)
+    np.testing.assert_array_equal(a.body_b, b.body_b)
+    np.testing.assert_array_equal(a.c0, b.c0)
+    np.testing.assert_array_equal(a.c1, b.c1)
+    # and the broadphase prunes: fewer candidates than pairs
+    assert all(len(co.broadphase(geo, st, w)) < len(allp) for w in range(3))
+
+
+def test_aabb_matches_brute_force_extremes():
+    """Box AABB = min / max over its 8 corners; capsule AABB = ends +- R
+    (checked against points sampled on the capsule surface); both grown by
+    margin / 2."""
+    geo = _random_geometry(5, n=20, with_plane=False, margin=0.004)
+    st = _random_poses(5, 1, 20)
+    rng = np.random.default_rng(9)
+    for g in range(20):
+        lo, hi = co.aabb(geo, g, st, 0, None)
+        R, x = co.geom_frame(geo, g, st, 0, None)
+        k = int(geo.kind[g])
+        if k == co.BOX:
+            h = geo.size[g]
+            pts = np.array([x + R @ (np.array([sx, sy, sz]) * h) for sx in (-1, 1) for sy in (-1, 1) for sz in (-1, 1)])
+            np.testing.assert_allclose(lo + 0.002, pts.min(0), atol=1e-15)
+            np.testing.assert_allclose(hi - 0.002, pts.max(0), atol=1e-15)
+        elif k == co.CAPSULE:
+            r, hl = geo.size[g, 0], geo.size[g, 1]
+            u = rng.normal(size=(20000, 3))
+            u /= np.linalg.norm(u, axis=1, keepdims=True)
+            ax = R[:, 2]
+            ends = np.concatenate([x + hl * ax + r * u, x - hl * ax + r * u])
+            assert np.all(ends >= lo + 0.002 - 1e-12) and np.all(ends <= hi - 0.002 + 1e-12)
+            np.testing.assert_allclose(ends.min(0), lo + 0.002, atol=2e-4 * r / 0.01)
+            np.testing.assert_allclose(ends.max(0), hi - 0.002, atol=2e-4 * r / 0.01)
+
+
+def test_pile_broadphase_covers_the_lattice_neighbours():
+    """Config-4 pile: every lattice-neighbour pair with a contact (the round-1
+    fixed candidate list) is a broadphase candidate."""
+    scene, st, _ = scenes.c4_pile(n_worlds=1, contacts_per_world=2000)
+    geo = scenes.pile_geometry((10, 10, 5))
+    so = st.astype(np.float64)
+    with_contacts = {(int(a), int(b)) for a, b in geo.pairs
+                     if co.pair_contacts(geo, None, so, 0, None, g12=(int(a), int(b)))}
+    geo.pairs = None
+    cand = set(co.broadphase(geo, so, 0))
+    assert with_contacts and with_contacts <= cand
+
+
+# ---------------------------------------------------------------- box-box edge-edge (reading R33)
+def _box_overlap(RA, xA, hA, RB, xB, hB, L):
+    rA = np.sum(hA * np.abs(L @ RA))
+    rB = np.sum(hB * np.abs(L @ RB))
+    return rA + rB - abs(L @ (xB - xA))
+
+
+def _rand_R(rng):
+    q = rng.normal(size=4)
+    return co.quat_R(q / np.linalg.norm(q))
+
+
+def test_box_edge_edge_depth_is_the_minimum_over_all_directions():
+    """For interpenetrating boxes the penetration depth is the minimum overlap
+    of the projections over ALL directions; the SAT's 15 axes attain it, so
+    densely sampled directions never go below R33's overlap and come close
+    it is attained along the contact normal, which is perpendicular to an
+    edge of each box."""
+    rng = np.random.default_rng(11)
+    u = rng.normal(size=(40000, 3))
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    found = 0
+    for trial in range(200):
+        RA, RB = _rand_R(rng), _rand_R(rng)
+        hA, hB = rng.uniform(0.5, 1.5, 3), rng.uniform(0.5, 1.5, 3)
+        xA = np.zeros(3)
+        xB = rng.normal(size=3)
+        xB *= (np.sum(hA) + np.sum(hB)) * 0.45 / np.linalg.norm(xB)
+        out = co._box_edge_edge(RA, xA, hA, RB, xB, hB, 1e9)
+        if not out:
+            continue
+        p, phi, n = out[0]
+        ov = np.array([_box_overlap(RA, xA, hA, RB, xB, hB, L) for L in u])
+        if phi > 0:                                   # separated along n: not a depth pin
+            continue
+        found += 1
+        assert ov.min() >= -phi - 1e-9                # no direction overlaps less (minimality)
+        assert abs(_box_overlap(RA, xA, hA, RB, xB, hB, n) + phi) < 1e-12   # attained along n
+        assert abs(np.linalg.norm(n) - 1) < 1e-12 and n @ (xB - xA) >= 0
+        # n is the cross product of one edge of each box
+        assert min(abs(n @ RA[:, i]) for i in range(3)) < 1e-9
+        assert min(abs(n @ RB[:, j]) for j in range(3)) < 1e-9
+        if found >= 12:
+            break
+    assert found >= 12
+
+
+def test_box_edge_edge_emitted_only_on_edge_axes_within_margin():
+    """Face-on stacked boxes: the minimum-overlap axis is a face normal, so no
+    edge-edge contact; boxes far apart along an edge axis: none either."""
+    I = np.eye(3)
+    h = np.ones(3)
+    assert co._box_edge_edge(I, np.zeros(3), h, I, np.array([0.1, 0.2, 1.99]), h, 0.01) == []
+    Rz = co.quat_R(np.array([np.cos(np.pi / 8), 0, 0, np.sin(np.pi / 8)]))
+    Rx = co.quat_R(np.array([np.cos(np.pi / 8), np.sin(np.pi / 8), 0, 0]))
+    assert co._box_edge_edge(Rz, np.zeros(3), h, Rx, np.array([0.0, 0.0, 10.0]), h, 0.01) == []
