@@ -73,6 +73,9 @@ def parse(argv=None):
                     help="closed loop: the GPU collision front-end (SURVEY 8(f) rank 1) builds the contacts every "
                          "step (count kept on the device); hand: then the upstream and the step (implies --upstream); "
                          "pile: lattice-neighbour candidate pairs, then the step (the full-step metric, P:389-390)")
+    ap.add_argument("--pair-list", action="store_true",
+                    help="with --collide on the pile: the fixed lattice-neighbour candidate list instead of the "
+                         "per-step broadphase")
     ap.add_argument("--workload", default="pile", choices=["pile", "hand", "mixed"],
                     help="pile: config 4 (the BASELINE metric); hand: config 3; mixed: config 5")
     a = ap.parse_args(argv)
@@ -203,7 +206,9 @@ def workload(args, rank, world_size):
     if args.collide:
         name += " + GPU collision front-end every step (closed loop)"
         if args.workload == "pile":
-            name += "; contacts from geometry, not the generator's 2000"
+            name += (" (fixed lattice-neighbour candidate list)" if args.pair_list else
+                     " (sort-and-sweep broadphase + narrowphase, one kernel)") + \
+                "; contacts from geometry, not the generator's"
     return parts, name, n
 
 
@@ -474,7 +479,8 @@ def run_ours(args, rank, world_size, local):
             from harness import scenes as _sc
             B = p.scene.n_bodies
             lat = {500: (10, 10, 5), 100: (5, 5, 4)}[B]
-            p.ctx.load_geometry(_sc.pile_geometry(lat))
+            # candidates every step (broadphase, reading R32), or the fixed lattice-neighbour list
+            p.ctx.load_geometry(_sc.pile_geometry(lat, broadphase=not args.pair_list))
             p.col = p.W * 4 * args.contacts         # output capacity
         if args.upstream and p.scene.n_trees > 0:     # articulated upstream every step
             from harness import scenes as _sc

@@ -278,11 +278,13 @@ def _pile_template(nx, ny, nz):
     return kinds, np.asarray(rows, np.int64)
 
 
-def pile_geometry(lattice=(10, 10, 5), margin=0.001, mu=(1.0, 0.005, 0.0001), condim=3):
+def pile_geometry(lattice=(10, 10, 5), margin=0.001, mu=(1.0, 0.005, 0.0001), condim=3, broadphase=False):
     """Collision geometry of the config-4 pile for the GPU front-end: the floor
     plane z = 0, one geom per body (sphere R 2.5 cm / box half 2.5 cm / capsule
     R 1.5 cm, half-length 2 cm, as PILE_SHAPES), candidate pairs = the floor with
-    the bottom layer and every lattice-neighbour pair (the generator's pairs)."""
+    the bottom layer and every lattice-neighbour pair (the generator's pairs);
+    broadphase=True: no candidate list, the front-end's broadphase finds the
+    pairs every step (reading R32)."""
     from .types import Geometry
     nx, ny, nz = lattice
     B = nx * ny * nz
@@ -301,7 +303,7 @@ def pile_geometry(lattice=(10, 10, 5), margin=0.001, mu=(1.0, 0.005, 0.0001), co
         pairs += [(1 + int(a), 1 + int(b)) for a, b in zip(da.ravel(), db.ravel())]
     G = B + 1
     return Geometry(np.array(kind, np.int32), np.array(body, np.int32), np.zeros(G, np.int32),
-                    np.array(size, np.float64), np.zeros((G, 3)), np.array(pairs, np.int32),
+                    np.array(size, np.float64), np.zeros((G, 3)), None if broadphase else np.array(pairs, np.int32),
                     margin=margin, mu=mu, condim=condim)
 
 

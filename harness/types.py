@@ -100,7 +100,7 @@ class Geometry:
     link: np.ndarray                         # (G,) int32
     size: np.ndarray                         # (G,3)
     local: np.ndarray                        # (G,3)
-    pairs: np.ndarray                        # (P,2) int32
+    pairs: np.ndarray                        # (P,2) int32, or None: broadphase mode (reading R32)
     margin: float = 0.001
     mu: tuple = (1.0, 0.005, 0.0001)         # (mu_t, mu_tor, mu_rol) of every contact
     condim: int = 3

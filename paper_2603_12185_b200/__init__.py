@@ -264,11 +264,13 @@ class Context:
         return self
 
     def load_geometry(self, geo):
-        """comfree_load_geometry from a harness.types.Geometry."""
+        """comfree_load_geometry from a harness.types.Geometry (pairs None or
+        empty: broadphase mode, candidates found every step, reading R32)."""
+        pairs = np.zeros((0, 2), np.int32) if geo.pairs is None else np.ascontiguousarray(geo.pairs, np.int32).reshape(-1, 2)
         arrs = [np.ascontiguousarray(geo.kind, np.int32), np.ascontiguousarray(geo.body, np.int32),
                 np.ascontiguousarray(geo.link, np.int32), np.ascontiguousarray(geo.size, np.float32),
-                np.ascontiguousarray(geo.local, np.float32), np.ascontiguousarray(geo.pairs, np.int32)]
-        g = _lib.comfree_geometry(int(arrs[0].shape[0]), int(arrs[5].shape[0]), *[a.ctypes.data for a in arrs],
+                np.ascontiguousarray(geo.local, np.float32), pairs if pairs.size else np.zeros((1, 2), np.int32)]
+        g = _lib.comfree_geometry(int(arrs[0].shape[0]), int(pairs.shape[0]), *[a.ctypes.data for a in arrs],
                                   float(geo.margin), (ct.c_float * 3)(*[float(m) for m in geo.mu]), int(geo.condim))
         self._check(self._lib.comfree_load_geometry(self.h, ct.byref(g)), "comfree_load_geometry")
         self._col = None

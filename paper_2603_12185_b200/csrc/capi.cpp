@@ -77,6 +77,7 @@ struct comfree_ctx {
   bool art_loaded = false;
   // collision front-end: device geometry (comfree_load_geometry) and scan scratch
   DevBuf geo, col_counts, col_offs, col_tmp, col_frames;
+  DevBuf bp_status, bp_queue, bp_count;   // broadphase mode scratch
   int32_t n_geoms = 0, n_pairs = 0;
   float col_margin = 0.f, col_mu[3] = {0.f, 0.f, 0.f};
   int32_t col_condim = 3;
@@ -161,6 +162,8 @@ comfree_status check_latched(comfree_ctx* ctx, cudaStream_t s) {
   CUDA_TRY(ctx, cudaMemcpy(ctx->d_first_bad, &none, sizeof none, cudaMemcpyHostToDevice));
   if (e & cf::ERR_CONTACT_CAP)
     return fail(ctx, COMFREE_ERR_CAPACITY, "collide: more contacts than the output capacity (flags 0x%x)", e);
+  if (e & cf::ERR_CANDIDATES)
+    return fail(ctx, COMFREE_ERR_CAPACITY, "collide: more broadphase candidate pairs in a world than fit shared memory (flags 0x%x)", e);
   if (e & (cf::ERR_UNSORTED | cf::ERR_WORLD_RANGE | cf::ERR_BODY_RANGE | cf::ERR_CONDIM | cf::ERR_IMPULSE_CAP |
            cf::ERR_IMPEDANCE | cf::ERR_WORLD_CONTACTS | cf::ERR_ARTICULATION))
     return fail(ctx, COMFREE_ERR_VALIDATION, "device validation failed (flags 0x%x):%s%s%s%s%s%s%s%s", e,
@@ -203,6 +206,11 @@ cudaEvent_t next_event(comfree_ctx* ctx, int* idx) {
 
 }  // namespace
 
+#ifdef CF_BP_TIMELINE
+extern "C" int comfree_debug_bp_timeline(comfree_ctx* ctx, unsigned long long* host, int64_t n_worlds) {
+  return cudaMemcpy(host, ctx->col_frames.p, (size_t)n_worlds * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+}
+#endif
 #ifdef CF_TIMELINE
 // Tuning builds only: per-CTA phase timestamps of the last step launch.
 static unsigned* g_tl = nullptr;
@@ -869,6 +877,14 @@ comfree_status comfree_load_geometry(comfree_ctx* ctx, const comfree_geometry* g
     pr[k] = make_int2(a, b);
   }
   if (chains && !ctx->art_loaded) return fail(ctx, COMFREE_ERR_STATE, "load_geometry: chain geoms need load_articulation first");
+  if (P == 0) {  // broadphase mode (reading R32): planes lead the geom list, geom ids fit 16 bits
+    bool seen_other = false;
+    for (int k = 0; k < G; ++k) {
+      if (g->kind[k] != 2) seen_other = true;
+      else if (seen_other) return fail(ctx, COMFREE_ERR_VALIDATION, "load_geometry: without pairs, planes must come first");
+    }
+    if (G > 65535) return fail(ctx, COMFREE_ERR_VALIDATION, "load_geometry: at most 65535 geoms");
+  }
   CUDA_TRY(ctx, cudaSetDevice(ctx->device));
   const size_t bytes = (size_t)gi.size() * (sizeof(int4) + 2 * sizeof(float4)) + pr.size() * sizeof(int2);
   CUDA_TRY(ctx, ensure(ctx->geo, bytes));
@@ -897,7 +913,7 @@ comfree_status comfree_collide(comfree_ctx* ctx, int64_t first, int64_t nw, int6
   if (first < 0 || nw < 0 || first + nw > ctx->W) return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "collide: world range");
   if (capacity < 0 || (capacity > 0 && (!world || !c0 || !c1 || !c2 || !c3 || !link)))
     return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "collide: output arrays");
-  if (nw * (int64_t)ctx->n_pairs * 16 >= INT32_MAX) return fail(ctx, COMFREE_ERR_CAPACITY, "collide: too many candidate pairs");
+  if (nw * (int64_t)ctx->n_pairs * 17 >= INT32_MAX) return fail(ctx, COMFREE_ERR_CAPACITY, "collide: too many candidate pairs");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   CUDA_TRY(ctx, cudaSetDevice(ctx->device));
   cf::CollideParams P{};
@@ -924,8 +940,41 @@ comfree_status comfree_collide(comfree_ctx* ctx, int64_t first, int64_t nw, int6
   P.c3 = reinterpret_cast<int4*>(c3);
   P.world = world;
   P.link = reinterpret_cast<int2*>(link);
-  const size_t m = (size_t)nw * ctx->n_pairs + 1;
   P.n_geoms = ctx->n_geoms;
+  if (ctx->n_pairs == 0) {
+    // broadphase mode (reading R32): one kernel, candidates found per world
+    int np2 = 1;
+    while (np2 < ctx->n_geoms) np2 <<= 1;
+    const size_t fixed = cf::collide_bp_smem(ctx->n_geoms, 0, np2);
+    const int64_t room = (int64_t)(110 * 1024) - (int64_t)fixed;  // two CTAs per SM
+    const int cap_c = (int)std::max<int64_t>(1024, std::min<int64_t>(room / 10 & ~7, 65535));
+    if (cf::collide_bp_smem(ctx->n_geoms, cap_c, np2) > 227 * 1024)
+      return fail(ctx, COMFREE_ERR_CAPACITY, "collide: %d geoms per world exceed the broadphase's shared memory", ctx->n_geoms);
+    CUDA_TRY(ctx, ensure(ctx->bp_status, std::max<int64_t>(1, nw) * sizeof(unsigned long long)));
+    CUDA_TRY(ctx, ensure(ctx->bp_queue, 4 * sizeof(int)));
+    CUDA_TRY(ctx, ensure(ctx->bp_count, 2 * sizeof(int64_t)));
+    int64_t* cnt = static_cast<int64_t*>(ctx->bp_count.p);
+#ifdef CF_BP_TIMELINE
+    CUDA_TRY(ctx, ensure(ctx->col_frames, std::max<size_t>(1, (size_t)nw) * 8 * sizeof(unsigned long long)));
+    P.frames = static_cast<float4*>(ctx->col_frames.p);
+#endif
+    CUDA_TRY(ctx, cf::collide_broadphase(P, cap_c, capacity, static_cast<unsigned long long*>(ctx->bp_status.p),
+                                         static_cast<int*>(ctx->bp_queue.p), n_device ? n_device : cnt, cnt + 1,
+                                         ctx->d_err, s));
+    ctx->launches += 1;
+    if (n_device) return COMFREE_OK;
+    int64_t h[2] = {0, 0};
+    CUDA_TRY(ctx, cudaMemcpyAsync(h, cnt, sizeof h, cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(ctx, cudaStreamSynchronize(s));
+    *n_out = h[1];
+    if (h[1] > capacity) {
+      int zero = 0;
+      CUDA_TRY(ctx, cudaMemcpy(ctx->d_err, &zero, sizeof zero, cudaMemcpyHostToDevice));  // reported here instead
+      return fail(ctx, COMFREE_ERR_CAPACITY, "collide: %lld contacts, capacity %lld", (long long)h[1], (long long)capacity);
+    }
+    return check_latched(ctx, s);
+  }
+  const size_t m = (size_t)nw * ctx->n_pairs + 1;
   CUDA_TRY(ctx, ensure(ctx->col_frames, std::max<size_t>(1, (size_t)nw * ctx->n_geoms) * 3 * sizeof(float4)));
   P.frames = static_cast<float4*>(ctx->col_frames.p);
   CUDA_TRY(ctx, cf::collide_frames(P, s));
@@ -1156,7 +1205,7 @@ void comfree_destroy(comfree_ctx* ctx) {
                     &ctx->sj, &ctx->skd, &ctx->nf, &ctx->foff, &ctx->cub_tmp, &ctx->in_world, &ctx->in_off, &ctx->in_c0,
                     &ctx->in_c1, &ctx->in_c2, &ctx->in_c3, &ctx->in_jrow, &ctx->in_kd, &ctx->in_fext, &ctx->in_L,
                     &ctx->in_tau, &ctx->imp, &ctx->st_tmp, &ctx->art, &ctx->geo, &ctx->col_counts,
-                    &ctx->col_offs, &ctx->col_tmp, &ctx->col_frames};
+                    &ctx->col_offs, &ctx->col_tmp, &ctx->col_frames, &ctx->bp_status, &ctx->bp_queue, &ctx->bp_count};
   for (DevBuf* b : bufs) release(*b);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->slab) cudaFree(ctx->slab);

@@ -25,7 +25,7 @@ namespace {
 using namespace chain;
 
 enum { G_SPHERE = 0, G_BOX = 1, G_PLANE = 2, G_CAPSULE = 3 };
-constexpr int kMaxPairContacts = 16;  // box-box vertex-face: 8 corners each way
+constexpr int kMaxPairContacts = 17;  // box-box: 8 corners each way + one edge-edge
 
 struct Frame {
   float R[9];
@@ -78,10 +78,11 @@ __device__ Frame geom_frame(const CollideParams& P, int g, int64_t w) {
   return F;
 }
 
-// Geom frame from the frame pass (one evaluation per (world, geom) instead of
-// one per candidate pair and pass).
-__device__ __forceinline__ Frame load_frame(const CollideParams& P, int g, int64_t w) {
-  const float4* f = P.frames + ((size_t)w * P.n_geoms + g) * 3;
+// Geom frame from the world's frame array (3 float4 per geom: the rows of R
+// with x in .w): the frame pass's global array, or the broadphase kernel's
+// shared-memory copy.
+__device__ __forceinline__ Frame load_frame(const float4* Fw, int g) {
+  const float4* f = Fw + (size_t)g * 3;
   const float4 a = f[0], b = f[1], c = f[2];
   Frame F;
   F.R[0] = a.x; F.R[1] = a.y; F.R[2] = a.z;
@@ -98,26 +99,25 @@ __device__ __forceinline__ V3 tangent(V3 n) {
   return v3(1.f + s * n.x * n.x * a, s * b, -s * n.x);
 }
 
-// Contact sink of one pair: EMIT = false only counts (no staging arrays: the
-// count pass has no stack frame); EMIT = true stages the records for the writes.
-#ifndef CF_COLLIDE_DIRECT
-#define CF_COLLIDE_DIRECT 1  // emit writes each record as it is found (no local-memory staging): pile full step 205 -> 196 us
-#endif
-template <bool EMIT>
+// Contact sink of one pair: counts, and with emit writes each record as it is
+// found (no local-memory staging).
+// The count and the emit passes must find the same contacts bit for bit (the
+// emit writes exactly the slots the count reserved), so both run the SAME
+// machine code: one non-inlined pair_contacts with a runtime emit flag (two
+// inlined specialisations may contract floating point differently and
+// disagree on a contact at the margin).
 struct Out {
-  V3 p[EMIT && !CF_COLLIDE_DIRECT ? kMaxPairContacts : 1], n[EMIT && !CF_COLLIDE_DIRECT ? kMaxPairContacts : 1];
-  float phi[EMIT && !CF_COLLIDE_DIRECT ? kMaxPairContacts : 1];
   int k;
+  bool emit;
   const CollideParams* P;
   int64_t base, w;
   int b1, b2, l1, l2;
   __device__ void add(V3 pp, float ph, V3 nn);
 };
 __device__ __forceinline__ V3 tangent(V3 n);
-template <bool EMIT>
-__device__ __forceinline__ void Out<EMIT>::add(V3 pp, float ph, V3 nn) {
+__device__ __forceinline__ void Out::add(V3 pp, float ph, V3 nn) {
   if (k < kMaxPairContacts) {
-    if (EMIT && CF_COLLIDE_DIRECT) {  // write the record now (no staging)
+    if (emit) {  // write the record now (no staging)
       const int64_t c = base + k;
       const V3 t1 = tangent(nn);
       P->c0[c] = make_float4(pp.x, pp.y, pp.z, ph);
@@ -126,17 +126,23 @@ __device__ __forceinline__ void Out<EMIT>::add(V3 pp, float ph, V3 nn) {
       P->c3[c] = make_int4(b1, b2, __float_as_int(P->mu_rol), P->condim);
       P->world[c] = (int32_t)w;
       P->link[c] = make_int2(l1, l2);
-    } else if (EMIT) {
-      p[k] = pp; phi[k] = ph; n[k] = nn;
     }
     ++k;
   }
 }
 
+// Per-scene geom table the narrowphase reads (global, or the broadphase
+// kernel's shared-memory copy): (kind, body, link, -), size, local.
+struct GeomTab {
+  const int4* geom;
+  const float4* size;
+  const float4* local;
+};
+
 // Capsule segment ends (end -1 first): x -+ half_len * the frame's z axis.
-__device__ __forceinline__ void capsule_ends(const CollideParams& P, int g, int64_t w, V3& a, V3& b) {
-  const Frame F = load_frame(P, g, w);
-  const float hl = P.size[g].y;
+__device__ __forceinline__ void capsule_ends(const GeomTab& T, const float4* Fw, int g, V3& a, V3& b) {
+  const Frame F = load_frame(Fw, g);
+  const float hl = T.size[g].y;
   const V3 z = v3(F.R[2], F.R[5], F.R[8]);
   a = sub(F.x, mul(hl, z));
   b = add(F.x, mul(hl, z));
@@ -237,16 +243,92 @@ __device__ __forceinline__ void box_corners_on(const Frame& A, float4 hA, const 
   }
 }
 
-// Contacts of pair pi in world w: returns the count; with out != null writes them
-// from index `base` on.
-template <bool EMIT>
-__device__ int pair_contacts(const CollideParams& P, int pi, int64_t w, int64_t base) {
-  constexpr bool emit = EMIT;
-  const int2 pr = P.pairs[pi];
-  const int4 g1 = P.geom[pr.x], g2 = P.geom[pr.y];
+// Exact early out for box-box: separated by more than the margin along a face
+// normal of either box (overlap < -margin) means no corner is within the
+// margin of a face (its signed distance exceeds the margin along that axis)
+// and the minimum overlap of R33 is below -margin too: no contact at all.
+__device__ __forceinline__ bool boxes_separated(const Frame& A, float4 hA4, const Frame& Bf, float4 hB4, float margin) {
+  const V3 d = sub(Bf.x, A.x);
+  const float hA[3] = {hA4.x, hA4.y, hA4.z}, hB[3] = {hB4.x, hB4.y, hB4.z};
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    const V3 L = k < 3 ? v3(A.R[k], A.R[3 + k], A.R[6 + k]) : v3(Bf.R[k - 3], Bf.R[k], Bf.R[k + 3]);
+    float r = -fabsf(dot(L, d));
+#pragma unroll
+    for (int m = 0; m < 3; ++m)
+      r += hA[m] * fabsf(L.x * A.R[m] + L.y * A.R[3 + m] + L.z * A.R[6 + m]) +
+           hB[m] * fabsf(L.x * Bf.R[m] + L.y * Bf.R[3 + m] + L.z * Bf.R[6 + m]);
+    if (r < -margin) return true;
+  }
+  return false;
+}
+
+// Box-box edge-edge (reading R33): separating-axis test over the 15 axes (face
+// normals of A, of B, the 9 edge cross products e_A,i x e_B,j, i-major, skipped
+// when |cross| <= 1e-6); when the first axis of minimum overlap is an edge axis
+// and -overlap < margin, one contact at the midpoint of the closest points of
+// A's edge through its support point along n and B's through its support
+// point along -n (n oriented from A to B).
+template <class O>
+__device__ __forceinline__ void box_edge_edge(const Frame& A, float4 hA4, const Frame& Bf, float4 hB4, float margin,
+                                              O& o) {
+  const float hA[3] = {hA4.x, hA4.y, hA4.z}, hB[3] = {hB4.x, hB4.y, hB4.z};
+  const V3 d = sub(Bf.x, A.x);
+  V3 ea[3], eb[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    ea[k] = v3(A.R[k], A.R[3 + k], A.R[6 + k]);    // column k of R: the frame's axis k
+    eb[k] = v3(Bf.R[k], Bf.R[3 + k], Bf.R[6 + k]);
+  }
+  float best = INFINITY;
+  int bi = -1, bj = -1;
+  V3 bL = v3(0.f, 0.f, 0.f);
+  auto overlap = [&](V3 L) {
+    float r = -fabsf(dot(L, d));
+#pragma unroll
+    for (int k = 0; k < 3; ++k) r += hA[k] * fabsf(dot(L, ea[k])) + hB[k] * fabsf(dot(L, eb[k]));
+    return r;
+  };
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    const float ov = overlap(k < 3 ? ea[k] : eb[k - 3]);
+    if (ov < best) { best = ov; bi = -1; }
+  }
+#pragma unroll 1
+  for (int i = 0; i < 3; ++i) {
+#pragma unroll 1
+    for (int j = 0; j < 3; ++j) {
+      V3 L = cross(ea[i], eb[j]);
+      const float nl = sqrtf(dot(L, L));
+      if (!(nl > 1e-6f)) continue;
+      L = mul(1.f / nl, L);
+      const float ov = overlap(L);
+      if (ov < best) { best = ov; bi = i; bj = j; bL = L; }
+    }
+  }
+  if (bi < 0 || !(-best < margin)) return;
+  const V3 n = dot(bL, d) >= 0.f ? bL : mul(-1.f, bL);
+  V3 pa = A.x, pb = Bf.x;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    if (k != bi) pa = add(pa, mul((dot(n, ea[k]) >= 0.f ? 1.f : -1.f) * hA[k], ea[k]));
+    if (k != bj) pb = sub(pb, mul((dot(n, eb[k]) >= 0.f ? 1.f : -1.f) * hB[k], eb[k]));
+  }
+  V3 c1, c2;
+  closest_segments(sub(pa, mul(hA[bi], ea[bi])), add(pa, mul(hA[bi], ea[bi])), sub(pb, mul(hB[bj], eb[bj])),
+                   add(pb, mul(hB[bj], eb[bj])), c1, c2);
+  o.add(mul(0.5f, add(c1, c2)), -best, n);
+}
+
+// Contacts of the geom pair pr = (g1, g2) in world w (frames Fw): returns the
+// count; EMIT writes them from record `base` on.
+__device__ __noinline__ int pair_contacts_rt(const CollideParams& P, const GeomTab T, const int2 pr, const float4* Fw,
+                                             int64_t w, int64_t base, bool emit) {
+  const int4 g1 = T.geom[pr.x], g2 = T.geom[pr.y];
   const float margin = P.margin;
-  Out<EMIT> o;
+  Out o;
   o.k = 0;
+  o.emit = emit;
   o.P = &P;
   o.base = base;
   o.w = w;
@@ -256,26 +338,26 @@ __device__ int pair_contacts(const CollideParams& P, int pi, int64_t w, int64_t 
   o.l2 = g2.y < -1 ? g2.z : 0;
   const int k1 = g1.x, k2 = g2.x;
   if (k1 == G_PLANE) {
-    const float4 s1 = P.size[pr.x];
+    const float4 s1 = T.size[pr.x];
     const V3 pn = v3(s1.x, s1.y, s1.z);
-    const float off = P.local[pr.x].x;
+    const float off = T.local[pr.x].x;
     if (k2 == G_CAPSULE) {
       V3 e[2];
-      capsule_ends(P, pr.y, w, e[0], e[1]);
-      const float R = P.size[pr.y].x;
+      capsule_ends(T, Fw, pr.y, e[0], e[1]);
+      const float R = T.size[pr.y].x;
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         const float phi = dot(pn, e[q]) - off - R;
         if (phi < margin) o.add(sub(e[q], mul(R + 0.5f * phi, pn)), phi, pn);
       }
     } else {
-      const Frame F2 = load_frame(P, pr.y, w);
+      const Frame F2 = load_frame(Fw, pr.y);
       if (k2 == G_SPHERE) {
-        const float R = P.size[pr.y].x;
+        const float R = T.size[pr.y].x;
         const float phi = dot(pn, F2.x) - off - R;
         if (phi < margin) o.add(sub(F2.x, mul(R + 0.5f * phi, pn)), phi, pn);
       } else {  // box: every corner within the margin
-        const float4 h = P.size[pr.y];
+        const float4 h = T.size[pr.y];
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const V3 sl = v3((k & 1) ? h.x : -h.x, (k & 2) ? h.y : -h.y, (k & 4) ? h.z : -h.z);
@@ -286,64 +368,58 @@ __device__ int pair_contacts(const CollideParams& P, int pi, int64_t w, int64_t 
       }
     }
   } else if ((k1 == G_SPHERE || k1 == G_CAPSULE) && (k2 == G_SPHERE || k2 == G_CAPSULE)) {
-    const float R1 = P.size[pr.x].x, R2 = P.size[pr.y].x;
+    const float R1 = T.size[pr.x].x, R2 = T.size[pr.y].x;
     V3 c1, c2;
     if (k1 == G_SPHERE && k2 == G_SPHERE) {
-      c1 = load_frame(P, pr.x, w).x;
-      c2 = load_frame(P, pr.y, w).x;
+      c1 = load_frame(Fw, pr.x).x;
+      c2 = load_frame(Fw, pr.y).x;
     } else if (k1 == G_CAPSULE && k2 == G_CAPSULE) {
       V3 a1, b1, a2, b2;
-      capsule_ends(P, pr.x, w, a1, b1);
-      capsule_ends(P, pr.y, w, a2, b2);
+      capsule_ends(T, Fw, pr.x, a1, b1);
+      capsule_ends(T, Fw, pr.y, a2, b2);
       closest_segments(a1, b1, a2, b2, c1, c2);
     } else if (k1 == G_CAPSULE) {
       V3 a1, b1;
-      capsule_ends(P, pr.x, w, a1, b1);
-      c2 = load_frame(P, pr.y, w).x;
+      capsule_ends(T, Fw, pr.x, a1, b1);
+      c2 = load_frame(Fw, pr.y).x;
       c1 = closest_on_segment(a1, b1, c2);
     } else {
       V3 a2, b2;
-      c1 = load_frame(P, pr.x, w).x;
-      capsule_ends(P, pr.y, w, a2, b2);
+      c1 = load_frame(Fw, pr.x).x;
+      capsule_ends(T, Fw, pr.y, a2, b2);
       c2 = closest_on_segment(a2, b2, c1);
     }
     two_spheres(c1, R1, c2, R2, margin, o);
   } else if (k1 == G_BOX && k2 == G_BOX) {
-    const Frame A = load_frame(P, pr.x, w), Bf = load_frame(P, pr.y, w);
-    const float4 hA = P.size[pr.x], hB = P.size[pr.y];
+    const Frame A = load_frame(Fw, pr.x), Bf = load_frame(Fw, pr.y);
+    const float4 hA = T.size[pr.x], hB = T.size[pr.y];
+    if (boxes_separated(A, hA, Bf, hB, margin)) return 0;  // no vertex-face nor edge-edge contact
     box_corners_on(A, hA, Bf, hB, margin, false, o);
     box_corners_on(Bf, hB, A, hA, margin, true, o);
+    box_edge_edge(A, hA, Bf, hB, margin, o);
   } else {  // sphere or capsule against a box
     const bool round_first = k1 != G_BOX;
     const int gr = round_first ? pr.x : pr.y, gb = round_first ? pr.y : pr.x;
-    const Frame Fb = load_frame(P, gb, w);
-    const float R = P.size[gr].x;
-    const float4 h4 = P.size[gb];
+    const Frame Fb = load_frame(Fw, gb);
+    const float R = T.size[gr].x;
+    const float4 h4 = T.size[gb];
     V3 e[2];
     int ne = 1;
-    if (P.geom[gr].x == G_CAPSULE) { capsule_ends(P, gr, w, e[0], e[1]); ne = 2; }
-    else e[0] = load_frame(P, gr, w).x;
+    if (T.geom[gr].x == G_CAPSULE) { capsule_ends(T, Fw, gr, e[0], e[1]); ne = 2; }
+    else e[0] = load_frame(Fw, gr).x;
     for (int q = 0; q < ne; ++q) {
       V3 nbox, qs;
       const float phi = sphere_box(e[q], R, Fb, h4, nbox, qs);
       if (phi < margin) o.add(mul(0.5f, add(qs, sub(e[q], mul(R, nbox)))), phi, round_first ? mul(-1.f, nbox) : nbox);
     }
   }
-  if (emit && !CF_COLLIDE_DIRECT) {
-    const int la = g1.y < -1 ? g1.z : 0, lb = g2.y < -1 ? g2.z : 0;
-#pragma unroll 1
-    for (int k = 0; k < o.k; ++k) {
-      const int64_t c = base + k;
-      const V3 t1 = tangent(o.n[k]);
-      P.c0[c] = make_float4(o.p[k].x, o.p[k].y, o.p[k].z, o.phi[k]);
-      P.c1[c] = make_float4(o.n[k].x, o.n[k].y, o.n[k].z, P.mu_t);
-      P.c2[c] = make_float4(t1.x, t1.y, t1.z, P.mu_tor);
-      P.c3[c] = make_int4(g1.y, g2.y, __float_as_int(P.mu_rol), P.condim);
-      P.world[c] = (int32_t)w;  // relative to the range's first world, like comfree_step
-      P.link[c] = make_int2(la, lb);
-    }
-  }
   return o.k;
+}
+
+template <bool EMIT>
+__device__ __forceinline__ int pair_contacts(const CollideParams& P, const int2 pr, const float4* Fw, int64_t w,
+                                             int64_t base, const GeomTab* T = nullptr) {
+  return pair_contacts_rt(P, T ? *T : GeomTab{P.geom, P.size, P.local}, pr, Fw, w, base, EMIT);
 }
 
 __global__ void k_geom_frames(const __grid_constant__ CollideParams P) {
@@ -363,7 +439,7 @@ __global__ void k_collide_count(const __grid_constant__ CollideParams P, int32_t
   if (id == P.n_worlds * P.n_pairs) counts[id] = 0;  // the scan's closing element (total = its prefix)
   if (id >= P.n_worlds * P.n_pairs) return;
   const int64_t w = id / P.n_pairs;
-  counts[id] = pair_contacts<false>(P, (int)(id - w * P.n_pairs), w, 0);
+  counts[id] = pair_contacts<false>(P, P.pairs[id - w * P.n_pairs], P.frames + (size_t)w * P.n_geoms * 3, w, 0);
 }
 
 __global__ void k_collide_emit(const __grid_constant__ CollideParams P, const int32_t* __restrict__ offs,
@@ -390,14 +466,455 @@ __global__ void k_collide_emit(const __grid_constant__ CollideParams P, const in
   const int64_t w = id / P.n_pairs;
   const int64_t base = offs[id];
   if (offs[id + 1] == base) return;  // the count pass found no contact for this pair
+  const int2 pr = P.pairs[id - w * P.n_pairs];
+  const float4* Fw = P.frames + (size_t)w * P.n_geoms * 3;
   if (base + kMaxPairContacts > capacity) {  // only the tail can overflow
-    const int n = pair_contacts<false>(P, (int)(id - w * P.n_pairs), w, 0);
+    const int n = pair_contacts<false>(P, pr, Fw, w, 0);
     if (base + n > capacity) return;
   }
-  pair_contacts<true>(P, (int)(id - w * P.n_pairs), w, base);
+  pair_contacts<true>(P, pr, Fw, w, base);
+}
+
+// ---------------------------------------------------------------- broadphase
+// Geometry without a candidate list (reading R32): one CTA per world finds the
+// world's candidate pairs and emits their contacts, in one launch:
+//   1  geom frames (thread per geom) and AABBs grown by margin/2, in shared memory;
+//   2  sort-and-sweep: the non-plane geoms sorted by their AABB's low end along
+//      the axis of largest spread (bitonic sort), each swept forward while the
+//      next low end is within its high end, the other two axes tested; a pair
+//      goes to the bucket of its lower geom id; plane g1 takes every geom whose
+//      AABB reaches below offset + margin/2 (bucket order = geom order, by a
+//      block scan); each bucket sorted -> candidates in (g1, g2) order, the
+//      order reading R32 defines;
+//   3  narrowphase count per candidate, block scan -> offsets in the world;
+//   4  the world's base offset by a chained scan over worlds (decoupled
+//      look-back on per-world status words; worlds are taken in launch order
+//      from a ticket counter, so a CTA only waits on running CTAs);
+//   5  narrowphase again for candidates with contacts, records written at
+//      base + offset: world-major, (g1, g2)-ordered, deterministic.
+// The last CTA to finish stores the device count (the offset of the first pair
+// that did not fit when the capacity is exceeded) and resets the counters.
+#ifndef CF_BP_THREADS
+#define CF_BP_THREADS 512  // 16 warps, 2 CTAs per SM: 0.83 vs 0.91 ms collide at 256 (profiles/r02_broadphase.txt)
+#endif
+constexpr int kBpThreads = CF_BP_THREADS;
+#ifdef CF_BP_TIMELINE  // tuning diagnostic: per-world phase timestamps (globaltimer ns) into P.frames
+#define BP_MARK(k)                                                                        \
+  if (tid == 0) {                                                                         \
+    unsigned long long t_;                                                                \
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_));                                 \
+    reinterpret_cast<unsigned long long*>(P.frames)[w * 8 + (k)] = t_;                    \
+  }
+#else
+#define BP_MARK(k)
+#endif
+
+__device__ __forceinline__ uint32_t f2key(float f) {  // order-preserving float -> uint32
+  const uint32_t u = __float_as_uint(f);
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+// exclusive block scan of v over kBpThreads threads; returns the prefix, *tot the sum
+__device__ __forceinline__ int block_exclusive(int v, int* tmp, int* tot) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) tmp[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int t = lane < kBpThreads / 32 ? tmp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    tmp[lane] = t;  // inclusive sums of the warps
+  }
+  __syncthreads();
+  const int before = wid ? tmp[wid - 1] : 0;
+  *tot = tmp[kBpThreads / 32 - 1];
+  __syncthreads();
+  return before + x - v;
+}
+
+struct BpParams {
+  int cap_c;                       // candidate capacity per world (shared memory)
+  int np2;                         // power of two >= non-plane geoms
+  int64_t capacity;                // output records
+  unsigned long long* status;      // [n_worlds] chained-scan words (zeroed before the launch)
+  int* queue;                      // [0] world ticket, [1] CTAs done, [2] cut (zeroed before the launch)
+  int64_t* n_dev;                  // device count out (whole pairs within the capacity)
+  int64_t* total;                  // all contacts of the launch (or null)
+  int* err;
+};
+
+__global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_constant__ CollideParams P,
+                                                              const __grid_constant__ BpParams Q) {
+  extern __shared__ float4 bsm[];
+  __shared__ int s_tmp[32];
+  __shared__ int s_misc[8];
+  const int G = P.n_geoms, tid = threadIdx.x;
+  float4* Fw = bsm;                                                   // [3 G]
+  float4* lo = Fw + 3 * G;                                            // [G] (.w: 1 = plane)
+  float4* hi = lo + G;                                                // [G]
+  uint32_t* key = reinterpret_cast<uint32_t*>(hi + G);                // [np2]
+  uint32_t* val = key + Q.np2;                                        // [np2]
+  int* gbody = reinterpret_cast<int*>(val + Q.np2);                   // [G] body of each geom
+  int* cnt = gbody + G;                                               // [G + 1]
+  int* start = cnt + G + 1;                                           // [G + 1]
+  uint32_t* list = reinterpret_cast<uint32_t*>(start + G + 1);        // [cap_c] (g1 << 16) | g2
+  int* ncon = reinterpret_cast<int*>(list + Q.cap_c);                 // [cap_c]
+  uint16_t* perm = reinterpret_cast<uint16_t*>(ncon + Q.cap_c);      // [cap_c] evaluation order
+  if (tid == 0) s_misc[0] = atomicAdd(&Q.queue[0], 1);
+  __syncthreads();
+  const int64_t w = s_misc[0];
+  const float hm = 0.5f * P.margin;
+
+  BP_MARK(0);
+  // 1: frames and grown AABBs
+  for (int g = tid; g < G; g += kBpThreads) {
+    const Frame F = geom_frame(P, g, w);
+    Fw[3 * g] = make_float4(F.R[0], F.R[1], F.R[2], F.x.x);
+    Fw[3 * g + 1] = make_float4(F.R[3], F.R[4], F.R[5], F.x.y);
+    Fw[3 * g + 2] = make_float4(F.R[6], F.R[7], F.R[8], F.x.z);
+    const int kind = P.geom[g].x;
+    gbody[g] = P.geom[g].y;
+    const float4 sz = P.size[g];
+    V3 l = F.x, h = F.x;
+    if (kind == G_SPHERE) {
+      l = sub(F.x, v3(sz.x, sz.x, sz.x));
+      h = add(F.x, v3(sz.x, sz.x, sz.x));
+    } else if (kind == G_BOX) {
+      const V3 e = v3(fabsf(F.R[0]) * sz.x + fabsf(F.R[1]) * sz.y + fabsf(F.R[2]) * sz.z,
+                      fabsf(F.R[3]) * sz.x + fabsf(F.R[4]) * sz.y + fabsf(F.R[5]) * sz.z,
+                      fabsf(F.R[6]) * sz.x + fabsf(F.R[7]) * sz.y + fabsf(F.R[8]) * sz.z);
+      l = sub(F.x, e);
+      h = add(F.x, e);
+    } else if (kind == G_CAPSULE) {
+      const V3 z = v3(F.R[2], F.R[5], F.R[8]);
+      const V3 a = sub(F.x, mul(sz.y, z)), b = add(F.x, mul(sz.y, z));
+      l = sub(v3(fminf(a.x, b.x), fminf(a.y, b.y), fminf(a.z, b.z)), v3(sz.x, sz.x, sz.x));
+      h = add(v3(fmaxf(a.x, b.x), fmaxf(a.y, b.y), fmaxf(a.z, b.z)), v3(sz.x, sz.x, sz.x));
+    }
+    lo[g] = make_float4(l.x - hm, l.y - hm, l.z - hm, kind == G_PLANE ? 1.f : 0.f);
+    hi[g] = make_float4(h.x + hm, h.y + hm, h.z + hm, 0.f);
+  }
+  for (int g = tid; g <= G; g += kBpThreads) cnt[g] = 0;
+  __syncthreads();
+  // sweep axis: the largest spread of the non-plane AABB centres (block reduction)
+  {
+    float mn[3] = {INFINITY, INFINITY, INFINITY}, mx[3] = {-INFINITY, -INFINITY, -INFINITY};
+    for (int g = tid; g < G; g += kBpThreads) {
+      if (lo[g].w != 0.f) continue;
+      const float c[3] = {lo[g].x + hi[g].x, lo[g].y + hi[g].y, lo[g].z + hi[g].z};
+#pragma unroll
+      for (int k = 0; k < 3; ++k) { mn[k] = fminf(mn[k], c[k]); mx[k] = fmaxf(mx[k], c[k]); }
+    }
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      for (int o = 16; o > 0; o >>= 1) {
+        mn[k] = fminf(mn[k], __shfl_xor_sync(0xffffffffu, mn[k], o));
+        mx[k] = fmaxf(mx[k], __shfl_xor_sync(0xffffffffu, mx[k], o));
+      }
+    }
+    __shared__ float red[6 * (kBpThreads / 32)];
+    if ((tid & 31) == 0)
+      for (int k = 0; k < 3; ++k) { red[(tid >> 5) * 6 + k] = mn[k]; red[(tid >> 5) * 6 + 3 + k] = mx[k]; }
+    __syncthreads();
+    if (tid == 0) {
+      float a[3] = {INFINITY, INFINITY, INFINITY}, b[3] = {-INFINITY, -INFINITY, -INFINITY};
+      for (int q = 0; q < kBpThreads / 32; ++q)
+        for (int k = 0; k < 3; ++k) { a[k] = fminf(a[k], red[q * 6 + k]); b[k] = fmaxf(b[k], red[q * 6 + 3 + k]); }
+      int ax = 0;
+      for (int k = 1; k < 3; ++k)
+        if (b[k] - a[k] > b[ax] - a[ax]) ax = k;
+      s_misc[1] = ax;
+    }
+    __syncthreads();
+  }
+  const int ax = s_misc[1];
+  BP_MARK(1);
+  // 2a: bitonic sort of (low end along ax, geom) over the non-plane geoms
+  for (int i = tid; i < Q.np2; i += kBpThreads) {
+    const bool real = i < G && lo[i].w == 0.f;
+    key[i] = real ? f2key(ax == 0 ? lo[i].x : (ax == 1 ? lo[i].y : lo[i].z)) : 0xffffffffu;
+    val[i] = real ? (uint32_t)i : 0xffffffffu;
+  }
+  __syncthreads();
+  for (int k = 2; k <= Q.np2; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int t = tid; t < (Q.np2 >> 1); t += kBpThreads) {
+        const int i = ((t & ~(j - 1)) << 1) | (t & (j - 1));  // lower index of the pair
+        const int l = i | j;
+        const bool up = (i & k) == 0;
+        const uint64_t a = ((uint64_t)key[i] << 32) | val[i], b = ((uint64_t)key[l] << 32) | val[l];
+        if ((a > b) == up) { key[i] = (uint32_t)(b >> 32); val[i] = (uint32_t)b; key[l] = (uint32_t)(a >> 32); val[l] = (uint32_t)a; }
+      }
+      __syncthreads();
+    }
+  }
+  BP_MARK(2);
+  // 2b: sweep, twice: count per bucket, then place
+  auto axis_of = [&](const float4& v) { return ax == 0 ? v.x : (ax == 1 ? v.y : v.z); };
+  auto overlap = [&](int a, int b) {
+    const float4 la = lo[a], ha = hi[a], lb = lo[b], hb = hi[b];
+    return la.x <= hb.x && lb.x <= ha.x && la.y <= hb.y && lb.y <= ha.y && la.z <= hb.z && lb.z <= ha.z;
+  };
+  auto plane_hit = [&](int p, int g) {  // g's grown AABB reaches below offset + margin/2
+    const float4 n = P.size[p], lg = lo[g], hg = hi[g];
+    const V3 c = v3(0.5f * (lg.x + hg.x), 0.5f * (lg.y + hg.y), 0.5f * (lg.z + hg.z));
+    const V3 e = v3(0.5f * (hg.x - lg.x), 0.5f * (hg.y - lg.y), 0.5f * (hg.z - lg.z));
+    return n.x * c.x + n.y * c.y + n.z * c.z - (fabsf(n.x) * e.x + fabsf(n.y) * e.y + fabsf(n.z) * e.z) -
+               P.local[p].x < hm;
+  };
+  int n_np = 0;  // non-plane geoms (sorted keys below 0xffffffff)
+  {
+    int c = 0;
+    for (int g = tid; g < G; g += kBpThreads) c += lo[g].w == 0.f;
+    int tot;
+    (void)block_exclusive(c, s_tmp, &tot);
+    n_np = tot;
+  }
+  // (i) warp-cooperative sweep: warp v takes sorted positions i = v, v + 8, ...;
+  // its lanes test the next 32 positions at once until the sorted low ends pass
+  // geom i's high end; every pair found goes to a temporary list (ncon's
+  // storage) and is counted in its bucket (the lower geom id)
+  uint32_t* tmp = reinterpret_cast<uint32_t*>(ncon);
+  if (tid == 0) s_misc[5] = 0;
+  __syncthreads();
+  {
+    const int lane = tid & 31, wv = tid >> 5;
+    for (int i = wv; i < n_np; i += kBpThreads / 32) {
+      const int gi = (int)val[i];
+      const float hiax = axis_of(hi[gi]);
+      const int bi = gbody[gi];
+      for (int j0 = i + 1; j0 < n_np; j0 += 32) {
+        const int jj = j0 + lane;
+        const int gj = jj < n_np ? (int)val[jj] : 0;
+        const bool in = jj < n_np && axis_of(lo[gj]) <= hiax;
+        const bool found = in && gbody[gj] != bi && overlap(gi, gj);
+        const unsigned fb = __ballot_sync(0xffffffffu, found);
+        if (fb) {  // one append per warp chunk
+          int t0 = 0;
+          if (lane == 0) t0 = atomicAdd(&s_misc[5], __popc(fb));
+          t0 = __shfl_sync(0xffffffffu, t0, 0);
+          if (found) {
+            const int a = min(gi, gj), b = max(gi, gj);
+            atomicAdd(&cnt[a], 1);
+            const int t = t0 + __popc(fb & ((1u << lane) - 1u));
+            if (t < Q.cap_c) tmp[t] = ((uint32_t)a << 16) | (uint32_t)b;
+          }
+        }
+        if (__ballot_sync(0xffffffffu, in) != 0xffffffffu) break;  // the sorted range ended in this chunk
+      }
+    }
+  }
+  // (ii) planes (lowest geom ids): count their hits
+  for (int p = 0; p < G && P.geom[p].x == G_PLANE; ++p) {
+    for (int g0 = 0; g0 < G; g0 += kBpThreads) {
+      const int g = g0 + tid;
+      const int hit = (g < G && g > p && lo[g].w == 0.f && gbody[g] != gbody[p] && plane_hit(p, g)) ? 1 : 0;
+      int tot;
+      (void)block_exclusive(hit, s_tmp, &tot);
+      if (tid == 0) cnt[p] += tot;
+    }
+  }
+  __syncthreads();
+  // (iii) bucket starts (exclusive scan of the counts)
+  {
+    int run = 0;
+    for (int g0 = 0; g0 <= G; g0 += kBpThreads) {
+      const int g = g0 + tid;
+      const int v = g < G ? cnt[g] : 0;
+      int tot;
+      const int ex = block_exclusive(v, s_tmp, &tot);
+      if (g <= G) start[g] = run + ex;
+      run += tot;
+    }
+    __syncthreads();
+    for (int g = tid; g < G; g += kBpThreads) cnt[g] = 0;
+    if (tid == 0) {
+      s_misc[2] = run;                                   // candidates of the world
+      if (run > Q.cap_c) atomicOr(Q.err, ERR_CANDIDATES);
+    }
+    __syncthreads();
+  }
+  // (iv) pairs into their buckets; plane buckets in geom order by a block scan
+  {
+    const int nt = min(s_misc[5], Q.cap_c);
+    for (int t = tid; t < nt; t += kBpThreads) {
+      const uint32_t pv = tmp[t];
+      const int a = (int)(pv >> 16);
+      const int slot = start[a] + atomicAdd(&cnt[a], 1);
+      if (slot < Q.cap_c) list[slot] = pv;
+    }
+    for (int p = 0; p < G && P.geom[p].x == G_PLANE; ++p) {
+      int base = start[p];
+      for (int g0 = 0; g0 < G; g0 += kBpThreads) {
+        const int g = g0 + tid;
+        const int hit = (g < G && g > p && lo[g].w == 0.f && gbody[g] != gbody[p] && plane_hit(p, g)) ? 1 : 0;
+        int tot;
+        const int ex = block_exclusive(hit, s_tmp, &tot);
+        if (hit && base + ex < Q.cap_c) list[base + ex] = ((uint32_t)p << 16) | (uint32_t)g;
+        base += tot;
+      }
+    }
+    __syncthreads();
+  }
+  // a world whose candidates overflow the list emits nothing (reported as
+  // COMFREE_ERR_CAPACITY): its truncated buckets would hold stale entries
+  const int n_cand = s_misc[2] > Q.cap_c ? 0 : s_misc[2];
+  BP_MARK(3);
+  // 2c: each non-plane bucket sorted by g2 (small: insertion sort by its geom's thread)
+  for (int g = tid; g < G; g += kBpThreads) {
+    if (P.geom[g].x == G_PLANE) continue;
+    const int b0 = start[g], b1 = min(start[g + 1], Q.cap_c);
+    for (int i = b0 + 1; i < b1; ++i) {
+      const uint32_t v = list[i];
+      int j = i - 1;
+      while (j >= b0 && list[j] > v) { list[j + 1] = list[j]; --j; }
+      list[j + 1] = v;
+    }
+  }
+  __syncthreads();
+  // the AABBs are dead: their storage takes the geom table for the narrowphase
+  for (int g = tid; g < G; g += kBpThreads) {
+    lo[g] = P.size[g];
+    reinterpret_cast<int4*>(hi)[g] = P.geom[g];
+  }
+  __syncthreads();
+  const GeomTab Ts{reinterpret_cast<const int4*>(hi), lo, P.local};
+  BP_MARK(4);
+  // 3: narrowphase count per candidate, in an evaluation order grouped by the
+  // pair's kinds (counting sort on kind(g1) * 4 + kind(g2)) so that a warp's
+  // lanes take the same narrowphase branch; block scan -> offsets in the world
+  {
+    int* ccount = s_tmp;  // 16 classes
+    if (tid < 16) ccount[tid] = 0;
+    __syncthreads();
+    for (int k = tid; k < n_cand; k += kBpThreads) {
+      const uint32_t pv = list[k];
+      atomicAdd(&ccount[Ts.geom[pv >> 16].x * 4 + Ts.geom[pv & 0xffffu].x], 1);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int run = 0;
+      for (int c = 0; c < 16; ++c) { const int v = ccount[c]; ccount[c] = run; run += v; }
+    }
+    __syncthreads();
+    for (int k = tid; k < n_cand; k += kBpThreads) {
+      const uint32_t pv = list[k];
+      perm[atomicAdd(&ccount[Ts.geom[pv >> 16].x * 4 + Ts.geom[pv & 0xffffu].x], 1)] = (uint16_t)k;
+    }
+    __syncthreads();
+  }
+  for (int i = tid; i < n_cand; i += kBpThreads) {
+    const int k = perm[i];
+    const uint32_t pv = list[k];
+    ncon[k] = pair_contacts<false>(P, make_int2((int)(pv >> 16), (int)(pv & 0xffffu)), Fw, w, 0, &Ts);
+  }
+  __syncthreads();
+  int world_total = 0;
+  {
+    int run = 0;
+    for (int k0 = 0; k0 < n_cand; k0 += kBpThreads) {
+      const int k = k0 + tid;
+      const int v = k < n_cand ? ncon[k] : 0;
+      int tot;
+      const int ex = block_exclusive(v, s_tmp, &tot);
+      if (k < n_cand) ncon[k] = run + ex;                 // now: offset of candidate k in the world
+      run += tot;
+    }
+    world_total = run;
+  }
+  BP_MARK(5);
+  // 4: chained scan over worlds (status: bits 62-63 flag 1 aggregate / 2 inclusive, low bits value)
+  if (tid == 0) {
+    const unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62, kVal = (1ull << 62) - 1;
+    volatile unsigned long long* st = Q.status;
+    long long prefix = 0;
+    if (w == 0) {
+      __threadfence();
+      atomicExch(&Q.status[0], kInc | (unsigned long long)world_total);
+    } else {
+      __threadfence();
+      atomicExch(&Q.status[w], kAgg | (unsigned long long)world_total);
+      for (int64_t j = w - 1; j >= 0;) {
+        const unsigned long long v = st[j];
+        const unsigned long long f = v >> 62;
+        if (f == 0) continue;                             // predecessor still counting
+        prefix += (long long)(v & kVal);
+        if (f == 2) break;
+        --j;
+      }
+      __threadfence();
+      atomicExch(&Q.status[w], kInc | (unsigned long long)(prefix + world_total));
+    }
+    s_misc[3] = (int)(prefix >> 31);
+    s_misc[4] = (int)(prefix & 0x7fffffff);
+  }
+  __syncthreads();
+  const int64_t base = ((int64_t)s_misc[3] << 31) | (int64_t)s_misc[4];
+  BP_MARK(6);
+  // 5: emit (records [base, base + world_total)); a candidate that does not fit
+  // is skipped, and the smallest such offset is the count of whole pairs
+  for (int i = tid; i < n_cand; i += kBpThreads) {
+    const int k = perm[i];
+    const int off = ncon[k];
+    const int next = (k + 1 < n_cand) ? ncon[k + 1] : world_total;
+    if (next == off) continue;
+    if (base + next > Q.capacity) {
+      atomicMin(reinterpret_cast<unsigned long long*>(Q.queue + 2), (unsigned long long)(base + off));
+      continue;
+    }
+    const uint32_t pv = list[k];
+    pair_contacts<true>(P, make_int2((int)(pv >> 16), (int)(pv & 0xffffu)), Fw, w, base + off, &Ts);
+  }
+  BP_MARK(7);
+  // the last CTA: device count, error, reset of the counters for the next launch
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(&Q.queue[1], 1) == (int)gridDim.x - 1) {
+      const unsigned long long vl = atomicAdd(&Q.status[P.n_worlds - 1], 0ull);
+      const int64_t total = (int64_t)(vl & ((1ull << 62) - 1));
+      const unsigned long long cut = atomicAdd(reinterpret_cast<unsigned long long*>(Q.queue + 2), 0ull);
+      if (total > Q.capacity) atomicOr(Q.err, ERR_CONTACT_CAP);
+      Q.n_dev[0] = (int64_t)cut < total ? (int64_t)cut : total;
+      if (Q.total) *Q.total = total;
+    }
+  }
 }
 
 }  // namespace
+
+size_t collide_bp_smem(int n_geoms, int cap_c, int np2) {
+  return (size_t)5 * n_geoms * sizeof(float4) + (size_t)2 * np2 * sizeof(uint32_t) +
+         (size_t)(3 * n_geoms + 2) * sizeof(int) + (size_t)cap_c * (sizeof(uint32_t) + sizeof(int) + sizeof(uint16_t));
+}
+
+cudaError_t collide_broadphase(const CollideParams& P, int cap_c, int64_t capacity, unsigned long long* status,
+                               int* queue, int64_t* n_dev, int64_t* total, int* err, cudaStream_t s) {
+  if (P.n_worlds == 0) return cudaMemsetAsync(n_dev, 0, sizeof(int64_t), s);
+  int np2 = 1;
+  while (np2 < P.n_geoms) np2 <<= 1;
+  const size_t smem = collide_bp_smem(P.n_geoms, cap_c, np2);
+  // zeroed status words and counters; queue[2..3]: the cut (int64) starts at
+  // 0x7f7f...7f (above any count); memsets only, so the launch is graph-capturable
+  cudaError_t e = cudaMemsetAsync(status, 0, (size_t)P.n_worlds * sizeof(unsigned long long), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(queue, 0, 2 * sizeof(int), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(queue + 2, 0x7f, sizeof(int64_t), s);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_collide_bp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  BpParams Q{cap_c, np2, capacity, status, queue, n_dev, total, err};
+  k_collide_bp<<<(unsigned)P.n_worlds, kBpThreads, smem, s>>>(P, Q);
+  return cudaGetLastError();
+}
 
 // counts: [n_worlds * n_pairs + 1] int32 scratch, offs: same size; temp: CUB
 // scratch (temp == nullptr queries *temp_bytes).  Writes the total to *total_dev.

@@ -19,7 +19,8 @@ enum : int {
   ERR_IMPEDANCE = 64,   // per-contact (k_user, d_user) negative or non-finite
   ERR_WORLD_CONTACTS = 128, // more contacts in one world than the S6 fixed-point bound (65536)
   ERR_ARTICULATION = 256,   // articulated upstream: M(q) not positive definite, or a bad chain/link id
-  ERR_CONTACT_CAP = 512     // collision front-end (device count): more contacts than the capacity
+  ERR_CONTACT_CAP = 512,    // collision front-end (device count): more contacts than the capacity
+  ERR_CANDIDATES = 1024     // broadphase: more candidate pairs in one world than the shared-memory list holds
 };
 
 // State slab: per world, 13 planes of Bp floats (px py pz qw qx qy qz vx vy vz
@@ -132,6 +133,13 @@ struct CollideParams {
   int n_geoms;
 };
 cudaError_t collide_frames(const CollideParams& P, cudaStream_t s);
+// Broadphase mode (no candidate list): one CTA per world finds the candidates
+// (sort-and-sweep on grown AABBs) and emits their contacts with a chained scan
+// over worlds.  status [n_worlds] and queue [4 ints] are scratch; n_dev gets
+// the count of whole pairs within `capacity`, total (optional) every contact.
+size_t collide_bp_smem(int n_geoms, int cap_c, int np2);
+cudaError_t collide_broadphase(const CollideParams& P, int cap_c, int64_t capacity, unsigned long long* status,
+                               int* queue, int64_t* n_dev, int64_t* total, int* err, cudaStream_t s);
 cudaError_t collide_count_scan(const CollideParams& P, int32_t* counts, int32_t* offs, void* temp,
                                size_t* temp_bytes, cudaStream_t s);
 // n_dev != null: also stores the (clamped) total for the asynchronous mode

@@ -142,6 +142,6 @@ def test_product_path_has_no_oracle_dependency():
     pkg = os.path.join(ROOT, "paper_2603_12185_b200")
     for dirpath, _, files in os.walk(pkg):
         for f in files:
-            if f.endswith((".py", ".cu", ".cpp", ".h")):
+            if f.endswith((".py", ".cu", ".cuh", ".cpp", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "oracle" not in txt.lower() or f == "__init__.py" and "oracle" not in txt, f

@@ -273,8 +273,8 @@ def test_random_capsules_boxes_spheres(seed):
 
 def test_closed_loop_pile_sampled_worlds():
     """The pile's full step at bench size (1024 worlds x 500 bodies, the
-    config-4 geometry, GPU collision then the step, as bench.py --collide
-    runs it) for 10 steps; sampled worlds run the same loop in the oracle
+    config-4 geometry in broadphase mode, GPU collision then the step, as
+    bench.py --collide runs it) for 10 steps; sampled worlds run the same loop in the oracle
     (oracle collision -> oracle step from its own state).  Contact counts
     agree each step up to candidates within 2e-5 of the emission threshold
     (where fp32 and fp64 may decide differently; such a contact's gap is
@@ -282,15 +282,15 @@ def test_closed_loop_pile_sampled_worlds():
     state element is within the trajectory tolerance after 10 steps."""
     import paper_2603_12185_b200 as cf
     scene, st, _ = scenes.c4_pile(n_worlds=1024, contacts_per_world=2000)
-    geo = scenes.pile_geometry((10, 10, 5))
+    geo = scenes.pile_geometry((10, 10, 5), broadphase=True)     # bench.py --collide's geometry
     ctx = cf.Context(CFG)
     ctx.load_scene(scene, st.n_worlds, st)
     ctx.load_geometry(geo)
     sample = (0, 517, 1023)
     so = st.astype(np.float64)
     so = State(*(getattr(so, k)[list(sample)] for k in ("pos", "quat", "vel", "omega", "qpos", "qvel")))
-    loose = Geometry(geo.kind, geo.body, geo.link, geo.size, geo.local, geo.pairs, margin=1e9, mu=geo.mu,
-                     condim=geo.condim)
+    loose = Geometry(geo.kind, geo.body, geo.link, geo.size, geo.local, geo.pairs, margin=geo.margin + 4e-5,
+                     mu=geo.mu, condim=geo.condim)
     for k in range(10):
         dc, _ = ctx.collide(capacity=1024 * 4000)
         wg = dc.world.cpu().numpy()
@@ -333,3 +333,107 @@ def test_device_count_overflow_keeps_whole_pairs():
     with pytest.raises(cf.ComfreeError) as ei:
         ctx.check()
     assert ei.value.status == 3
+
+
+# ---------------------------------------------------------------- broadphase mode (reading R32)
+def _compare_off_threshold(dc, link, ref, margin, band=2e-6):
+    """Contact lists equal (ids exact, same order; records within fp32
+    tolerance) once the records whose gap lies within `band` of the emission
+    threshold are dropped from both (there fp32 and fp64 may decide
+    differently; 2e-6 m is ~20x the fp32 error of a gap at these sizes)."""
+    g_phi = dc.c0.cpu().numpy()[:, 3]
+    gk = np.abs(g_phi - margin) >= band
+    rk = np.abs(ref.c0[:, 3] - margin) >= band
+    assert gk.sum() == rk.sum(), (gk.sum(), rk.sum())
+    c3 = dc.c3.cpu().numpy()[gk]
+    np.testing.assert_array_equal(dc.world.cpu().numpy()[gk], ref.world[rk])
+    np.testing.assert_array_equal(c3[:, 0], ref.body_a[rk])
+    np.testing.assert_array_equal(c3[:, 1], ref.body_b[rk])
+    np.testing.assert_array_equal(link.cpu().numpy()[gk], ref.meta["link"][rk])
+    assert_close(dc.c0.cpu().numpy()[gk, :3], ref.c0[rk, :3], rtol=0, atol=2e-6, what="contact point")
+    assert_close(g_phi[gk], ref.c0[rk, 3], rtol=0, atol=1e-6, what="phi")
+    assert_close(dc.c1.cpu().numpy()[gk], ref.c1[rk], rtol=0, atol=2e-5, what="normal, mu_t")
+    assert_close(dc.c2.cpu().numpy()[gk], ref.c2[rk], rtol=0, atol=2e-5, what="t1, mu_tor")
+
+
+def test_broadphase_pile_matches_oracle():
+    """Config-4 pile geometry without a candidate list: the GPU's sort-and-
+    sweep broadphase + narrowphase (one kernel, chained scan over worlds) gives
+    the oracle's contact list -- ids exact and in the same order (candidate
+    pairs in (g1, g2) order), records within fp32 tolerance -- including the
+    diagonal neighbours and box-box edge-edge contacts the fixed lattice list
+    missed."""
+    import paper_2603_12185_b200 as cf
+    scene, st, _ = scenes.c4_pile(n_worlds=6, contacts_per_world=2000)
+    geo = scenes.pile_geometry((10, 10, 5), broadphase=True)
+    ctx = cf.Context(CFG)
+    ctx.load_scene(scene, st.n_worlds, st)
+    ctx.load_geometry(geo)
+    dc, link = ctx.collide(capacity=6 * 4000)
+    st64 = st.astype(np.float64)
+    ref = co.collide(geo, st64, None)
+    assert ref.n > 6 * 1100
+    lattice = co.collide(scenes.pile_geometry((10, 10, 5)), st64, None)
+    assert ref.n > lattice.n                       # more than the fixed candidate list found
+    _compare_off_threshold(dc, link, ref, geo.margin)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_broadphase_random_scenes_match_oracle(seed):
+    """Random spheres / boxes / capsules above a plane, random orientations
+    (every pair kind, edge-edge included), broadphase mode."""
+    import paper_2603_12185_b200 as cf
+    from harness.types import Scene
+    from test_oracle_collision import _random_geometry, _random_poses
+    geo = _random_geometry(seed, n=14)
+    stt = _random_poses(seed, 12, 14)
+    st32 = stt.astype(np.float32)
+    st64 = st32.astype(np.float64)
+    scene = Scene(np.full(14, 2.0, np.float32), np.full((14, 3), 500.0, np.float32))
+    ctx = cf.Context(CFG)
+    ctx.load_scene(scene, 12, st32)
+    ctx.load_geometry(geo)
+    dc, link = ctx.collide(capacity=12 * 200)
+    ref = co.collide(geo, st64, None)
+    assert ref.n > 50
+    _compare_off_threshold(dc, link, ref, geo.margin)
+
+
+def test_broadphase_device_count_overflow_and_graph():
+    """Device-count mode of the broadphase: the whole-pair count on overflow
+    (records below it equal the unbounded run's), COMFREE_ERR_CAPACITY at the
+    next check; and the launch replays in a CUDA graph (memsets + one kernel,
+    the counters reset themselves) with the same records."""
+    import torch
+    import paper_2603_12185_b200 as cf
+    scene, st, _ = scenes.c4_pile(n_worlds=5, contacts_per_world=2000)
+    geo = scenes.pile_geometry((10, 10, 5), broadphase=True)
+    ctx = cf.Context(CFG)
+    ctx.load_scene(scene, 5, st)
+    ctx.load_geometry(geo)
+    full, _ = ctx.collide(capacity=5 * 4000, device_count=True)
+    nf = int(full.n_dev.item())
+    ref = {k: getattr(full, k)[:nf].cpu().numpy().copy() for k in ("world", "c0", "c3")}
+    ctx2 = cf.Context(CFG)
+    ctx2.load_scene(scene, 5, st)
+    ctx2.load_geometry(geo)
+    part, _ = ctx2.collide(capacity=nf // 2, device_count=True)
+    n = int(part.n_dev.item())
+    assert 0 < n <= nf // 2
+    for k in ("world", "c0", "c3"):
+        np.testing.assert_array_equal(getattr(part, k)[:n].cpu().numpy(), ref[k][:n])
+    with pytest.raises(cf.ComfreeError) as ei:
+        ctx2.check()
+    assert ei.value.status == 3
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        ctx.collide(capacity=5 * 4000, device_count=True, stream=s)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    dc, _ = ctx.collide(capacity=5 * 4000, device_count=True)
+    assert int(dc.n_dev.item()) == nf
+    for k in ("world", "c0", "c3"):
+        np.testing.assert_array_equal(getattr(dc, k)[:nf].cpu().numpy(), ref[k])

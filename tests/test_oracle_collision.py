@@ -267,10 +267,9 @@ def _rand_R(rng):
 
 def test_box_edge_edge_depth_is_the_minimum_over_all_directions():
     """For interpenetrating boxes the penetration depth is the minimum overlap
-    of the projections over ALL directions; the SAT's 15 axes attain it, so
-    densely sampled directions never go below R33's overlap and come close
-    it is attained along the contact normal, which is perpendicular to an
-    edge of each box."""
+    of the projections over ALL directions and the SAT's 15 axes attain it:
+    densely sampled directions never go below R33's overlap, which is attained
+    along the contact normal, itself perpendicular to an edge of each box."""
     rng = np.random.default_rng(11)
     u = rng.normal(size=(40000, 3))
     u /= np.linalg.norm(u, axis=1, keepdims=True)
