@@ -63,6 +63,7 @@ struct comfree_ctx {
   // host-input staging
   DevBuf in_world, in_off, in_c0, in_c1, in_c2, in_c3, in_jrow, in_kd, in_fext, in_L, in_tau, imp;
   DevBuf st_tmp;
+  DevBuf gscratch;  // step working sets of worlds beyond shared memory
   // COMFREE_MEM_HOST_ASYNC: two staging slots, a copy-in and a copy-out stream
   struct AsyncSlot {
     DevBuf world, off, c0, c1, c2, c3, jrow, kd, fext, L, tau, out;
@@ -656,9 +657,14 @@ comfree_status comfree_step(comfree_ctx* ctx, const comfree_worlds* wd, const co
     if (v == 1 || v == 2 || v == 4 || v == 8) wpw = v;
   }
   const size_t smem_need = cf::step_smem_bytes(sc, wpw);
-  if (smem_need > 227 * 1024)
-    return fail(ctx, COMFREE_ERR_CAPACITY, "step: %d bodies per world need %zu B of shared memory (> 227 KB)", sc.B,
-                smem_need);
+  P.gscratch = nullptr;
+  if (smem_need > 227 * 1024) {
+    // the world's working set does not fit a CTA's shared memory: one CTA of 8
+    // warps per world over a global (L2-resident) scratch slab
+    wpw = 8;
+    CUDA_TRY(ctx, ensure(ctx->gscratch, std::max<int64_t>(1, nw) * cf::step_world_floats(sc) * sizeof(float)));
+    P.gscratch = static_cast<float*>(ctx->gscratch.p);
+  }
   int st_e0 = -1, st_e1 = -1;
   if (ctx->timing) {
     cudaEvent_t e = next_event(ctx, &st_e0);
@@ -1205,7 +1211,7 @@ void comfree_destroy(comfree_ctx* ctx) {
                     &ctx->sj, &ctx->skd, &ctx->nf, &ctx->foff, &ctx->cub_tmp, &ctx->in_world, &ctx->in_off, &ctx->in_c0,
                     &ctx->in_c1, &ctx->in_c2, &ctx->in_c3, &ctx->in_jrow, &ctx->in_kd, &ctx->in_fext, &ctx->in_L,
                     &ctx->in_tau, &ctx->imp, &ctx->st_tmp, &ctx->art, &ctx->geo, &ctx->col_counts,
-                    &ctx->col_offs, &ctx->col_tmp, &ctx->col_frames, &ctx->bp_status, &ctx->bp_queue, &ctx->bp_count};
+                    &ctx->col_offs, &ctx->col_tmp, &ctx->col_frames, &ctx->bp_status, &ctx->bp_queue, &ctx->bp_count, &ctx->gscratch};
   for (DevBuf* b : bufs) release(*b);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->slab) cudaFree(ctx->slab);

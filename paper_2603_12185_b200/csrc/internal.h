@@ -73,6 +73,7 @@ struct StepParams {
   unsigned long long* first_bad;// min world id with a non-finite state
   int* queue;                   // persistent kernel: [next world ticket, CTAs done], 0 between launches
   int64_t pf_ahead;             // > 0: prefetch world w + pf_ahead into L2 during world w (resident world slots)
+  float* gscratch;              // non-null: per-world working set in global memory (worlds beyond shared memory)
   int64_t world_base;           // absolute id of world 0 of the range (error reporting)
   int check_finite;
   int exact_diag;               // per-facet impedance, general variants only: 1 Eq. (11) (COMFREE_FLAG_EXACT_DIAGONAL),
@@ -82,6 +83,7 @@ struct StepParams {
 
 // Launchers (return cudaError_t of the launch).
 cudaError_t launch_step(const StepParams& p, int warps_per_world, cudaStream_t s);
+size_t step_world_floats(const SceneDev& sc);  // floats of one world's working set (shared or global)
 // persistent variant (free bodies only): one 32-warp CTA per SM, worlds staged by TMA
 cudaError_t launch_step_persist(const StepParams& p, cudaStream_t s);
 size_t step_persist_smem_bytes(const SceneDev& sc);

@@ -8,6 +8,8 @@ cudaError_t launch_step_w2(const StepParams& p, cudaStream_t s);
 cudaError_t launch_step_w4(const StepParams& p, cudaStream_t s);
 cudaError_t launch_step_w8(const StepParams& p, cudaStream_t s);
 
+size_t step_world_floats(const SceneDev& sc) { return (size_t)group_layout(sc).total; }
+
 size_t step_smem_bytes(const SceneDev& sc, int wpw) {
   return (size_t)(kWarps / wpw) * group_layout(sc).total * sizeof(float);
 }

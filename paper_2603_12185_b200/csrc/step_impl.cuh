@@ -576,7 +576,11 @@ __device__ __forceinline__ void prefetch_world_l2(const StepParams& P, int64_t w
 // One world's step (S0-S8) by the world group `group` (WPW warps) of the CTA.
 // stg: the world's slab planes 0-12 already staged in shared memory (the
 // persistent kernel's TMA bulk copy), else null (S1 and S7 read the slab in HBM).
-template <int CW, int WPW, bool FAST, bool TREES, bool IMP>
+// GMEM: the world's working set (body records, fixed-point accumulators, chain
+// data) lives in a global scratch slab (P.gscratch, L2-resident) instead of
+// shared memory, for worlds too large for a CTA's 227 KB (about 2070 bodies):
+// the same code with global loads and global integer atomics.
+template <int CW, int WPW, bool FAST, bool TREES, bool IMP, bool GMEM = false>
 __device__ __forceinline__ void world_step(const StepParams& P, float* smem, const int64_t w, const int group,
                                            const float* stg) {
   const SceneDev& sc = P.sc;
@@ -586,7 +590,7 @@ __device__ __forceinline__ void world_step(const StepParams& P, float* smem, con
   const int lane = threadIdx.x & 31;
 
   TL_MARK(0);
-  float* G = smem + (size_t)group * GL.total;
+  float* G = GMEM ? P.gscratch + (size_t)w * GL.total : smem + (size_t)group * GL.total;
   float4* rec = reinterpret_cast<float4*>(G + GL.rec);
   unsigned* accl = reinterpret_cast<unsigned*>(G + GL.accl);
   float4* tq = reinterpret_cast<float4*>(G + GL.tq);
@@ -1238,14 +1242,14 @@ __device__ __forceinline__ void world_step(const StepParams& P, float* smem, con
   }
 }
 
-template <int CW, int WPW, bool FAST, bool TREES, bool IMP>
+template <int CW, int WPW, bool FAST, bool TREES, bool IMP, bool GMEM = false>
 __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 2 : (CW == 32 ? 1 : 16))) k_step(const __grid_constant__ StepParams P) {
   extern __shared__ float4 smem4[];
   constexpr int kGroups = CW / WPW;
   const int group = threadIdx.x / (WPW * 32);
   const int64_t w = (int64_t)blockIdx.x * kGroups + group;
   if (w >= P.n_worlds) return;  // whole group leaves together
-  world_step<CW, WPW, FAST, TREES, IMP>(P, reinterpret_cast<float*>(smem4), w, group, nullptr);
+  world_step<CW, WPW, FAST, TREES, IMP, GMEM>(P, reinterpret_cast<float*>(smem4), w, group, nullptr);
 }
 
 // ---- persistent variant: CTAs that step their worlds in turn ----
@@ -1359,13 +1363,13 @@ cudaError_t launch_persist_variant(const StepParams& p, cudaStream_t s, int n_sm
   return cudaGetLastError();
 }
 
-template <int CW, int WPW, bool FAST, bool TREES, bool IMP>
+template <int CW, int WPW, bool FAST, bool TREES, bool IMP, bool GMEM = false>
 cudaError_t launch_variant(const StepParams& p, cudaStream_t s) {
   const int groups = CW / WPW;
-  const size_t smem = (size_t)groups * group_layout(p.sc).total * sizeof(float);
+  const size_t smem = GMEM ? 0 : (size_t)groups * group_layout(p.sc).total * sizeof(float);
   const unsigned grid = (unsigned)((p.n_worlds + groups - 1) / groups);
   if (grid == 0) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(k_step<CW, WPW, FAST, TREES, IMP>,
+  cudaError_t e = cudaFuncSetAttribute(k_step<CW, WPW, FAST, TREES, IMP, GMEM>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   StepParams q = p;
@@ -1374,11 +1378,11 @@ cudaError_t launch_variant(const StepParams& p, cudaStream_t s) {
   if (pf && atoi(pf) != 0) {
     int dev = 0, n_sm = 0, per_sm = 0;
     if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step<CW, WPW, FAST, TREES, IMP>, CW * 32, smem) == cudaSuccess &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step<CW, WPW, FAST, TREES, IMP, GMEM>, CW * 32, smem) == cudaSuccess &&
         (int64_t)grid > (int64_t)n_sm * per_sm)
       q.pf_ahead = (int64_t)n_sm * per_sm * groups;  // worlds resident at once
   }
-  k_step<CW, WPW, FAST, TREES, IMP><<<grid, CW * 32, smem, s>>>(q);
+  k_step<CW, WPW, FAST, TREES, IMP, GMEM><<<grid, CW * 32, smem, s>>>(q);
   return cudaGetLastError();
 }
 
@@ -1387,6 +1391,10 @@ cudaError_t launch_variant(const StepParams& p, cudaStream_t s) {
 template <int CW, int WPW>
 cudaError_t launch_cfg(const StepParams& p, cudaStream_t s) {
     const bool trees = p.sc.T > 0, imp = p.impulses != nullptr || p.wstats != nullptr;
+  if (WPW == kWarps && p.gscratch) {  // worlds beyond shared memory: the global-scratch variant (general facets)
+    if (trees) return imp ? launch_variant<CW, WPW, false, true, true, true>(p, s) : launch_variant<CW, WPW, false, true, false, true>(p, s);
+    return imp ? launch_variant<CW, WPW, false, false, true, true>(p, s) : launch_variant<CW, WPW, false, false, false, true>(p, s);
+  }
   if (p.n_t == 4 && p.power_is_2 && !p.exact_diag) {
     if (trees) return imp ? launch_variant<CW, WPW, true, true, true>(p, s) : launch_variant<CW, WPW, true, true, false>(p, s);
     return imp ? launch_variant<CW, WPW, true, false, true>(p, s) : launch_variant<CW, WPW, true, false, false>(p, s);
