@@ -51,6 +51,10 @@ def parse(argv=None):
                     help="L2 flush between timed steps: write 256 MB (leaves L2 full of dirty lines whose "
                          "write-back the next step pays), or write then read it back (cold, clean L2)")
     ap.add_argument("--no-graph", action="store_true", help="direct launches instead of CUDA-graph replay")
+    ap.add_argument("--reset-state", action="store_true",
+                    help="restore the initial state before every step (untimed, with the L2 flush): for variants "
+                         "whose dynamics do not stay bounded over hundreds of steps of the same contact set "
+                         "(e.g. --impedance exact_diagonal, Eq. (11) per facet, reading R24)")
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -79,8 +83,8 @@ def parse(argv=None):
     ap.add_argument("--workload", default="pile", choices=["pile", "hand", "mixed"],
                     help="pile: config 4 (the BASELINE metric); hand: config 3; mixed: config 5")
     a = ap.parse_args(argv)
-    if a.collide:
-        a.upstream = True
+    if a.collide and a.workload != "pile":
+        a.upstream = True              # closed-loop hands: collide -> upstream -> step
     if a.worlds is None:
         a.worlds = {"hand": 4096, "mixed": 65536}.get(a.workload, 1024)
     return a
@@ -495,10 +499,21 @@ def run_ours(args, rank, world_size, local):
     flush = None if args.no_flush else torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     flush_sink = torch.empty(1, dtype=torch.float32, device=dev)
 
+    if args.reset_state:               # initial states kept on the device
+        for p in parts:
+            p.init_dev = {k: torch.from_numpy(np.ascontiguousarray(getattr(p.st, k), np.float32)).to(dev)
+                          for k in ("pos", "quat", "vel", "omega", "qpos", "qvel")}
+
+    def reset():
+        if args.reset_state:
+            for p in parts:
+                p.ctx.set_state_device(p.init_dev, stream=stream)
+
     def flush_l2():
         """Evict L2 between timed steps (untimed): write a 256 MB buffer (> the
         126 MB L2); in write+read mode read it back so the lines left in L2 are
         clean (the dirty lines' write-back happens here, not in the next step)."""
+        reset()
         flush.zero_()
         if args.flush_mode == "write+read":
             torch.sum(flush, dim=0, keepdim=True, out=flush_sink)
@@ -524,6 +539,7 @@ def run_ours(args, rank, world_size, local):
             s0.wait_stream(p.stream)
 
     for _ in range(max(args.warmup, 3)):
+        reset()
         one_step(stream)
     torch.cuda.synchronize()
     for p in parts:                                   # collision-built contacts: the step's real count
@@ -648,9 +664,14 @@ def run_ours(args, rank, world_size, local):
     def pinned(a):
         return None if a is None else torch.from_numpy(np.ascontiguousarray(a, np.float32)).pin_memory().numpy()
     for p in parts:
+        if args.collide:                 # closed loop: contacts come from the GPU front-end, no host inputs
+            p.out_host = {k: torch.empty(v.shape, dtype=torch.float32).pin_memory().numpy() for k, v in p.final.items()}
+            d2h += sum(v.nbytes for v in p.out_host.values())
+            continue
         p.hc = cf.HostContacts.from_arrays(p.c, pin=True, n_worlds=None if args.world_ids else p.W)
         p.hca = cf.HostContacts.from_arrays(p.c, pin=True, asynchronous=True, n_worlds=None if args.world_ids else p.W)
         p.inp_h = None if p.inp is None else Inputs(*(pinned(a) for a in (p.inp.f_ext, p.inp.tree_L, p.inp.tree_tau)))
+        reset()
         p.ctx.step(p.hc, p.inp_h, dt=cfg.dt)          # warm the staging buffers
         p.ctx.step(p.hca, p.inp_h, dt=cfg.dt)
         p.ctx.step(p.hca, p.inp_h, dt=cfg.dt)
@@ -673,6 +694,12 @@ def run_ours(args, rank, world_size, local):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(e2e_steps):
+            if args.collide:             # the closed-loop step on the device, the state read back
+                one_step(stream)
+                for p in parts:
+                    p.ctx.get_state_async(p.out_host, stream=stream)
+                continue
+            reset()                      # --reset-state only: a device-side state copy (~10 us)
             for p in parts:
                 if asynchronous:
                     p.ctx.step(p.hca, p.inp_h, dt=cfg.dt, stream=stream)
@@ -689,10 +716,10 @@ def run_ours(args, rank, world_size, local):
         for p in parts:
             p.ctx.check(stream)                       # latched errors of the asynchronous calls
         return reduce_max(e0.elapsed_time(e1), dev)
-    e2e_serial_ms = e2e_run(False)
+    e2e_serial_ms = e2e_run(False) if not args.collide else float("nan")
     e2e_ms = e2e_run(True)
     e2e_value = total_worlds * e2e_steps / (e2e_ms * 1e-3)
-    e2e_serial_value = total_worlds * e2e_steps / (e2e_serial_ms * 1e-3)
+    e2e_serial_value = total_worlds * e2e_steps / (e2e_serial_ms * 1e-3) if not args.collide else None
 
     cpu = None
     if rank == 0:                      # rank 0 only (the other ranks wait at the barrier)
@@ -718,6 +745,8 @@ def run_ours(args, rank, world_size, local):
                                if args.flush_mode == "write+read" else "flushed between timed steps (256 MB write)")
                               if flush is not None else "not flushed"),
                        "footprint_mb_per_step": alg_total / 1e6,
+                       "state": "reset to the initial state before every step (untimed)" if args.reset_state
+                                else "evolving",
                        "articulated_upstream": bool(args.upstream),
                        "upstream_mb_per_step": alg_up / 1e6,
                        "parallelism": f"world-sharded x{world_size}"},
@@ -735,11 +764,15 @@ def run_ours(args, rank, world_size, local):
             "clocks": clock.summary(),
             "e2e": {"value": e2e_value, "unit": "world-steps/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "steps": e2e_steps,
-                    "mode": "pinned host buffers through comfree_step / comfree_get_state (COMFREE_MEM_HOST_ASYNC): "
-                            "step k+1's upload overlaps step k's kernel and download",
+                    "mode": ("closed loop on the device (collision front-end every step), the state downloaded "
+                             "every step into pinned host memory (COMFREE_MEM_HOST_ASYNC); no per-step host inputs"
+                             if args.collide else
+                             "pinned host buffers through comfree_step / comfree_get_state (COMFREE_MEM_HOST_ASYNC): "
+                             "step k+1's upload overlaps step k's kernel and download"),
                     "ms_per_step": e2e_ms / e2e_steps,
                     "pcie_gbs": (h2d + d2h) / (e2e_ms / e2e_steps * 1e-3) / 1e9,
-                    "serial_value": e2e_serial_value, "serial_ms_per_step": e2e_serial_ms / e2e_steps},
+                    "serial_value": e2e_serial_value,
+                    "serial_ms_per_step": None if args.collide else e2e_serial_ms / e2e_steps},
             "cpu_baseline": cpu,
             "allgather_final_state_mb": gathered_mb,
             "sharded_verification": verification,

@@ -277,6 +277,13 @@ comfree_status comfree_get_state(comfree_ctx* ctx, int64_t first_world, int64_t 
 comfree_status comfree_set_state(comfree_ctx* ctx, int64_t first_world, int64_t n_worlds,
                                   const comfree_state* in, void* stream);
 
+/* World first_world + i (0 <= i < n_src * repeat) takes source state i / repeat
+ * of *in (n_src worlds in the public layout, HOST or DEVICE): e.g. MPPI's
+ * live states broadcast to every rollout world of their problem, with only
+ * the n_src source states crossing PCIe (the replication runs on the device). */
+comfree_status comfree_set_state_broadcast(comfree_ctx* ctx, int64_t first_world, int64_t n_src, int64_t repeat,
+                                           const comfree_state* in, void* stream);
+
 /* ---- Articulated upstream ----------------------------
  * The step takes each chain's Cholesky factor of M(q), tau - c(q, v) and the
  * J rows of chain-side contacts as inputs (Eq. (1)-(2), P:80-97;
@@ -424,6 +431,14 @@ comfree_status comfree_mppi_cost_control(comfree_ctx* ctx, int64_t first_world, 
 comfree_status comfree_mppi_update(comfree_ctx* ctx, int32_t n_problems, int32_t n_samples, int32_t horizon,
                                    const float* J, const float* U, float lambda, float lo, float hi, float* plan,
                                    float* weights, void* stream);
+
+/* comfree_mppi_update plus the receding-horizon shift, in the same launch:
+ * u0[P][Q] (DEVICE) receives the new plan's first action and plan[P][H][Q]
+ * the new plan advanced by one step (its last step 0).  A problem whose costs
+ * are all non-finite keeps its plan (shifted the same way). */
+comfree_status comfree_mppi_update_shift(comfree_ctx* ctx, int32_t n_problems, int32_t n_samples, int32_t horizon,
+                                         const float* J, const float* U, float lambda, float lo, float hi, float* plan,
+                                         float* weights, float* u0, void* stream);
 
 /* Aggregate statistics of the last step (requires COMFREE_FLAG_STATS for
  * contacts / facets / penetration / energy; the non-finite check is always

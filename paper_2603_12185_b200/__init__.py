@@ -415,6 +415,24 @@ class Context:
         self._check(self._lib.comfree_set_state(self.h, int(first_world), nw, ct.byref(st),
                                                 _stream_handle(stream)), "comfree_set_state")
 
+    def set_state_device(self, state: dict, first_world: int = 0, stream=None):
+        """comfree_set_state from caller-owned device tensors (async)."""
+        nw = int(state["pos"].shape[0])
+        st = _lib.comfree_state(*[_ptr(state.get(k)) if state.get(k) is not None and state[k].numel() else None
+                                  for k in ("pos", "quat", "vel", "omega", "qpos", "qvel")], MEM_DEVICE)
+        self._check(self._lib.comfree_set_state(self.h, int(first_world), nw, ct.byref(st), _stream_handle(stream)),
+                    "comfree_set_state")
+
+    def set_state_broadcast(self, state, repeat: int, first_world: int = 0, stream=None):
+        """comfree_set_state_broadcast: world first_world + i takes source
+        state i // repeat (host numpy State of n_src worlds)."""
+        arrs = [np.ascontiguousarray(getattr(state, k), np.float32)
+                for k in ("pos", "quat", "vel", "omega", "qpos", "qvel")]
+        n_src = int(arrs[0].shape[0])
+        st = _lib.comfree_state(*[a.ctypes.data if a.size else None for a in arrs], MEM_HOST)
+        self._check(self._lib.comfree_set_state_broadcast(self.h, int(first_world), n_src, int(repeat), ct.byref(st),
+                                                          _stream_handle(stream)), "comfree_set_state_broadcast")
+
     def get_stats(self, stream=None) -> dict:
         s = _lib.comfree_stats()
         self._check(self._lib.comfree_get_stats(self.h, ct.byref(s), _stream_handle(stream)),

@@ -111,6 +111,9 @@ SIGNATURES = {
                                              P, ct.c_int32, ct.c_int32, ct.c_float, ct.c_float, P, P, P]),
     "comfree_mppi_update": (ct.c_int, [P, ct.c_int32, ct.c_int32, ct.c_int32, P, P, ct.c_float, ct.c_float, ct.c_float,
                                        P, P, P]),
+    "comfree_mppi_update_shift": (ct.c_int, [P, ct.c_int32, ct.c_int32, ct.c_int32, P, P, ct.c_float, ct.c_float,
+                                             ct.c_float, P, P, P, P]),
+    "comfree_set_state_broadcast": (ct.c_int, [P, ct.c_int64, ct.c_int64, ct.c_int64, P, P]),
     "comfree_collide": (ct.c_int, [P, ct.c_int64, ct.c_int64, ct.c_int64, P, P, P, P, P, P, P, P, P]),
     "comfree_articulation_update": (ct.c_int, [P, ct.c_int64, ct.c_int64, P, P, P, ct.c_int64, P, P, P, P, P, P, P]),
     "comfree_get_world_stats": (ct.c_int, [P, ct.c_int64, ct.c_int64, P, ct.c_int32, P]),

@@ -1104,6 +1104,55 @@ comfree_status comfree_mppi_update(comfree_ctx* ctx, int32_t P, int32_t N, int32
   return COMFREE_OK;
 }
 
+comfree_status comfree_mppi_update_shift(comfree_ctx* ctx, int32_t P, int32_t N, int32_t H, const float* J,
+                                         const float* U, float lambda, float lo, float hi, float* plan, float* weights,
+                                         float* u0, void* stream) {
+  if (!ctx) return COMFREE_ERR_INVALID_ARGUMENT;
+  if (!ctx->loaded) return fail(ctx, COMFREE_ERR_STATE, "mppi_update_shift before load_scene");
+  if (P < 0 || N < 1 || H < 1 || (P > 0 && (!J || !U || !plan || !u0)))
+    return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "mppi_update_shift: sizes / arrays");
+  if (!(lambda > 0.f) || !(lo <= hi)) return fail(ctx, COMFREE_ERR_VALIDATION, "mppi_update_shift: lambda > 0 and lo <= hi");
+  if ((size_t)N * sizeof(float) > 48 * 1024) return fail(ctx, COMFREE_ERR_CAPACITY, "mppi_update_shift: more than 12288 samples per problem");
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  CUDA_TRY(ctx, cf::mppi_update(J, U, P, N, H, ctx->sc.Q, lambda, lo, hi, plan, weights, static_cast<cudaStream_t>(stream), u0));
+  ctx->launches += P > 0;
+  return COMFREE_OK;
+}
+
+comfree_status comfree_set_state_broadcast(comfree_ctx* ctx, int64_t first, int64_t n_src, int64_t repeat,
+                                           const comfree_state* in, void* stream) {
+  if (!ctx || !in) return COMFREE_ERR_INVALID_ARGUMENT;
+  if (!ctx->loaded) return fail(ctx, COMFREE_ERR_STATE, "set_state_broadcast before load_scene");
+  if (first < 0 || n_src < 0 || repeat < 1 || first + n_src * repeat > ctx->W)
+    return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "set_state_broadcast: range");
+  const cf::SceneDev& sc = ctx->sc;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  const float *pos = in->pos, *quat = in->quat, *vel = in->vel, *om = in->omega, *qp = in->qpos, *qv = in->qvel;
+  if (in->location == COMFREE_MEM_HOST) {  // the n_src source states only go over PCIe
+    const size_t nb = (size_t)n_src * sc.B, nq = (size_t)n_src * sc.Q;
+    CUDA_TRY(ctx, ensure(ctx->st_tmp, std::max<size_t>(1, nb * 13 + nq * 2) * sizeof(float)));
+    float* d = static_cast<float*>(ctx->st_tmp.p);
+    float* dp[6] = {d, d + 3 * nb, d + 7 * nb, d + 10 * nb, d + 13 * nb, d + 13 * nb + nq};
+    const float* hp[6] = {pos, quat, vel, om, qp, qv};
+    const size_t cnt[6] = {3 * nb, 4 * nb, 3 * nb, 3 * nb, nq, nq};
+    const float* res[6];
+    for (int k = 0; k < 6; ++k) {
+      res[k] = nullptr;
+      if (hp[k] && cnt[k]) {
+        CUDA_TRY(ctx, cudaMemcpyAsync(dp[k], hp[k], cnt[k] * sizeof(float), cudaMemcpyHostToDevice, s));
+        res[k] = dp[k];
+      }
+    }
+    pos = res[0]; quat = res[1]; vel = res[2]; om = res[3]; qp = res[4]; qv = res[5];
+  }
+  CUDA_TRY(ctx, cf::launch_public_to_slab(pos, quat, vel, om, qp, qv, n_src * repeat, sc,
+                                          ctx->slab + (size_t)first * sc.slab, s, repeat));
+  ctx->launches += 1;
+  if (in->location == COMFREE_MEM_HOST) CUDA_TRY(ctx, cudaStreamSynchronize(s));
+  return COMFREE_OK;
+}
+
 comfree_status comfree_set_state(comfree_ctx* ctx, int64_t first, int64_t nw, const comfree_state* in, void* stream) {
   if (!ctx || !in) return COMFREE_ERR_INVALID_ARGUMENT;
   if (!ctx->loaded) return fail(ctx, COMFREE_ERR_STATE, "set_state before load_scene");

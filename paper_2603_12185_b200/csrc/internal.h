@@ -170,13 +170,15 @@ cudaError_t mppi_control(const SceneDev& sc, const float* slab, int64_t W, const
 cudaError_t mppi_cost(const MppiCostParams& C, float* J, cudaStream_t s);
 cudaError_t mppi_cost_control(const MppiCostParams& C, float* J, const float* U, int t, int H, float kp, float kd,
                               float* command, float* tau, cudaStream_t s);
+// u0 != null: also the receding-horizon shift -- u0[P][Q] = the new plan's first
+// action, plan stores the new plan advanced by one step (last step 0)
 cudaError_t mppi_update(const float* J, const float* U, int P, int N, int H, int Q, float lambda, float lo, float hi,
-                        float* plan, float* weights, cudaStream_t s);
+                        float* plan, float* weights, cudaStream_t s, float* u0 = nullptr);
 
 // state layout conversion
 cudaError_t launch_public_to_slab(const float* pos, const float* quat, const float* vel,
                                   const float* omega, const float* qpos, const float* qvel,
-                                  int64_t n_worlds, const SceneDev& sc, float* slab, cudaStream_t s);
+                                  int64_t n_worlds, const SceneDev& sc, float* slab, cudaStream_t s, int64_t repeat = 1);
 cudaError_t launch_slab_to_public(const float* slab, int64_t n_worlds, const SceneDev& sc,
                                   float* pos, float* quat, float* vel, float* omega, float* qpos,
                                   float* qvel, cudaStream_t s);

@@ -136,7 +136,8 @@ __global__ void k_mppi_cost_control(const __grid_constant__ MppiCostParams C, fl
 __device__ __forceinline__ float finite_cost(float j) { return isfinite(j) ? j : INFINITY; }
 
 __global__ void k_mppi_update(const float* __restrict__ J, const float* __restrict__ U, int N, int H, int Q,
-                              float lambda, float lo, float hi, float* __restrict__ plan, float* __restrict__ weights) {
+                              float lambda, float lo, float hi, float* __restrict__ plan, float* __restrict__ weights,
+                              float* __restrict__ u0) {
   extern __shared__ float sw[];  // N weights
   __shared__ float red[32];
   const int p = blockIdx.x;
@@ -157,6 +158,19 @@ __global__ void k_mppi_update(const float* __restrict__ J, const float* __restri
   if (!isfinite(jmin)) {  // every rollout of this problem diverged: keep the plan
     for (int i = threadIdx.x; i < N; i += blockDim.x)
       if (weights) weights[(size_t)p * N + i] = 0.f;
+    if (u0) {  // receding horizon on the kept plan: u0 = its first action, then advance it
+      const int hq = H * Q;
+      float* pl = plan + (size_t)p * hq;
+      for (int j = threadIdx.x; j < Q; j += blockDim.x) u0[(size_t)p * Q + j] = pl[j];
+      __syncthreads();
+      float v[8];
+      for (int e0 = 0; e0 < hq; e0 += 8 * blockDim.x) {  // in-place shift: read a block, sync, write it
+        for (int k = 0; k < 8; ++k) { const int e = e0 + k * blockDim.x + threadIdx.x; v[k] = (e + Q < hq && e < hq) ? pl[e + Q] : 0.f; }
+        __syncthreads();
+        for (int k = 0; k < 8; ++k) { const int e = e0 + k * blockDim.x + threadIdx.x; if (e < hq) pl[e] = v[k]; }
+        __syncthreads();
+      }
+    }
     return;
   }
   float s = 0.f;
@@ -186,7 +200,14 @@ __global__ void k_mppi_update(const float* __restrict__ J, const float* __restri
   for (int e = threadIdx.x; e < hq; e += blockDim.x) {
     float acc = 0.f;
     for (int i = 0; i < N; ++i) acc = fmaf(sw[i], Up[(size_t)i * hq + e], acc);
-    plan[(size_t)p * hq + e] = fminf(fmaxf(acc, lo), hi);
+    const float a = fminf(fmaxf(acc, lo), hi);
+    if (!u0) {
+      plan[(size_t)p * hq + e] = a;
+    } else {  // receding horizon: u0 = the first action, the plan advanced by one step
+      if (e < Q) u0[(size_t)p * Q + e] = a;
+      else plan[(size_t)p * hq + e - Q] = a;
+      if (e >= hq - Q) plan[(size_t)p * hq + e] = 0.f;
+    }
   }
 }
 
@@ -226,9 +247,9 @@ cudaError_t mppi_cost_control(const MppiCostParams& C, float* J, const float* U,
 }
 
 cudaError_t mppi_update(const float* J, const float* U, int P, int N, int H, int Q, float lambda, float lo, float hi,
-                        float* plan, float* weights, cudaStream_t s) {
+                        float* plan, float* weights, cudaStream_t s, float* u0) {
   if (P == 0) return cudaSuccess;
-  k_mppi_update<<<P, 256, (size_t)N * sizeof(float), s>>>(J, U, N, H, Q, lambda, lo, hi, plan, weights);
+  k_mppi_update<<<P, 256, (size_t)N * sizeof(float), s>>>(J, U, N, H, Q, lambda, lo, hi, plan, weights, u0);
   return cudaGetLastError();
 }
 

@@ -8,13 +8,14 @@ namespace cf {
 __global__ void k_public_to_slab(const float* __restrict__ pos, const float* __restrict__ quat,
                                  const float* __restrict__ vel, const float* __restrict__ omega,
                                  const float* __restrict__ qpos, const float* __restrict__ qvel,
-                                 int64_t W, SceneDev sc, float* __restrict__ slab) {
+                                 int64_t W, SceneDev sc, float* __restrict__ slab, int64_t repeat) {
   const int64_t per = (int64_t)sc.Bp + sc.Qp;
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= W * per) return;
-  const int64_t w = idx / per;
+  const int64_t wd = idx / per;       // destination world
+  const int64_t w = wd / repeat;      // source world (repeat > 1: broadcast)
   const int i = (int)(idx % per);
-  float* S = slab + (size_t)w * sc.slab;
+  float* S = slab + (size_t)wd * sc.slab;
   const int Bp = sc.Bp;
   if (i < Bp) {
     if (i < sc.B) {
@@ -80,10 +81,11 @@ __global__ void k_slab_to_public(const float* __restrict__ slab, int64_t W, Scen
 
 cudaError_t launch_public_to_slab(const float* pos, const float* quat, const float* vel, const float* omega,
                                   const float* qpos, const float* qvel, int64_t W, const SceneDev& sc,
-                                  float* slab, cudaStream_t s) {
+                                  float* slab, cudaStream_t s, int64_t repeat) {
   const int64_t n = W * ((int64_t)sc.Bp + sc.Qp);
   if (n == 0) return cudaSuccess;
-  k_public_to_slab<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(pos, quat, vel, omega, qpos, qvel, W, sc, slab);
+  k_public_to_slab<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(pos, quat, vel, omega, qpos, qvel, W, sc, slab,
+                                                                repeat < 1 ? 1 : repeat);
   return cudaGetLastError();
 }
 

@@ -88,9 +88,9 @@ class MPPI:
         from harness.types import State
         torch = self.torch
         mc, P, N, H = self.mc, self.mc.n_problems, self.mc.n_samples, self.mc.horizon
-        rep = State(*(np.repeat(np.asarray(getattr(live_state, k), np.float32), N, axis=0)
-                      for k in ("pos", "quat", "vel", "omega", "qpos", "qvel")))
-        self.ctx.set_state(rep, stream=stream)
+        # the P live states go up once; the device replicates them to the N
+        # rollout worlds of each problem (comfree_set_state_broadcast)
+        self.ctx.set_state_broadcast(live_state, N, stream=stream)
         self.command.copy_(torch.as_tensor(np.repeat(np.asarray(command, np.float32), N, axis=0),
                                            device=self.command.device))
         self.J.zero_()
@@ -149,12 +149,16 @@ class MPPI:
                                                 _stream_handle(stream)), "comfree_mppi_update")
 
     def control_step(self, live_state, command, stream=None):
-        """One MPPI control step: returns u_0 (P, Q) as numpy; shifts the plan."""
+        """One MPPI control step: returns u_0 (P, Q) as numpy; the update
+        kernel also advances the plan (comfree_mppi_update_shift)."""
+        mc, P, N, H = self.mc, self.mc.n_problems, self.mc.n_samples, self.mc.horizon
         self.rollout_costs(live_state, command, stream)
-        self.update(stream)
+        if not hasattr(self, "u0"):
+            self.u0 = self.torch.zeros((P, self.Q), dtype=self.torch.float32, device=self.plan.device)
+        self._chk(self._lib.comfree_mppi_update_shift(self.ctx.h, P, N, H, _ptr(self.J), _ptr(self.U), mc.lam,
+                                                      mc.u_min, mc.u_max, _ptr(self.plan), _ptr(self.weights),
+                                                      _ptr(self.u0), _stream_handle(stream)),
+                  "comfree_mppi_update_shift")
         self.ctx.check(stream)          # collision overflow / non-finite rollouts surface here
-        u0 = self.plan[:, 0].cpu().numpy()
-        self.plan[:, :-1] = self.plan[:, 1:].clone()
-        self.plan[:, -1] = 0.0
         self.iteration += 1
-        return u0
+        return self.u0.cpu().numpy()

@@ -166,3 +166,38 @@ def test_control_step_shifts_plan_and_is_reproducible():
     np.testing.assert_array_equal(u1, u2)                 # counter-based noise, deterministic step
     assert np.all(np.abs(u1) <= 0.1 + 1e-7)
     assert np.all(m1.plan[:, -1].cpu().numpy() == 0.0)
+
+
+def test_update_shift_and_state_broadcast():
+    """comfree_mppi_update_shift: u0 = the new plan's first action and the plan
+    advanced by one step (last step 0), against the oracle's update; a problem
+    whose costs all diverged keeps its plan, advanced the same way.
+    comfree_set_state_broadcast: the P live states replicated to the N rollout
+    worlds of each problem on the device equal a host-side repeat."""
+    import torch
+    import paper_2603_12185_b200 as cf
+    from paper_2603_12185_b200 import _lib
+    m, scene, st = _mppi(3, 16, 5)
+    rng = np.random.default_rng(4)
+    m.plan.copy_(torch.as_tensor(rng.uniform(-0.08, 0.08, tuple(m.plan.shape)), dtype=torch.float32))
+    m.rollout_costs(st, np.zeros((3, 16)))
+    U = m.U.cpu().numpy().astype(np.float64)
+    plan0 = m.plan.cpu().numpy().astype(np.float64)
+    J = rng.uniform(0, 0.05, (3, 16)).astype(np.float32)
+    J[2, :] = np.inf
+    m.J.copy_(torch.as_tensor(J.reshape(-1)))
+    u0 = torch.zeros((3, 16), device="cuda")
+    m._chk(m._lib.comfree_mppi_update_shift(m.ctx.h, 3, 16, 5, cf._ptr(m.J), cf._ptr(m.U), m.mc.lam, -0.1, 0.1,
+                                            cf._ptr(m.plan), cf._ptr(m.weights), cf._ptr(u0), None), "shift")
+    plan, w = om.update(J.astype(np.float64), U, m.mc.lam, -0.1, 0.1, plan_prev=plan0)
+    assert_close(u0.cpu().numpy(), plan[:, 0], rtol=1e-4, atol=1e-7, what="u0")
+    g = m.plan.cpu().numpy()
+    assert_close(g[:, :-1], plan[:, 1:], rtol=1e-4, atol=1e-7, what="shifted plan")
+    assert np.all(g[:, -1] == 0.0)
+    # broadcast of 3 live states to 3 x 16 rollout worlds
+    live = State(*(np.asarray(getattr(st, k), np.float32) for k in ("pos", "quat", "vel", "omega", "qpos", "qvel")))
+    live.vel[:] = rng.normal(size=live.vel.shape).astype(np.float32)
+    m.ctx.set_state_broadcast(live, 16)
+    got = m.ctx.get_state()
+    for k in ("pos", "quat", "vel", "omega", "qpos", "qvel"):
+        np.testing.assert_array_equal(got[k], np.repeat(getattr(live, k), 16, axis=0))

@@ -16,7 +16,7 @@ timeout 600 python tools/mppi_bench.py > gpurun_out/${TAG}_mppi_p16.json 2> /dev
 timeout 600 python tools/mppi_bench.py --problems 1 > gpurun_out/${TAG}_mppi_p1.json 2> /dev/null
 timeout 900 python bench.py --workload mixed --cpu-seconds 5 --steps 100 > gpurun_out/${TAG}_bench_mixed.json 2> gpurun_out/${TAG}_bench_mixed.err
 $B --kd --cpu-seconds 0.5 > gpurun_out/${TAG}_bench_pile_kd.json 2> /dev/null
-$B --impedance exact_diagonal --cpu-seconds 0.5 > gpurun_out/${TAG}_bench_pile_exact_diag.json 2> /dev/null
+$B --impedance exact_diagonal --reset-state --cpu-seconds 0.5 > gpurun_out/${TAG}_bench_pile_exact_diag.json 2> /dev/null
 $B --impedance facet_diagonal --cpu-seconds 0.5 > gpurun_out/${TAG}_bench_pile_facet_diag.json 2> /dev/null
 for cd in 1 4 6; do
   $B --condim $cd --cpu-seconds 0.5 > gpurun_out/${TAG}_bench_pile_condim$cd.json 2> /dev/null
