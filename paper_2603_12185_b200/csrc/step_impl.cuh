@@ -102,17 +102,26 @@ __device__ __forceinline__ void group_sync(int group) {
   }
 }
 
-// 128-bit streaming loads: read once, do not allocate in L1.
+// 128-bit streaming loads: read once, do not allocate in L1 (CF_LD_HINT 2:
+// 256-byte L2 fetch granularity, measured neutral: 57.25 vs 57.24 us).
+#ifndef CF_LD_HINT
+#define CF_LD_HINT 0
+#endif
+#if CF_LD_HINT == 2
+#define CF_LD_Q ".L2::256B"
+#else
+#define CF_LD_Q ""
+#endif
 __device__ __forceinline__ float4 ld_stream(const float4* p) {
   float4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+  asm volatile("ld.global.nc.L1::no_allocate" CF_LD_Q ".v4.f32 {%0,%1,%2,%3}, [%4];"
                : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
                : "l"(p));
   return r;
 }
 __device__ __forceinline__ int4 ld_stream(const int4* p) {
   int4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+  asm volatile("ld.global.nc.L1::no_allocate" CF_LD_Q ".v4.s32 {%0,%1,%2,%3}, [%4];"
                : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
                : "l"(p));
   return r;

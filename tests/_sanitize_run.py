@@ -30,6 +30,29 @@ c = scenes.shuffle_contacts(c, 2)
 c.kd = np.tile(np.array([0.3, 0.002], np.float32), (c.n, 1))
 gpu_step(cfg, scene, st, c, inp)                                                 # per-contact impedance, sort + gather
 gpu_step(cfg.with_(impedance="exact_diagonal"), scene, st, c, inp)            # exact-diagonal impedance (Eq. (11))
+gpu_step(cfg.with_(impedance="facet_diagonal"), scene, st, c, inp)            # facet-diagonal impedance (R28)
+# a world beyond shared memory: the global-scratch step variant
+scene_l, st_l, c_l, inp_l = scenes.random_instance(14, n_worlds=2, n_bodies=2100, contacts_per_world=[60, 11])
+gpu_step(cfg, scene_l, st_l, c_l, inp_l)
+# pipelined host buffers (COMFREE_MEM_HOST_ASYNC)
+scene_p, st_p, c_p = scenes.c4_pile(n_worlds=3, contacts_per_world=200, lattice=(5, 5, 2))
+ctx_p = cf.Context(cfg)
+ctx_p.load_scene(scene_p, 3, st_p)
+hca = cf.HostContacts.from_arrays(c_p, pin=True, asynchronous=True, n_worlds=3)
+import torch as _t  # noqa: E402
+outs = [{k: _t.empty(v.shape, dtype=_t.float32).pin_memory().numpy() for k, v in ctx_p.get_state().items()}
+        for _ in range(3)]
+for o in outs:
+    ctx_p.step(hca, None)
+    ctx_p.get_state_async(o)
+ctx_p.wait_async()
+ctx_p.check()
+# broadphase collision (one CTA per world, chained scan) in both count modes
+ctx_p.load_geometry(scenes.pile_geometry((5, 5, 2), broadphase=True))
+ctx_p.collide(capacity=3 * 400)
+dcb, _ = ctx_p.collide(capacity=3 * 400, device_count=True)
+ctx_p.step(dcb, None)
+ctx_p.check()
 # articulated upstream + collision front-end + step (the closed-loop hand)
 import torch  # noqa: E402
 from harness.types import Inputs  # noqa: E402
