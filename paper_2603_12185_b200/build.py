@@ -19,6 +19,9 @@ NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["step.cu", "step_w1.cu", "step_w2.cu", "step_w4.cu", "step_w8.cu", "step_p32.cu", "segment.cu", "state.cu", "articulation.cu", "collide.cu", "mppi.cu"]
 CPP_SOURCES = ["capi.cpp"]
+# collide.cu: no FMA contraction, so the narrowphase's count and emit
+# specialisations compute bit-identical contacts (collide.cu, CF_NP_INLINE)
+PER_FILE_FLAGS = {"collide.cu": ["-fmad=false"]}
 
 
 def _stale(target, deps):
@@ -44,7 +47,7 @@ def build(force: bool = False, verbose: bool = False, defines=(), tag: str = "")
         o = os.path.join(objdir, src + ".o")
         objs.append(o)
         if force or _stale(o, [s] + headers):
-            jobs.append([NVCC, *ARCH, *dflags, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+            jobs.append([NVCC, *ARCH, *dflags, *PER_FILE_FLAGS.get(src, []), "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                          "-Xptxas", "-v" if verbose else "-O3", "-I", INCLUDE, "-I", CSRC, "-c", s, "-o", o])
     from concurrent.futures import ThreadPoolExecutor
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:

@@ -102,10 +102,9 @@ __device__ __forceinline__ V3 tangent(V3 n) {
 // Contact sink of one pair: counts, and with emit writes each record as it is
 // found (no local-memory staging).
 // The count and the emit passes must find the same contacts bit for bit (the
-// emit writes exactly the slots the count reserved), so both run the SAME
-// machine code: one non-inlined pair_contacts with a runtime emit flag (two
-// inlined specialisations may contract floating point differently and
-// disagree on a contact at the margin).
+// emit writes exactly the slots the count reserved): either both run one
+// non-inlined pair_contacts with a runtime emit flag, or (default) both
+// inline it from a file compiled without FMA contraction (see CF_NP_INLINE).
 struct Out {
   int k;
   bool emit;
@@ -322,7 +321,19 @@ __device__ __forceinline__ void box_edge_edge(const Frame& A, float4 hA4, const 
 
 // Contacts of the geom pair pr = (g1, g2) in world w (frames Fw): returns the
 // count; EMIT writes them from record `base` on.
-__device__ __noinline__ int pair_contacts_rt(const CollideParams& P, const GeomTab T, const int2 pr, const float4* Fw,
+// CF_NP_INLINE: the count and emit specialisations inlined instead, which is
+// only safe because collide.cu is compiled without FMA contraction
+// (-fmad=false, build.py): every floating-point operation is then one IEEE
+// operation in source order in both specialisations, so they agree bit for bit.
+#ifndef CF_NP_INLINE
+#define CF_NP_INLINE 1
+#endif
+#if CF_NP_INLINE
+#define CF_NP_ATTR __forceinline__
+#else
+#define CF_NP_ATTR __noinline__
+#endif
+__device__ CF_NP_ATTR int pair_contacts_rt(const CollideParams& P, const GeomTab T, const int2 pr, const float4* Fw,
                                              int64_t w, int64_t base, bool emit) {
   const int4 g1 = T.geom[pr.x], g2 = T.geom[pr.y];
   const float margin = P.margin;
