@@ -27,8 +27,10 @@ t1 = (1 + s n_x^2 a, s b, -s n_x).
                  segment point as a sphere; capsule-capsule: the closest points of
                  the two segments (Ericson, Real-Time Collision Detection 5.1.9,
                  parallel when a e - b^2 <= 1e-12 a e: s = 0) as spheres;
-                 capsule-box / box-capsule: each end as a sphere against the box
-                 (reading R25: the capsule's side is not tested against the box)
+                 capsule-box / box-capsule: each end as a sphere against the box,
+                 then (reading R34) the segment point nearest the box centre,
+                 a + t d with t = (x_box - a) . d / |d|^2, as a third sphere when
+                 0 < t < 1 (a capsule lying across a box touches it there)
   box-box        vertex-face (reading R25): every corner of g2 whose largest
                  signed face distance s = max_i (|c_i| - h_i) in g1's frame is below
                  the margin and lies within the other two face extents emits on
@@ -290,7 +292,13 @@ def pair_contacts(geo, pi, state, w, art, g12=None):
         gc, gbx = (g1, g2) if k1 == CAPSULE else (g2, g1)
         Rb, xb = geom_frame(geo, gbx, state, w, art)
         Rr = float(geo.size[gc, 0])
-        for e in _segment(geo, gc, state, w, art):
+        a, b = _segment(geo, gc, state, w, art)
+        pts = [a, b]
+        d = b - a
+        t = float((xb - a) @ d / (d @ d))              # the box centre projected onto the segment (R34)
+        if 0.0 < t < 1.0:
+            pts.append(a + t * d)
+        for e in pts:
             phi, nbox, qs = _sphere_box(e, Rr, Rb, xb, np.asarray(geo.size[gbx], float))
             if phi < m:
                 out.append((0.5 * (qs + (e - Rr * nbox)), phi, -nbox if k1 == CAPSULE else nbox))

@@ -414,10 +414,19 @@ __device__ CF_NP_ATTR int pair_contacts_rt(const CollideParams& P, const GeomTab
     const Frame Fb = load_frame(Fw, gb);
     const float R = T.size[gr].x;
     const float4 h4 = T.size[gb];
-    V3 e[2];
+    V3 e[3];
     int ne = 1;
-    if (T.geom[gr].x == G_CAPSULE) { capsule_ends(T, Fw, gr, e[0], e[1]); ne = 2; }
-    else e[0] = load_frame(Fw, gr).x;
+    if (T.geom[gr].x == G_CAPSULE) {
+      capsule_ends(T, Fw, gr, e[0], e[1]);
+      ne = 2;
+      // reading R34: the segment point nearest the box centre as a third sphere
+      // when strictly inside the segment (a capsule lying across a box)
+      const V3 d = sub(e[1], e[0]);
+      const float t = dot(sub(Fb.x, e[0]), d) / dot(d, d);
+      if (t > 0.f && t < 1.f) e[ne++] = add(e[0], mul(t, d));
+    } else {
+      e[0] = load_frame(Fw, gr).x;
+    }
     for (int q = 0; q < ne; ++q) {
       V3 nbox, qs;
       const float phi = sphere_box(e[q], R, Fb, h4, nbox, qs);

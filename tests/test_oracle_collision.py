@@ -308,3 +308,28 @@ def test_box_edge_edge_emitted_only_on_edge_axes_within_margin():
     Rz = co.quat_R(np.array([np.cos(np.pi / 8), 0, 0, np.sin(np.pi / 8)]))
     Rx = co.quat_R(np.array([np.cos(np.pi / 8), np.sin(np.pi / 8), 0, 0]))
     assert co._box_edge_edge(Rz, np.zeros(3), h, Rx, np.array([0.0, 0.0, 10.0]), h, 0.01) == []
+
+
+# ---------------------------------------------------------------- capsule side against a box (reading R34)
+def test_capsule_lying_across_a_box_touches_in_the_middle():
+    """A horizontal capsule (R 1 cm, half-length 5 cm) lying across a 2 cm box
+    with both ends overhanging: the end spheres are far from the box, the
+    segment point above the box centre gives the one contact, with the closed
+    form phi = z_c - R - h_z and the normal +z (box -> capsule when the capsule
+    is g2, so from g1 = box to g2 = capsule)."""
+    from harness.types import Geometry, State
+    geo = Geometry(np.array([co.BOX, co.CAPSULE], np.int32), np.array([0, 1], np.int32), np.zeros(2, np.int32),
+                   np.array([(0.01, 0.01, 0.01), (0.01, 0.05, 0.0)]), np.zeros((2, 3)),
+                   np.array([(0, 1)], np.int32), margin=0.001)
+    z = 0.01 + 0.01 - 0.0004                         # 0.4 mm penetration
+    q_cap = np.array([np.cos(np.pi / 4), 0.0, np.sin(np.pi / 4), 0.0])   # capsule axis z -> x
+    st = State(np.array([[[0, 0, 0], [0.003, 0.0, z]]], float), np.array([[[1.0, 0, 0, 0], q_cap]]),
+               np.zeros((1, 2, 3)), np.zeros((1, 2, 3)), np.zeros((1, 0)), np.zeros((1, 0)))
+    c = co.collide(geo, st, None)
+    assert c.n == 1
+    np.testing.assert_allclose(c.c0[0, 3], z - 0.01 - 0.01, atol=1e-12)
+    np.testing.assert_allclose(c.c1[0, :3], [0, 0, 1], atol=1e-12)
+    np.testing.assert_allclose(c.c0[0, :2], [0.0, 0.0], atol=1e-12)   # above the box centre (t at x = 0)
+    # the ends alone (round-1 reading) would have found nothing
+    assert all(co._sphere_box(e, 0.01, np.eye(3), np.zeros(3), np.full(3, 0.01))[0] > 0.001
+               for e in co._segment(geo, 1, st, 0, None))
