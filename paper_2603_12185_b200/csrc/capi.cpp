@@ -209,7 +209,7 @@ cudaEvent_t next_event(comfree_ctx* ctx, int* idx) {
 
 #ifdef CF_BP_TIMELINE
 extern "C" int comfree_debug_bp_timeline(comfree_ctx* ctx, unsigned long long* host, int64_t n_worlds) {
-  return cudaMemcpy(host, ctx->col_frames.p, (size_t)n_worlds * 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  return cudaMemcpy(host, ctx->col_frames.p, (size_t)n_worlds * 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
 }
 #endif
 #ifdef CF_TIMELINE
@@ -961,7 +961,7 @@ comfree_status comfree_collide(comfree_ctx* ctx, int64_t first, int64_t nw, int6
     CUDA_TRY(ctx, ensure(ctx->bp_count, 2 * sizeof(int64_t)));
     int64_t* cnt = static_cast<int64_t*>(ctx->bp_count.p);
 #ifdef CF_BP_TIMELINE
-    CUDA_TRY(ctx, ensure(ctx->col_frames, std::max<size_t>(1, (size_t)nw) * 8 * sizeof(unsigned long long)));
+    CUDA_TRY(ctx, ensure(ctx->col_frames, std::max<size_t>(1, (size_t)nw) * 16 * sizeof(unsigned long long)));
     P.frames = static_cast<float4*>(ctx->col_frames.p);
 #endif
     CUDA_TRY(ctx, cf::collide_broadphase(P, cap_c, capacity, static_cast<unsigned long long*>(ctx->bp_status.p),

@@ -523,7 +523,7 @@ constexpr int kBpThreads = CF_BP_THREADS;
   if (tid == 0) {                                                                         \
     unsigned long long t_;                                                                \
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_));                                 \
-    reinterpret_cast<unsigned long long*>(P.frames)[w * 8 + (k)] = t_;                    \
+    reinterpret_cast<unsigned long long*>(P.frames)[w * 16 + (k)] = t_;                    \
   }
 #else
 #define BP_MARK(k)
@@ -699,6 +699,7 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
     (void)block_exclusive(c, s_tmp, &tot);
     n_np = tot;
   }
+  BP_MARK(8);
   // (i) warp-cooperative sweep: warp v takes sorted positions i = v, v + 8, ...;
   // its lanes test the next 32 positions at once until the sorted low ends pass
   // geom i's high end; every pair found goes to a temporary list (ncon's
@@ -733,6 +734,7 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
       }
     }
   }
+  BP_MARK(9);
   // (ii) planes (lowest geom ids): count their hits
   for (int p = 0; p < G && P.geom[p].x == G_PLANE; ++p) {
     for (int g0 = 0; g0 < G; g0 += kBpThreads) {
@@ -744,6 +746,7 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
     }
   }
   __syncthreads();
+  BP_MARK(10);
   // (iii) bucket starts (exclusive scan of the counts)
   {
     int run = 0;
@@ -763,6 +766,7 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
     }
     __syncthreads();
   }
+  BP_MARK(11);
   // (iv) pairs into their buckets; plane buckets in geom order by a block scan
   {
     const int nt = min(s_misc[5], Q.cap_c);
