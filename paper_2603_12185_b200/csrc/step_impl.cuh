@@ -334,6 +334,35 @@ __device__ __forceinline__ void fx_add(unsigned* lo, int* hi, float v, float sca
   atomicAdd(hi, h);
 #endif
 }
+// The six components of one body: every lo-word atomic first (their return
+// latencies overlap), then the carries and the six hi-word atomics -- instead
+// of lo, wait, carry, hi per component (atomics keep program order, so the
+// order of the source is the order of issue).
+#ifndef CF_FX_BATCH
+#define CF_FX_BATCH 1
+#endif
+template <class LoAddr, class HiAddr>
+__device__ __forceinline__ void fx_add6(LoAddr lo_of, HiAddr hi_of, const float v[6], float sl, float sa) {
+#if CF_FX_SPLIT || !CF_FX_BATCH
+#pragma unroll
+  for (int q = 0; q < 6; ++q) fx_add(lo_of(q), hi_of(q), v[q], q < 3 ? sl : sa);
+#else
+  long long x[6];
+  unsigned old[6];
+#pragma unroll
+  for (int q = 0; q < 6; ++q) x[q] = __float2ll_rn(v[q] * (q < 3 ? sl : sa));
+#pragma unroll
+  for (int q = 0; q < 6; ++q) old[q] = atomicAdd(lo_of(q), (unsigned)x[q]);
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+    int h;
+    asm("{\n\t.reg .u32 t;\n\tadd.cc.u32 t, %1, %2;\n\taddc.s32 %0, %3, 0;\n\t}"
+        : "=r"(h) : "r"(old[q]), "r"((unsigned)x[q]), "r"((int)(x[q] >> 32)));
+    atomicAdd(hi_of(q), h);
+  }
+#endif
+}
+
 // Per-add range.  Every add is |x| = |v| * scale < thr, thr = 2^62 / (2 n_c + 2)
 // for a world of n_c contacts (a body receives at most 2 n_c adds per
 // component), so no sum can wrap and the 64-bit total stays below 2^62; the
@@ -521,8 +550,7 @@ __device__ __forceinline__ void scatter_side(unsigned* accl, const float4* rec, 
     }
     const float sl = fx_scale(im), sa = fx_scale(dmax);
     mag = max_nan(mag, fx_mag(v, sl, sa));
-#pragma unroll
-    for (int q = 0; q < 6; ++q) fx_add(ACC_LO(q, key), ACC_HI(q, key), v[q], q < 3 ? sl : sa);
+    fx_add6([&](int q) { return ACC_LO(q, key); }, [&](int q) { return ACC_HI(q, key); }, v, sl, sa);
   }
 }
 
@@ -533,8 +561,7 @@ __device__ __forceinline__ void scatter_own(unsigned* accl, int Bp, int key, con
   if (key >= 0) {
     const float sl = fx_scale(im), sa = fx_scale(dmax);
     mag = max_nan(mag, fx_mag(v, sl, sa));
-#pragma unroll
-    for (int q = 0; q < 6; ++q) fx_add(ACC_LO(q, key), ACC_HI(q, key), v[q], q < 3 ? sl : sa);
+    fx_add6([&](int q) { return ACC_LO(q, key); }, [&](int q) { return ACC_HI(q, key); }, v, sl, sa);
   }
 }
 
