@@ -341,6 +341,9 @@ __device__ __forceinline__ void fx_add(unsigned* lo, int* hi, float v, float sca
 #ifndef CF_FX_BATCH
 #define CF_FX_BATCH 1
 #endif
+#ifndef CF_HI_SKIP
+#define CF_HI_SKIP 0
+#endif
 template <class LoAddr, class HiAddr>
 __device__ __forceinline__ void fx_add6(LoAddr lo_of, HiAddr hi_of, const float v[6], float sl, float sa) {
 #if CF_FX_SPLIT || !CF_FX_BATCH
@@ -358,7 +361,11 @@ __device__ __forceinline__ void fx_add6(LoAddr lo_of, HiAddr hi_of, const float 
     int h;
     asm("{\n\t.reg .u32 t;\n\tadd.cc.u32 t, %1, %2;\n\taddc.s32 %0, %3, 0;\n\t}"
         : "=r"(h) : "r"(old[q]), "r"((unsigned)x[q]), "r"((int)(x[q] >> 32)));
+#if CF_HI_SKIP  // skip a zero hi add (most adds): measured 57.32 vs 56.77 us, so not the default
+    if (h != 0) atomicAdd(hi_of(q), h);
+#else
     atomicAdd(hi_of(q), h);
+#endif
   }
 #endif
 }
