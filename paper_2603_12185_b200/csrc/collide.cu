@@ -680,10 +680,6 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
   BP_MARK(2);
   // 2b: sweep, twice: count per bucket, then place
   auto axis_of = [&](const float4& v) { return ax == 0 ? v.x : (ax == 1 ? v.y : v.z); };
-  auto overlap = [&](int a, int b) {
-    const float4 la = lo[a], ha = hi[a], lb = lo[b], hb = hi[b];
-    return la.x <= hb.x && lb.x <= ha.x && la.y <= hb.y && lb.y <= ha.y && la.z <= hb.z && lb.z <= ha.z;
-  };
   auto plane_hit = [&](int p, int g) {  // g's grown AABB reaches below offset + margin/2
     const float4 n = P.size[p], lg = lo[g], hg = hi[g];
     const V3 c = v3(0.5f * (lg.x + hg.x), 0.5f * (lg.y + hg.y), 0.5f * (lg.z + hg.z));
@@ -711,13 +707,21 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
     const int lane = tid & 31, wv = tid >> 5;
     for (int i = wv; i < n_np; i += kBpThreads / 32) {
       const int gi = (int)val[i];
-      const float hiax = axis_of(hi[gi]);
+      const float4 li = lo[gi], hv = hi[gi];
+      const uint32_t hk = f2key(axis_of(hv));  // the sorted keys are f2key(low end): compare keys
       const int bi = gbody[gi];
       for (int j0 = i + 1; j0 < n_np; j0 += 32) {
         const int jj = j0 + lane;
-        const int gj = jj < n_np ? (int)val[jj] : 0;
-        const bool in = jj < n_np && axis_of(lo[gj]) <= hiax;
-        const bool found = in && gbody[gj] != bi && overlap(gi, gj);
+        const bool in = jj < n_np && key[jj] <= hk;
+        bool found = false;
+        int gj = 0;
+        if (in) {
+          gj = (int)val[jj];
+          if (gbody[gj] != bi) {
+            const float4 lj = lo[gj], hj = hi[gj];
+            found = li.x <= hj.x && lj.x <= hv.x && li.y <= hj.y && lj.y <= hv.y && li.z <= hj.z && lj.z <= hv.z;
+          }
+        }
         const unsigned fb = __ballot_sync(0xffffffffu, found);
         if (fb) {  // one append per warp chunk
           int t0 = 0;
