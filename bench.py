@@ -455,8 +455,11 @@ def run_ours(args, rank, world_size, local):
     dev = torch.device("cuda", local)
     if world_size > 1:
         if args.dist_backend == "nccl":
-            os.environ.setdefault("NCCL_DEBUG", "INFO")          # communicator init in the log
+            # communicator init (ranks, NVLink/NVLS paths) logged to a file per
+            # process, so stdout keeps the one JSON line
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
             os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", os.path.join("/tmp", "comfree_nccl.%h.%p.log"))
             dist.init_process_group("nccl", device_id=dev)
         else:                              # plumbing check with several ranks on one GPU
             dist.init_process_group(args.dist_backend)
@@ -776,6 +779,8 @@ def run_ours(args, rank, world_size, local):
             "cpu_baseline": cpu,
             "allgather_final_state_mb": gathered_mb,
             "sharded_verification": verification,
+            "nccl_debug_file": os.environ.get("NCCL_DEBUG_FILE") if (world_size > 1 and args.dist_backend == "nccl")
+                               else None,
             "context": "paper: 2-3x MJWarp throughput in dense contact on one RTX 4090 (PAPER.md P:11, P:274); "
                        "full-step numbers, not this path alone",
             "final_state_finite": finite,
