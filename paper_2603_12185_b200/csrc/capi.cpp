@@ -78,7 +78,7 @@ struct comfree_ctx {
   bool art_loaded = false;
   // collision front-end: device geometry (comfree_load_geometry) and scan scratch
   DevBuf geo, col_counts, col_offs, col_tmp, col_frames;
-  DevBuf bp_status, bp_queue, bp_count;   // broadphase mode scratch
+  DevBuf bp_status, bp_queue, bp_count, bp_stage;   // broadphase mode scratch
   int32_t n_geoms = 0, n_pairs = 0;
   float col_margin = 0.f, col_mu[3] = {0.f, 0.f, 0.f};
   int32_t col_condim = 3;
@@ -950,7 +950,7 @@ comfree_status comfree_collide(comfree_ctx* ctx, int64_t first, int64_t nw, int6
   if (ctx->n_pairs == 0) {
     // broadphase mode (reading R32): one kernel, candidates found per world
     int np2 = 1;
-    while (np2 < ctx->n_geoms) np2 <<= 1;
+    while (np2 < ctx->n_geoms + 1) np2 <<= 1;  // as collide_broadphase
     const size_t fixed = cf::collide_bp_smem(ctx->n_geoms, 0, np2);
     const int64_t room = (int64_t)(110 * 1024) - (int64_t)fixed;  // two CTAs per SM
     const int cap_c = (int)std::max<int64_t>(1024, std::min<int64_t>(room / 10 & ~7, 65535));
@@ -964,9 +964,16 @@ comfree_status comfree_collide(comfree_ctx* ctx, int64_t first, int64_t nw, int6
     CUDA_TRY(ctx, ensure(ctx->col_frames, std::max<size_t>(1, (size_t)nw) * 16 * sizeof(unsigned long long)));
     P.frames = static_cast<float4*>(ctx->col_frames.p);
 #endif
+    // staged records per world: 16 per geom (the settled pile: ~10 per geom)
+    static const int stage_env = [] {  // test override of the staging size (exercises the second pass)
+      const char* e = getenv("COMFREE_BP_STAGE_CAP");
+      return e ? atoi(e) : 0;
+    }();
+    const int stage_cap = stage_env > 0 ? stage_env : (int)std::min<int64_t>(16 * (int64_t)ctx->n_geoms + 256, 1 << 20);
+    CUDA_TRY(ctx, ensure(ctx->bp_stage, std::max<int64_t>(1, nw) * 2 * (size_t)stage_cap * sizeof(float4)));
     CUDA_TRY(ctx, cf::collide_broadphase(P, cap_c, capacity, static_cast<unsigned long long*>(ctx->bp_status.p),
                                          static_cast<int*>(ctx->bp_queue.p), n_device ? n_device : cnt, cnt + 1,
-                                         ctx->d_err, s));
+                                         ctx->d_err, static_cast<float4*>(ctx->bp_stage.p), stage_cap, s));
     ctx->launches += 1;
     if (n_device) return COMFREE_OK;
     int64_t h[2] = {0, 0};
@@ -1260,7 +1267,7 @@ void comfree_destroy(comfree_ctx* ctx) {
                     &ctx->sj, &ctx->skd, &ctx->nf, &ctx->foff, &ctx->cub_tmp, &ctx->in_world, &ctx->in_off, &ctx->in_c0,
                     &ctx->in_c1, &ctx->in_c2, &ctx->in_c3, &ctx->in_jrow, &ctx->in_kd, &ctx->in_fext, &ctx->in_L,
                     &ctx->in_tau, &ctx->imp, &ctx->st_tmp, &ctx->art, &ctx->geo, &ctx->col_counts,
-                    &ctx->col_offs, &ctx->col_tmp, &ctx->col_frames, &ctx->bp_status, &ctx->bp_queue, &ctx->bp_count, &ctx->gscratch};
+                    &ctx->col_offs, &ctx->col_tmp, &ctx->col_frames, &ctx->bp_status, &ctx->bp_queue, &ctx->bp_count, &ctx->bp_stage, &ctx->gscratch};
   for (DevBuf* b : bufs) release(*b);
   for (cudaEvent_t e : ctx->ev_pool) cudaEventDestroy(e);
   if (ctx->slab) cudaFree(ctx->slab);

@@ -99,24 +99,37 @@ __device__ __forceinline__ V3 tangent(V3 n) {
   return v3(1.f + s * n.x * n.x * a, s * b, -s * n.x);
 }
 
-// Contact sink of one pair: counts, and with emit writes each record as it is
-// found (no local-memory staging).
+// Broadphase staging of one world (global, L2-resident while the world's CTA
+// runs): the records found by the single narrowphase pass, in the order they
+// were found: s0 = (point, phi), s1 = (normal, tag = candidate << 5 | index in
+// the pair); the copy pass places them after the world's offsets are known.
+struct Stage {
+  float4* s0;
+  float4* s1;
+  int cap;
+  int* count;  // shared-memory slot counter
+};
+
+// Contact sink of one pair: counts; with mode 1 (emit) writes each record as
+// it is found (no local-memory staging), with mode 2 (stage) appends it to the
+// world's staging area.
 // The count and the emit passes must find the same contacts bit for bit (the
 // emit writes exactly the slots the count reserved): either both run one
-// non-inlined pair_contacts with a runtime emit flag, or (default) both
-// inline it from a file compiled without FMA contraction (see CF_NP_INLINE).
+// non-inlined pair_contacts with a runtime mode, or (default) both inline it
+// from a file compiled without FMA contraction (see CF_NP_INLINE).
 struct Out {
   int k;
-  bool emit;
+  int mode;  // 0 count, 1 emit, 2 stage
   const CollideParams* P;
+  const Stage* S;
   int64_t base, w;
-  int b1, b2, l1, l2;
+  int b1, b2, l1, l2, cand;
   __device__ void add(V3 pp, float ph, V3 nn);
 };
 __device__ __forceinline__ V3 tangent(V3 n);
 __device__ __forceinline__ void Out::add(V3 pp, float ph, V3 nn) {
   if (k < kMaxPairContacts) {
-    if (emit) {  // write the record now (no staging)
+    if (mode == 1) {  // write the record now (no staging)
       const int64_t c = base + k;
       const V3 t1 = tangent(nn);
       P->c0[c] = make_float4(pp.x, pp.y, pp.z, ph);
@@ -125,6 +138,12 @@ __device__ __forceinline__ void Out::add(V3 pp, float ph, V3 nn) {
       P->c3[c] = make_int4(b1, b2, __float_as_int(P->mu_rol), P->condim);
       P->world[c] = (int32_t)w;
       P->link[c] = make_int2(l1, l2);
+    } else if (mode == 2) {
+      const int slot = atomicAdd(S->count, 1);
+      if (slot < S->cap) {
+        S->s0[slot] = make_float4(pp.x, pp.y, pp.z, ph);
+        S->s1[slot] = make_float4(nn.x, nn.y, nn.z, __int_as_float((cand << 5) | k));
+      }
     }
     ++k;
   }
@@ -334,13 +353,15 @@ __device__ __forceinline__ void box_edge_edge(const Frame& A, float4 hA4, const 
 #define CF_NP_ATTR __noinline__
 #endif
 __device__ CF_NP_ATTR int pair_contacts_rt(const CollideParams& P, const GeomTab T, const int2 pr, const float4* Fw,
-                                             int64_t w, int64_t base, bool emit) {
+                                             int64_t w, int64_t base, int mode, const Stage* S = nullptr, int cand = 0) {
   const int4 g1 = T.geom[pr.x], g2 = T.geom[pr.y];
   const float margin = P.margin;
   Out o;
   o.k = 0;
-  o.emit = emit;
+  o.mode = mode;
   o.P = &P;
+  o.S = S;
+  o.cand = cand;
   o.base = base;
   o.w = w;
   o.b1 = g1.y;
@@ -439,7 +460,13 @@ __device__ CF_NP_ATTR int pair_contacts_rt(const CollideParams& P, const GeomTab
 template <bool EMIT>
 __device__ __forceinline__ int pair_contacts(const CollideParams& P, const int2 pr, const float4* Fw, int64_t w,
                                              int64_t base, const GeomTab* T = nullptr) {
-  return pair_contacts_rt(P, T ? *T : GeomTab{P.geom, P.size, P.local}, pr, Fw, w, base, EMIT);
+  return pair_contacts_rt(P, T ? *T : GeomTab{P.geom, P.size, P.local}, pr, Fw, w, base, EMIT ? 1 : 0);
+}
+
+// the broadphase's single pass: count and stage the records of candidate `cand`
+__device__ __forceinline__ int pair_contacts_stage(const CollideParams& P, const int2 pr, const float4* Fw, int64_t w,
+                                                   const GeomTab* T, const Stage* S, int cand) {
+  return pair_contacts_rt(P, *T, pr, Fw, w, 0, 2, S, cand);
 }
 
 __global__ void k_geom_frames(const __grid_constant__ CollideParams P) {
@@ -514,6 +541,9 @@ __global__ void k_collide_emit(const __grid_constant__ CollideParams P, const in
 //      base + offset: world-major, (g1, g2)-ordered, deterministic.
 // The last CTA to finish stores the device count (the offset of the first pair
 // that did not fit when the capacity is exceeded) and resets the counters.
+#ifndef CF_BP_FLAT
+#define CF_BP_FLAT 1  // flat sweep (tests split evenly over the threads); 0: warp per sorted position
+#endif
 #ifndef CF_BP_THREADS
 #define CF_BP_THREADS 512  // 16 warps, 2 CTAs per SM: 0.83 vs 0.91 ms collide at 256 (profiles/r02_broadphase.txt)
 #endif
@@ -570,6 +600,8 @@ struct BpParams {
   int64_t* n_dev;                  // device count out (whole pairs within the capacity)
   int64_t* total;                  // all contacts of the launch (or null)
   int* err;
+  float4* stage;                   // [n_worlds][2][stage_cap] staged records
+  int stage_cap;                   // records per world (a world with more runs the narrowphase twice)
 };
 
 __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_constant__ CollideParams P,
@@ -696,7 +728,88 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
     n_np = tot;
   }
   BP_MARK(8);
-  // (i) warp-cooperative sweep: warp v takes sorted positions i = v, v + 8, ...;
+#if CF_BP_FLAT
+  // (i) flat sweep: the range of sorted position i is (i, e_i], the positions
+  // whose low end is within its high end (binary search on the sorted keys);
+  // the ranges' tests are numbered by an exclusive scan and split evenly over
+  // the threads, each walking its contiguous share (one test per iteration,
+  // every lane busy); every pair found goes to a temporary list (ncon's
+  // storage) and is counted in its bucket (the lower geom id)
+  uint32_t* tmp = reinterpret_cast<uint32_t*>(ncon);
+  if (tid == 0) s_misc[5] = 0;
+  for (int i = tid; i < n_np; i += kBpThreads) {
+    const uint32_t hk = f2key(axis_of(hi[val[i]]));
+    int a = i, b = n_np;  // key[a] <= hk < key[b] (b virtual)
+    while (b - a > 1) {
+      const int m = (a + b) >> 1;
+      if (key[m] <= hk) a = m; else b = m;
+    }
+    start[i] = a - i;
+  }
+  __syncthreads();
+  int* tpre = reinterpret_cast<int*>(key);  // [n_np + 1] (np2 > n_np): the keys are dead
+  int n_tests = 0;
+  for (int i0 = 0; i0 < n_np; i0 += kBpThreads) {
+    const int i = i0 + tid;
+    const int v = i < n_np ? start[i] : 0;
+    int tot;
+    const int ex = block_exclusive(v, s_tmp, &tot);
+    if (i < n_np) tpre[i] = n_tests + ex;
+    n_tests += tot;
+  }
+  if (tid == 0) tpre[n_np] = n_tests;
+  __syncthreads();
+  {
+    const int lane = tid & 31;
+    const int per = (n_tests + kBpThreads - 1) / kBpThreads;
+    int t = tid * per;
+    const int tend = min(n_tests, t + per);
+    int i = 0, j = 0, e = 0, gi = 0, bi = 0;
+    float4 li = make_float4(0.f, 0.f, 0.f, 0.f), hv = li;
+    if (t < tend) {
+      int a = 0, b = n_np;  // tpre[a] <= t < tpre[b]
+      while (b - a > 1) {
+        const int m = (a + b) >> 1;
+        if (tpre[m] <= t) a = m; else b = m;
+      }
+      i = a;
+      j = i + 1 + (t - tpre[i]);
+      e = i + (tpre[i + 1] - tpre[i]);
+      gi = (int)val[i]; li = lo[gi]; hv = hi[gi]; bi = gbody[gi];
+    }
+    for (int it = 0; it < per; ++it) {
+      bool found = false;
+      uint32_t pv = 0;
+      if (t < tend) {
+        const int gj = (int)val[j];
+        if (gbody[gj] != bi) {
+          const float4 lj = lo[gj], hj = hi[gj];
+          found = li.x <= hj.x && lj.x <= hv.x && li.y <= hj.y && lj.y <= hv.y && li.z <= hj.z && lj.z <= hv.z;
+          pv = ((uint32_t)min(gi, gj) << 16) | (uint32_t)max(gi, gj);
+        }
+        ++t;
+        if (++j > e && t < tend) {  // the next position with a non-empty range
+          do { ++i; } while (tpre[i + 1] == tpre[i]);
+          j = i + 1;
+          e = i + (tpre[i + 1] - tpre[i]);
+          gi = (int)val[i]; li = lo[gi]; hv = hi[gi]; bi = gbody[gi];
+        }
+      }
+      const unsigned fb = __ballot_sync(0xffffffffu, found);
+      if (fb) {  // one append per warp and iteration
+        int t0 = 0;
+        if (lane == 0) t0 = atomicAdd(&s_misc[5], __popc(fb));
+        t0 = __shfl_sync(0xffffffffu, t0, 0);
+        if (found) {
+          atomicAdd(&cnt[pv >> 16], 1);
+          const int q = t0 + __popc(fb & ((1u << lane) - 1u));
+          if (q < Q.cap_c) tmp[q] = pv;
+        }
+      }
+    }
+  }
+#else
+  // (i) warp-cooperative sweep (the previous layout, for A/B): warp v takes sorted positions i = v, v + 8, ...;
   // its lanes test the next 32 positions at once until the sorted low ends pass
   // geom i's high end; every pair found goes to a temporary list (ncon's
   // storage) and is counted in its bucket (the lower geom id)
@@ -738,6 +851,7 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
       }
     }
   }
+#endif
   BP_MARK(9);
   // (ii) planes (lowest geom ids): count their hits
   for (int p = 0; p < G && P.geom[p].x == G_PLANE; ++p) {
@@ -840,10 +954,15 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
     }
     __syncthreads();
   }
+  // one narrowphase pass: counts, and the records staged (in the order found)
+  if (tid == 0) s_misc[6] = 0;
+  __syncthreads();
+  const Stage S{Q.stage + (size_t)w * 2 * Q.stage_cap, Q.stage + ((size_t)w * 2 + 1) * Q.stage_cap, Q.stage_cap,
+                &s_misc[6]};
   for (int i = tid; i < n_cand; i += kBpThreads) {
     const int k = perm[i];
     const uint32_t pv = list[k];
-    ncon[k] = pair_contacts<false>(P, make_int2((int)(pv >> 16), (int)(pv & 0xffffu)), Fw, w, 0, &Ts);
+    ncon[k] = pair_contacts_stage(P, make_int2((int)(pv >> 16), (int)(pv & 0xffffu)), Fw, w, &Ts, &S, k);
   }
   __syncthreads();
   int world_total = 0;
@@ -890,17 +1009,43 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
   BP_MARK(6);
   // 5: emit (records [base, base + world_total)); a candidate that does not fit
   // is skipped, and the smallest such offset is the count of whole pairs
-  for (int i = tid; i < n_cand; i += kBpThreads) {
-    const int k = perm[i];
-    const int off = ncon[k];
-    const int next = (k + 1 < n_cand) ? ncon[k + 1] : world_total;
-    if (next == off) continue;
-    if (base + next > Q.capacity) {
-      atomicMin(reinterpret_cast<unsigned long long*>(Q.queue + 2), (unsigned long long)(base + off));
-      continue;
+  if (world_total <= Q.stage_cap) {
+    // the staged records to their places (thread per record)
+    for (int r = tid; r < world_total; r += kBpThreads) {
+      const float4 a = S.s0[r], b = S.s1[r];
+      const int tag = __float_as_int(b.w), k = tag >> 5;
+      const int off = ncon[k];
+      const int next = (k + 1 < n_cand) ? ncon[k + 1] : world_total;
+      if (base + next > Q.capacity) {
+        atomicMin(reinterpret_cast<unsigned long long*>(Q.queue + 2), (unsigned long long)(base + off));
+        continue;
+      }
+      const uint32_t pv = list[k];
+      const int4 g1 = Ts.geom[pv >> 16], g2 = Ts.geom[pv & 0xffffu];
+      const int64_t c = base + off + (tag & 31);
+      const V3 nn = v3(b.x, b.y, b.z);
+      const V3 t1 = tangent(nn);
+      P.c0[c] = a;
+      P.c1[c] = make_float4(nn.x, nn.y, nn.z, P.mu_t);
+      P.c2[c] = make_float4(t1.x, t1.y, t1.z, P.mu_tor);
+      P.c3[c] = make_int4(g1.y, g2.y, __float_as_int(P.mu_rol), P.condim);
+      P.world[c] = (int32_t)w;
+      P.link[c] = make_int2(g1.y < -1 ? g1.z : 0, g2.y < -1 ? g2.z : 0);
     }
-    const uint32_t pv = list[k];
-    pair_contacts<true>(P, make_int2((int)(pv >> 16), (int)(pv & 0xffffu)), Fw, w, base + off, &Ts);
+  } else {
+    // more records than the staging area holds: the narrowphase again, written in place
+    for (int i = tid; i < n_cand; i += kBpThreads) {
+      const int k = perm[i];
+      const int off = ncon[k];
+      const int next = (k + 1 < n_cand) ? ncon[k + 1] : world_total;
+      if (next == off) continue;
+      if (base + next > Q.capacity) {
+        atomicMin(reinterpret_cast<unsigned long long*>(Q.queue + 2), (unsigned long long)(base + off));
+        continue;
+      }
+      const uint32_t pv = list[k];
+      pair_contacts<true>(P, make_int2((int)(pv >> 16), (int)(pv & 0xffffu)), Fw, w, base + off, &Ts);
+    }
   }
   BP_MARK(7);
   // the last CTA: device count, error, reset of the counters for the next launch
@@ -926,10 +1071,11 @@ size_t collide_bp_smem(int n_geoms, int cap_c, int np2) {
 }
 
 cudaError_t collide_broadphase(const CollideParams& P, int cap_c, int64_t capacity, unsigned long long* status,
-                               int* queue, int64_t* n_dev, int64_t* total, int* err, cudaStream_t s) {
+                               int* queue, int64_t* n_dev, int64_t* total, int* err, float4* stage, int stage_cap,
+                               cudaStream_t s) {
   if (P.n_worlds == 0) return cudaMemsetAsync(n_dev, 0, sizeof(int64_t), s);
   int np2 = 1;
-  while (np2 < P.n_geoms) np2 <<= 1;
+  while (np2 < P.n_geoms + 1) np2 <<= 1;  // the flat sweep's prefix takes n_np + 1 <= G + 1 entries
   const size_t smem = collide_bp_smem(P.n_geoms, cap_c, np2);
   // zeroed status words and counters; queue[2..3]: the cut (int64) starts at
   // 0x7f7f...7f (above any count); memsets only, so the launch is graph-capturable
@@ -939,7 +1085,7 @@ cudaError_t collide_broadphase(const CollideParams& P, int cap_c, int64_t capaci
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(k_collide_bp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  BpParams Q{cap_c, np2, capacity, status, queue, n_dev, total, err};
+  BpParams Q{cap_c, np2, capacity, status, queue, n_dev, total, err, stage, stage_cap};
   k_collide_bp<<<(unsigned)P.n_worlds, kBpThreads, smem, s>>>(P, Q);
   return cudaGetLastError();
 }

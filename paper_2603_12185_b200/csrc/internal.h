@@ -140,8 +140,11 @@ cudaError_t collide_frames(const CollideParams& P, cudaStream_t s);
 // over worlds.  status [n_worlds] and queue [4 ints] are scratch; n_dev gets
 // the count of whole pairs within `capacity`, total (optional) every contact.
 size_t collide_bp_smem(int n_geoms, int cap_c, int np2);
+// stage: [n_worlds][2][stage_cap] float4 scratch for the records of the single
+// narrowphase pass (a world with more records evaluates the narrowphase again).
 cudaError_t collide_broadphase(const CollideParams& P, int cap_c, int64_t capacity, unsigned long long* status,
-                               int* queue, int64_t* n_dev, int64_t* total, int* err, cudaStream_t s);
+                               int* queue, int64_t* n_dev, int64_t* total, int* err, float4* stage, int stage_cap,
+                               cudaStream_t s);
 cudaError_t collide_count_scan(const CollideParams& P, int32_t* counts, int32_t* offs, void* temp,
                                size_t* temp_bytes, cudaStream_t s);
 // n_dev != null: also stores the (clamped) total for the asynchronous mode

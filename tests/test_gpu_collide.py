@@ -437,3 +437,31 @@ def test_broadphase_device_count_overflow_and_graph():
     assert int(dc.n_dev.item()) == nf
     for k in ("world", "c0", "c3"):
         np.testing.assert_array_equal(getattr(dc, k)[:nf].cpu().numpy(), ref[k])
+
+
+def test_broadphase_stage_fallback_identical(tmp_path):
+    """The broadphase stages the records of its single narrowphase pass and
+    places them once the world's base is known; a world with more records
+    than the staging area evaluates the narrowphase again in place.  Both give
+    bitwise the same contact list (host and device count, overflow cut):
+    default staging vs a 600-record staging area (every pile world falls back)
+    vs 1350 (some do: 1328-1362 records per world)."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    outs = []
+    for cap in ("0", "600", "1350"):
+        out = str(tmp_path / f"bp_{cap}.npz")
+        env = dict(os.environ)
+        if cap != "0":
+            env["COMFREE_BP_STAGE_CAP"] = cap
+        subprocess.run([sys.executable, os.path.join(here, "_bp_stage_dump.py"), out], check=True, env=env,
+                       cwd=os.path.dirname(here), timeout=300)
+        outs.append(np.load(out))
+    a = outs[0]
+    assert a["0_world"].shape[0] > 7 * 1000 and 0 < int(a["cut_n"]) <= 3001
+    for b in outs[1:]:
+        assert set(a.files) == set(b.files)
+        for k in a.files:
+            np.testing.assert_array_equal(a[k], b[k], err_msg=k)
