@@ -952,7 +952,10 @@ comfree_status comfree_collide(comfree_ctx* ctx, int64_t first, int64_t nw, int6
     int np2 = 1;
     while (np2 < ctx->n_geoms + 1) np2 <<= 1;  // as collide_broadphase
     const size_t fixed = cf::collide_bp_smem(ctx->n_geoms, 0, np2);
-    const int64_t room = (int64_t)(110 * 1024) - (int64_t)fixed;  // two CTAs per SM
+    // candidate capacity: two CTAs per SM when that leaves room for 8
+    // candidates per geom (a dense pile has ~7), else one CTA per SM
+    int64_t room = (int64_t)(110 * 1024) - (int64_t)fixed;
+    if (room / 10 < 8 * (int64_t)ctx->n_geoms) room = (int64_t)(220 * 1024) - (int64_t)fixed;
     const int cap_c = (int)std::max<int64_t>(1024, std::min<int64_t>(room / 10 & ~7, 65535));
     if (cf::collide_bp_smem(ctx->n_geoms, cap_c, np2) > 227 * 1024)
       return fail(ctx, COMFREE_ERR_CAPACITY, "collide: %d geoms per world exceed the broadphase's shared memory", ctx->n_geoms);

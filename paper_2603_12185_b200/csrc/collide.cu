@@ -729,14 +729,49 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
   }
   BP_MARK(8);
 #if CF_BP_FLAT
-  // (i) flat sweep: the range of sorted position i is (i, e_i], the positions
+  // (i) sweep; every pair found goes to a temporary list (ncon's storage) and
+  // is counted in its bucket (the lower geom id).  Appends go through a
+  // 32-entry buffer per warp, one list atomic per 32 pairs.
+  uint32_t* tmp = reinterpret_cast<uint32_t*>(ncon);
+  if (tid == 0) s_misc[5] = 0;
+  __shared__ uint32_t s_wbuf[kBpThreads];
+  const int lane = tid & 31;
+  uint32_t* wbuf = s_wbuf + (tid & ~31);
+  int wn = 0;  // pairs in the warp's buffer (warp-uniform)
+  auto append = [&](bool found, uint32_t pv) {
+    const unsigned fb = __ballot_sync(0xffffffffu, found);
+    if (!fb) return;
+    const int nf = __popc(fb);
+    if (wn + nf > 32) {
+      int t0 = 0;
+      if (lane == 0) t0 = atomicAdd(&s_misc[5], wn);
+      t0 = __shfl_sync(0xffffffffu, t0, 0);
+      if (lane < wn && t0 + lane < Q.cap_c) tmp[t0 + lane] = wbuf[lane];
+      __syncwarp();
+      wn = 0;
+    }
+    if (found) {
+      atomicAdd(&cnt[pv >> 16], 1);
+      wbuf[wn + __popc(fb & ((1u << lane) - 1u))] = pv;
+    }
+    wn += nf;
+    __syncwarp();
+  };
+  auto flush = [&]() {
+    if (!wn) return;
+    int t0 = 0;
+    if (lane == 0) t0 = atomicAdd(&s_misc[5], wn);
+    t0 = __shfl_sync(0xffffffffu, t0, 0);
+    if (lane < wn && t0 + lane < Q.cap_c) tmp[t0 + lane] = wbuf[lane];
+    wn = 0;
+  };
+  {
+  // flat sweep: the range of sorted position i is (i, e_i], the positions
   // whose low end is within its high end (binary search on the sorted keys);
   // the ranges' tests are numbered by an exclusive scan and split evenly over
   // the threads, each walking its contiguous share (one test per iteration,
-  // every lane busy); every pair found goes to a temporary list (ncon's
-  // storage) and is counted in its bucket (the lower geom id)
-  uint32_t* tmp = reinterpret_cast<uint32_t*>(ncon);
-  if (tid == 0) s_misc[5] = 0;
+  // every lane busy).  (A warp per sorted position over sorted, contiguous
+  // AABB copies measured slower: 75 vs 55 us per world CTA.)
   for (int i = tid; i < n_np; i += kBpThreads) {
     const uint32_t hk = f2key(axis_of(hi[val[i]]));
     int a = i, b = n_np;  // key[a] <= hk < key[b] (b virtual)
@@ -760,7 +795,6 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
   if (tid == 0) tpre[n_np] = n_tests;
   __syncthreads();
   {
-    const int lane = tid & 31;
     const int per = (n_tests + kBpThreads - 1) / kBpThreads;
     int t = tid * per;
     const int tend = min(n_tests, t + per);
@@ -795,18 +829,10 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
           gi = (int)val[i]; li = lo[gi]; hv = hi[gi]; bi = gbody[gi];
         }
       }
-      const unsigned fb = __ballot_sync(0xffffffffu, found);
-      if (fb) {  // one append per warp and iteration
-        int t0 = 0;
-        if (lane == 0) t0 = atomicAdd(&s_misc[5], __popc(fb));
-        t0 = __shfl_sync(0xffffffffu, t0, 0);
-        if (found) {
-          atomicAdd(&cnt[pv >> 16], 1);
-          const int q = t0 + __popc(fb & ((1u << lane) - 1u));
-          if (q < Q.cap_c) tmp[q] = pv;
-        }
-      }
+      append(found, pv);
     }
+    flush();
+  }
   }
 #else
   // (i) warp-cooperative sweep (the previous layout, for A/B): warp v takes sorted positions i = v, v + 8, ...;

@@ -378,6 +378,47 @@ def test_broadphase_pile_matches_oracle():
     _compare_off_threshold(dc, link, ref, geo.margin)
 
 
+def test_broadphase_large_pile_one_cta_per_sm():
+    """An 801-geom pile (16 x 10 x 5 lattice): the candidate list gets the
+    one-CTA-per-SM shared-memory budget (two CTAs would leave room for fewer
+    than 8 candidates per geom); same list as the oracle."""
+    import paper_2603_12185_b200 as cf
+    scene, st, _ = scenes.c4_pile(n_worlds=3, contacts_per_world=2000, lattice=(16, 10, 5))
+    geo = scenes.pile_geometry((16, 10, 5), broadphase=True)
+    ctx = cf.Context(CFG)
+    ctx.load_scene(scene, st.n_worlds, st)
+    ctx.load_geometry(geo)
+    dc, link = ctx.collide(capacity=3 * 6000)
+    ref = co.collide(geo, st.astype(np.float64), None)
+    assert ref.n > 3 * 1800
+    _compare_off_threshold(dc, link, ref, geo.margin)
+
+
+def test_broadphase_sparse_1500_spheres():
+    """1500 spheres scattered over a 1.5 m x 1.5 m x 0.3 m box above a plane
+    (one CTA per SM, a 2048-entry sort, sparse candidates): same list as the
+    oracle."""
+    import paper_2603_12185_b200 as cf
+    from harness.types import Scene
+    rng = np.random.default_rng(7)
+    W, B = 2, 1500
+    geo = Geometry(np.array([2] + [0] * B, np.int32), np.array([-1] + list(range(B)), np.int32),
+                   np.zeros(B + 1, np.int32), np.array([(0, 0, 1.0)] + [(0.02, 0, 0)] * B), np.zeros((B + 1, 3)),
+                   None, margin=0.004, mu=(0.7, 0.01, 0.001), condim=3)
+    pos = rng.uniform([0, 0, 0.01], [1.5, 1.5, 0.3], (W, B, 3))
+    quat = np.zeros((W, B, 4))
+    quat[..., 0] = 1
+    st = State(pos, quat, np.zeros((W, B, 3)), np.zeros((W, B, 3)), np.zeros((W, 0)), np.zeros((W, 0))).astype(np.float32)
+    scene = Scene(np.full(B, 2.0, np.float32), np.full((B, 3), 500.0, np.float32))
+    ctx = cf.Context(CFG)
+    ctx.load_scene(scene, W, st)
+    ctx.load_geometry(geo)
+    dc, link = ctx.collide(capacity=W * 3000)
+    ref = co.collide(geo, st.astype(np.float64), None)
+    assert ref.n > W * 100
+    _compare_off_threshold(dc, link, ref, geo.margin)
+
+
 @pytest.mark.parametrize("seed", range(3))
 def test_broadphase_random_scenes_match_oracle(seed):
     """Random spheres / boxes / capsules above a plane, random orientations
