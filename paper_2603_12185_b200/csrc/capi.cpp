@@ -956,28 +956,32 @@ comfree_status comfree_collide(comfree_ctx* ctx, int64_t first, int64_t nw, int6
     // candidates per geom (a dense pile has ~7), else one CTA per SM
     int64_t room = (int64_t)(110 * 1024) - (int64_t)fixed;
     if (room / 10 < 8 * (int64_t)ctx->n_geoms) room = (int64_t)(220 * 1024) - (int64_t)fixed;
-    const int cap_c = (int)std::max<int64_t>(1024, std::min<int64_t>(room / 10 & ~7, 65535));
+    // (at least collide_bp_min_cap: the candidate list's storage holds the
+    // sort's and the sweep's scratch before the candidates)
+    const int min_cap = (cf::collide_bp_min_cap(ctx->n_geoms, np2) + 7) & ~7;
+    const int cap_c = (int)std::max<int64_t>(std::max(1024, min_cap), std::min<int64_t>(room / 10 & ~7, 65535));
     if (cf::collide_bp_smem(ctx->n_geoms, cap_c, np2) > 227 * 1024)
       return fail(ctx, COMFREE_ERR_CAPACITY, "collide: %d geoms per world exceed the broadphase's shared memory", ctx->n_geoms);
-    CUDA_TRY(ctx, ensure(ctx->bp_status, std::max<int64_t>(1, nw) * sizeof(unsigned long long)));
-    CUDA_TRY(ctx, ensure(ctx->bp_queue, 4 * sizeof(int)));
+    CUDA_TRY(ctx, ensure(ctx->bp_status, (std::max<int64_t>(1, nw) + (std::max<int64_t>(1, nw) + 255) / 256) * sizeof(unsigned long long)));  // + group sums
+    CUDA_TRY(ctx, ensure(ctx->bp_queue, 8 * sizeof(int)));
     CUDA_TRY(ctx, ensure(ctx->bp_count, 2 * sizeof(int64_t)));
     int64_t* cnt = static_cast<int64_t*>(ctx->bp_count.p);
 #ifdef CF_BP_TIMELINE
     CUDA_TRY(ctx, ensure(ctx->col_frames, std::max<size_t>(1, (size_t)nw) * 16 * sizeof(unsigned long long)));
     P.frames = static_cast<float4*>(ctx->col_frames.p);
 #endif
-    // staged records per world: 16 per geom (the settled pile: ~10 per geom)
+    // staged records per world: 16 per geom (the settled pile: ~10 per geom),
+    // found order and placed (two areas of 2 x stage_cap float4)
     static const int stage_env = [] {  // test override of the staging size (exercises the second pass)
       const char* e = getenv("COMFREE_BP_STAGE_CAP");
       return e ? atoi(e) : 0;
     }();
     const int stage_cap = stage_env > 0 ? stage_env : (int)std::min<int64_t>(16 * (int64_t)ctx->n_geoms + 256, 1 << 20);
-    CUDA_TRY(ctx, ensure(ctx->bp_stage, std::max<int64_t>(1, nw) * 2 * (size_t)stage_cap * sizeof(float4)));
+    CUDA_TRY(ctx, ensure(ctx->bp_stage, std::max<int64_t>(1, nw) * 4 * (size_t)stage_cap * sizeof(float4)));
     CUDA_TRY(ctx, cf::collide_broadphase(P, cap_c, capacity, static_cast<unsigned long long*>(ctx->bp_status.p),
                                          static_cast<int*>(ctx->bp_queue.p), n_device ? n_device : cnt, cnt + 1,
                                          ctx->d_err, static_cast<float4*>(ctx->bp_stage.p), stage_cap, s));
-    ctx->launches += 1;
+    ctx->launches += 2;
     if (n_device) return COMFREE_OK;
     int64_t h[2] = {0, 0};
     CUDA_TRY(ctx, cudaMemcpyAsync(h, cnt, sizeof h, cudaMemcpyDeviceToHost, s));

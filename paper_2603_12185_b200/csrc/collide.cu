@@ -10,6 +10,7 @@
 // free tangent (Duff et al. 2017).
 // Three passes, one thread per (world, pair): count, exclusive scan (CUB),
 // emit at the scanned offset -> world-major, pair-ordered, deterministic.
+#include <algorithm>
 #include <cub/cub.cuh>
 #include <cuda_runtime.h>
 #include <math.h>
@@ -591,17 +592,49 @@ __device__ __forceinline__ int block_exclusive(int v, int* tmp, int* tot) {
   return before + x - v;
 }
 
+// Chained-scan status words (one per world): bits 62-63 flag (1 the world's
+// total is published; 2 an inclusive prefix, the virtual word before world 0),
+// bit 61 "records already written" (the staging fallback), low 61 bits the value.
+constexpr int kGsumShift = 8;  // worlds per group sum: 256
+constexpr unsigned long long kStAgg = 1ull << 62, kStInc = 2ull << 62, kStDone = 1ull << 61,
+                             kStVal = (1ull << 61) - 1;
+
+// Sum of the totals of worlds [0, w), one warp: 32 status words per round,
+// walking back to the nearest inclusive prefix; re-reads a round while a world
+// before that prefix has not published its total yet.
+__device__ __forceinline__ long long lookback_warp(unsigned long long* status, int64_t w, int lane) {
+  const unsigned full = 0xffffffffu;
+  const volatile unsigned long long* st = status;
+  long long prefix = 0;
+  for (int64_t j = w - 1; j >= 0;) {
+    const int64_t jj = j - lane;
+    const unsigned long long v = jj >= 0 ? st[jj] : kStInc;  // before world 0: an inclusive 0
+    const unsigned f = (unsigned)(v >> 62);
+    const unsigned inc = __ballot_sync(full, f == 2);
+    const unsigned upto = inc ? ((inc & (0u - inc)) << 1) - 1u : full;  // lanes up to the nearest inclusive
+    if (__ballot_sync(full, f == 0) & upto) continue;                   // a total still missing: re-read
+    long long x = ((upto >> lane) & 1u) ? (long long)(v & kStVal) : 0ll;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(full, x, o);
+    prefix += x;
+    if (inc) break;
+    j -= 32;
+  }
+  return prefix;
+}
+
 struct BpParams {
   int cap_c;                       // candidate capacity per world (shared memory)
   int np2;                         // power of two >= non-plane geoms
   int64_t capacity;                // output records
   unsigned long long* status;      // [n_worlds] chained-scan words (zeroed before the launch)
-  int* queue;                      // [0] world ticket, [1] CTAs done, [2] cut (zeroed before the launch)
+  int* queue;                      // [0] world ticket, [2..3] cut (int64), [4] emit ticket, [5] emit CTAs done
   int64_t* n_dev;                  // device count out (whole pairs within the capacity)
   int64_t* total;                  // all contacts of the launch (or null)
   int* err;
-  float4* stage;                   // [n_worlds][2][stage_cap] staged records
+  float4* stage;                   // [n_worlds][4][stage_cap]: staged records (found order), placed records
   int stage_cap;                   // records per world (a world with more runs the narrowphase twice)
+  unsigned long long* gsum;        // [ceil(n_worlds / 256)] totals of groups of worlds (zeroed before the launch)
 };
 
 __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_constant__ CollideParams P,
@@ -613,13 +646,16 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
   float4* Fw = bsm;                                                   // [3 G]
   float4* lo = Fw + 3 * G;                                            // [G] (.w: 1 = plane)
   float4* hi = lo + G;                                                // [G]
-  uint32_t* key = reinterpret_cast<uint32_t*>(hi + G);                // [np2]
+  uint32_t* list = reinterpret_cast<uint32_t*>(hi + G);               // [cap_c] (g1 << 16) | g2
+  // list is dead until the bucket placement: it holds the sort's exchange
+  // buffer and then the sweep's sorted cross-axis extents (collide_bp_min_cap)
+  float4* sxa = reinterpret_cast<float4*>(list);                      // [np2]
+  uint32_t* key = list + Q.cap_c;                                     // [np2]
   uint32_t* val = key + Q.np2;                                        // [np2]
   int* gbody = reinterpret_cast<int*>(val + Q.np2);                   // [G] body of each geom
   int* cnt = gbody + G;                                               // [G + 1]
   int* start = cnt + G + 1;                                           // [G + 1]
-  uint32_t* list = reinterpret_cast<uint32_t*>(start + G + 1);        // [cap_c] (g1 << 16) | g2
-  int* ncon = reinterpret_cast<int*>(list + Q.cap_c);                 // [cap_c]
+  int* ncon = start + G + 1;                                          // [cap_c]
   uint16_t* perm = reinterpret_cast<uint16_t*>(ncon + Q.cap_c);      // [cap_c] evaluation order
   if (tid == 0) s_misc[0] = atomicAdd(&Q.queue[0], 1);
   __syncthreads();
@@ -697,6 +733,37 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
     val[i] = real ? (uint32_t)i : 0xffffffffu;
   }
   __syncthreads();
+  if (Q.np2 <= kBpThreads) {
+    // one element per thread (threads >= np2 idle along): the network's
+    // stages with partner distance j < 32 are register shuffles, the others
+    // one exchange through a double-buffered shared array
+    const int n2 = Q.np2;
+    uint64_t x = tid < n2 ? (((uint64_t)key[tid] << 32) | val[tid]) : ~0ull;
+    uint64_t* xb = reinterpret_cast<uint64_t*>(sxa);  // 2 x np2 (list's storage, dead here)
+    int buf = 0;
+#pragma unroll 1
+    for (int k = 2; k <= n2; k <<= 1) {
+#pragma unroll 1
+      for (int j = k >> 1; j > 0; j >>= 1) {
+        uint64_t y;
+        if (j >= 32) {
+          if (tid < n2) xb[buf * n2 + tid] = x;
+          __syncthreads();
+          y = tid < n2 ? xb[buf * n2 + (tid ^ j)] : x;
+          buf ^= 1;
+        } else {
+          y = __shfl_xor_sync(0xffffffffu, x, j);
+        }
+        const bool keep_min = ((tid & k) == 0) == ((tid & j) == 0);
+        x = keep_min ? (x < y ? x : y) : (x < y ? y : x);
+      }
+    }
+    __syncthreads();
+    if (tid < Q.np2) {
+      key[tid] = (uint32_t)(x >> 32);
+      val[tid] = (uint32_t)x;
+    }
+  } else {
   for (int k = 2; k <= Q.np2; k <<= 1) {
     for (int j = k >> 1; j > 0; j >>= 1) {
       for (int t = tid; t < (Q.np2 >> 1); t += kBpThreads) {
@@ -708,6 +775,7 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
       }
       __syncthreads();
     }
+  }
   }
   BP_MARK(2);
   // 2b: sweep, twice: count per bucket, then place
@@ -772,8 +840,16 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
   // the threads, each walking its contiguous share (one test per iteration,
   // every lane busy).  (A warp per sorted position over sorted, contiguous
   // AABB copies measured slower: 75 vs 55 us per world CTA.)
+  // sorted copies of the two other axes' extents (lo1, lo2, hi1, hi2): a test
+  // reads one contiguous float4; the sweep axis needs no test inside a range
+  // (lo_i <= lo_j <= hi_i there, and lo_j <= hi_j)
+  const int a1 = ax == 0 ? 1 : 0, a2 = ax == 2 ? 1 : 2;
+  auto comp = [](const float4& v, int k) { return k == 0 ? v.x : (k == 1 ? v.y : v.z); };
   for (int i = tid; i < n_np; i += kBpThreads) {
-    const uint32_t hk = f2key(axis_of(hi[val[i]]));
+    const int g = (int)val[i];
+    const float4 l = lo[g], h = hi[g];
+    sxa[i] = make_float4(comp(l, a1), comp(l, a2), comp(h, a1), comp(h, a2));
+    const uint32_t hk = f2key(axis_of(h));
     int a = i, b = n_np;  // key[a] <= hk < key[b] (b virtual)
     while (b - a > 1) {
       const int m = (a + b) >> 1;
@@ -799,7 +875,7 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
     int t = tid * per;
     const int tend = min(n_tests, t + per);
     int i = 0, j = 0, e = 0, gi = 0, bi = 0;
-    float4 li = make_float4(0.f, 0.f, 0.f, 0.f), hv = li;
+    float4 si = make_float4(0.f, 0.f, 0.f, 0.f);
     if (t < tend) {
       int a = 0, b = n_np;  // tpre[a] <= t < tpre[b]
       while (b - a > 1) {
@@ -809,16 +885,16 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
       i = a;
       j = i + 1 + (t - tpre[i]);
       e = i + (tpre[i + 1] - tpre[i]);
-      gi = (int)val[i]; li = lo[gi]; hv = hi[gi]; bi = gbody[gi];
+      gi = (int)val[i]; si = sxa[i]; bi = gbody[gi];
     }
     for (int it = 0; it < per; ++it) {
       bool found = false;
       uint32_t pv = 0;
       if (t < tend) {
-        const int gj = (int)val[j];
-        if (gbody[gj] != bi) {
-          const float4 lj = lo[gj], hj = hi[gj];
-          found = li.x <= hj.x && lj.x <= hv.x && li.y <= hj.y && lj.y <= hv.y && li.z <= hj.z && lj.z <= hv.z;
+        const float4 sj = sxa[j];
+        if (si.x <= sj.z && sj.x <= si.z && si.y <= sj.w && sj.y <= si.w) {
+          const int gj = (int)val[j];
+          found = gbody[gj] != bi;
           pv = ((uint32_t)min(gi, gj) << 16) | (uint32_t)max(gi, gj);
         }
         ++t;
@@ -826,7 +902,7 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
           do { ++i; } while (tpre[i + 1] == tpre[i]);
           j = i + 1;
           e = i + (tpre[i + 1] - tpre[i]);
-          gi = (int)val[i]; li = lo[gi]; hv = hi[gi]; bi = gbody[gi];
+          gi = (int)val[i]; si = sxa[i]; bi = gbody[gi];
         }
       }
       append(found, pv);
@@ -983,7 +1059,7 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
   // one narrowphase pass: counts, and the records staged (in the order found)
   if (tid == 0) s_misc[6] = 0;
   __syncthreads();
-  const Stage S{Q.stage + (size_t)w * 2 * Q.stage_cap, Q.stage + ((size_t)w * 2 + 1) * Q.stage_cap, Q.stage_cap,
+  const Stage S{Q.stage + (size_t)w * 4 * Q.stage_cap, Q.stage + ((size_t)w * 4 + 1) * Q.stage_cap, Q.stage_cap,
                 &s_misc[6]};
   for (int i = tid; i < n_cand; i += kBpThreads) {
     const int k = perm[i];
@@ -1005,50 +1081,107 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
     world_total = run;
   }
   BP_MARK(5);
-  // 4: chained scan over worlds (status: bits 62-63 flag 1 aggregate / 2 inclusive, low bits value)
-  if (tid == 0) {
-    const unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62, kVal = (1ull << 62) - 1;
-    volatile unsigned long long* st = Q.status;
-    long long prefix = 0;
-    if (w == 0) {
-      __threadfence();
-      atomicExch(&Q.status[0], kInc | (unsigned long long)world_total);
-    } else {
-      __threadfence();
-      atomicExch(&Q.status[w], kAgg | (unsigned long long)world_total);
-      for (int64_t j = w - 1; j >= 0;) {
-        const unsigned long long v = st[j];
-        const unsigned long long f = v >> 62;
-        if (f == 0) continue;                             // predecessor still counting
-        prefix += (long long)(v & kVal);
-        if (f == 2) break;
-        --j;
-      }
-      __threadfence();
-      atomicExch(&Q.status[w], kInc | (unsigned long long)(prefix + world_total));
+  // 4: publish the world's total; the records go to their places in
+  // k_collide_bp_emit, which finds the world's base by a look-back over the
+  // published totals without waiting (every total is there when it runs)
+  if (world_total <= Q.stage_cap) {
+    // the staged records (found order, L2-resident) to their places in the
+    // world, with their pair's (g1, g2) instead of the tag
+    float4* o0 = Q.stage + ((size_t)w * 4 + 2) * Q.stage_cap;
+    float4* o1 = o0 + Q.stage_cap;
+    for (int r = tid; r < world_total; r += kBpThreads) {
+      const float4 a = S.s0[r], b = S.s1[r];
+      const int tag = __float_as_int(b.w), k = tag >> 5;
+      const int l = ncon[k] + (tag & 31);
+      o0[l] = a;
+      o1[l] = make_float4(b.x, b.y, b.z, __uint_as_float(list[k]));
     }
-    s_misc[3] = (int)(prefix >> 31);
-    s_misc[4] = (int)(prefix & 0x7fffffff);
+    if (tid == 0) {
+      atomicAdd(&Q.gsum[w >> kGsumShift], (unsigned long long)world_total);
+      atomicExch(&Q.status[w], kStAgg | (unsigned long long)world_total);
+    }
+    BP_MARK(6);
+    return;
+  }
+  // more records than the staging area holds: the world's base now (a look-
+  // back that may wait for predecessors still counting), then the narrowphase
+  // again, written in place; the emit kernel skips the world (kStDone)
+  if (tid == 0) {
+    atomicAdd(&Q.gsum[w >> kGsumShift], (unsigned long long)world_total);
+    atomicExch(&Q.status[w], kStAgg | (unsigned long long)world_total);
+  }
+  if (tid < 32) {
+    const long long prefix = lookback_warp(Q.status, w, tid);
+    if (tid == 0) {  // the total stays in the word (the emit kernel sums totals)
+      atomicExch(&Q.status[w], kStAgg | kStDone | (unsigned long long)world_total);
+      s_misc[3] = (int)(prefix >> 31);
+      s_misc[4] = (int)(prefix & 0x7fffffff);
+    }
   }
   __syncthreads();
   const int64_t base = ((int64_t)s_misc[3] << 31) | (int64_t)s_misc[4];
   BP_MARK(6);
-  // 5: emit (records [base, base + world_total)); a candidate that does not fit
-  // is skipped, and the smallest such offset is the count of whole pairs
-  if (world_total <= Q.stage_cap) {
-    // the staged records to their places (thread per record)
-    for (int r = tid; r < world_total; r += kBpThreads) {
-      const float4 a = S.s0[r], b = S.s1[r];
-      const int tag = __float_as_int(b.w), k = tag >> 5;
-      const int off = ncon[k];
-      const int next = (k + 1 < n_cand) ? ncon[k + 1] : world_total;
-      if (base + next > Q.capacity) {
-        atomicMin(reinterpret_cast<unsigned long long*>(Q.queue + 2), (unsigned long long)(base + off));
-        continue;
+  // a candidate that does not fit is skipped; the smallest such offset is the
+  // count of whole pairs
+  for (int i = tid; i < n_cand; i += kBpThreads) {
+    const int k = perm[i];
+    const int off = ncon[k];
+    const int next = (k + 1 < n_cand) ? ncon[k + 1] : world_total;
+    if (next == off) continue;
+    if (base + next > Q.capacity) {
+      atomicMin(reinterpret_cast<unsigned long long*>(Q.queue + 2), (unsigned long long)(base + off));
+      continue;
+    }
+    const uint32_t pv = list[k];
+    pair_contacts<true>(P, make_int2((int)(pv >> 16), (int)(pv & 0xffffu)), Fw, w, base + off, &Ts);
+  }
+  BP_MARK(7);
+}
+
+// The broadphase's second launch: one CTA per world takes the world's base
+// offset from the totals k_collide_bp published (group sums of 2^kGsumShift
+// worlds before the world's group, then the single totals inside it: one
+// load per thread, one block reduction, no waiting) and writes the staged
+// records to their places (thread per record): world-major, (g1, g2)-ordered,
+// deterministic.  The last CTA stores the device count (the offset of the
+// first pair that did not fit when the capacity is exceeded).
+constexpr int kBpEmitThreads = 256;
+__global__ void __launch_bounds__(kBpEmitThreads) k_collide_bp_emit(const __grid_constant__ CollideParams P,
+                                                                    const __grid_constant__ BpParams Q) {
+  __shared__ long long s_red[kBpEmitThreads / 32];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int64_t w = blockIdx.x;
+  const unsigned long long sw = Q.status[w];
+  const int world_total = (int)(sw & kStVal);
+  long long x = 0;
+  const int64_t g = w >> kGsumShift, t0 = g << kGsumShift;
+  for (int64_t i = tid; i < g; i += kBpEmitThreads) x += (long long)Q.gsum[i];
+  for (int64_t i = t0 + tid; i < w; i += kBpEmitThreads) x += (long long)(Q.status[i] & kStVal);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  if (lane == 0) s_red[tid >> 5] = x;
+  __syncthreads();
+  if (!(sw & kStDone)) {
+    long long base = 0;
+#pragma unroll
+    for (int q = 0; q < kBpEmitThreads / 32; ++q) base += s_red[q];
+    const float4* o0 = Q.stage + ((size_t)w * 4 + 2) * Q.stage_cap;
+    const float4* o1 = o0 + Q.stage_cap;
+    const bool cut = base + world_total > Q.capacity;  // only whole pairs within the capacity
+    for (int l = tid; l < world_total; l += kBpEmitThreads) {
+      const float4 a = o0[l], b = o1[l];
+      const uint32_t pv = __float_as_uint(b.w);
+      if (cut) {  // the pair's records [off, next) are the neighbours with its (g1, g2)
+        int off = l, next = l + 1;
+        while (off > 0 && __float_as_uint(o1[off - 1].w) == pv) --off;
+        while (next < world_total && __float_as_uint(o1[next].w) == pv) ++next;
+        if (base + next > Q.capacity) {
+          atomicMin(reinterpret_cast<unsigned long long*>(Q.queue + 2), (unsigned long long)(base + off));
+          continue;
+        }
       }
-      const uint32_t pv = list[k];
-      const int4 g1 = Ts.geom[pv >> 16], g2 = Ts.geom[pv & 0xffffu];
-      const int64_t c = base + off + (tag & 31);
+      const int4 g1 = P.geom[pv >> 16], g2 = P.geom[pv & 0xffffu];
+      const int64_t c = base + l;
       const V3 nn = v3(b.x, b.y, b.z);
       const V3 t1 = tangent(nn);
       P.c0[c] = a;
@@ -1058,29 +1191,15 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
       P.world[c] = (int32_t)w;
       P.link[c] = make_int2(g1.y < -1 ? g1.z : 0, g2.y < -1 ? g2.z : 0);
     }
-  } else {
-    // more records than the staging area holds: the narrowphase again, written in place
-    for (int i = tid; i < n_cand; i += kBpThreads) {
-      const int k = perm[i];
-      const int off = ncon[k];
-      const int next = (k + 1 < n_cand) ? ncon[k + 1] : world_total;
-      if (next == off) continue;
-      if (base + next > Q.capacity) {
-        atomicMin(reinterpret_cast<unsigned long long*>(Q.queue + 2), (unsigned long long)(base + off));
-        continue;
-      }
-      const uint32_t pv = list[k];
-      pair_contacts<true>(P, make_int2((int)(pv >> 16), (int)(pv & 0xffffu)), Fw, w, base + off, &Ts);
-    }
   }
-  BP_MARK(7);
-  // the last CTA: device count, error, reset of the counters for the next launch
+  // the last CTA: device count, error
   __syncthreads();
   if (tid == 0) {
     __threadfence();
-    if (atomicAdd(&Q.queue[1], 1) == (int)gridDim.x - 1) {
-      const unsigned long long vl = atomicAdd(&Q.status[P.n_worlds - 1], 0ull);
-      const int64_t total = (int64_t)(vl & ((1ull << 62) - 1));
+    if (atomicAdd(&Q.queue[5], 1) == (int)gridDim.x - 1) {
+      __threadfence();
+      int64_t total = 0;
+      for (int64_t i = 0; i <= (P.n_worlds - 1) >> kGsumShift; ++i) total += (int64_t)atomicAdd(&Q.gsum[i], 0ull);
       const unsigned long long cut = atomicAdd(reinterpret_cast<unsigned long long*>(Q.queue + 2), 0ull);
       if (total > Q.capacity) atomicOr(Q.err, ERR_CONTACT_CAP);
       Q.n_dev[0] = (int64_t)cut < total ? (int64_t)cut : total;
@@ -1090,6 +1209,12 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
 }
 
 }  // namespace
+
+// candidate-list words the sort (np2 <= block: 2 x np2 uint64 exchange) and
+// the sweep (n_np <= n_geoms float4) borrow before the candidates go in
+int collide_bp_min_cap(int n_geoms, int np2) {
+  return std::max(4 * n_geoms, np2 <= kBpThreads ? 4 * np2 : 0);
+}
 
 size_t collide_bp_smem(int n_geoms, int cap_c, int np2) {
   return (size_t)5 * n_geoms * sizeof(float4) + (size_t)2 * np2 * sizeof(uint32_t) +
@@ -1104,15 +1229,20 @@ cudaError_t collide_broadphase(const CollideParams& P, int cap_c, int64_t capaci
   while (np2 < P.n_geoms + 1) np2 <<= 1;  // the flat sweep's prefix takes n_np + 1 <= G + 1 entries
   const size_t smem = collide_bp_smem(P.n_geoms, cap_c, np2);
   // zeroed status words and counters; queue[2..3]: the cut (int64) starts at
-  // 0x7f7f...7f (above any count); memsets only, so the launch is graph-capturable
-  cudaError_t e = cudaMemsetAsync(status, 0, (size_t)P.n_worlds * sizeof(unsigned long long), s);
-  if (e == cudaSuccess) e = cudaMemsetAsync(queue, 0, 2 * sizeof(int), s);
+  // 0x7f7f...7f (above any count); memsets only, so the launches are graph-capturable
+  // status words followed by the group sums (one allocation)
+  const size_t n_status = (size_t)P.n_worlds + (((size_t)P.n_worlds + 255) >> kGsumShift);
+  cudaError_t e = cudaMemsetAsync(status, 0, n_status * sizeof(unsigned long long), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(queue, 0, 8 * sizeof(int), s);
   if (e == cudaSuccess) e = cudaMemsetAsync(queue + 2, 0x7f, sizeof(int64_t), s);
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(k_collide_bp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  BpParams Q{cap_c, np2, capacity, status, queue, n_dev, total, err, stage, stage_cap};
+  BpParams Q{cap_c, np2, capacity, status, queue, n_dev, total, err, stage, stage_cap, status + P.n_worlds};
   k_collide_bp<<<(unsigned)P.n_worlds, kBpThreads, smem, s>>>(P, Q);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_collide_bp_emit<<<(unsigned)P.n_worlds, kBpEmitThreads, 0, s>>>(P, Q);
   return cudaGetLastError();
 }
 

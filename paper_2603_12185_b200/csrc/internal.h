@@ -140,6 +140,7 @@ cudaError_t collide_frames(const CollideParams& P, cudaStream_t s);
 // over worlds.  status [n_worlds] and queue [4 ints] are scratch; n_dev gets
 // the count of whole pairs within `capacity`, total (optional) every contact.
 size_t collide_bp_smem(int n_geoms, int cap_c, int np2);
+int collide_bp_min_cap(int n_geoms, int np2);
 // stage: [n_worlds][2][stage_cap] float4 scratch for the records of the single
 // narrowphase pass (a world with more records evaluates the narrowphase again).
 cudaError_t collide_broadphase(const CollideParams& P, int cap_c, int64_t capacity, unsigned long long* status,
