@@ -953,8 +953,9 @@ comfree_status comfree_collide(comfree_ctx* ctx, int64_t first, int64_t nw, int6
     while (np2 < ctx->n_geoms + 1) np2 <<= 1;  // as collide_broadphase
     const size_t fixed = cf::collide_bp_smem(ctx->n_geoms, 0, np2);
     // candidate capacity: two CTAs per SM when that leaves room for 8
-    // candidates per geom (a dense pile has ~7), else one CTA per SM
-    int64_t room = (int64_t)(110 * 1024) - (int64_t)fixed;
+    // candidates per geom (a dense pile has ~7), else one CTA per SM (the
+    // kernel's static shared memory, ~5 KB, comes on top of each)
+    int64_t room = (int64_t)(108 * 1024) - (int64_t)fixed;
     if (room / 10 < 8 * (int64_t)ctx->n_geoms) room = (int64_t)(220 * 1024) - (int64_t)fixed;
     // (at least collide_bp_min_cap: the candidate list's storage holds the
     // sort's and the sweep's scratch before the candidates)

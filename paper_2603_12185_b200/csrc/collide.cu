@@ -529,8 +529,9 @@ __global__ void k_collide_emit(const __grid_constant__ CollideParams P, const in
 //   1  geom frames (thread per geom) and AABBs grown by margin/2, in shared memory;
 //   2  sort-and-sweep: the non-plane geoms sorted by their AABB's low end along
 //      the axis of largest spread (bitonic sort), each swept forward while the
-//      next low end is within its high end, the other two axes tested; a pair
-//      goes to the bucket of its lower geom id; plane g1 takes every geom whose
+//      next low end is within its high end, the other two axes and the grown
+//      bounding spheres tested (lane per sorted position, a counting and a
+//      placing pass); a pair goes to the bucket of its lower geom id; plane g1 takes every geom whose
 //      AABB reaches below offset + margin/2 (bucket order = geom order, by a
 //      block scan); each bucket sorted -> candidates in (g1, g2) order, the
 //      order reading R32 defines;
@@ -542,9 +543,6 @@ __global__ void k_collide_emit(const __grid_constant__ CollideParams P, const in
 //      base + offset: world-major, (g1, g2)-ordered, deterministic.
 // The last CTA to finish stores the device count (the offset of the first pair
 // that did not fit when the capacity is exceeded) and resets the counters.
-#ifndef CF_BP_FLAT
-#define CF_BP_FLAT 1  // flat sweep (tests split evenly over the threads); 0: warp per sorted position
-#endif
 #ifndef CF_BP_THREADS
 #define CF_BP_THREADS 512  // 16 warps, 2 CTAs per SM: 0.83 vs 0.91 ms collide at 256 (profiles/r02_broadphase.txt)
 #endif
@@ -649,7 +647,6 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
   uint32_t* list = reinterpret_cast<uint32_t*>(hi + G);               // [cap_c] (g1 << 16) | g2
   // list is dead until the bucket placement: it holds the sort's exchange
   // buffer and then the sweep's sorted cross-axis extents (collide_bp_min_cap)
-  float4* sxa = reinterpret_cast<float4*>(list);                      // [np2]
   uint32_t* key = list + Q.cap_c;                                     // [np2]
   uint32_t* val = key + Q.np2;                                        // [np2]
   int* gbody = reinterpret_cast<int*>(val + Q.np2);                   // [G] body of each geom
@@ -688,8 +685,14 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
       l = sub(v3(fminf(a.x, b.x), fminf(a.y, b.y), fminf(a.z, b.z)), v3(sz.x, sz.x, sz.x));
       h = add(v3(fmaxf(a.x, b.x), fmaxf(a.y, b.y), fmaxf(a.z, b.z)), v3(sz.x, sz.x, sz.x));
     }
+    // bounding-sphere radius about the frame origin (sphere R, box |h|,
+    // capsule R + half length) grown by margin/2, with fp32 slack for the
+    // AABB-centre round-off (the test must never reject a contact pair)
+    const float rb = kind == G_SPHERE ? sz.x
+                   : kind == G_BOX    ? sqrtf(sz.x * sz.x + sz.y * sz.y + sz.z * sz.z)
+                   : kind == G_CAPSULE ? sz.x + sz.y : INFINITY;
     lo[g] = make_float4(l.x - hm, l.y - hm, l.z - hm, kind == G_PLANE ? 1.f : 0.f);
-    hi[g] = make_float4(h.x + hm, h.y + hm, h.z + hm, 0.f);
+    hi[g] = make_float4(h.x + hm, h.y + hm, h.z + hm, (rb + hm) * 1.001f + 1e-6f);
   }
   for (int g = tid; g <= G; g += kBpThreads) cnt[g] = 0;
   __syncthreads();
@@ -739,7 +742,7 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
     // one exchange through a double-buffered shared array
     const int n2 = Q.np2;
     uint64_t x = tid < n2 ? (((uint64_t)key[tid] << 32) | val[tid]) : ~0ull;
-    uint64_t* xb = reinterpret_cast<uint64_t*>(sxa);  // 2 x np2 (list's storage, dead here)
+    uint64_t* xb = reinterpret_cast<uint64_t*>(list);  // 2 x np2 (list's storage, dead here)
     int buf = 0;
 #pragma unroll 1
     for (int k = 2; k <= n2; k <<= 1) {
@@ -778,7 +781,17 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
   }
   }
   BP_MARK(2);
-  // 2b: sweep, twice: count per bucket, then place
+  // 2b: sort-and-sweep.  The walk of sorted position i is (i, e_i], the
+  // positions whose low end is within i's high end along the sweep axis (the
+  // sweep axis needs no test inside it: lo_i <= lo_j <= hi_i); the walks'
+  // tests are numbered by an exclusive scan and split evenly over the threads,
+  // each walking its contiguous share with one sorted cross-axis float4 per
+  // test.  A test that overlaps on the two other axes is an AABB hit, kept as
+  // the sorted positions (i << 16 | j) in a 64-entry buffer per warp (one
+  // ballot per test, one list atomic per 32 hits).  The hits are then
+  // filtered by the grown bounding spheres (centre distance <= rho_i + rho_j:
+  // conservative, no pair closer than the margin fails it, R32) and by the
+  // owning body, counted per bucket (the lower geom id) and placed.
   auto axis_of = [&](const float4& v) { return ax == 0 ? v.x : (ax == 1 ? v.y : v.z); };
   auto plane_hit = [&](int p, int g) {  // g's grown AABB reaches below offset + margin/2
     const float4 n = P.size[p], lg = lo[g], hg = hi[g];
@@ -796,85 +809,59 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
     n_np = tot;
   }
   BP_MARK(8);
-#if CF_BP_FLAT
-  // (i) sweep; every pair found goes to a temporary list (ncon's storage) and
-  // is counted in its bucket (the lower geom id).  Appends go through a
-  // 32-entry buffer per warp, one list atomic per 32 pairs.
-  uint32_t* tmp = reinterpret_cast<uint32_t*>(ncon);
-  if (tid == 0) s_misc[5] = 0;
-  __shared__ uint32_t s_wbuf[kBpThreads];
+  const unsigned full = 0xffffffffu;
   const int lane = tid & 31;
-  uint32_t* wbuf = s_wbuf + (tid & ~31);
-  int wn = 0;  // pairs in the warp's buffer (warp-uniform)
-  auto append = [&](bool found, uint32_t pv) {
-    const unsigned fb = __ballot_sync(0xffffffffu, found);
-    if (!fb) return;
-    const int nf = __popc(fb);
-    if (wn + nf > 32) {
-      int t0 = 0;
-      if (lane == 0) t0 = atomicAdd(&s_misc[5], wn);
-      t0 = __shfl_sync(0xffffffffu, t0, 0);
-      if (lane < wn && t0 + lane < Q.cap_c) tmp[t0 + lane] = wbuf[lane];
+  uint32_t* tmp = reinterpret_cast<uint32_t*>(ncon);  // AABB hits (ncon's storage, dead until the narrowphase)
+  if (tid == 0) s_misc[5] = 0;
+  {
+    // sorted copies of the two other axes' extents (lo1, lo2, hi1, hi2), in
+    // the list's storage (dead until the bucket placement), and the walk lengths
+    float4* sxa = reinterpret_cast<float4*>(list);  // [n_np]
+    const int a1 = ax == 0 ? 1 : 0, a2 = ax == 2 ? 1 : 2;
+    auto comp = [](const float4& v, int k) { return k == 0 ? v.x : (k == 1 ? v.y : v.z); };
+    for (int i = tid; i < n_np; i += kBpThreads) {
+      const int g = (int)val[i];
+      const float4 l = lo[g], h = hi[g];
+      sxa[i] = make_float4(comp(l, a1), comp(l, a2), comp(h, a1), comp(h, a2));
+      const uint32_t hk = f2key(axis_of(h));
+      int a = i, b = n_np;  // key[a] <= hk < key[b] (b virtual)
+      while (b - a > 1) {
+        const int m = (a + b) >> 1;
+        if (key[m] <= hk) a = m; else b = m;
+      }
+      start[i] = a - i;
+    }
+    __syncthreads();
+    int* tpre = reinterpret_cast<int*>(key);  // [n_np + 1] (np2 > n_np): the keys are dead
+    int n_tests = 0;
+    for (int i0 = 0; i0 < n_np; i0 += kBpThreads) {
+      const int i = i0 + tid;
+      const int v = i < n_np ? start[i] : 0;
+      int tot;
+      const int ex = block_exclusive(v, s_tmp, &tot);
+      if (i < n_np) tpre[i] = n_tests + ex;
+      n_tests += tot;
+    }
+    if (tid == 0) tpre[n_np] = n_tests;
+    __syncthreads();
+    __shared__ uint32_t s_wbuf[2 * kBpThreads];
+    uint32_t* wbuf = s_wbuf + 2 * (tid & ~31);
+    const unsigned lt = (1u << lane) - 1u;
+    int wn = 0;  // hits in the warp's buffer (warp-uniform)
+    auto flush = [&]() {
+      int b0 = 0;
+      if (lane == 0) b0 = atomicAdd(&s_misc[5], wn);
+      b0 = __shfl_sync(full, b0, 0);
+      __syncwarp();
+      for (int q = lane; q < wn; q += 32)
+        if (b0 + q < Q.cap_c) tmp[b0 + q] = wbuf[q];
       __syncwarp();
       wn = 0;
-    }
-    if (found) {
-      atomicAdd(&cnt[pv >> 16], 1);
-      wbuf[wn + __popc(fb & ((1u << lane) - 1u))] = pv;
-    }
-    wn += nf;
-    __syncwarp();
-  };
-  auto flush = [&]() {
-    if (!wn) return;
-    int t0 = 0;
-    if (lane == 0) t0 = atomicAdd(&s_misc[5], wn);
-    t0 = __shfl_sync(0xffffffffu, t0, 0);
-    if (lane < wn && t0 + lane < Q.cap_c) tmp[t0 + lane] = wbuf[lane];
-    wn = 0;
-  };
-  {
-  // flat sweep: the range of sorted position i is (i, e_i], the positions
-  // whose low end is within its high end (binary search on the sorted keys);
-  // the ranges' tests are numbered by an exclusive scan and split evenly over
-  // the threads, each walking its contiguous share (one test per iteration,
-  // every lane busy).  (A warp per sorted position over sorted, contiguous
-  // AABB copies measured slower: 75 vs 55 us per world CTA.)
-  // sorted copies of the two other axes' extents (lo1, lo2, hi1, hi2): a test
-  // reads one contiguous float4; the sweep axis needs no test inside a range
-  // (lo_i <= lo_j <= hi_i there, and lo_j <= hi_j)
-  const int a1 = ax == 0 ? 1 : 0, a2 = ax == 2 ? 1 : 2;
-  auto comp = [](const float4& v, int k) { return k == 0 ? v.x : (k == 1 ? v.y : v.z); };
-  for (int i = tid; i < n_np; i += kBpThreads) {
-    const int g = (int)val[i];
-    const float4 l = lo[g], h = hi[g];
-    sxa[i] = make_float4(comp(l, a1), comp(l, a2), comp(h, a1), comp(h, a2));
-    const uint32_t hk = f2key(axis_of(h));
-    int a = i, b = n_np;  // key[a] <= hk < key[b] (b virtual)
-    while (b - a > 1) {
-      const int m = (a + b) >> 1;
-      if (key[m] <= hk) a = m; else b = m;
-    }
-    start[i] = a - i;
-  }
-  __syncthreads();
-  int* tpre = reinterpret_cast<int*>(key);  // [n_np + 1] (np2 > n_np): the keys are dead
-  int n_tests = 0;
-  for (int i0 = 0; i0 < n_np; i0 += kBpThreads) {
-    const int i = i0 + tid;
-    const int v = i < n_np ? start[i] : 0;
-    int tot;
-    const int ex = block_exclusive(v, s_tmp, &tot);
-    if (i < n_np) tpre[i] = n_tests + ex;
-    n_tests += tot;
-  }
-  if (tid == 0) tpre[n_np] = n_tests;
-  __syncthreads();
-  {
+    };
     const int per = (n_tests + kBpThreads - 1) / kBpThreads;
     int t = tid * per;
     const int tend = min(n_tests, t + per);
-    int i = 0, j = 0, e = 0, gi = 0, bi = 0;
+    int i = 0, j = 0, e = 0;
     float4 si = make_float4(0.f, 0.f, 0.f, 0.f);
     if (t < tend) {
       int a = 0, b = n_np;  // tpre[a] <= t < tpre[b]
@@ -885,75 +872,46 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
       i = a;
       j = i + 1 + (t - tpre[i]);
       e = i + (tpre[i + 1] - tpre[i]);
-      gi = (int)val[i]; si = sxa[i]; bi = gbody[gi];
+      si = sxa[i];
     }
+    uint32_t ihi = (uint32_t)i << 16;
     for (int it = 0; it < per; ++it) {
-      bool found = false;
-      uint32_t pv = 0;
+      bool hit = false;
+      const uint32_t pv = ihi | (uint32_t)j;
       if (t < tend) {
         const float4 sj = sxa[j];
-        if (si.x <= sj.z && sj.x <= si.z && si.y <= sj.w && sj.y <= si.w) {
-          const int gj = (int)val[j];
-          found = gbody[gj] != bi;
-          pv = ((uint32_t)min(gi, gj) << 16) | (uint32_t)max(gi, gj);
-        }
+        hit = si.x <= sj.z && sj.x <= si.z && si.y <= sj.w && sj.y <= si.w;
         ++t;
-        if (++j > e && t < tend) {  // the next position with a non-empty range
+        if (++j > e && t < tend) {  // the next position with a non-empty walk
           do { ++i; } while (tpre[i + 1] == tpre[i]);
           j = i + 1;
           e = i + (tpre[i + 1] - tpre[i]);
-          gi = (int)val[i]; si = sxa[i]; bi = gbody[gi];
+          si = sxa[i];
+          ihi = (uint32_t)i << 16;
         }
       }
-      append(found, pv);
+      const unsigned fb = __ballot_sync(full, hit);
+      if (hit) wbuf[wn + __popc(fb & lt)] = pv;
+      wn += __popc(fb);
+      if (wn >= 32) flush();
     }
-    flush();
+    if (wn) flush();
   }
-  }
-#else
-  // (i) warp-cooperative sweep (the previous layout, for A/B): warp v takes sorted positions i = v, v + 8, ...;
-  // its lanes test the next 32 positions at once until the sorted low ends pass
-  // geom i's high end; every pair found goes to a temporary list (ncon's
-  // storage) and is counted in its bucket (the lower geom id)
-  uint32_t* tmp = reinterpret_cast<uint32_t*>(ncon);
-  if (tid == 0) s_misc[5] = 0;
   __syncthreads();
-  {
-    const int lane = tid & 31, wv = tid >> 5;
-    for (int i = wv; i < n_np; i += kBpThreads / 32) {
-      const int gi = (int)val[i];
-      const float4 li = lo[gi], hv = hi[gi];
-      const uint32_t hk = f2key(axis_of(hv));  // the sorted keys are f2key(low end): compare keys
-      const int bi = gbody[gi];
-      for (int j0 = i + 1; j0 < n_np; j0 += 32) {
-        const int jj = j0 + lane;
-        const bool in = jj < n_np && key[jj] <= hk;
-        bool found = false;
-        int gj = 0;
-        if (in) {
-          gj = (int)val[jj];
-          if (gbody[gj] != bi) {
-            const float4 lj = lo[gj], hj = hi[gj];
-            found = li.x <= hj.x && lj.x <= hv.x && li.y <= hj.y && lj.y <= hv.y && li.z <= hj.z && lj.z <= hv.z;
-          }
-        }
-        const unsigned fb = __ballot_sync(0xffffffffu, found);
-        if (fb) {  // one append per warp chunk
-          int t0 = 0;
-          if (lane == 0) t0 = atomicAdd(&s_misc[5], __popc(fb));
-          t0 = __shfl_sync(0xffffffffu, t0, 0);
-          if (found) {
-            const int a = min(gi, gj), b = max(gi, gj);
-            atomicAdd(&cnt[a], 1);
-            const int t = t0 + __popc(fb & ((1u << lane) - 1u));
-            if (t < Q.cap_c) tmp[t] = ((uint32_t)a << 16) | (uint32_t)b;
-          }
-        }
-        if (__ballot_sync(0xffffffffu, in) != 0xffffffffu) break;  // the sorted range ended in this chunk
-      }
-    }
+  const int n_hit = s_misc[5];
+  // hits -> candidates: bounding spheres (twice the centres, from the AABBs)
+  // and owners; counted per bucket, the rejected marked 0xffffffff
+  for (int k = tid; k < min(n_hit, Q.cap_c); k += kBpThreads) {
+    const uint32_t pv = tmp[k];
+    const int gi = (int)val[pv >> 16], gj = (int)val[pv & 0xffffu];
+    const float4 li = lo[gi], hi_ = hi[gi], lj = lo[gj], hj = hi[gj];
+    const float dx = (li.x + hi_.x) - (lj.x + hj.x), dy = (li.y + hi_.y) - (lj.y + hj.y),
+                dz = (li.z + hi_.z) - (lj.z + hj.z), r = 2.f * (hi_.w + hj.w);
+    const bool ok = dx * dx + dy * dy + dz * dz <= r * r && gbody[gi] != gbody[gj];
+    const int a = min(gi, gj);
+    if (ok) atomicAdd(&cnt[a], 1);
+    tmp[k] = ok ? ((uint32_t)a << 16) | (uint32_t)max(gi, gj) : 0xffffffffu;
   }
-#endif
   BP_MARK(9);
   // (ii) planes (lowest geom ids): count their hits
   for (int p = 0; p < G && P.geom[p].x == G_PLANE; ++p) {
@@ -981,6 +939,8 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
     __syncthreads();
     for (int g = tid; g < G; g += kBpThreads) cnt[g] = 0;
     if (tid == 0) {
+      // more AABB hits than the hit list holds: candidates were lost
+      if (n_hit > Q.cap_c) run = Q.cap_c + 1;
       s_misc[2] = run;                                   // candidates of the world
       if (run > Q.cap_c) atomicOr(Q.err, ERR_CANDIDATES);
     }
@@ -989,9 +949,9 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
   BP_MARK(11);
   // (iv) pairs into their buckets; plane buckets in geom order by a block scan
   {
-    const int nt = min(s_misc[5], Q.cap_c);
-    for (int t = tid; t < nt; t += kBpThreads) {
-      const uint32_t pv = tmp[t];
+    for (int k = tid; k < min(n_hit, Q.cap_c); k += kBpThreads) {
+      const uint32_t pv = tmp[k];
+      if (pv == 0xffffffffu) continue;
       const int a = (int)(pv >> 16);
       const int slot = start[a] + atomicAdd(&cnt[a], 1);
       if (slot < Q.cap_c) list[slot] = pv;
