@@ -783,12 +783,11 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
   BP_MARK(2);
   // 2b: sort-and-sweep.  The walk of sorted position i is (i, e_i], the
   // positions whose low end is within i's high end along the sweep axis (the
-  // sweep axis needs no test inside it: lo_i <= lo_j <= hi_i); the walks'
-  // tests are numbered by an exclusive scan and split evenly over the threads,
-  // each walking its contiguous share with one sorted cross-axis float4 per
-  // test.  A test that overlaps on the two other axes is an AABB hit, kept as
-  // the sorted positions (i << 16 | j) in a 64-entry buffer per warp (one
-  // ballot per test, one list atomic per 32 hits).  The hits are then
+  // sweep axis needs no test inside it: lo_i <= lo_j <= hi_i); the walks are
+  // cut into tiles of 32 tests, a thread tests a whole tile (one sorted
+  // cross-axis float4 per test, unrolled) into a hit mask.  A test that
+  // overlaps on the two other axes is an AABB hit, appended as the sorted
+  // positions (i << 16 | j) with one list atomic per warp.  The hits are then
   // filtered by the grown bounding spheres (centre distance <= rho_i + rho_j:
   // conservative, no pair closer than the margin fails it, R32) and by the
   // owning body, counted per bucket (the lower geom id) and placed.
@@ -832,70 +831,67 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
       start[i] = a - i;
     }
     __syncthreads();
-    int* tpre = reinterpret_cast<int*>(key);  // [n_np + 1] (np2 > n_np): the keys are dead
-    int n_tests = 0;
+    // the walks cut into tiles of 32 tests; a thread tests one tile at a time
+    // (fixed i, 32 consecutive j: unrolled, predicated, no bookkeeping inside)
+    // into a 32-bit hit mask, then the warp appends its hits with one atomic
+    int* tpre = reinterpret_cast<int*>(key);  // [n_np + 1] tile offsets (np2 > n_np): the keys are dead
+    int n_tiles = 0;
     for (int i0 = 0; i0 < n_np; i0 += kBpThreads) {
       const int i = i0 + tid;
-      const int v = i < n_np ? start[i] : 0;
+      const int v = i < n_np ? (start[i] + 31) >> 5 : 0;
       int tot;
       const int ex = block_exclusive(v, s_tmp, &tot);
-      if (i < n_np) tpre[i] = n_tests + ex;
-      n_tests += tot;
+      if (i < n_np) tpre[i] = n_tiles + ex;
+      n_tiles += tot;
     }
-    if (tid == 0) tpre[n_np] = n_tests;
+    if (tid == 0) tpre[n_np] = n_tiles;
     __syncthreads();
-    __shared__ uint32_t s_wbuf[2 * kBpThreads];
-    uint32_t* wbuf = s_wbuf + 2 * (tid & ~31);
-    const unsigned lt = (1u << lane) - 1u;
-    int wn = 0;  // hits in the warp's buffer (warp-uniform)
-    auto flush = [&]() {
-      int b0 = 0;
-      if (lane == 0) b0 = atomicAdd(&s_misc[5], wn);
-      b0 = __shfl_sync(full, b0, 0);
-      __syncwarp();
-      for (int q = lane; q < wn; q += 32)
-        if (b0 + q < Q.cap_c) tmp[b0 + q] = wbuf[q];
-      __syncwarp();
-      wn = 0;
-    };
-    const int per = (n_tests + kBpThreads - 1) / kBpThreads;
-    int t = tid * per;
-    const int tend = min(n_tests, t + per);
-    int i = 0, j = 0, e = 0;
-    float4 si = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (t < tend) {
-      int a = 0, b = n_np;  // tpre[a] <= t < tpre[b]
-      while (b - a > 1) {
-        const int m = (a + b) >> 1;
-        if (tpre[m] <= t) a = m; else b = m;
-      }
-      i = a;
-      j = i + 1 + (t - tpre[i]);
-      e = i + (tpre[i + 1] - tpre[i]);
-      si = sxa[i];
-    }
-    uint32_t ihi = (uint32_t)i << 16;
-    for (int it = 0; it < per; ++it) {
-      bool hit = false;
-      const uint32_t pv = ihi | (uint32_t)j;
-      if (t < tend) {
-        const float4 sj = sxa[j];
-        hit = si.x <= sj.z && sj.x <= si.z && si.y <= sj.w && sj.y <= si.w;
-        ++t;
-        if (++j > e && t < tend) {  // the next position with a non-empty walk
-          do { ++i; } while (tpre[i + 1] == tpre[i]);
-          j = i + 1;
-          e = i + (tpre[i + 1] - tpre[i]);
-          si = sxa[i];
-          ihi = (uint32_t)i << 16;
+    for (int q0 = 0; q0 < n_tiles; q0 += kBpThreads) {
+      const int q = q0 + tid;
+      uint32_t m = 0;
+      int i = 0, j0 = 0;
+      if (q < n_tiles) {
+        int a = 0, b = n_np;  // tpre[a] <= q < tpre[b]
+        while (b - a > 1) {
+          const int mid = (a + b) >> 1;
+          if (tpre[mid] <= q) a = mid; else b = mid;
+        }
+        i = a;
+        const int k0 = (q - tpre[i]) << 5;
+        j0 = i + 1 + k0;
+        const int nb = min(32, start[i] - k0);
+        const float4 si = sxa[i];
+        const float4* sp = sxa + j0;
+#pragma unroll
+        for (int bb = 0; bb < 32; ++bb) {
+          if (bb < nb) {
+            const float4 sj = sp[bb];
+            m |= (si.x <= sj.z && sj.x <= si.z && si.y <= sj.w && sj.y <= si.w ? 1u : 0u) << bb;
+          }
         }
       }
-      const unsigned fb = __ballot_sync(full, hit);
-      if (hit) wbuf[wn + __popc(fb & lt)] = pv;
-      wn += __popc(fb);
-      if (wn >= 32) flush();
+      const int nh = __popc(m);
+      int incl = nh;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(full, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int wt = __shfl_sync(full, incl, 31);
+      if (wt) {
+        int b0 = 0;
+        if (lane == 31) b0 = atomicAdd(&s_misc[5], wt);
+        b0 = __shfl_sync(full, b0, 31);
+        int pos = b0 + incl - nh;
+        const uint32_t ihi = ((uint32_t)i << 16) | (uint32_t)j0;
+        while (m) {
+          const int bb = __ffs(m) - 1;
+          m &= m - 1u;
+          if (pos < Q.cap_c) tmp[pos] = ihi + (uint32_t)bb;
+          ++pos;
+        }
+      }
     }
-    if (wn) flush();
   }
   __syncthreads();
   const int n_hit = s_misc[5];
