@@ -262,10 +262,10 @@ __device__ __forceinline__ void box_corners_on(const Frame& A, float4 hA, const 
   }
 }
 
-// Exact early out for box-box: separated by more than the margin along a face
-// normal of either box (overlap < -margin) means no corner is within the
-// margin of a face (its signed distance exceeds the margin along that axis)
-// and the minimum overlap of R33 is below -margin too: no contact at all.
+#ifndef CF_BP_SAT1
+#define CF_BP_SAT1 1  // face-axis early out, corners, then the 15 axes for the edge contact: 446 vs 467 us full step (profiles/r02_broadphase.txt)
+#endif
+// Exact early out over the 6 face axes only (CF_BP_SAT1 variant).
 __device__ __forceinline__ bool boxes_separated(const Frame& A, float4 hA4, const Frame& Bf, float4 hB4, float margin) {
   const V3 d = sub(Bf.x, A.x);
   const float hA[3] = {hA4.x, hA4.y, hA4.z}, hB[3] = {hB4.x, hB4.y, hB4.z};
@@ -282,15 +282,21 @@ __device__ __forceinline__ bool boxes_separated(const Frame& A, float4 hA4, cons
   return false;
 }
 
-// Box-box edge-edge (reading R33): separating-axis test over the 15 axes (face
-// normals of A, of B, the 9 edge cross products e_A,i x e_B,j, i-major, skipped
-// when |cross| <= 1e-6); when the first axis of minimum overlap is an edge axis
-// and -overlap < margin, one contact at the midpoint of the closest points of
-// A's edge through its support point along n and B's through its support
-// point along -n (n oriented from A to B).
-template <class O>
-__device__ __forceinline__ void box_edge_edge(const Frame& A, float4 hA4, const Frame& Bf, float4 hB4, float margin,
-                                              O& o) {
+// Box-box separating-axis test (reading R33's 15 axes: face normals of A, of
+// B, then the 9 edge cross products e_A,i x e_B,j, i-major, skipped when
+// |cross| <= 1e-6), overlap(L) = sum_k hA_k |L.eA_k| + hB_k |L.eB_k| - |L.d|.
+// Returns false when some axis separates the boxes by more than the margin:
+// then no corner is within the margin of a face either (a corner within the
+// margin of a face, projected inside it, is within the margin of the box), so
+// the pair has no contact at all.  Otherwise best / bi, bj / bL hold the
+// first minimum overlap and its axis (bi = -1: a face axis).
+struct BoxSat {
+  float best;
+  int bi, bj;
+  V3 bL;
+};
+__device__ __forceinline__ bool box_sat(const Frame& A, float4 hA4, const Frame& Bf, float4 hB4, float margin,
+                                        BoxSat& S) {
   const float hA[3] = {hA4.x, hA4.y, hA4.z}, hB[3] = {hB4.x, hB4.y, hB4.z};
   const V3 d = sub(Bf.x, A.x);
   V3 ea[3], eb[3];
@@ -299,19 +305,21 @@ __device__ __forceinline__ void box_edge_edge(const Frame& A, float4 hA4, const 
     ea[k] = v3(A.R[k], A.R[3 + k], A.R[6 + k]);    // column k of R: the frame's axis k
     eb[k] = v3(Bf.R[k], Bf.R[3 + k], Bf.R[6 + k]);
   }
-  float best = INFINITY;
-  int bi = -1, bj = -1;
-  V3 bL = v3(0.f, 0.f, 0.f);
   auto overlap = [&](V3 L) {
     float r = -fabsf(dot(L, d));
 #pragma unroll
     for (int k = 0; k < 3; ++k) r += hA[k] * fabsf(dot(L, ea[k])) + hB[k] * fabsf(dot(L, eb[k]));
     return r;
   };
+  S.best = INFINITY;
+  S.bi = -1;
+  S.bj = -1;
+  S.bL = v3(0.f, 0.f, 0.f);
 #pragma unroll
   for (int k = 0; k < 6; ++k) {
     const float ov = overlap(k < 3 ? ea[k] : eb[k - 3]);
-    if (ov < best) { best = ov; bi = -1; }
+    if (ov < -margin) return false;
+    if (ov < S.best) S.best = ov;
   }
 #pragma unroll 1
   for (int i = 0; i < 3; ++i) {
@@ -322,11 +330,31 @@ __device__ __forceinline__ void box_edge_edge(const Frame& A, float4 hA4, const 
       if (!(nl > 1e-6f)) continue;
       L = mul(1.f / nl, L);
       const float ov = overlap(L);
-      if (ov < best) { best = ov; bi = i; bj = j; bL = L; }
+      if (ov < -margin) return false;
+      if (ov < S.best) { S.best = ov; S.bi = i; S.bj = j; S.bL = L; }
     }
   }
-  if (bi < 0 || !(-best < margin)) return;
-  const V3 n = dot(bL, d) >= 0.f ? bL : mul(-1.f, bL);
+  return true;
+}
+
+// Box-box edge-edge contact (reading R33): when the first axis of minimum
+// overlap is an edge axis and -overlap < margin, one contact at the midpoint
+// of the closest points of A's edge through its support point along n and
+// B's through its support point along -n (n oriented from A to B).
+template <class O>
+__device__ __forceinline__ void box_edge_edge(const Frame& A, float4 hA4, const Frame& Bf, float4 hB4, float margin,
+                                              const BoxSat& S, O& o) {
+  if (S.bi < 0 || !(-S.best < margin)) return;
+  const float hA[3] = {hA4.x, hA4.y, hA4.z}, hB[3] = {hB4.x, hB4.y, hB4.z};
+  const V3 d = sub(Bf.x, A.x);
+  V3 ea[3], eb[3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    ea[k] = v3(A.R[k], A.R[3 + k], A.R[6 + k]);
+    eb[k] = v3(Bf.R[k], Bf.R[3 + k], Bf.R[6 + k]);
+  }
+  const int bi = S.bi, bj = S.bj;
+  const V3 n = dot(S.bL, d) >= 0.f ? S.bL : mul(-1.f, S.bL);
   V3 pa = A.x, pb = Bf.x;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
@@ -336,7 +364,7 @@ __device__ __forceinline__ void box_edge_edge(const Frame& A, float4 hA4, const 
   V3 c1, c2;
   closest_segments(sub(pa, mul(hA[bi], ea[bi])), add(pa, mul(hA[bi], ea[bi])), sub(pb, mul(hB[bj], eb[bj])),
                    add(pb, mul(hB[bj], eb[bj])), c1, c2);
-  o.add(mul(0.5f, add(c1, c2)), -best, n);
+  o.add(mul(0.5f, add(c1, c2)), -S.best, n);
 }
 
 // Contacts of the geom pair pr = (g1, g2) in world w (frames Fw): returns the
@@ -426,10 +454,19 @@ __device__ CF_NP_ATTR int pair_contacts_rt(const CollideParams& P, const GeomTab
   } else if (k1 == G_BOX && k2 == G_BOX) {
     const Frame A = load_frame(Fw, pr.x), Bf = load_frame(Fw, pr.y);
     const float4 hA = T.size[pr.x], hB = T.size[pr.y];
+    BoxSat S;
+#if CF_BP_SAT1
     if (boxes_separated(A, hA, Bf, hB, margin)) return 0;  // no vertex-face nor edge-edge contact
     box_corners_on(A, hA, Bf, hB, margin, false, o);
     box_corners_on(Bf, hB, A, hA, margin, true, o);
-    box_edge_edge(A, hA, Bf, hB, margin, o);
+    if (!box_sat(A, hA, Bf, hB, margin, S)) return o.k;
+    box_edge_edge(A, hA, Bf, hB, margin, S, o);
+    return o.k;
+#endif
+    if (!box_sat(A, hA, Bf, hB, margin, S)) return 0;  // separated beyond the margin: no contact of any kind
+    box_corners_on(A, hA, Bf, hB, margin, false, o);
+    box_corners_on(Bf, hB, A, hA, margin, true, o);
+    box_edge_edge(A, hA, Bf, hB, margin, S, o);
   } else {  // sphere or capsule against a box
     const bool round_first = k1 != G_BOX;
     const int gr = round_first ? pr.x : pr.y, gb = round_first ? pr.y : pr.x;
@@ -744,6 +781,7 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
     uint64_t x = tid < n2 ? (((uint64_t)key[tid] << 32) | val[tid]) : ~0ull;
     uint64_t* xb = reinterpret_cast<uint64_t*>(list);  // 2 x np2 (list's storage, dead here)
     int buf = 0;
+#if CF_BP_SORT_OLD
 #pragma unroll 1
     for (int k = 2; k <= n2; k <<= 1) {
 #pragma unroll 1
@@ -761,6 +799,29 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
         x = keep_min ? (x < y ? x : y) : (x < y ? y : x);
       }
     }
+#else
+#pragma unroll 1
+    for (int k = 2; k <= n2; k <<= 1) {
+      const bool up = (tid & k) == 0;
+#pragma unroll 1
+      for (int j = k >> 1; j >= 32; j >>= 1) {
+        if (tid < n2) xb[buf * n2 + tid] = x;
+        __syncthreads();
+        const uint64_t y = tid < n2 ? xb[buf * n2 + (tid ^ j)] : x;
+        buf ^= 1;
+        const bool keep_min = up == ((tid & j) == 0);
+        x = (keep_min == (y < x)) ? y : x;
+      }
+#pragma unroll
+      for (int j = 16; j > 0; j >>= 1) {  // compile-time partner distances
+        if (j < k) {
+          const uint64_t y = __shfl_xor_sync(0xffffffffu, x, j);
+          const bool keep_min = up == ((tid & j) == 0);
+          x = (keep_min == (y < x)) ? y : x;
+        }
+      }
+    }
+#endif
     __syncthreads();
     if (tid < Q.np2) {
       key[tid] = (uint32_t)(x >> 32);
