@@ -213,6 +213,41 @@ def test_broadphase_loses_no_contact(seed):
     assert all(len(co.broadphase(geo, st, w)) < len(allp) for w in range(3))
 
 
+def _bounding_radius(geo, g):
+    """Reading R32's bounding-sphere filter: sphere R, box |h|, capsule R +
+    half length, about the geom's frame origin (R32)."""
+    k, sz = int(geo.kind[g]), np.asarray(geo.size[g], float)
+    return {co.SPHERE: sz[0], co.BOX: float(np.linalg.norm(sz)), co.CAPSULE: sz[0] + sz[1]}[k]
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_bounding_sphere_filter_keeps_every_contact_pair(seed):
+    """The GPU broadphase drops a candidate whose grown bounding spheres do
+    not overlap (|c1 - c2| > rho1 + rho2 + margin, R32).  Conservative: every
+    non-plane pair the oracle finds a contact for (phi < margin) passes the
+    test with room to spare; on the pile it still prunes AABB candidates."""
+    from harness import scenes
+    cases = [(_random_geometry(seed), _random_poses(seed, 3, 12), False)]
+    if seed == 0:
+        scene, st, _ = scenes.c4_pile(n_worlds=1, contacts_per_world=2000)
+        cases.append((scenes.pile_geometry((10, 10, 5), broadphase=True), st.astype(np.float64), True))
+    for geo, st, pile in cases:
+        n_cand = n_pass = 0
+        for w in range(st.n_worlds):
+            for (g1, g2) in co.broadphase(geo, st, w):
+                if geo.kind[g1] == co.PLANE:
+                    continue
+                c1 = co.geom_frame(geo, g1, st, w, None)[1]
+                c2 = co.geom_frame(geo, g2, st, w, None)[1]
+                slack = _bounding_radius(geo, g1) + _bounding_radius(geo, g2) + geo.margin - np.linalg.norm(c1 - c2)
+                n_cand += 1
+                n_pass += slack >= 0
+                if co.pair_contacts(geo, None, st, w, None, g12=(g1, g2)):
+                    assert slack > 0, (w, g1, g2, slack)
+        if pile:
+            assert n_pass < 0.7 * n_cand              # 3431 AABB candidates -> ~2100
+
+
 def test_aabb_matches_brute_force_extremes():
     """Box AABB = min / max over its 8 corners; capsule AABB = ends +- R
     (checked against points sampled on the capsule surface); both grown by
