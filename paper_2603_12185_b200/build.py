@@ -17,7 +17,7 @@ OBJDIR = os.path.join(HERE, "_build")
 CUDA_HOME = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA_HOME, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["step.cu", "step_w1.cu", "step_w2.cu", "step_w4.cu", "step_w8.cu", "step_p32.cu", "segment.cu", "state.cu", "articulation.cu", "collide.cu", "mppi.cu"]
+CU_SOURCES = ["step.cu", "step_w1.cu", "step_w2.cu", "step_w4.cu", "step_w8.cu", "step_w16.cu", "step_p32.cu", "segment.cu", "state.cu", "articulation.cu", "collide.cu", "mppi.cu"]
 CPP_SOURCES = ["capi.cpp"]
 # collide.cu: no FMA contraction, so the narrowphase's count and emit
 # specialisations compute bit-identical contacts (collide.cu, CF_NP_INLINE)

@@ -652,9 +652,9 @@ comfree_status comfree_step(comfree_ctx* ctx, const comfree_worlds* wd, const co
   P.timeline = cf_debug_timeline_buf();
 #endif
   int wpw = pick_wpw(sc, n, nw);
-  if (const char* e = getenv("COMFREE_WPW")) {  // tuning override (1, 2, 4 or 8 warps per world)
+  if (const char* e = getenv("COMFREE_WPW")) {  // tuning override (1, 2, 4, 8 or 16 warps per world)
     const int v = atoi(e);
-    if (v == 1 || v == 2 || v == 4 || v == 8) wpw = v;
+    if (v == 1 || v == 2 || v == 4 || v == 8 || v == 16) wpw = v;
   }
   const size_t smem_need = cf::step_smem_bytes(sc, wpw);
   P.gscratch = nullptr;
