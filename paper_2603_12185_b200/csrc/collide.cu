@@ -202,7 +202,7 @@ __device__ __forceinline__ float sphere_box(V3 c, float R, const Frame& Fb, floa
   const float cl[3] = {cl3.x, cl3.y, cl3.z};
   float ql[3], nl[3] = {0.f, 0.f, 0.f}, dist;
   const bool inside = fabsf(cl[0]) <= h[0] && fabsf(cl[1]) <= h[1] && fabsf(cl[2]) <= h[2];
-  if (inside) {
+  if (inside) {  // per-component selects (no dynamic index: the arrays stay in registers)
     int i = 0;
     float best = h[0] - fabsf(cl[0]);
 #pragma unroll
@@ -211,9 +211,10 @@ __device__ __forceinline__ float sphere_box(V3 c, float R, const Frame& Fb, floa
       if (dk < best) { best = dk; i = k; }
     }
 #pragma unroll
-    for (int k = 0; k < 3; ++k) ql[k] = cl[k];
-    nl[i] = cl[i] >= 0.f ? 1.f : -1.f;
-    ql[i] = nl[i] * h[i];
+    for (int k = 0; k < 3; ++k) {
+      nl[k] = k == i ? (cl[k] >= 0.f ? 1.f : -1.f) : 0.f;
+      ql[k] = k == i ? nl[k] * h[k] : cl[k];
+    }
     dist = -best;
   } else {
     float d2 = 0.f, dd[3];
@@ -246,16 +247,18 @@ __device__ __forceinline__ void box_corners_on(const Frame& A, float4 hA, const 
     float ex[3];
 #pragma unroll
     for (int j = 0; j < 3; ++j) ex[j] = fabsf(cl[j]) - ha[j];
+    // largest excess (first of equals), by selects (no dynamic index)
     int i = 0;
-    if (ex[1] > ex[i]) i = 1;
-    if (ex[2] > ex[i]) i = 2;
-    const float sd = ex[i];
+    float sd = ex[0];
+    if (ex[1] > sd) { i = 1; sd = ex[1]; }
+    if (ex[2] > sd) { i = 2; sd = ex[2]; }
     bool ok = sd < margin;
 #pragma unroll
     for (int j = 0; j < 3; ++j) ok &= (j == i) || ex[j] <= 0.f;
     if (ok) {
-      float nl[3] = {0.f, 0.f, 0.f};
-      nl[i] = cl[i] >= 0.f ? 1.f : -1.f;
+      float nl[3];
+#pragma unroll
+      for (int j = 0; j < 3; ++j) nl[j] = j == i ? (cl[j] >= 0.f ? 1.f : -1.f) : 0.f;
       const V3 nn = rmul(A.R, v3(nl[0], nl[1], nl[2]));
       o.add(sub(corner, mul(0.5f * sd, nn)), sd, flip ? mul(-1.f, nn) : nn);
     }
@@ -321,10 +324,10 @@ __device__ __forceinline__ bool box_sat(const Frame& A, float4 hA4, const Frame&
     if (ov < -margin) return false;
     if (ov < S.best) S.best = ov;
   }
-#pragma unroll 1
+#pragma unroll
   for (int i = 0; i < 3; ++i) {
-#pragma unroll 1
-    for (int j = 0; j < 3; ++j) {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {  // unrolled: ea / eb stay in registers
       V3 L = cross(ea[i], eb[j]);
       const float nl = sqrtf(dot(L, L));
       if (!(nl > 1e-6f)) continue;
@@ -355,6 +358,9 @@ __device__ __forceinline__ void box_edge_edge(const Frame& A, float4 hA4, const 
   }
   const int bi = S.bi, bj = S.bj;
   const V3 n = dot(S.bL, d) >= 0.f ? S.bL : mul(-1.f, S.bL);
+  // the edges' axes and half lengths by selects (no dynamic index)
+  const V3 eai = bi == 0 ? ea[0] : (bi == 1 ? ea[1] : ea[2]), ebj = bj == 0 ? eb[0] : (bj == 1 ? eb[1] : eb[2]);
+  const float hai = bi == 0 ? hA[0] : (bi == 1 ? hA[1] : hA[2]), hbj = bj == 0 ? hB[0] : (bj == 1 ? hB[1] : hB[2]);
   V3 pa = A.x, pb = Bf.x;
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
@@ -362,8 +368,7 @@ __device__ __forceinline__ void box_edge_edge(const Frame& A, float4 hA4, const 
     if (k != bj) pb = sub(pb, mul((dot(n, eb[k]) >= 0.f ? 1.f : -1.f) * hB[k], eb[k]));
   }
   V3 c1, c2;
-  closest_segments(sub(pa, mul(hA[bi], ea[bi])), add(pa, mul(hA[bi], ea[bi])), sub(pb, mul(hB[bj], eb[bj])),
-                   add(pb, mul(hB[bj], eb[bj])), c1, c2);
+  closest_segments(sub(pa, mul(hai, eai)), add(pa, mul(hai, eai)), sub(pb, mul(hbj, ebj)), add(pb, mul(hbj, ebj)), c1, c2);
   o.add(mul(0.5f, add(c1, c2)), -S.best, n);
 }
 
@@ -482,14 +487,18 @@ __device__ CF_NP_ATTR int pair_contacts_rt(const CollideParams& P, const GeomTab
       // when strictly inside the segment (a capsule lying across a box)
       const V3 d = sub(e[1], e[0]);
       const float t = dot(sub(Fb.x, e[0]), d) / dot(d, d);
-      if (t > 0.f && t < 1.f) e[ne++] = add(e[0], mul(t, d));
+      e[2] = add(e[0], mul(t, d));
+      if (t > 0.f && t < 1.f) ne = 3;
     } else {
       e[0] = load_frame(Fw, gr).x;
     }
-    for (int q = 0; q < ne; ++q) {
-      V3 nbox, qs;
-      const float phi = sphere_box(e[q], R, Fb, h4, nbox, qs);
-      if (phi < margin) o.add(mul(0.5f, add(qs, sub(e[q], mul(R, nbox)))), phi, round_first ? mul(-1.f, nbox) : nbox);
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {  // unrolled with a predicate: e[] stays in registers
+      if (q < ne) {
+        V3 nbox, qs;
+        const float phi = sphere_box(e[q], R, Fb, h4, nbox, qs);
+        if (phi < margin) o.add(mul(0.5f, add(qs, sub(e[q], mul(R, nbox)))), phi, round_first ? mul(-1.f, nbox) : nbox);
+      }
     }
   }
   return o.k;
