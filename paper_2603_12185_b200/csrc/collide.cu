@@ -118,19 +118,22 @@ struct Stage {
 // emit writes exactly the slots the count reserved): either both run one
 // non-inlined pair_contacts with a runtime mode, or (default) both inline it
 // from a file compiled without FMA contraction (see CF_NP_INLINE).
+// MODE is a compile-time constant at every call site (0 count, 1 emit, 2
+// stage), so a sink carries only what its mode uses in registers.
+template <int MODE>
 struct Out {
   int k;
-  int mode;  // 0 count, 1 emit, 2 stage
   const CollideParams* P;
-  const Stage* S;
+  Stage S;  // by value: no pointer to a local struct (which would live in local memory)
   int64_t base, w;
   int b1, b2, l1, l2, cand;
-  __device__ void add(V3 pp, float ph, V3 nn);
+  __device__ __forceinline__ void add(V3 pp, float ph, V3 nn);
 };
 __device__ __forceinline__ V3 tangent(V3 n);
-__device__ __forceinline__ void Out::add(V3 pp, float ph, V3 nn) {
+template <int MODE>
+__device__ __forceinline__ void Out<MODE>::add(V3 pp, float ph, V3 nn) {
   if (k < kMaxPairContacts) {
-    if (mode == 1) {  // write the record now (no staging)
+    if (MODE == 1) {  // write the record now (no staging)
       const int64_t c = base + k;
       const V3 t1 = tangent(nn);
       P->c0[c] = make_float4(pp.x, pp.y, pp.z, ph);
@@ -139,11 +142,11 @@ __device__ __forceinline__ void Out::add(V3 pp, float ph, V3 nn) {
       P->c3[c] = make_int4(b1, b2, __float_as_int(P->mu_rol), P->condim);
       P->world[c] = (int32_t)w;
       P->link[c] = make_int2(l1, l2);
-    } else if (mode == 2) {
-      const int slot = atomicAdd(S->count, 1);
-      if (slot < S->cap) {
-        S->s0[slot] = make_float4(pp.x, pp.y, pp.z, ph);
-        S->s1[slot] = make_float4(nn.x, nn.y, nn.z, __int_as_float((cand << 5) | k));
+    } else if (MODE == 2) {
+      const int slot = atomicAdd(S.count, 1);
+      if (slot < S.cap) {
+        S.s0[slot] = make_float4(pp.x, pp.y, pp.z, ph);
+        S.s1[slot] = make_float4(nn.x, nn.y, nn.z, __int_as_float((cand << 5) | k));
       }
     }
     ++k;
@@ -386,13 +389,13 @@ __device__ __forceinline__ void box_edge_edge(const Frame& A, float4 hA4, const 
 #else
 #define CF_NP_ATTR __noinline__
 #endif
+template <int MODE>
 __device__ CF_NP_ATTR int pair_contacts_rt(const CollideParams& P, const GeomTab T, const int2 pr, const float4* Fw,
-                                             int64_t w, int64_t base, int mode, const Stage* S = nullptr, int cand = 0) {
+                                             int64_t w, int64_t base, const Stage S = Stage{}, int cand = 0) {
   const int4 g1 = T.geom[pr.x], g2 = T.geom[pr.y];
   const float margin = P.margin;
-  Out o;
+  Out<MODE> o;
   o.k = 0;
-  o.mode = mode;
   o.P = &P;
   o.S = S;
   o.cand = cand;
@@ -507,13 +510,13 @@ __device__ CF_NP_ATTR int pair_contacts_rt(const CollideParams& P, const GeomTab
 template <bool EMIT>
 __device__ __forceinline__ int pair_contacts(const CollideParams& P, const int2 pr, const float4* Fw, int64_t w,
                                              int64_t base, const GeomTab* T = nullptr) {
-  return pair_contacts_rt(P, T ? *T : GeomTab{P.geom, P.size, P.local}, pr, Fw, w, base, EMIT ? 1 : 0);
+  return pair_contacts_rt<EMIT ? 1 : 0>(P, T ? *T : GeomTab{P.geom, P.size, P.local}, pr, Fw, w, base);
 }
 
 // the broadphase's single pass: count and stage the records of candidate `cand`
 __device__ __forceinline__ int pair_contacts_stage(const CollideParams& P, const int2 pr, const float4* Fw, int64_t w,
-                                                   const GeomTab* T, const Stage* S, int cand) {
-  return pair_contacts_rt(P, *T, pr, Fw, w, 0, 2, S, cand);
+                                                   const GeomTab* T, const Stage S, int cand) {
+  return pair_contacts_rt<2>(P, *T, pr, Fw, w, 0, S, cand);
 }
 
 __global__ void k_geom_frames(const __grid_constant__ CollideParams P) {
@@ -593,6 +596,9 @@ __global__ void k_collide_emit(const __grid_constant__ CollideParams P, const in
 #define CF_BP_THREADS 512  // 16 warps, 2 CTAs per SM: 0.83 vs 0.91 ms collide at 256 (profiles/r02_broadphase.txt)
 #endif
 constexpr int kBpThreads = CF_BP_THREADS;
+#ifndef CF_BP_TILE_BRANCHY
+#define CF_BP_TILE_BRANCHY 1
+#endif
 #ifdef CF_BP_TIMELINE  // tuning diagnostic: per-world phase timestamps (globaltimer ns) into P.frames
 #define BP_MARK(k)                                                                        \
   if (tid == 0) {                                                                         \
@@ -932,6 +938,11 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
         const int nb = min(32, start[i] - k0);
         const float4 si = sxa[i];
         const float4* sp = sxa + j0;
+        // unconditional loads (a tile's tail reads up to 31 float4 past the
+        // copies, still inside the CTA's shared memory: the list storage and
+        // the arrays after it) and branch-free tests, so the 32 loads overlap;
+        // the tail is masked off once
+#if CF_BP_TILE_BRANCHY  // default 1: the predicated loads measured faster (418 vs 424 us full step) than branch-free unconditional ones
 #pragma unroll
         for (int bb = 0; bb < 32; ++bb) {
           if (bb < nb) {
@@ -939,6 +950,14 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
             m |= (si.x <= sj.z && sj.x <= si.z && si.y <= sj.w && sj.y <= si.w ? 1u : 0u) << bb;
           }
         }
+#else
+#pragma unroll
+        for (int bb = 0; bb < 32; ++bb) {
+          const float4 sj = sp[bb];
+          m |= (uint32_t)((si.x <= sj.z) & (sj.x <= si.z) & (si.y <= sj.w) & (sj.y <= si.w)) << bb;
+        }
+        m &= nb >= 32 ? 0xffffffffu : ((1u << nb) - 1u);
+#endif
       }
       const int nh = __popc(m);
       int incl = nh;
@@ -1090,7 +1109,7 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
   for (int i = tid; i < n_cand; i += kBpThreads) {
     const int k = perm[i];
     const uint32_t pv = list[k];
-    ncon[k] = pair_contacts_stage(P, make_int2((int)(pv >> 16), (int)(pv & 0xffffu)), Fw, w, &Ts, &S, k);
+    ncon[k] = pair_contacts_stage(P, make_int2((int)(pv >> 16), (int)(pv & 0xffffu)), Fw, w, &Ts, S, k);
   }
   __syncthreads();
   int world_total = 0;
