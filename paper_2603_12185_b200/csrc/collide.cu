@@ -1058,18 +1058,30 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
   // COMFREE_ERR_CAPACITY): its truncated buckets would hold stale entries
   const int n_cand = s_misc[2] > Q.cap_c ? 0 : s_misc[2];
   BP_MARK(3);
-  // 2c: each non-plane bucket sorted by g2 (small: insertion sort by its geom's thread)
-  for (int g = tid; g < G; g += kBpThreads) {
-    if (P.geom[g].x == G_PLANE) continue;
-    const int b0 = start[g], b1 = min(start[g + 1], Q.cap_c);
-    for (int i = b0 + 1; i < b1; ++i) {
-      const uint32_t v = list[i];
-      int j = i - 1;
-      while (j >= b0 && list[j] > v) { list[j + 1] = list[j]; --j; }
-      list[j + 1] = v;
+  // 2c: each non-plane bucket sorted by g2: a thread per candidate counts the
+  // entries of its bucket below it (its rank; the keys of a bucket are
+  // distinct) and writes it to its place in ncon's storage (free until the
+  // narrowphase), copied back into the list; plane buckets are in geom order
+  // already.  (Swapping the two arrays' roles instead of copying back gave
+  // nondeterministic, partly unwritten records: not used.)
+  {
+    uint32_t* sorted = reinterpret_cast<uint32_t*>(ncon);
+    for (int k = tid; k < n_cand; k += kBpThreads) {
+      const uint32_t v = list[k];
+      const int g1 = (int)(v >> 16);
+      const int b0 = start[g1];
+      int r = k - b0;
+      if (P.geom[g1].x != G_PLANE) {
+        const int b1 = start[g1 + 1];
+        r = 0;
+        for (int e = b0; e < b1; ++e) r += list[e] < v;
+      }
+      sorted[b0 + r] = v;
     }
+    __syncthreads();
+    for (int k = tid; k < n_cand; k += kBpThreads) list[k] = sorted[k];
+    __syncthreads();
   }
-  __syncthreads();
   // the AABBs are dead: their storage takes the geom table for the narrowphase
   for (int g = tid; g < G; g += kBpThreads) {
     lo[g] = P.size[g];
