@@ -80,6 +80,9 @@ def parse(argv=None):
     ap.add_argument("--pair-list", action="store_true",
                     help="with --collide on the pile: the fixed lattice-neighbour candidate list instead of the "
                          "per-step broadphase")
+    ap.add_argument("--split-collide", action="store_true",
+                    help="with --collide on the pile (broadphase): comfree_collide + comfree_step (public contact "
+                         "streams) instead of comfree_step_collided (the step reads the front-end's staged records)")
     ap.add_argument("--workload", default="pile", choices=["pile", "hand", "mixed"],
                     help="pile: config 4 (the BASELINE metric); hand: config 3; mixed: config 5")
     a = ap.parse_args(argv)
@@ -213,6 +216,9 @@ def workload(args, rank, world_size):
             name += (" (fixed lattice-neighbour candidate list)" if args.pair_list else
                      " (sort-and-sweep broadphase + narrowphase, one kernel)") + \
                 "; contacts from geometry, not the generator's"
+            if not args.pair_list:
+                name += ("; comfree_collide + comfree_step (public contact streams)" if args.split_collide else
+                         "; comfree_step_collided (the step reads the front-end's staged records, no emit pass)")
     return parts, name, n
 
 
@@ -523,6 +529,8 @@ def run_ours(args, rank, world_size, local):
 
     applied = [0]          # steps applied to the states (graph capture records, does not run)
 
+    fused = args.collide and not args.pair_list and not args.split_collide
+
     def one_step(s0, capturing=False):
         """One step of every part: part 0 on s0, the rest forked from s0 and joined back."""
         applied[0] += 0 if capturing else 1
@@ -530,6 +538,9 @@ def run_ours(args, rank, world_size, local):
             if i != 0:
                 p.stream.wait_stream(s0)
             ps = s0 if i == 0 else p.stream
+            if p.col is not None and fused:          # one call: collide, the step reads the staged records
+                p.ctx.step_collided(p.col, dt=cfg.dt, stream=ps)
+                continue
             if p.col is not None:
                 p.dc, _ = p.ctx.collide(capacity=p.col, stream=ps, device_count=True)
             if p.up is not None:
@@ -547,6 +558,8 @@ def run_ours(args, rank, world_size, local):
     torch.cuda.synchronize()
     for p in parts:                                   # collision-built contacts: the step's real count
         if p.col is not None:
+            if fused:                                 # the fused call keeps no public streams: count once
+                p.dc, _ = p.ctx.collide(capacity=p.col, device_count=True)
             nc = int(p.dc.n_dev.item())
             p.alg_bytes = nc * BYTES_PER_CONTACT + p.W * p.scene.n_bodies * BYTES_PER_BODY
             p.c_count = nc

@@ -381,6 +381,26 @@ comfree_status comfree_collide(comfree_ctx* ctx, int64_t first_world, int64_t n_
                                int32_t* world, float* c0, float* c1, float* c2, int32_t* c3, int32_t* link,
                                int64_t* n_contacts, int64_t* n_device, void* stream);
 
+/* One full step from the geometry: comfree_collide (the broadphase mode of
+ * reading R32 and the narrowphase, §II, §IV) followed by
+ * comfree_step (Alg. 1) on worlds [first_world, first_world +
+ * n_worlds), with the contact records kept where the front-end leaves them:
+ * the step reads each world's placed records (point, phi, normal, geom pair:
+ * 32 B) from the front-end's staging area and expands them (tangent,
+ * friction, condim, bodies) as the emit pass would, so no public contact
+ * streams are written or read.  The state is bit-identical to comfree_collide
+ * + comfree_step (the step's result does not depend on the contacts' memory
+ * layout).  A world with more records than the staging area is written in
+ * place into library-owned streams of `capacity` records (whole pairs; an
+ * overflow sets COMFREE_ERR_CAPACITY, reported by the next synchronising
+ * call).  Requires a geometry without a candidate list (broadphase mode) and
+ * a scene without chains; `worlds` as comfree_step takes it (DEVICE inputs).
+ * Configurations the staged kernel does not cover (general facet sets,
+ * per-facet impedance, statistics) run comfree_collide + comfree_step on the
+ * library-owned streams instead.  Asynchronous, graph-capturable. */
+comfree_status comfree_step_collided(comfree_ctx* ctx, const comfree_worlds* worlds, int64_t capacity, float dt,
+                                     void* stream);
+
 /* ---- MPPI on the batched step -------------------------
  * PAPER.md §V, Eq. (14)-(15), P:490-512 (reading R27).  The rollout
  * worlds of a context are P problems x N samples, world w belonging to problem

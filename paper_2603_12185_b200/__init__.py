@@ -371,6 +371,19 @@ class Context:
                                            float(self.dt if dt is None else dt),
                                            _stream_handle(stream)), "comfree_step")
 
+    def step_collided(self, capacity: int, dt: Optional[float] = None, inputs=None, first_world: int = 0,
+                      n_worlds: Optional[int] = None, stream=None):
+        """comfree_step_collided: collision front-end (broadphase mode) and the
+        contact step in one call, the contact records read by the step from the
+        front-end's staging area (no public contact streams).  ``inputs``:
+        optional device f_ext (no chains).  Asynchronous."""
+        nw = self.n_worlds - first_world if n_worlds is None else int(n_worlds)
+        fe = None if inputs is None else getattr(inputs, "f_ext", None)
+        w = _lib.comfree_worlds(int(first_world), nw, _ptr(fe), None, None, MEM_DEVICE)
+        self._check(self._lib.comfree_step_collided(self.h, ct.byref(w), int(capacity),
+                                                    float(self.dt if dt is None else dt), _stream_handle(stream)),
+                    "comfree_step_collided")
+
     def get_state(self, first_world: int = 0, n_worlds: Optional[int] = None, stream=None) -> dict:
         """comfree_get_state into host numpy arrays (synchronises)."""
         nw = self.n_worlds - first_world if n_worlds is None else int(n_worlds)

@@ -115,6 +115,7 @@ SIGNATURES = {
                                              ct.c_float, P, P, P, P]),
     "comfree_set_state_broadcast": (ct.c_int, [P, ct.c_int64, ct.c_int64, ct.c_int64, P, P]),
     "comfree_collide": (ct.c_int, [P, ct.c_int64, ct.c_int64, ct.c_int64, P, P, P, P, P, P, P, P, P]),
+    "comfree_step_collided": (ct.c_int, [P, ct.POINTER(comfree_worlds), ct.c_int64, ct.c_float, P]),
     "comfree_articulation_update": (ct.c_int, [P, ct.c_int64, ct.c_int64, P, P, P, ct.c_int64, P, P, P, P, P, P, P]),
     "comfree_get_world_stats": (ct.c_int, [P, ct.c_int64, ct.c_int64, P, ct.c_int32, P]),
     "comfree_segment_info": (ct.c_int, [P, P, P, P]),

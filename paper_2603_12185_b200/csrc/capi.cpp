@@ -79,6 +79,19 @@ struct comfree_ctx {
   // collision front-end: device geometry (comfree_load_geometry) and scan scratch
   DevBuf geo, col_counts, col_offs, col_tmp, col_frames;
   DevBuf bp_status, bp_queue, bp_count, bp_stage;   // broadphase mode scratch
+  // comfree_step_collided: library-owned contact streams (records of worlds the
+  // front-end writes in place), per-world in-place bases, and the staged-source
+  // description the step picks up (active only inside that call)
+  DevBuf fs_world, fs_c0, fs_c1, fs_c2, fs_c3, fs_link, bp_fbase;
+  int64_t* bp_fbase_hook = nullptr;  // set by comfree_step_collided for its collide call
+  struct {
+    bool active = false;
+    const unsigned long long* status = nullptr;
+    const float4* stage = nullptr;
+    int64_t cap = 0;
+    const int64_t* fbase = nullptr;
+    const int64_t* cut = nullptr;
+  } stg;
   int32_t n_geoms = 0, n_pairs = 0;
   float col_margin = 0.f, col_mu[3] = {0.f, 0.f, 0.f};
   int32_t col_condim = 3;
@@ -525,11 +538,12 @@ comfree_status comfree_step(comfree_ctx* ctx, const comfree_worlds* wd, const co
   ctx->last_sorted_copy = false;
   const int32_t* fused_world = nullptr;
   int seg_e0 = -1, seg_e1 = -1;
-  if (!off && ctx->timing && !(c->flags & COMFREE_CONTACTS_SORTED)) {
+  const bool stg_mode = ctx->stg.active;  // contacts from the front-end's staging area (comfree_step_collided)
+  if (!off && ctx->timing && !(c->flags & COMFREE_CONTACTS_SORTED) && !stg_mode) {
     cudaEvent_t e = next_event(ctx, &seg_e0);
     if (e) cudaEventRecord(e, s);
   }
-  if (!off) {
+  if (!off && !stg_mode) {
     CUDA_TRY(ctx, ensure(ctx->off, (size_t)(nw + 1) * sizeof(int64_t)));
     int64_t* doff = static_cast<int64_t*>(ctx->off.p);
     if ((c->flags & COMFREE_CONTACTS_SORTED) && (n > 0 || c->n_device)) {
@@ -651,6 +665,18 @@ comfree_status comfree_step(comfree_ctx* ctx, const comfree_worlds* wd, const co
 #ifdef CF_TIMELINE
   P.timeline = cf_debug_timeline_buf();
 #endif
+  if (stg_mode) {
+    P.st_status = ctx->stg.status;
+    P.st_base = ctx->stg.stage;
+    P.st_cap = ctx->stg.cap;
+    P.st_fbase = ctx->stg.fbase;
+    P.st_cut = ctx->stg.cut;
+    P.st_geom = static_cast<const int4*>(ctx->geo.p);
+    P.st_mu_t = ctx->col_mu[0];
+    P.st_mu_tor = ctx->col_mu[1];
+    P.st_mu_rol = ctx->col_mu[2];
+    P.st_condim = ctx->col_condim;
+  }
   int wpw = pick_wpw(sc, n, nw);
   if (const char* e = getenv("COMFREE_WPW")) {  // tuning override (1, 2, 4, 8 or 16 warps per world)
     const int v = atoi(e);
@@ -676,7 +702,7 @@ comfree_status comfree_step(comfree_ctx* ctx, const comfree_worlds* wd, const co
   // mode (profiles/r02_ab_kernel.txt), so not the default.
   bool persist = false;
   if (const char* e = getenv("COMFREE_PERSIST"))
-    persist = atoi(e) != 0 && sc.T == 0 && wpw == 8 && cf::step_persist_smem_bytes(sc) <= 227 * 1024;
+    persist = atoi(e) != 0 && sc.T == 0 && wpw == 8 && !stg_mode && cf::step_persist_smem_bytes(sc) <= 227 * 1024;
   if (persist) {
     CUDA_TRY(ctx, cf::launch_step_persist(P, s));
   } else {
@@ -981,7 +1007,17 @@ comfree_status comfree_collide(comfree_ctx* ctx, int64_t first, int64_t nw, int6
     CUDA_TRY(ctx, ensure(ctx->bp_stage, std::max<int64_t>(1, nw) * 4 * (size_t)stage_cap * sizeof(float4)));
     CUDA_TRY(ctx, cf::collide_broadphase(P, cap_c, capacity, static_cast<unsigned long long*>(ctx->bp_status.p),
                                          static_cast<int*>(ctx->bp_queue.p), n_device ? n_device : cnt, cnt + 1,
-                                         ctx->d_err, static_cast<float4*>(ctx->bp_stage.p), stage_cap, s));
+                                         ctx->d_err, static_cast<float4*>(ctx->bp_stage.p), stage_cap, s,
+                                         ctx->bp_fbase_hook));
+    if (ctx->bp_fbase_hook) {  // comfree_step_collided: the step reads the staged records
+      ctx->stg.status = static_cast<const unsigned long long*>(ctx->bp_status.p);
+      ctx->stg.stage = static_cast<const float4*>(ctx->bp_stage.p);
+      ctx->stg.cap = stage_cap;
+      ctx->stg.fbase = ctx->bp_fbase_hook;
+      ctx->stg.cut = reinterpret_cast<const int64_t*>(static_cast<int*>(ctx->bp_queue.p) + 2);
+      ctx->launches += 1;
+      return COMFREE_OK;
+    }
     ctx->launches += 2;
     if (n_device) return COMFREE_OK;
     int64_t h[2] = {0, 0};
@@ -1022,6 +1058,65 @@ comfree_status comfree_collide(comfree_ctx* ctx, int64_t first, int64_t nw, int6
   CUDA_TRY(ctx, cf::collide_emit(P, offs, capacity, nullptr, nullptr, s));
   ctx->launches += 1;
   return COMFREE_OK;
+}
+
+// One full step from the geometry (comfree.h): the broadphase without its emit
+// pass, then the step reading each world's staged records (the STG kernel), or
+// collide + step on library-owned streams when the staged kernel does not
+// cover the configuration.
+comfree_status comfree_step_collided(comfree_ctx* ctx, const comfree_worlds* wd, int64_t capacity, float dt,
+                                     void* stream) {
+  if (!ctx) return COMFREE_ERR_INVALID_ARGUMENT;
+  if (!ctx->loaded) return fail(ctx, COMFREE_ERR_STATE, "step_collided before load_scene");
+  if (!ctx->geo_loaded) return fail(ctx, COMFREE_ERR_STATE, "step_collided before load_geometry");
+  if (!wd) return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "step_collided: null worlds");
+  if (ctx->n_pairs != 0) return fail(ctx, COMFREE_ERR_STATE, "step_collided: the geometry has a candidate list (broadphase mode only)");
+  if (ctx->sc.T != 0) return fail(ctx, COMFREE_ERR_STATE, "step_collided: scenes with chains take collide + articulation_update + step");
+  if (wd->location != COMFREE_MEM_DEVICE) return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "step_collided: DEVICE world inputs");
+  if (capacity <= 0 || capacity > INT32_MAX) return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "step_collided: capacity");
+  const int64_t first = wd->first_world, nw = wd->n_worlds;
+  if (first < 0 || nw < 0 || first + nw > ctx->W) return fail(ctx, COMFREE_ERR_INVALID_ARGUMENT, "step_collided: world range");
+  CUDA_TRY(ctx, cudaSetDevice(ctx->device));
+  const size_t cap = (size_t)capacity;
+  CUDA_TRY(ctx, ensure(ctx->fs_world, cap * sizeof(int32_t)));
+  CUDA_TRY(ctx, ensure(ctx->fs_c0, cap * 16));
+  CUDA_TRY(ctx, ensure(ctx->fs_c1, cap * 16));
+  CUDA_TRY(ctx, ensure(ctx->fs_c2, cap * 16));
+  CUDA_TRY(ctx, ensure(ctx->fs_c3, cap * 16));
+  CUDA_TRY(ctx, ensure(ctx->fs_link, cap * 8));
+  CUDA_TRY(ctx, ensure(ctx->bp_count, 2 * sizeof(int64_t)));
+  int64_t* ndev = static_cast<int64_t*>(ctx->bp_count.p);
+  const comfree_config& c = ctx->cfg;
+  const bool staged_ok = c.n_t == 4 && c.power == 2.0f &&
+                         !(c.flags & (COMFREE_FLAG_EXACT_DIAGONAL | COMFREE_FLAG_FACET_DIAGONAL | COMFREE_FLAG_STATS)) &&
+                         cf::step_smem_bytes(ctx->sc, 8) <= 227 * 1024;
+  if (staged_ok) {
+    CUDA_TRY(ctx, ensure(ctx->bp_fbase, std::max<int64_t>(1, nw) * sizeof(int64_t)));
+    ctx->bp_fbase_hook = static_cast<int64_t*>(ctx->bp_fbase.p);
+  }
+  comfree_status st = comfree_collide(ctx, first, nw, capacity, static_cast<int32_t*>(ctx->fs_world.p),
+                                      static_cast<float*>(ctx->fs_c0.p), static_cast<float*>(ctx->fs_c1.p),
+                                      static_cast<float*>(ctx->fs_c2.p), static_cast<int32_t*>(ctx->fs_c3.p),
+                                      static_cast<int32_t*>(ctx->fs_link.p), nullptr, ndev, stream);
+  ctx->bp_fbase_hook = nullptr;
+  if (st != COMFREE_OK) return st;
+  comfree_contacts cd{};
+  cd.world = static_cast<const int32_t*>(ctx->fs_world.p);
+  cd.c0 = static_cast<const float*>(ctx->fs_c0.p);
+  cd.c1 = static_cast<const float*>(ctx->fs_c1.p);
+  cd.c2 = static_cast<const float*>(ctx->fs_c2.p);
+  cd.c3 = static_cast<const int32_t*>(ctx->fs_c3.p);
+  cd.flags = COMFREE_CONTACTS_SORTED;
+  cd.location = COMFREE_MEM_DEVICE;
+  cd.n_contacts = capacity;
+  if (!staged_ok) {
+    cd.n_device = ndev;
+    return comfree_step(ctx, wd, &cd, dt, stream);
+  }
+  ctx->stg.active = true;
+  st = comfree_step(ctx, wd, &cd, dt, stream);
+  ctx->stg.active = false;
+  return st;
 }
 
 comfree_status comfree_mppi_sample(comfree_ctx* ctx, int32_t P, int32_t N, int32_t H, const float* plan, float sigma,

@@ -685,6 +685,7 @@ struct BpParams {
   float4* stage;                   // [n_worlds][4][stage_cap]: staged records (found order), placed records
   int stage_cap;                   // records per world (a world with more runs the narrowphase twice)
   unsigned long long* gsum;        // [ceil(n_worlds / 256)] totals of groups of worlds (zeroed before the launch)
+  int64_t* fbase;                  // [n_worlds] or null: base offset of a world written in place (the fused step reads it)
 };
 
 __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_constant__ CollideParams P,
@@ -1177,6 +1178,7 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
   }
   __syncthreads();
   const int64_t base = ((int64_t)s_misc[3] << 31) | (int64_t)s_misc[4];
+  if (tid == 0 && Q.fbase) Q.fbase[w] = base;
   BP_MARK(6);
   // a candidate that does not fit is skipped; the smallest such offset is the
   // count of whole pairs
@@ -1187,6 +1189,7 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
     if (next == off) continue;
     if (base + next > Q.capacity) {
       atomicMin(reinterpret_cast<unsigned long long*>(Q.queue + 2), (unsigned long long)(base + off));
+      atomicOr(Q.err, ERR_CONTACT_CAP);
       continue;
     }
     const uint32_t pv = list[k];
@@ -1280,7 +1283,7 @@ size_t collide_bp_smem(int n_geoms, int cap_c, int np2) {
 
 cudaError_t collide_broadphase(const CollideParams& P, int cap_c, int64_t capacity, unsigned long long* status,
                                int* queue, int64_t* n_dev, int64_t* total, int* err, float4* stage, int stage_cap,
-                               cudaStream_t s) {
+                               cudaStream_t s, int64_t* fbase) {
   if (P.n_worlds == 0) return cudaMemsetAsync(n_dev, 0, sizeof(int64_t), s);
   int np2 = 1;
   while (np2 < P.n_geoms + 1) np2 <<= 1;  // the flat sweep's prefix takes n_np + 1 <= G + 1 entries
@@ -1295,10 +1298,11 @@ cudaError_t collide_broadphase(const CollideParams& P, int cap_c, int64_t capaci
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(k_collide_bp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  BpParams Q{cap_c, np2, capacity, status, queue, n_dev, total, err, stage, stage_cap, status + P.n_worlds};
+  BpParams Q{cap_c, np2, capacity, status, queue, n_dev, total, err, stage, stage_cap, status + P.n_worlds, fbase};
   k_collide_bp<<<(unsigned)P.n_worlds, kBpThreads, smem, s>>>(P, Q);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
+  if (fbase) return cudaSuccess;  // the fused step reads the staged records itself: no emit pass
   k_collide_bp_emit<<<(unsigned)P.n_worlds, kBpEmitThreads, 0, s>>>(P, Q);
   return cudaGetLastError();
 }

@@ -79,7 +79,18 @@ struct StepParams {
   int exact_diag;               // per-facet impedance, general variants only: 1 Eq. (11) (COMFREE_FLAG_EXACT_DIAGONAL),
                                 // 2 Eq. (12) with the facet diagonal (COMFREE_FLAG_FACET_DIAGONAL)
   unsigned* timeline;           // CF_TIMELINE builds only: per CTA (smid, t0, t1, t2, t3) globaltimer ns
+  // contacts from the collision front-end's staging area (comfree_step_collided), else st_status null
+  const unsigned long long* st_status;  // [n_worlds] broadphase status words: ST_VAL total, ST_DONE written in place
+  const float4* st_base;        // world w's placed records: st_base + (4 w + 2) st_cap (point, phi), + st_cap (normal, key)
+  int64_t st_cap;
+  const int64_t* st_fbase;      // [n_worlds] base offset in c0..c3 of a world written in place
+  const int64_t* st_cut;        // whole-pair cut of the in-place records (the capacity)
+  const int4* st_geom;          // geom table (kind, body, link, -)
+  float st_mu_t, st_mu_tor, st_mu_rol;
+  int st_condim;
 };
+// broadphase status word fields (collide.cu's chained-scan words)
+constexpr unsigned long long ST_DONE = 1ull << 61, ST_VAL = (1ull << 61) - 1;
 
 // Launchers (return cudaError_t of the launch).
 cudaError_t launch_step(const StepParams& p, int warps_per_world, cudaStream_t s);
@@ -143,9 +154,11 @@ size_t collide_bp_smem(int n_geoms, int cap_c, int np2);
 int collide_bp_min_cap(int n_geoms, int np2);
 // stage: [n_worlds][2][stage_cap] float4 scratch for the records of the single
 // narrowphase pass (a world with more records evaluates the narrowphase again).
+// fbase non-null (comfree_step_collided): no emit pass; the staged records stay
+// in `stage` for the step and a world written in place stores its base in fbase.
 cudaError_t collide_broadphase(const CollideParams& P, int cap_c, int64_t capacity, unsigned long long* status,
                                int* queue, int64_t* n_dev, int64_t* total, int* err, float4* stage, int stage_cap,
-                               cudaStream_t s);
+                               cudaStream_t s, int64_t* fbase = nullptr);
 cudaError_t collide_count_scan(const CollideParams& P, int32_t* counts, int32_t* offs, void* temp,
                                size_t* temp_bytes, cudaStream_t s);
 // n_dev != null: also stores the (clamped) total for the asynchronous mode

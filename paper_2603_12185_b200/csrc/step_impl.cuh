@@ -623,7 +623,27 @@ __device__ __forceinline__ void prefetch_world_l2(const StepParams& P, int64_t w
 // data) lives in a global scratch slab (P.gscratch, L2-resident) instead of
 // shared memory, for worlds too large for a CTA's 227 KB (about 2070 bodies):
 // the same code with global loads and global integer atomics.
-template <int CW, int WPW, bool FAST, bool TREES, bool IMP, bool GMEM = false>
+// Contact of the collision front-end's staging area (STG, comfree_step_collided):
+// the placed record (point, phi), (normal, pair key g1 << 16 | g2) expanded to
+// the step's four streams: the tangent of the normal exactly as the
+// front-end's emit pass computes it (IEEE operations in its order, no
+// contraction, so the step sees bit-identical records), the geometry's
+// friction coefficients and condim, the bodies of the pair's geoms.
+__device__ __forceinline__ void stg_expand(const StepParams& P, const float4 b, float4& c1, float4& c2, int4& c3) {
+  const float nx = b.x, ny = b.y, nz = b.z;
+  const uint32_t key = __float_as_uint(b.w);
+  const int g1 = (int)(key >> 16), g2 = (int)(key & 0xffffu);
+  const float sg = copysignf(1.f, nz);
+  const float a = __fdiv_rn(-1.f, __fadd_rn(sg, nz));
+  const float bb = __fmul_rn(__fmul_rn(nx, ny), a);
+  const float t1x = __fadd_rn(1.f, __fmul_rn(__fmul_rn(__fmul_rn(sg, nx), nx), a));
+  const float t1y = __fmul_rn(sg, bb), t1z = __fmul_rn(-sg, nx);
+  c1 = make_float4(nx, ny, nz, P.st_mu_t);
+  c2 = make_float4(t1x, t1y, t1z, P.st_mu_tor);
+  c3 = make_int4(__ldg(&P.st_geom[g1].y), __ldg(&P.st_geom[g2].y), __float_as_int(P.st_mu_rol), P.st_condim);
+}
+
+template <int CW, int WPW, bool FAST, bool TREES, bool IMP, bool GMEM = false, bool STG = false>
 __device__ __forceinline__ void world_step(const StepParams& P, float* smem, const int64_t w, const int group,
                                            const float* stg) {
   const SceneDev& sc = P.sc;
@@ -811,11 +831,32 @@ __device__ __forceinline__ void world_step(const StepParams& P, float* smem, con
   if (P.pf_ahead > 0 && gt == 0 && !stg && w + P.pf_ahead < P.n_worlds) prefetch_world_l2(P, w + P.pf_ahead);
 
   // Contact range of this world.
-  if (!CF_EARLY_RANGE) {
+  // STG: from the front-end's status word: a world whose records stayed in
+  // the staging area reads them there (placed order, local indices); a world
+  // the front-end wrote in place (more records than the staging area) reads
+  // the public streams from its base, up to the whole-pair cut of the capacity
+  bool staged = false;
+  const float4* S0p = nullptr;
+  const float4* S1p = nullptr;
+  if (STG) {
+    const unsigned long long sw = P.st_status[w];
+    const int64_t total = (int64_t)(sw & ST_VAL);
+    staged = !(sw & ST_DONE);
+    if (staged) {
+      cbeg = 0;
+      nloc = (int)total;
+      S0p = P.st_base + ((size_t)w * 4 + 2) * P.st_cap;
+      S1p = S0p + P.st_cap;
+    } else {
+      cbeg = P.st_fbase[w];
+      const int64_t cut = *P.st_cut;
+      nloc = (int)max((int64_t)0, min(total, cut - cbeg));
+    }
+  } else if (!CF_EARLY_RANGE) {
     cbeg = P.world_sorted ? rng[0] : P.off[w];
     nloc = (int)((P.world_sorted ? rng[1] : P.off[w + 1]) - cbeg);
   }
-  if (!P.world_sorted) {  // caller's off[]: monotone, inside [0, n], off[0] = 0, off[W] = n
+  if (!STG && !P.world_sorted) {  // caller's off[]: monotone, inside [0, n], off[0] = 0, off[W] = n
     const int64_t cend = cbeg + nloc;
     if (cbeg < 0 || nloc < 0 || cend > ncon || (w == 0 && cbeg != 0) || (w == P.n_worlds - 1 && cend != ncon)) {
       if (gt == 0) atomicOr(P.err, ERR_WORLD_RANGE);
@@ -834,7 +875,9 @@ __device__ __forceinline__ void world_step(const StepParams& P, float* smem, con
   // ---------------- S2-S6: contacts ----------------
   // Warp-uniform loop: lane l of warp j handles local contact base + l; base
   // advances by the group's thread count; the next contact is prefetched.
-  if (!CF_EARLY_RANGE && base + lane < nloc) {
+  if (STG && staged) {
+    if (base + lane < nloc) { C0 = ld_stream(S0p + base + lane); C1 = ld_stream(S1p + base + lane); }
+  } else if (!CF_EARLY_RANGE && base + lane < nloc) {
     const int j = base + lane;
     C0 = ld_stream(C0p + j); C1 = ld_stream(C1p + j); C2 = ld_stream(C2p + j); C3 = ld_stream(C3p + j);
     if (Wp) WID = ld_id(Wp + j);
@@ -866,11 +909,18 @@ __device__ __forceinline__ void world_step(const StepParams& P, float* smem, con
 #define CF_EARLY_PF 0
 #endif
     constexpr bool kLatePrefetch = !TREES && !CF_EARLY_PF;
-    const float4 c0 = C0, c1 = C1, c2 = C2;
-    const int4 c3 = C3;
+    const float4 c0 = C0;
+    float4 c1 = C1, c2 = C2;
+    int4 c3 = C3;
+    if (STG && staged) stg_expand(P, C1, c1, c2, c3);
     const int wid = WID;
     auto prefetch_next = [&]() {  // index clamped: no branch
       const int jn = min(j + kGT, nloc - 1);
+      if (STG && staged) {
+        C0 = ld_stream(S0p + jn);
+        C1 = ld_stream(S1p + jn);
+        return;
+      }
       // global index made opaque so the stream addresses are formed from the
       // kernel parameters each time (no per-stream 64-bit pointers held live)
       int64_t g = cbeg + jn;
@@ -962,7 +1012,7 @@ __device__ __forceinline__ void world_step(const StepParams& P, float* smem, con
     const float tr = trs2[0] + trs2[1];
     const float3 ra = rs2[0], rb = rs2[1];
     const float ima = ims2[0], dma = dms2[0], imb = ims2[1], dmb = dms2[1];  // S6 scales
-    if (CF_EARLY_C3 && kLatePrefetch && FAST) {  // the next contact's ids first: the loop head waits on them
+    if (CF_EARLY_C3 && kLatePrefetch && FAST && !(STG && staged)) {  // the next contact's ids first: the loop head waits on them
       int64_t g = cbeg + min(j + kGT, nloc - 1);
       asm volatile("" : "+l"(g));
       C3 = ld_stream(P.c3 + g);
@@ -1285,14 +1335,14 @@ __device__ __forceinline__ void world_step(const StepParams& P, float* smem, con
   }
 }
 
-template <int CW, int WPW, bool FAST, bool TREES, bool IMP, bool GMEM = false>
+template <int CW, int WPW, bool FAST, bool TREES, bool IMP, bool GMEM = false, bool STG = false>
 __global__ void __launch_bounds__(CW * 32, CW == kWarps ? CF_MINB : (CW == 16 ? 2 : (CW == 32 ? 1 : 16))) k_step(const __grid_constant__ StepParams P) {
   extern __shared__ float4 smem4[];
   constexpr int kGroups = CW / WPW;
   const int group = threadIdx.x / (WPW * 32);
   const int64_t w = (int64_t)blockIdx.x * kGroups + group;
   if (w >= P.n_worlds) return;  // whole group leaves together
-  world_step<CW, WPW, FAST, TREES, IMP, GMEM>(P, reinterpret_cast<float*>(smem4), w, group, nullptr);
+  world_step<CW, WPW, FAST, TREES, IMP, GMEM, STG>(P, reinterpret_cast<float*>(smem4), w, group, nullptr);
 }
 
 // ---- persistent variant: CTAs that step their worlds in turn ----
@@ -1406,13 +1456,13 @@ cudaError_t launch_persist_variant(const StepParams& p, cudaStream_t s, int n_sm
   return cudaGetLastError();
 }
 
-template <int CW, int WPW, bool FAST, bool TREES, bool IMP, bool GMEM = false>
+template <int CW, int WPW, bool FAST, bool TREES, bool IMP, bool GMEM = false, bool STG = false>
 cudaError_t launch_variant(const StepParams& p, cudaStream_t s) {
   const int groups = CW / WPW;
   const size_t smem = GMEM ? 0 : (size_t)groups * group_layout(p.sc).total * sizeof(float);
   const unsigned grid = (unsigned)((p.n_worlds + groups - 1) / groups);
   if (grid == 0) return cudaSuccess;
-  cudaError_t e = cudaFuncSetAttribute(k_step<CW, WPW, FAST, TREES, IMP, GMEM>,
+  cudaError_t e = cudaFuncSetAttribute(k_step<CW, WPW, FAST, TREES, IMP, GMEM, STG>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   StepParams q = p;
@@ -1421,11 +1471,11 @@ cudaError_t launch_variant(const StepParams& p, cudaStream_t s) {
   if (pf && atoi(pf) != 0) {
     int dev = 0, n_sm = 0, per_sm = 0;
     if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step<CW, WPW, FAST, TREES, IMP, GMEM>, CW * 32, smem) == cudaSuccess &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step<CW, WPW, FAST, TREES, IMP, GMEM, STG>, CW * 32, smem) == cudaSuccess &&
         (int64_t)grid > (int64_t)n_sm * per_sm)
       q.pf_ahead = (int64_t)n_sm * per_sm * groups;  // worlds resident at once
   }
-  k_step<CW, WPW, FAST, TREES, IMP, GMEM><<<grid, CW * 32, smem, s>>>(q);
+  k_step<CW, WPW, FAST, TREES, IMP, GMEM, STG><<<grid, CW * 32, smem, s>>>(q);
   return cudaGetLastError();
 }
 
@@ -1437,6 +1487,10 @@ cudaError_t launch_cfg(const StepParams& p, cudaStream_t s) {
   if (WPW == kWarps && p.gscratch) {  // worlds beyond shared memory: the global-scratch variant (general facets)
     if (trees) return imp ? launch_variant<CW, WPW, false, true, true, true>(p, s) : launch_variant<CW, WPW, false, true, false, true>(p, s);
     return imp ? launch_variant<CW, WPW, false, false, true, true>(p, s) : launch_variant<CW, WPW, false, false, false, true>(p, s);
+  }
+  if (p.st_status) {  // contacts from the front-end's staging area (comfree_step_collided: FAST, no chains, no outputs)
+    if (trees || imp || !(p.n_t == 4 && p.power_is_2 && !p.exact_diag) || p.gscratch) return cudaErrorInvalidValue;
+    return launch_variant<CW, WPW, true, false, false, false, true>(p, s);
   }
   if (p.n_t == 4 && p.power_is_2 && !p.exact_diag) {
     if (trees) return imp ? launch_variant<CW, WPW, true, true, true>(p, s) : launch_variant<CW, WPW, true, true, false>(p, s);

@@ -506,3 +506,31 @@ def test_broadphase_stage_fallback_identical(tmp_path):
         assert set(a.files) == set(b.files)
         for k in a.files:
             np.testing.assert_array_equal(a[k], b[k], err_msg=k)
+
+
+def test_step_collided_bitwise(tmp_path):
+    """comfree_step_collided (the step reading each world's staged records
+    from the front-end, no emit pass, no public contact streams) gives the
+    bit-identical state of comfree_collide + comfree_step over 6 pile steps:
+    with the default staging area, with a 600-record area (every world written
+    in place: the step reads the library-owned streams from the world's base)
+    and with 1350 (some worlds each way)."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    for cap in ("0", "600", "1350"):
+        out = str(tmp_path / f"fused_{cap}.npz")
+        env = dict(os.environ)
+        if cap != "0":
+            env["COMFREE_BP_STAGE_CAP"] = cap
+        subprocess.run([sys.executable, os.path.join(here, "_bp_fused_run.py"), out], check=True, env=env,
+                       cwd=os.path.dirname(here), timeout=300)
+        r = np.load(out)
+        keys = [k[len("split_"):] for k in r.files if k.startswith("split_")]
+        assert "vel" in keys and "pos" in keys
+        for k in keys:
+            a, b = r["split_" + k], r["fused_" + k]
+            assert np.all(np.isfinite(a))
+            np.testing.assert_array_equal(a, b, err_msg=f"{k} (stage cap {cap})")
+        assert np.abs(r["split_vel"]).max() > 0
