@@ -52,6 +52,7 @@ ctx_p.load_geometry(scenes.pile_geometry((5, 5, 2), broadphase=True))
 ctx_p.collide(capacity=3 * 400)
 dcb, _ = ctx_p.collide(capacity=3 * 400, device_count=True)
 ctx_p.step(dcb, None)
+ctx_p.step_collided(3 * 400)                     # fused: the step reads the staged records
 ctx_p.check()
 # articulated upstream + collision front-end + step (the closed-loop hand)
 import torch  # noqa: E402
