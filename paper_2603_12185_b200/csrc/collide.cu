@@ -597,7 +597,7 @@ __global__ void k_collide_emit(const __grid_constant__ CollideParams P, const in
 #endif
 constexpr int kBpThreads = CF_BP_THREADS;
 #ifndef CF_BP_TILE_BRANCHY
-#define CF_BP_TILE_BRANCHY 1
+#define CF_BP_TILE_BRANCHY 2  // 2: groups of 8 loads (362 vs 365 us full step), 1: per-test predicated loads, 0: all 32 unconditional
 #endif
 #ifdef CF_BP_TIMELINE  // tuning diagnostic: per-world phase timestamps (globaltimer ns) into P.frames
 #define BP_MARK(k)                                                                        \
@@ -943,7 +943,7 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
         // copies, still inside the CTA's shared memory: the list storage and
         // the arrays after it) and branch-free tests, so the 32 loads overlap;
         // the tail is masked off once
-#if CF_BP_TILE_BRANCHY  // default 1: the predicated loads measured faster (418 vs 424 us full step) than branch-free unconditional ones
+#if CF_BP_TILE_BRANCHY == 1  // per-test predicated loads: faster (418 vs 424 us full step) than all-unconditional ones
 #pragma unroll
         for (int bb = 0; bb < 32; ++bb) {
           if (bb < nb) {
@@ -951,6 +951,21 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
             m |= (si.x <= sj.z && sj.x <= si.z && si.y <= sj.w && sj.y <= si.w ? 1u : 0u) << bb;
           }
         }
+#elif CF_BP_TILE_BRANCHY == 2
+        // groups of 8 tests: a group is skipped past the tile's end, its loads
+        // are unconditional (up to 7 past the end, inside shared memory) so
+        // they overlap; the tail is masked off once
+#pragma unroll
+        for (int g8 = 0; g8 < 32; g8 += 8) {
+          if (g8 < nb) {
+#pragma unroll
+            for (int bb = g8; bb < g8 + 8; ++bb) {
+              const float4 sj = sp[bb];
+              m |= (uint32_t)((si.x <= sj.z) & (sj.x <= si.z) & (si.y <= sj.w) & (sj.y <= si.w)) << bb;
+            }
+          }
+        }
+        m &= nb >= 32 ? 0xffffffffu : ((1u << nb) - 1u);
 #else
 #pragma unroll
         for (int bb = 0; bb < 32; ++bb) {
