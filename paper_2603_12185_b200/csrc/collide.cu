@@ -95,7 +95,7 @@ __device__ __forceinline__ Frame load_frame(const float4* Fw, int g) {
 
 __device__ __forceinline__ V3 tangent(V3 n) {
   const float s = copysignf(1.f, n.z);
-  const float a = -1.f / (s + n.z);
+  const float a = __fdiv_rn(-1.f, s + n.z);  // IEEE division whatever the file's -prec-div (the fused step repeats it)
   const float b = n.x * n.y * a;
   return v3(1.f + s * n.x * n.x * a, s * b, -s * n.x);
 }
@@ -228,14 +228,23 @@ __device__ __forceinline__ float sphere_box(V3 c, float R, const Frame& Fb, floa
       d2 += dd[k] * dd[k];
     }
     dist = sqrtf(d2);
+#if CF_NP_FASTDIV
+    const float idist = 1.f / dist;  // one division for the three components
+#pragma unroll
+    for (int k = 0; k < 3; ++k) nl[k] = dd[k] * idist;
+#else
 #pragma unroll
     for (int k = 0; k < 3; ++k) nl[k] = dd[k] / dist;
+#endif
   }
   nbox = rmul(Fb.R, v3(nl[0], nl[1], nl[2]));
   qs = add(Fb.x, rmul(Fb.R, v3(ql[0], ql[1], ql[2])));
   return dist - R;
 }
 
+#ifndef CF_NP_FASTDIV
+#define CF_NP_FASTDIV 1  // one reciprocal per normal: 365 -> 331 us fused full step (IEEE divisions are subroutine calls)
+#endif
 // Corners of box B against the faces of box A (vertex-face).
 template <class O>
 __device__ __forceinline__ void box_corners_on(const Frame& A, float4 hA, const Frame& Bf, float4 hB, float margin,
@@ -332,9 +341,15 @@ __device__ __forceinline__ bool box_sat(const Frame& A, float4 hA4, const Frame&
 #pragma unroll
     for (int j = 0; j < 3; ++j) {  // unrolled: ea / eb stay in registers
       V3 L = cross(ea[i], eb[j]);
+#if CF_NP_FASTDIV
+      const float l2 = dot(L, L);
+      if (!(l2 > 1e-12f)) continue;  // |cross| <= 1e-6 (R33)
+      L = mul(rsqrtf(l2), L);
+#else
       const float nl = sqrtf(dot(L, L));
       if (!(nl > 1e-6f)) continue;
       L = mul(1.f / nl, L);
+#endif
       const float ov = overlap(L);
       if (ov < -margin) return false;
       if (ov < S.best) { S.best = ov; S.bi = i; S.bj = j; S.bL = L; }
