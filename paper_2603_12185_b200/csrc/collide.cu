@@ -198,6 +198,9 @@ __device__ __forceinline__ void two_spheres(V3 c1, float R1, V3 c2, float R2, fl
   if (phi < margin) o.add(add(c1, mul(R1 + 0.5f * phi, nn)), phi, nn);
 }
 
+#ifndef CF_NP_FASTDIV
+#define CF_NP_FASTDIV 1  // one reciprocal per normal: 365 -> 331 us fused full step (IEEE divisions are subroutine calls)
+#endif
 // Sphere (centre c, radius R) against a box frame: phi, box-outward normal, box surface point.
 __device__ __forceinline__ float sphere_box(V3 c, float R, const Frame& Fb, float4 h4, V3& nbox, V3& qs) {
   const float h[3] = {h4.x, h4.y, h4.z};
@@ -242,9 +245,6 @@ __device__ __forceinline__ float sphere_box(V3 c, float R, const Frame& Fb, floa
   return dist - R;
 }
 
-#ifndef CF_NP_FASTDIV
-#define CF_NP_FASTDIV 1  // one reciprocal per normal: 365 -> 331 us fused full step (IEEE divisions are subroutine calls)
-#endif
 // Corners of box B against the faces of box A (vertex-face).
 template <class O>
 __device__ __forceinline__ void box_corners_on(const Frame& A, float4 hA, const Frame& Bf, float4 hB, float margin,
