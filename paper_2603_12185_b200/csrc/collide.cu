@@ -170,9 +170,22 @@ __device__ __forceinline__ void capsule_ends(const GeomTab& T, const float4* Fw,
   b = add(F.x, mul(hl, z));
 }
 
+#ifndef CF_NP_FASTDIV
+#define CF_NP_FASTDIV 1  // one reciprocal per normal: 365 -> 331 us fused full step (IEEE divisions are subroutine calls)
+#endif
+// Quotients of the segment parameters (clamped to [0, 1] afterwards): the
+// approximate division (2 ulp) with CF_NP_FASTDIV, IEEE division otherwise.
+__device__ __forceinline__ float np_div(float x, float y) {
+#if CF_NP_FASTDIV
+  return __fdividef(x, y);
+#else
+  return x / y;
+#endif
+}
+
 __device__ __forceinline__ V3 closest_on_segment(V3 a, V3 b, V3 c) {
   const V3 d = sub(b, a);
-  const float t = fminf(fmaxf(dot(sub(c, a), d) / dot(d, d), 0.f), 1.f);
+  const float t = fminf(fmaxf(np_div(dot(sub(c, a), d), dot(d, d)), 0.f), 1.f);
   return add(a, mul(t, d));
 }
 
@@ -181,10 +194,10 @@ __device__ __forceinline__ void closest_segments(V3 p1, V3 q1, V3 p2, V3 q2, V3&
   const V3 d1 = sub(q1, p1), d2 = sub(q2, p2), r = sub(p1, p2);
   const float a = dot(d1, d1), e = dot(d2, d2), f = dot(d2, r), c = dot(d1, r), b = dot(d1, d2);
   const float denom = a * e - b * b;
-  float s = denom > 1e-12f * a * e ? fminf(fmaxf((b * f - c * e) / denom, 0.f), 1.f) : 0.f;
-  float t = (b * s + f) / e;
-  if (t < 0.f) { t = 0.f; s = fminf(fmaxf(-c / a, 0.f), 1.f); }
-  else if (t > 1.f) { t = 1.f; s = fminf(fmaxf((b - c) / a, 0.f), 1.f); }
+  float s = denom > 1e-12f * a * e ? fminf(fmaxf(np_div(b * f - c * e, denom), 0.f), 1.f) : 0.f;
+  float t = np_div(b * s + f, e);
+  if (t < 0.f) { t = 0.f; s = fminf(fmaxf(np_div(-c, a), 0.f), 1.f); }
+  else if (t > 1.f) { t = 1.f; s = fminf(fmaxf(np_div(b - c, a), 0.f), 1.f); }
   c1 = add(p1, mul(s, d1));
   c2 = add(p2, mul(t, d2));
 }
@@ -192,15 +205,17 @@ __device__ __forceinline__ void closest_segments(V3 p1, V3 q1, V3 p2, V3 q2, V3&
 template <class O>
 __device__ __forceinline__ void two_spheres(V3 c1, float R1, V3 c2, float R2, float margin, O& o) {
   const V3 d = sub(c2, c1);
+#if CF_NP_FASTDIV
+  const float d2 = dot(d, d), idist = rsqrtf(d2), dist = d2 * idist;
+  const V3 nn = mul(idist, d);
+#else
   const float dist = sqrtf(dot(d, d));
   const V3 nn = mul(1.f / dist, d);
+#endif
   const float phi = dist - R1 - R2;
   if (phi < margin) o.add(add(c1, mul(R1 + 0.5f * phi, nn)), phi, nn);
 }
 
-#ifndef CF_NP_FASTDIV
-#define CF_NP_FASTDIV 1  // one reciprocal per normal: 365 -> 331 us fused full step (IEEE divisions are subroutine calls)
-#endif
 // Sphere (centre c, radius R) against a box frame: phi, box-outward normal, box surface point.
 __device__ __forceinline__ float sphere_box(V3 c, float R, const Frame& Fb, float4 h4, V3& nbox, V3& qs) {
   const float h[3] = {h4.x, h4.y, h4.z};
@@ -504,7 +519,7 @@ __device__ CF_NP_ATTR int pair_contacts_rt(const CollideParams& P, const GeomTab
       // reading R34: the segment point nearest the box centre as a third sphere
       // when strictly inside the segment (a capsule lying across a box)
       const V3 d = sub(e[1], e[0]);
-      const float t = dot(sub(Fb.x, e[0]), d) / dot(d, d);
+      const float t = np_div(dot(sub(Fb.x, e[0]), d), dot(d, d));
       e[2] = add(e[0], mul(t, d));
       if (t > 0.f && t < 1.f) ne = 3;
     } else {
