@@ -12,6 +12,8 @@ $B --workload hand --upstream --cpu-seconds 2 > gpurun_out/${TAG}_bench_hand_ups
 $B --workload hand --collide --cpu-seconds 1 > gpurun_out/${TAG}_bench_hand_closed_loop.json 2> /dev/null
 $B --collide --cpu-seconds 1 > gpurun_out/${TAG}_bench_pile_full_step_broadphase.json 2> /dev/null
 $B --collide --pair-list --cpu-seconds 1 > gpurun_out/${TAG}_bench_pile_full_step_pairlist.json 2> /dev/null
+$B --collide --split-collide --cpu-seconds 1 > gpurun_out/${TAG}_bench_pile_full_step_split.json 2> /dev/null
+$B --collide --steps 20 --cpu-seconds 1 > gpurun_out/${TAG}_bench_pile_full_step_20steps.json 2> /dev/null
 timeout 600 python tools/mppi_bench.py > gpurun_out/${TAG}_mppi_p16.json 2> /dev/null
 timeout 600 python tools/mppi_bench.py --problems 1 > gpurun_out/${TAG}_mppi_p1.json 2> /dev/null
 timeout 900 python bench.py --workload mixed --cpu-seconds 5 --steps 100 > gpurun_out/${TAG}_bench_mixed.json 2> gpurun_out/${TAG}_bench_mixed.err
