@@ -534,3 +534,29 @@ def test_step_collided_bitwise(tmp_path):
             assert np.all(np.isfinite(a))
             np.testing.assert_array_equal(a, b, err_msg=f"{k} (stage cap {cap})")
         assert np.abs(r["split_vel"]).max() > 0
+
+
+def test_step_collided_refuses_list_geometry_and_chains():
+    """comfree_step_collided needs the broadphase mode and a chain-free scene:
+    a geometry with a candidate list, or the hand with chains, is refused with
+    COMFREE_ERR_STATE and leaves the state untouched."""
+    import paper_2603_12185_b200 as cf
+    scene, st, _ = scenes.c4_pile(n_worlds=2, contacts_per_world=200, lattice=(5, 5, 2))
+    ctx = cf.Context(CFG)
+    ctx.load_scene(scene, st.n_worlds, st)
+    ctx.load_geometry(scenes.pile_geometry((5, 5, 2)))            # lattice candidate list
+    before = ctx.get_state()
+    with pytest.raises(cf.ComfreeError) as e:
+        ctx.step_collided(2 * 2000)
+    assert e.value.status == 6                       # COMFREE_ERR_STATE
+    after = ctx.get_state()
+    for k in before:
+        np.testing.assert_array_equal(before[k], after[k])
+    scene, st, _, _ = scenes.c3_hand(n_worlds=2)
+    ctx = cf.Context(CFG)
+    ctx.load_scene(scene, 2, st)
+    ctx.load_articulation(scenes.hand_articulation())
+    ctx.load_geometry(scenes.hand_geometry(margin=0.002))
+    with pytest.raises(cf.ComfreeError) as e:
+        ctx.step_collided(2 * 40)
+    assert e.value.status == 6                       # COMFREE_ERR_STATE
