@@ -640,6 +640,15 @@ constexpr int kBpThreads = CF_BP_THREADS;
 #define BP_MARK(k)
 #endif
 
+#ifndef CF_BP_PUB
+#define CF_BP_PUB 4
+#endif
+// L2 load of a record this CTA staged earlier (cache-global: not from L1)
+__device__ __forceinline__ float4 ld_cg4(const float4* p) {
+  float4 r;
+  asm volatile("ld.global.cg.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+  return r;
+}
 __device__ __forceinline__ uint32_t f2key(float f) {  // order-preserving float -> uint32
   const uint32_t u = __float_as_uint(f);
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
@@ -1192,12 +1201,26 @@ __global__ void __launch_bounds__(kBpThreads, 2) k_collide_bp(const __grid_const
     // world, with their pair's (g1, g2) instead of the tag
     float4* o0 = Q.stage + ((size_t)w * 4 + 2) * Q.stage_cap;
     float4* o1 = o0 + Q.stage_cap;
-    for (int r = tid; r < world_total; r += kBpThreads) {
-      const float4 a = S.s0[r], b = S.s1[r];
-      const int tag = __float_as_int(b.w), k = tag >> 5;
-      const int l = ncon[k] + (tag & 31);
-      o0[l] = a;
-      o1[l] = make_float4(b.x, b.y, b.z, __uint_as_float(list[k]));
+    // CF_BP_PUB records per thread loaded before any is stored (the staging
+    // reads are L2 round trips that would otherwise wait behind the stores)
+    constexpr int kPub = CF_BP_PUB;
+    for (int r0 = 0; r0 < world_total; r0 += kPub * kBpThreads) {
+      float4 a[kPub], b[kPub];
+#pragma unroll
+      for (int u = 0; u < kPub; ++u) {
+        const int r = r0 + u * kBpThreads + tid;
+        if (r < world_total) { a[u] = ld_cg4(S.s0 + r); b[u] = ld_cg4(S.s1 + r); }
+      }
+#pragma unroll
+      for (int u = 0; u < kPub; ++u) {
+        const int r = r0 + u * kBpThreads + tid;
+        if (r < world_total) {
+          const int tag = __float_as_int(b[u].w), k = tag >> 5;
+          const int l = ncon[k] + (tag & 31);
+          o0[l] = a[u];
+          o1[l] = make_float4(b[u].x, b[u].y, b[u].z, __uint_as_float(list[k]));
+        }
+      }
     }
     if (tid == 0) {
       atomicAdd(&Q.gsum[w >> kGsumShift], (unsigned long long)world_total);
