@@ -18,6 +18,8 @@ def main(out, n_worlds=40, steps=6):
     scene, st, _ = scenes.c4_pile(n_worlds=n_worlds, contacts_per_world=2000)
     geo = scenes.pile_geometry((10, 10, 5), broadphase=True)
     cfg = Config()
+    if os.environ.get("FUSED_NT"):  # a facet set the staged kernel does not cover: the call's collide + step path
+        cfg = cfg.with_(n_t=int(os.environ["FUSED_NT"]))
     cap = n_worlds * 6000
     res = {}
     for mode in ("split", "fused"):

@@ -514,15 +514,18 @@ def test_step_collided_bitwise(tmp_path):
     bit-identical state of comfree_collide + comfree_step over 6 pile steps:
     with the default staging area, with a 600-record area (every world written
     in place: the step reads the library-owned streams from the world's base)
-    and with 1350 (some worlds each way)."""
+    and with 1350 (some worlds each way); and with 8 tangent facets, which the
+    call runs as collide + step on its own streams."""
     import os
     import subprocess
     import sys
     here = os.path.dirname(os.path.abspath(__file__))
-    for cap in ("0", "600", "1350"):
+    for cap in ("0", "600", "1350", "nt8"):
         out = str(tmp_path / f"fused_{cap}.npz")
         env = dict(os.environ)
-        if cap != "0":
+        if cap == "nt8":                  # 8 tangent facets: comfree_step_collided's collide + step path
+            env["FUSED_NT"] = "8"
+        elif cap != "0":
             env["COMFREE_BP_STAGE_CAP"] = cap
         subprocess.run([sys.executable, os.path.join(here, "_bp_fused_run.py"), out], check=True, env=env,
                        cwd=os.path.dirname(here), timeout=300)
