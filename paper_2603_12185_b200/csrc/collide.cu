@@ -1296,8 +1296,19 @@ __global__ void __launch_bounds__(kBpEmitThreads) k_collide_bp_emit(const __grid
     const float4* o0 = Q.stage + ((size_t)w * 4 + 2) * Q.stage_cap;
     const float4* o1 = o0 + Q.stage_cap;
     const bool cut = base + world_total > Q.capacity;  // only whole pairs within the capacity
-    for (int l = tid; l < world_total; l += kBpEmitThreads) {
-      const float4 a = o0[l], b = o1[l];
+    constexpr int kPub = CF_BP_PUB;  // records per thread loaded before any is written
+    for (int l0 = 0; l0 < world_total; l0 += kPub * kBpEmitThreads) {
+    float4 aa[kPub], bb[kPub];
+#pragma unroll
+    for (int u = 0; u < kPub; ++u) {
+      const int l = l0 + u * kBpEmitThreads + tid;
+      if (l < world_total) { aa[u] = ld_cg4(o0 + l); bb[u] = ld_cg4(o1 + l); }
+    }
+#pragma unroll
+    for (int u = 0; u < kPub; ++u) {
+      const int l = l0 + u * kBpEmitThreads + tid;
+      if (l >= world_total) continue;
+      const float4 a = aa[u], b = bb[u];
       const uint32_t pv = __float_as_uint(b.w);
       if (cut) {  // the pair's records [off, next) are the neighbours with its (g1, g2)
         int off = l, next = l + 1;
@@ -1318,6 +1329,7 @@ __global__ void __launch_bounds__(kBpEmitThreads) k_collide_bp_emit(const __grid
       P.c3[c] = make_int4(g1.y, g2.y, __float_as_int(P.mu_rol), P.condim);
       P.world[c] = (int32_t)w;
       P.link[c] = make_int2(g1.y < -1 ? g1.z : 0, g2.y < -1 ? g2.z : 0);
+    }
     }
   }
   // the last CTA: device count, error
