@@ -674,6 +674,13 @@ __device__ __forceinline__ void world_step(const StepParams& P, float* smem, con
   // contacts in use: the device-side count when given (the streams' capacity is P.n_contacts)
   const int64_t ncon = P.n_dev ? min(*P.n_dev, P.n_contacts) : P.n_contacts;
   if (P.world_sorted && (CF_EARLY_RANGE || gt < 32)) probe = probe_issue(P.world_sorted, ncon, P.n_worlds, w, w + 1, lane);
+#ifndef CF_SELF_PF
+#define CF_SELF_PF 1  // C4: 56.3 -> 55.4 us (profiles/r02_ab_kernel.txt)
+#endif
+  // the world's own slab planes requested into L2 by one bulk prefetch at the
+  // start, so S1's second round of body loads waits on L2 rather than HBM
+  if (CF_SELF_PF && gt == 0 && !stg && !GMEM)
+    bulk_prefetch_l2(slab, (uint32_t)(N_BODY_PLANES * Bp * sizeof(float)));
   const float k = P.k, kappa_g = P.kappa;
   int n_active = 0;
   float max_pen = 0.f;
